@@ -1,0 +1,415 @@
+// ORACLE TEST INFRASTRUCTURE -- golden-vector exporter.
+//
+// Links the reference library compiled in place from /root/reference
+// (oracle/Makefile) and writes:
+//   <out>/programs/<id>.kcp        front-end output per suite kernel whose
+//                                  symbolic extraction succeeds (program_text)
+//   <out>/programs/index.json      per kernel: role, params, symbolic status
+//   <gold>/suite_cases.json        bound PVs (cap 2e7) + noiseless simdev-v1
+//                                  times for the 406 manifest cases
+//   <gold>/oracle_draws.json       20 oracle-lattice draws per kernel, seed
+//                                  0x5eed (acceptance.cpp:58-131)
+//   <gold>/fit_suite.json          fit over the 390 measurement cases + the
+//                                  16 test-case predictions (config 1)
+//   <gold>/weights_suite.json      the same weights via write_weights_json
+//   <gold>/fit_synthetic.json      test_model.cpp-style synthetic designs
+//   <gold>/grid_samples.json       evaluate_properties + predict at sampled
+//                                  grid points, incl. counts > 2^64
+// Every double is written twice: %.17g and C99 hex (%a) for bit-exact checks.
+#include <cstdio>
+#include <filesystem>
+#include <fstream>
+#include <iostream>
+#include <random>
+
+#include "json.hpp"
+#include "kcref_program.hpp"
+#include "kernelcost/csvio.hpp"
+#include "kernelcost/error.hpp"
+#include "kernelcost/jsonio.hpp"
+#include "kernelcost/model.hpp"
+#include "kernelcost/parser.hpp"
+#include "kernelcost/props.hpp"
+#include "kernelcost/schema.hpp"
+#include "kernelcost/simdevice.hpp"
+#include "kernelcost/suite.hpp"
+
+namespace kc = kernelcost;
+using json = nlohmann::ordered_json;
+
+namespace {
+
+std::string hexd(double v) {
+  char buf[64];
+  std::snprintf(buf, sizeof buf, "%a", v);
+  return buf;
+}
+
+json dbl(double v) { return json::array({v, hexd(v)}); }
+
+json pv_json(const kc::PropertyVector& pv) {
+  json o = json::object();
+  const auto& keys = kc::schema_keys();
+  for (size_t i = 0; i < pv.entries.size(); ++i) {
+    if (pv.entries[i].is_zero()) continue;
+    if (pv.entries[i].is_constant())
+      o[keys[i]] = kc::rat_str(pv.entries[i].constant_value());
+    else
+      o[keys[i]] = pv.entries[i].str();
+  }
+  return o;
+}
+
+json binding_json(const kc::Binding& b) {
+  json o = json::object();
+  for (const auto& [k, v] : b) o[k] = v.str();
+  return o;
+}
+
+void write(const std::string& path, const json& j) {
+  std::ofstream out(path);
+  out << j.dump(1) << "\n";
+}
+
+const kc::Int kCap(20000000);
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 3) {
+    std::cerr << "usage: kcref_export <programs_dir> <golden_dir>\n";
+    return 2;
+  }
+  const std::string pdir = argv[1], gdir = argv[2];
+  std::filesystem::create_directories(pdir);
+  std::filesystem::create_directories(gdir);
+
+  const kc::SuiteLibrary lib = kc::build_suite();
+  const kc::SimDevice ref = kc::SimDevice::reference();
+  std::map<std::string, kc::KernelIR> irs;
+  std::map<std::string, kc::PropertyVector> sym;
+
+  // ---- programs ---------------------------------------------------------
+  json index = json::array();
+  for (const auto& sk : lib.kernels) {
+    kc::KernelIR k = kc::parse_kernel(sk.text);
+    json e;
+    e["id"] = sk.id;
+    e["role"] = sk.role;
+    e["group_config"] = sk.group_config;
+    json params = json::array();
+    for (const auto& p : k.params) params.push_back(p.name);
+    e["params"] = params;
+    json assumes = json::array();
+    for (const auto& c : k.assumptions) assumes.push_back(c.str());
+    e["assume"] = assumes;
+    try {
+      kc::PropertyVector pv = kc::extract_properties(k);
+      const std::string text = kcref::program_text(k, pv);
+      std::ofstream(pdir + "/" + sk.id + ".kcp") << text;
+      e["symbolic"] = true;
+      e["file"] = sk.id + ".kcp";
+      sym.emplace(sk.id, std::move(pv));
+    } catch (const kc::Error& err) {
+      e["symbolic"] = false;
+      e["error"] = kc::errc_name(err.code());
+      e["message"] = err.what();
+    }
+    index.push_back(e);
+    irs.emplace(sk.id, std::move(k));
+  }
+  write(pdir + "/index.json", json{{"schema_version", kc::kSchemaVersion},
+                                    {"kernels", index}});
+  std::cerr << "programs: " << sym.size() << "/" << lib.kernels.size()
+            << " symbolic\n";
+
+  // ---- 406 suite cases --------------------------------------------------
+  std::vector<kc::FitCase> fit_cases;
+  std::vector<std::pair<kc::SuiteCase, kc::PropertyVector>> test_pvs;
+  json cases = json::array();
+  for (const char* role : {"measurement", "test"}) {
+    const auto list = std::string(role) == "measurement" ? lib.measurement_cases()
+                                                         : lib.test_cases();
+    for (const auto& c : list) {
+      json e;
+      e["kernel"] = c.kernel_id;
+      e["role"] = role;
+      e["binding"] = binding_json(c.binding);
+      const kc::PropertyVector pv = kc::extract_properties(irs.at(c.kernel_id), c.binding, kCap);
+      e["counts"] = pv_json(pv);
+      const double t = kc::noiseless_time(ref, pv);
+      e["time_s"] = dbl(t);
+      if (std::string(role) == "measurement")
+        fit_cases.push_back({pv, t});
+      else
+        test_pvs.push_back({c, pv});
+      cases.push_back(e);
+    }
+  }
+  write(gdir + "/suite_cases.json", json{{"cap", kCap.str()}, {"cases", cases}});
+  std::cerr << "suite cases: " << cases.size() << "\n";
+
+  // ---- config 1: fit on the measurement suite, predict the test kernels --
+  {
+    const kc::DesignMatrix d = kc::build_design_matrix(fit_cases);
+    auto [w, rep] = kc::fit_weights(d, ref.name);
+    kc::write_weights_json(gdir + "/weights_suite.json", w, rep);
+    json o;
+    o["device"] = w.device;
+    json alpha = json::object(), covered = json::array();
+    const auto& keys = kc::schema_keys();
+    for (size_t i = 0; i < keys.size(); ++i) {
+      if (w.covered[i]) {
+        alpha[keys[i]] = dbl(w.alpha[i]);
+        covered.push_back(keys[i]);
+      }
+    }
+    o["alpha"] = alpha;
+    o["covered"] = covered;
+    o["objective"] = dbl(rep.objective);
+    json res = json::array();
+    for (double r : rep.residuals) res.push_back(hexd(r));
+    o["residuals"] = res;
+    json preds = json::array();
+    for (const auto& [c, pv] : test_pvs) {
+      const kc::Prediction p = kc::predict(w, pv);
+      const kc::Prediction pr = kc::predict(
+          kc::ModelWeights{"ref", kc::kSchemaVersion, ref.alpha,
+                           std::vector<bool>(kc::schema_size(), true), 0, 0},
+          pv);
+      preds.push_back({{"kernel", c.kernel_id},
+                       {"binding", binding_json(c.binding)},
+                       {"predicted_s", dbl(p.seconds)},
+                       {"predicted_simdev_s", dbl(pr.seconds)},
+                       {"noiseless_s", dbl(kc::noiseless_time(ref, pv))},
+                       {"warnings", p.warnings}});
+    }
+    o["test_predictions"] = preds;
+    write(gdir + "/fit_suite.json", o);
+  }
+
+  // ---- oracle-lattice draws (acceptance.cpp:58-131 pattern) --------------
+  {
+    std::mt19937_64 rng(0x5eed);
+    json draws = json::array();
+    for (const auto& sk : lib.kernels) {
+      for (int d = 0; d < 20; ++d) {
+        const kc::Binding b = kc::sample_oracle_binding(sk, rng);
+        json e;
+        e["kernel"] = sk.id;
+        e["binding"] = binding_json(b);
+        const kc::PropertyVector pv = kc::extract_properties(irs.at(sk.id), b, kCap);
+        e["counts"] = pv_json(pv);
+        if (sym.count(sk.id)) {
+          const kc::PropertyVector ev = kc::evaluate_properties(irs.at(sk.id), sym.at(sk.id), b);
+          e["symbolic_equal"] = ev.integers() == pv.integers();
+        }
+        draws.push_back(e);
+      }
+    }
+    write(gdir + "/oracle_draws.json", json{{"seed", "0x5eed"}, {"draws", draws}});
+    std::cerr << "oracle draws: " << draws.size() << "\n";
+  }
+
+  // ---- synthetic fits (test_model.cpp:24-120 patterns) --------------------
+  {
+    json fits = json::array();
+    auto run = [&](const std::string& name, unsigned long seed,
+                   const std::vector<std::pair<std::string, double>>& truth,
+                   int n_cases, long cmax, bool dup) {
+      std::mt19937_64 rng(seed);
+      std::vector<kc::FitCase> cs;
+      json rows = json::array(), times = json::array();
+      for (int i = 0; i < n_cases; ++i) {
+        kc::PropertyVector pv;
+        double t = 0;
+        json row = json::array();
+        long first = 0;
+        for (size_t j = 0; j < truth.size(); ++j) {
+          long c = static_cast<long>(1 + rng() % static_cast<unsigned long>(cmax));
+          if (dup && j == 1) c = first;
+          if (j == 0) first = c;
+          pv.at(truth[j].first) = kc::CountExpr::from_int(kc::Int(c));
+          t += truth[j].second * static_cast<double>(c);
+          row.push_back(c);
+        }
+        cs.push_back({pv, t});
+        rows.push_back(row);
+        times.push_back(hexd(t));
+      }
+      auto [w, rep] = kc::fit_weights(kc::build_design_matrix(cs), "synthetic");
+      json keys = json::array(), tr = json::array(), got = json::array();
+      for (const auto& [k, a] : truth) {
+        keys.push_back(k);
+        tr.push_back(hexd(a));
+        got.push_back(hexd(w.alpha[kc::schema_index(k)]));
+      }
+      fits.push_back({{"name", name}, {"keys", keys}, {"truth", tr},
+                      {"counts", rows}, {"times", times}, {"alpha", got},
+                      {"objective", dbl(rep.objective)}});
+    };
+    run("noiseless_4242", 4242,
+        {{"flop.f32.addsub", 6.81e-13}, {"mem.global.load.s32.1/1", 8.27e-12},
+         {"sync.barrier", 4.26e-11}, {"launch.const", 1.29e-04}},
+        40, 10000, false);
+    run("scaling_7", 7, {{"flop.f32.mul", 5.68e-13}, {"launch.groups", 3.75e-09}},
+        25, 10000, false);
+    run("duplicate_columns", 3,
+        {{"flop.f32.addsub", 1e-12}, {"flop.f32.mul", 1e-12}, {"sync.barrier", 4e-11}},
+        12, 1000, true);
+    // config-3 shape at oracle scale: 40 columns, Table 2 weights + 24
+    // log-uniform weights in [1e-13, 1e-9] on further schema keys
+    {
+      std::vector<std::pair<std::string, double>> truth;
+      const auto& keys = kc::schema_keys();
+      for (size_t i = 0; i < keys.size(); ++i)
+        if (ref.alpha[i] != 0.0) truth.push_back({keys[i], ref.alpha[i]});
+      std::mt19937_64 wr(4242);
+      std::uniform_real_distribution<double> lu(std::log(1e-13), std::log(1e-9));
+      for (size_t i = 0; i < keys.size() && truth.size() < 40; ++i)
+        if (ref.alpha[i] == 0.0) truth.push_back({keys[i], std::exp(lu(wr))});
+      run("config3_f40_n4000", 4242, truth, 4000, 10000, false);
+    }
+    write(gdir + "/fit_synthetic.json", json{{"fits", fits}});
+  }
+
+  // ---- grid samples: evaluate_properties + predict (config 2/4 shapes) ----
+  {
+    kc::ModelWeights w;
+    {
+      const kc::DesignMatrix d = kc::build_design_matrix(fit_cases);
+      w = kc::fit_weights(d, ref.name).first;
+    }
+    json samples = json::array();
+    std::mt19937_64 rng(1604);
+    auto add = [&](const std::string& id, const kc::Binding& b) {
+      const kc::KernelIR& k = irs.at(id);
+      json e;
+      e["kernel"] = id;
+      e["binding"] = binding_json(b);
+      try {
+        const kc::PropertyVector pv = kc::evaluate_properties(k, sym.at(id), b);
+        e["counts"] = pv_json(pv);
+        e["predicted_s"] = dbl(kc::predict(w, pv).seconds);
+        e["status"] = "ok";
+      } catch (const kc::Error& err) {
+        e["status"] = kc::errc_name(err.code());
+      }
+      samples.push_back(e);
+    };
+    auto draw_u = [&](long lo, long hi) {
+      return std::uniform_int_distribution<long>(lo, hi)(rng);
+    };
+    // config 2: skinny (16u, 128u, 16u) and conv n=16u, u in [1, 250000]
+    for (long u : {1L, 2L, 3L, 250000L}) {
+      add("matmul_skinny_g16x16", {{"n", 16 * u}, {"m", 128 * u}, {"l", 16 * u}});
+      add("conv_g16x16", {{"n", 16 * u}});
+    }
+    for (int i = 0; i < 200; ++i) {
+      const long u = draw_u(1, 250000);
+      add("matmul_skinny_g16x16", {{"n", 16 * u}, {"m", 128 * u}, {"l", 16 * u}});
+      add("conv_g16x16", {{"n", 16 * draw_u(1, 250000)}});
+    }
+    // config 4: the six matmul variants at (n,m,l) = 336 (u,v,w)
+    for (const char* id : {"matmul_tiled_g12x12", "matmul_tiled_g14x14",
+                           "matmul_tiled_g16x16", "matmul_naive_g16x12",
+                           "matmul_naive_g16x14", "matmul_naive_g16x16"}) {
+      add(id, {{"n", 336}, {"m", 336}, {"l", 336}});
+      add(id, {{"n", 336 * 551}, {"m", 336 * 551}, {"l", 336 * 551}});
+      for (int i = 0; i < 100; ++i)
+        add(id, {{"n", 336 * draw_u(1, 551)}, {"m", 336 * draw_u(1, 551)},
+                 {"l", 336 * draw_u(1, 551)}});
+    }
+    // every symbolic kernel at a few lattice points, plus inadmissible ones
+    for (const auto& sk : lib.kernels) {
+      if (!sym.count(sk.id)) continue;
+      for (const auto& b : sk.cases) add(sk.id, b);
+      kc::Binding bad = sk.cases.front();
+      bad.begin()->second += 1;
+      add(sk.id, bad);
+      kc::Binding neg = sk.cases.front();
+      neg.begin()->second = -neg.begin()->second;
+      add(sk.id, neg);
+    }
+    // huge magnitudes: counts beyond 2^64 (int128 path) and beyond 2^53
+    for (long long n : {1LL << 20, 1LL << 24, 3LL << 24, 1LL << 28, 1LL << 30}) {
+      add("matmul_skinny_g16x16", {{"n", n}, {"m", 8 * n}, {"l", n}});
+      add("matmul_tiled_g16x16", {{"n", n}, {"m", n}, {"l", n}});
+    }
+    write(gdir + "/grid_samples.json", json{{"samples", samples}});
+    std::cerr << "grid samples: " << samples.size() << "\n";
+
+    // ---- extra kernels whose symbolic PVs keep floordiv / min / max atoms
+    // and non-unit rational coefficients (test_counting.cpp:36-131 shapes)
+    const std::vector<std::pair<std::string, std::string>> extra = {
+        {"x_triangle",
+         "kernel x_triangle\nparam n\nassume n >= 1\n"
+         "array o : f32 [n] global row_major out\n"
+         "axis g0 = group(0) extent 1\naxis l0 = local(0) extent 1\n"
+         "loop i = 0 .. n\nloop j = 0 .. i + 1\n"
+         "o[i] = o[i] + 1.0\nend\nend\n"},
+        {"x_simplex",
+         "kernel x_simplex\nparam n\nassume n >= 3\n"
+         "array o : f32 [n] global row_major out\n"
+         "axis g0 = group(0) extent 1\naxis l0 = local(0) extent 1\n"
+         "loop i = 0 .. n\nloop j = 0 .. i\nloop p = 0 .. j\n"
+         "o[i] = o[i] * 2.0 + 1.0\nend\nend\nend\n"},
+        {"x_minmax",
+         "kernel x_minmax\nparam n, m\nassume n >= 1 and m >= 1\n"
+         "array o : f32 [n] global row_major out\n"
+         "axis g0 = group(0) extent 1\naxis l0 = local(0) extent 1\n"
+         "loop i = 0 .. n\nguard i < m\no[i] = 1.0\nend\nend\n"},
+        {"x_floordiv",
+         "kernel x_floordiv\nparam n, m\nassume n >= 1 and m >= 16\n"
+         "array o : f32 [n] global row_major out\n"
+         "axis g0 = group(0) extent n\naxis l0 = local(0) extent 1\n"
+         "loop kk = 0 .. m // 16\no[g0] = o[g0] + 1.0\nend\n"},
+        {"x_floordiv2",
+         "kernel x_floordiv2\nparam n, m\nassume n >= 7 and m >= 5\n"
+         "array o : f32 [n] global row_major out\n"
+         "axis g0 = group(0) extent n // 7\naxis l0 = local(0) extent 1\n"
+         "loop kk = 0 .. (m + n) // 5\no[g0] = o[g0] * 3.0\nend\n"},
+        {"x_guarded",
+         "kernel x_guarded\nparam n, m\nassume n >= 1 and m >= 1\n"
+         "array o : f32 [n] global row_major out\n"
+         "axis g0 = group(0) extent 1\naxis l0 = local(0) extent 1\n"
+         "loop i = 0 .. n\nloop j = 0 .. m\nguard j < i\n"
+         "o[i] = 2.0\nend\nend\nend\n"},
+    };
+    json xprogs = json::array();
+    json xsamples = json::array();
+    std::mt19937_64 xr(77);
+    for (const auto& [id, text] : extra) {
+      json pe{{"id", id}};
+      try {
+        const kc::KernelIR k = kc::parse_kernel(text);
+        const kc::PropertyVector pv = kc::extract_properties(k);
+        pe["program"] = kcref::program_text(k, pv);
+        for (int i = 0; i < 60; ++i) {
+          kc::Binding b;
+          const long span = i < 20 ? 12 : (i < 40 ? 5000 : 3000000000L);
+          for (const auto& p : k.params)
+            b[p.name] = kc::Int(std::uniform_int_distribution<long>(0, span)(xr));
+          json e{{"kernel", id}, {"binding", binding_json(b)}};
+          try {
+            const kc::PropertyVector bv = kc::evaluate_properties(k, pv, b);
+            e["counts"] = pv_json(bv);
+            e["predicted_s"] = dbl(kc::predict(w, bv).seconds);
+            e["status"] = "ok";
+          } catch (const kc::Error& err) {
+            e["status"] = kc::errc_name(err.code());
+          } catch (const std::logic_error& err) {
+            e["status"] = "NONINTEGRAL";
+          }
+          xsamples.push_back(e);
+        }
+      } catch (const std::exception& err) {
+        pe["error"] = err.what();
+      }
+      xprogs.push_back(pe);
+    }
+    write(gdir + "/extra_programs.json",
+          json{{"programs", xprogs}, {"samples", xsamples}});
+  }
+  return 0;
+}
