@@ -1,0 +1,212 @@
+/*
+ * kcg.h -- C ABI of the B200-native batched back end for kernelcost
+ * (reference: arXiv 1604.04997 artifact, /root/reference/proj).
+ *
+ * The reference has no plugin layer; its public C++ API is the boundary
+ * (SURVEY.md §8b). These entry points are what the reference's C++ calls
+ * (or a ctypes / cgo binding) use to implement *batched* overloads of:
+ *
+ *   evaluate_properties(k, pv, b)   proj/core/include/kernelcost/props.hpp:49-50
+ *                                   proj/core/src/props.cpp:259-271
+ *   CountExpr::evaluate(b)          proj/core/src/countexpr.cpp:340-383
+ *   AssumeCtx::admits(b)            proj/core/src/decide.cpp:153-170
+ *   predict(w, bound)               proj/core/include/kernelcost/model.hpp:61
+ *                                   proj/core/src/model.cpp:95-117
+ *   noiseless_time(dev, bound)      proj/core/src/simdevice.cpp:76-90
+ *   build_design_matrix(cases)      proj/core/src/model.cpp:11-35
+ *   fit_weights(d, device)          proj/core/src/model.cpp:37-93
+ *   read_weights_json / write_...   proj/core/src/jsonio.cpp:96-143
+ *
+ * Conventions
+ *   - Every function returns an int status: KCG_OK (0) or a KCG_E_* code.
+ *     No C++ exception crosses this boundary; kcg_last_error() returns the
+ *     message of the calling thread's last failure.
+ *   - Buffers are caller-owned. Unless stated otherwise, array arguments of
+ *     the launch functions are DEVICE pointers and `stream` is a cudaStream_t
+ *     (NULL = legacy default stream). Launch functions are asynchronous.
+ *   - Handles are thread-compatible (externally synchronised), not
+ *     thread-safe.
+ *   - There is no CPU fallback: launch functions return KCG_E_CUDA when no
+ *     CUDA device is usable.
+ */
+#ifndef KCG_H_
+#define KCG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes: 1..11 mirror kernelcost::Errc (error.hpp:10-22) ---- */
+enum kcg_status {
+  KCG_OK = 0,
+  KCG_E_PARSE = 1,               /* Errc::parse               E_PARSE */
+  KCG_E_NEEDS_BINDING = 2,       /* Errc::needs_binding       */
+  KCG_E_NEEDS_FALLBACK = 3,      /* Errc::needs_fallback      */
+  KCG_E_CAP_EXCEEDED = 4,        /* Errc::cap_exceeded        */
+  KCG_E_TYPE_CONFLICT = 5,       /* Errc::type_conflict       */
+  KCG_E_ASSUMPTION_VIOLATED = 6, /* Errc::assumption_violated */
+  KCG_E_SCHEMA_MISMATCH = 7,     /* Errc::schema_mismatch     */
+  KCG_E_NONPOSITIVE_TIME = 8,    /* Errc::nonpositive_time    */
+  KCG_E_EMPTY = 9,               /* Errc::empty_input         */
+  KCG_E_IO = 10,                 /* Errc::io                  */
+  KCG_E_INVALID_ARGUMENT = 11,   /* Errc::invalid_argument    */
+  KCG_E_CUDA = 100,              /* CUDA runtime failure / no device */
+  KCG_E_JIT = 101,               /* NVRTC specialisation failed */
+  KCG_E_UNSUPPORTED = 102,       /* program exceeds a static table limit */
+  KCG_E_INTERNAL = 103
+};
+
+/* ---- per-point status bytes written by the launch functions ----------- */
+enum kcg_point_status {
+  KCG_PT_OK = 0,
+  KCG_PT_ASSUMPTION_VIOLATED = 1, /* admits() false: E_ASSUMPTION_VIOLATED  */
+  KCG_PT_NONINTEGRAL = 2,         /* countexpr.cpp:380-381 logic_error       */
+  KCG_PT_OVERFLOW = 3,            /* |param| beyond the 128-bit safe bound:
+                                     the reference (bigint) would succeed;
+                                     never wrapped silently                 */
+  KCG_PT_COUNT_WIDE = 4           /* counts requested as int64 only but one
+                                     needs 128 bits; prediction is valid     */
+};
+
+enum kcg_engine {
+  KCG_ENGINE_JIT = 0,    /* NVRTC-specialised straight-line kernel (default) */
+  KCG_ENGINE_INTERP = 1  /* ahead-of-time compiled table interpreter */
+};
+
+typedef struct kcg_program kcg_program;
+
+/* ---- schema v1 (schema.cpp:16-38) --------------------------------------- */
+int kcg_schema_size(void);               /* 149 */
+const char* kcg_schema_key(int index);   /* NULL when out of range */
+int kcg_schema_index(const char* key);   /* -1 when unknown */
+const char* kcg_schema_version(void);    /* "v1" */
+
+/* ---- programs ----------------------------------------------------------
+ * `text` is the reference front end's output for one kernel, i.e.
+ *   kernelcost-program v1
+ *   kernel <name>
+ *   param <name>                       (KernelIR::params, in order)
+ *   assume <LinCmp::str()>             (KernelIR::assumptions)
+ *   prop <schema key> <CountExpr::str()>   (nonzero entries of the
+ *                                      symbolic PropertyVector)
+ *   end
+ * as printed by program_text(). Parsing and lowering to the
+ * integer program are host-only; no GPU is touched.                      */
+int kcg_program_create(const char* text, size_t len, kcg_program** out);
+void kcg_program_destroy(kcg_program* prog);
+int kcg_program_num_params(const kcg_program* prog);
+const char* kcg_program_param_name(const kcg_program* prog, int i);
+int kcg_program_num_props(const kcg_program* prog);     /* F_nz */
+int kcg_program_prop_schema_index(const kcg_program* prog, int j);
+const char* kcg_program_kernel_name(const kcg_program* prog);
+/* largest uniform parameter value for which every intermediate fits int64
+ * (fast path) and int128 (wide path); diagnostics for tests/DESIGN.md     */
+int kcg_program_safe_bounds(const kcg_program* prog, int64_t* b64, int64_t* b128);
+int kcg_program_set_engine(kcg_program* prog, int engine);
+/* CUDA source the JIT path compiles for this program (NUL-terminated,
+ * owned by the program) -- for inspection and tests                       */
+const char* kcg_program_jit_source(kcg_program* prog);
+
+/* ---- fused evaluate_properties + predict -------------------------------
+ * param_cols: host array of n_params DEVICE pointers, each n_points int64
+ *             (SoA bindings, column order = kcg_program_param_name order).
+ * alpha:      HOST pointer to 149 schema-indexed fp64 weights
+ *             (ModelWeights::alpha, model.hpp:29). May be NULL when
+ *             pred_out is NULL.
+ * pred_out:   nullable, n_points fp64: sum over nonzero counts in schema
+ *             order of alpha_j * double(count_j) (model.cpp:106-115), no
+ *             FMA; NaN where the point status is 1..3.
+ * status_out: nullable, n_points bytes (kcg_point_status).
+ * counts_lo:  nullable, F_nz x n_points int64, prop-major (column j of the
+ *             program at counts_lo + j*n_points): the exact counts.
+ * counts_hi:  nullable, same shape: high 64 bits (two's complement int128).
+ * simulate:   0 = predict order (skip zero counts, model.cpp:106-111);
+ *             1 = noiseless_time order (skip zero weights,
+ *                 simdevice.cpp:84-88).                                    */
+int kcg_eval_predict(const kcg_program* prog, const int64_t* const* param_cols,
+                     size_t n_points, const double* alpha, double* pred_out,
+                     uint8_t* status_out, int64_t* counts_lo,
+                     int64_t* counts_hi, int simulate, void* stream);
+
+/* ---- autotuning: evaluate + predict over variants, argmin --------------
+ * progs: n_variants programs with identical parameter-name sets; param_cols
+ * follow progs[0]'s parameter order. For each size i: best_idx[i] = lowest
+ * variant index with status OK and the smallest prediction (-1 if none),
+ * best_t[i] its prediction (+inf if none). preds_out (nullable) receives
+ * n_variants x n_sizes predictions, variant-major.                        */
+int kcg_argmin(const kcg_program* const* progs, int n_variants,
+               const int64_t* const* param_cols, size_t n_sizes,
+               const double* alpha, int32_t* best_idx, double* best_t,
+               double* preds_out, void* stream);
+
+/* ---- Gram reduction for the relative-error least squares --------------
+ * Materialised design X (n_rows x n_cols fp64, row stride ld >= n_cols):
+ * accumulates (+=) G = X^T X (full n_cols x n_cols, row-major), xt1 = X^T 1
+ * and colmax = max(colmax, |x|) per column. Accumulate into zeroed buffers;
+ * repeated calls over row blocks / ranks combine by sum (G, xt1) and max
+ * (colmax).                                                              */
+int kcg_gram_accumulate(const double* X, size_t n_rows, int n_cols, size_t ld,
+                        double* G, double* xt1, double* colmax, void* stream);
+
+/* Fused evaluate -> row -> Gram: row r is x_rj = double(count_rj) / T_r
+ * (build_design_matrix, model.cpp:29) over the program's F_nz props, never
+ * materialised in HBM. G is F_nz x F_nz. bad_rows (device int64, nullable)
+ * counts rows skipped because the point status was not OK or T <= 0.     */
+int kcg_gram_fused(const kcg_program* prog, const int64_t* const* param_cols,
+                   const double* T, size_t n_rows, double* G, double* xt1,
+                   double* colmax, unsigned long long* bad_rows, void* stream);
+
+/* Residual pass: obj += sum_r (1 - x_r . alpha)^2 over a materialised X
+ * (alpha: DEVICE pointer to n_cols fp64) ...                              */
+int kcg_residual_accumulate(const double* X, size_t n_rows, int n_cols,
+                            size_t ld, const double* alpha, double* obj,
+                            void* stream);
+/* ... or fused from bindings + T (alpha: HOST, 149 schema-indexed).       */
+int kcg_residual_fused(const kcg_program* prog,
+                       const int64_t* const* param_cols, const double* T,
+                       size_t n_rows, const double* alpha, double* obj,
+                       void* stream);
+
+/* ---- host-side solve (fit_weights, model.cpp:37-93) --------------------
+ * From the reduced Gram statistics of an n_cases-row design over F columns:
+ * columns with colmax == 0 are uncovered (weight pinned to 0); the rest are
+ * equilibrated by 1/colmax (model.cpp:71-76) and solved in the minimum-norm
+ * least-squares sense (COD semantics, model.cpp:79-80) via a symmetric
+ * eigendecomposition of the equilibrated Gram. alpha_out (host, F) gets
+ * x * scale (model.cpp:84-86); rank_out (nullable) the numerical rank.    */
+int kcg_solve_gram(int F, const double* G, const double* xt1,
+                   const double* colmax, double* alpha_out, int* rank_out);
+
+/* One step of iterative refinement for the semi-normal equations: given
+ * g = X^T (1 - X alpha) (from kcg_gram_residual_grad), update alpha.      */
+int kcg_refine_gram(int F, const double* G, const double* colmax,
+                    const double* g, double* alpha_inout);
+
+/* g += X^T (1 - X alpha) over a materialised X (alpha DEVICE, n_cols)    */
+int kcg_gram_residual_grad(const double* X, size_t n_rows, int n_cols,
+                           size_t ld, const double* alpha, double* g,
+                           void* stream);
+
+/* ---- weights file (jsonio.cpp:96-143) ---------------------------------- */
+int kcg_weights_read_json(const char* path, double* alpha149,
+                          uint8_t* covered149, double* objective,
+                          uint64_t* n_cases);
+int kcg_weights_write_json(const char* path, const char* device,
+                           const double* alpha149, const uint8_t* covered149,
+                           double objective, uint64_t n_cases);
+
+/* ---- diagnostics -------------------------------------------------------- */
+const char* kcg_status_str(int status);
+const char* kcg_point_status_str(int point_status);
+const char* kcg_last_error(void);
+/* number of kernels this library launched since load (all entry points)  */
+uint64_t kcg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KCG_H_ */

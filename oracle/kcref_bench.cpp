@@ -1,0 +1,120 @@
+// ORACLE TEST INFRASTRUCTURE -- CPU timing of the reference's own hot path.
+//
+// Runs the reference library (compiled in place from /root/reference against
+// oracle/shim: "reference code + shim bigint/COD") exactly as
+// proj/benchmarks/bench.cpp:47-56 does -- symbolic extract_properties once per
+// kernel, then per binding evaluate_properties + predict -- fanned out over
+// std::thread workers (safe after single-threaded extraction).
+//
+//   kcref_bench autotune <threads> <n_sizes> [offset]
+//       the 6 matmul variants at (n,m,l) = 336*(u,v,w), u,v,w in [1,551],
+//       sizes enumerated in the GPU bench's order from `offset`
+//   kcref_bench suite <threads> <n_points>
+//       config 2: skinny (16u,128u,16u) and conv n=16u, u = 1..n/2
+// Prints one JSON object: points, seconds, points_per_s, threads, checksum.
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "kernelcost/model.hpp"
+#include "kernelcost/parser.hpp"
+#include "kernelcost/props.hpp"
+#include "kernelcost/simdevice.hpp"
+#include "kernelcost/suite.hpp"
+
+namespace kc = kernelcost;
+
+namespace {
+
+struct Kern {
+  kc::KernelIR ir;
+  kc::PropertyVector sym;
+};
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 4) {
+    std::fprintf(stderr, "usage: kcref_bench autotune|suite <threads> <n> [offset]\n");
+    return 2;
+  }
+  const std::string mode = argv[1];
+  const int threads = std::max(1, std::atoi(argv[2]));
+  const long n = std::atol(argv[3]);
+  const long offset = argc > 4 ? std::atol(argv[4]) : 0;
+
+  const kc::SuiteLibrary lib = kc::build_suite();
+  const kc::SimDevice dev = kc::SimDevice::reference();
+  kc::ModelWeights w;
+  w.device = dev.name;
+  w.schema_version = kc::kSchemaVersion;
+  w.alpha = dev.alpha;
+  w.covered.assign(kc::schema_size(), true);
+
+  std::vector<std::string> ids;
+  if (mode == "autotune")
+    ids = {"matmul_tiled_g12x12", "matmul_tiled_g14x14", "matmul_tiled_g16x16",
+           "matmul_naive_g16x12", "matmul_naive_g16x14", "matmul_naive_g16x16"};
+  else
+    ids = {"matmul_skinny_g16x16", "conv_g16x16"};
+  std::vector<Kern> ks;
+  for (const auto& id : ids) {
+    kc::KernelIR k = kc::parse_kernel(lib.find(id)->text);
+    kc::PropertyVector pv = kc::extract_properties(k);
+    ks.push_back({std::move(k), std::move(pv)});
+  }
+
+  std::atomic<long> points{0};
+  std::vector<double> sums(threads, 0.0);
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> pool;
+  for (int t = 0; t < threads; ++t) {
+    pool.emplace_back([&, t] {
+      const long b = n * t / threads, e = n * (t + 1) / threads;
+      double acc = 0;
+      long local = 0;
+      for (long i = b; i < e; ++i) {
+        if (mode == "autotune") {
+          const long s = offset + i;
+          const long u = s / (551L * 551L) + 1, v = (s / 551L) % 551L + 1, x = s % 551L + 1;
+          const kc::Binding bind{{"n", kc::Int(336 * u)}, {"m", kc::Int(336 * v)},
+                                 {"l", kc::Int(336 * x)}};
+          double best = 1e300;
+          for (const auto& k : ks) {
+            const kc::PropertyVector bound = kc::evaluate_properties(k.ir, k.sym, bind);
+            const double sec = kc::predict(w, bound).seconds;
+            if (sec < best) best = sec;
+            ++local;
+          }
+          acc += best;
+        } else {
+          const long u = i / 2 + 1;
+          const Kern& k = ks[i % 2];
+          kc::Binding bind;
+          if (i % 2 == 0)
+            bind = {{"n", kc::Int(16 * u)}, {"m", kc::Int(128 * u)}, {"l", kc::Int(16 * u)}};
+          else
+            bind = {{"n", kc::Int(16 * u)}};
+          const kc::PropertyVector bound = kc::evaluate_properties(k.ir, k.sym, bind);
+          acc += kc::predict(w, bound).seconds;
+          ++local;
+        }
+      }
+      sums[t] = acc;
+      points += local;
+    });
+  }
+  for (auto& th : pool) th.join();
+  const double sec =
+      std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  double checksum = 0;
+  for (double s : sums) checksum += s;
+  std::printf("{\"points\": %ld, \"seconds\": %.6f, \"points_per_s\": %.6g, \"threads\": %d, "
+              "\"checksum\": %.17g}\n",
+              points.load(), sec, points.load() / sec, threads, checksum);
+  return 0;
+}

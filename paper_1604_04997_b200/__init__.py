@@ -1,0 +1,31 @@
+"""B200-native batched back end for kernelcost (arXiv 1604.04997).
+
+The package is the hot path only: exact evaluation of a kernel's symbolic
+operation counts over grids of parameter bindings, fused with the linear
+run-time prediction, the argmin over kernel variants and the Gram reduction
+of the least-squares fit. See DESIGN.md; the C ABI is include/kcg.h.
+"""
+from .api import (  # noqa: F401
+    BoundBatch,
+    FitResult,
+    GramStats,
+    ModelWeights,
+    Program,
+    argmin,
+    evaluate_properties,
+    fit_weights,
+    gram_accumulate,
+    gram_fused,
+    launch_count,
+    load_program,
+    noiseless_time,
+    predict,
+    read_weights_json,
+    schema_index,
+    schema_keys,
+    schema_size,
+    solve_gram,
+    suite_index,
+    write_weights_json,
+)
+from ._capi import KcgError  # noqa: F401

@@ -1,0 +1,365 @@
+"""Python host mirror of the reference API for the batched hot path.
+
+Names and meaning follow kernelcost's C++ API (proj/core/include/kernelcost):
+``evaluate_properties`` (props.hpp:49-50), ``predict`` (model.hpp:61),
+``noiseless_time`` (simdevice.hpp:33), ``build_design_matrix`` /
+``fit_weights`` (model.hpp:43-49), ``read_weights_json`` /
+``write_weights_json`` (jsonio.hpp:27-29) -- batched over SoA bindings that
+live in HBM. Every call goes through the C ABI of libkcg.so (include/kcg.h);
+PyTorch only provides device memory and the current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Mapping, Sequence
+
+from . import _capi
+from ._capi import check, lib
+
+PROGRAM_DIR = Path(__file__).resolve().parent / "programs"
+
+
+# ---------------------------------------------------------------------------
+# schema v1 (schema.cpp:16-38)
+
+def schema_keys() -> list[str]:
+    L = lib()
+    return [L.kcg_schema_key(i).decode() for i in range(L.kcg_schema_size())]
+
+
+def schema_size() -> int:
+    return lib().kcg_schema_size()
+
+
+def schema_index(key: str) -> int:
+    i = lib().kcg_schema_index(key.encode())
+    if i < 0:
+        raise _capi.KcgError(_capi.E_SCHEMA_MISMATCH, f"unknown property key '{key}'")
+    return i
+
+
+# ---------------------------------------------------------------------------
+# programs
+
+class Program:
+    """A kernel's symbolic PropertyVector + assumptions, lowered for the GPU.
+
+    ``text`` is the front end's program text (kernelcost-program v1), i.e.
+    what ``program_text(k, extract_properties(k))`` prints on the reference
+    side.
+    """
+
+    def __init__(self, text: str):
+        self.text = text
+        h = _capi.P()
+        raw = text.encode()
+        check(lib().kcg_program_create(raw, len(raw), ctypes.byref(h)))
+        self._h = h
+        L = lib()
+        self.name = L.kcg_program_kernel_name(h).decode()
+        self.params = [L.kcg_program_param_name(h, i).decode()
+                       for i in range(L.kcg_program_num_params(h))]
+        self.props = [L.kcg_program_prop_schema_index(h, j)
+                      for j in range(L.kcg_program_num_props(h))]
+        keys = schema_keys()
+        self.keys = [keys[i] for i in self.props]
+
+    @classmethod
+    def from_file(cls, path) -> "Program":
+        return cls(Path(path).read_text())
+
+    @property
+    def handle(self):
+        return self._h
+
+    def safe_bounds(self) -> tuple[int, int]:
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        check(lib().kcg_program_safe_bounds(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def set_engine(self, engine: str) -> None:
+        code = {"jit": _capi.ENGINE_JIT, "interp": _capi.ENGINE_INTERP}[engine]
+        check(lib().kcg_program_set_engine(self._h, code))
+
+    def jit_source(self) -> str:
+        return lib().kcg_program_jit_source(self._h).decode()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _capi._lib is not None:
+            _capi._lib.kcg_program_destroy(h)
+            self._h = None
+
+    def __repr__(self):
+        return f"Program({self.name!r}, params={self.params}, props={len(self.props)})"
+
+
+def suite_index() -> list[dict]:
+    import json
+    return json.loads((PROGRAM_DIR / "index.json").read_text())["kernels"]
+
+
+def load_program(kernel_id: str) -> Program:
+    """Front-end output for one bundled suite kernel (programs/<id>.kcp)."""
+    path = PROGRAM_DIR / f"{kernel_id}.kcp"
+    if not path.exists():
+        raise FileNotFoundError(f"no symbolic program for '{kernel_id}' (extraction needs a binding)")
+    return Program.from_file(path)
+
+
+# ---------------------------------------------------------------------------
+# weights (jsonio.cpp:96-143)
+
+@dataclass
+class ModelWeights:
+    device: str = ""
+    schema_version: str = "v1"
+    alpha: list = field(default_factory=lambda: [0.0] * 149)
+    covered: list = field(default_factory=lambda: [False] * 149)
+    objective: float = 0.0
+    n_cases: int = 0
+
+    def alpha_array(self):
+        n = schema_size()
+        if self.schema_version != "v1" or len(self.alpha) != n:
+            raise _capi.KcgError(_capi.E_SCHEMA_MISMATCH,
+                                 f"model weights use schema '{self.schema_version}', expected 'v1'")
+        return (ctypes.c_double * n)(*self.alpha)
+
+
+def read_weights_json(path) -> ModelWeights:
+    n = schema_size()
+    a = (ctypes.c_double * n)()
+    c = (ctypes.c_uint8 * n)()
+    obj = ctypes.c_double()
+    nc = ctypes.c_uint64()
+    check(lib().kcg_weights_read_json(str(path).encode(), a, c, ctypes.byref(obj), ctypes.byref(nc)))
+    import json
+    dev = json.loads(Path(path).read_text()).get("device", "")
+    return ModelWeights(dev, "v1", list(a), [bool(x) for x in c], obj.value, nc.value)
+
+
+def write_weights_json(path, w: ModelWeights) -> None:
+    n = schema_size()
+    a = w.alpha_array()
+    c = (ctypes.c_uint8 * n)(*[1 if x else 0 for x in w.covered])
+    check(lib().kcg_weights_write_json(str(path).encode(), w.device.encode(), a, c,
+                                        float(w.objective), int(w.n_cases)))
+
+
+# ---------------------------------------------------------------------------
+# launches
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream(stream=None) -> int:
+    torch = _torch()
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _columns(prog: Program, bindings):
+    """SoA int64 device columns in ``prog.params`` order."""
+    torch = _torch()
+    if isinstance(bindings, Mapping):
+        cols = [bindings[p] for p in prog.params]
+    elif isinstance(bindings, torch.Tensor) and bindings.dim() == 2:
+        cols = [bindings[j] for j in range(bindings.shape[0])]
+    else:
+        cols = list(bindings)
+    if len(cols) != len(prog.params):
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT,
+                             f"binding has {len(cols)} columns, kernel has params {prog.params}")
+    n = None
+    out = []
+    for c in cols:
+        if not (c.is_cuda and c.dtype == torch.int64 and c.is_contiguous()):
+            raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "binding columns must be contiguous int64 CUDA tensors")
+        if n is None:
+            n = c.numel()
+        elif c.numel() != n:
+            raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "ragged binding columns")
+        out.append(c)
+    arr = (ctypes.c_void_p * max(1, len(out)))(*[c.data_ptr() for c in out])
+    return arr, (n or 0), out
+
+
+@dataclass
+class BoundBatch:
+    """Batched evaluate_properties result: exact counts + per-point status."""
+    program: Program
+    counts_lo: object          # [F_nz, N] int64
+    counts_hi: object | None   # [F_nz, N] int64 (high words) or None
+    status: object             # [N] uint8
+
+    def counts_int(self, j: int, i: int) -> int:
+        lo = int(self.counts_lo[j, i]) & ((1 << 64) - 1)
+        hi = int(self.counts_hi[j, i]) if self.counts_hi is not None else (-1 if lo >> 63 else 0)
+        return (hi << 64) | lo
+
+
+def evaluate_properties(prog: Program, bindings, wide: bool = True, stream=None) -> BoundBatch:
+    """Batched ``evaluate_properties`` (props.cpp:259-271): exact counts of
+    the program's nonzero keys at every binding, plus a status per point
+    (E_ASSUMPTION_VIOLATED etc. instead of an exception)."""
+    torch = _torch()
+    arr, n, cols = _columns(prog, bindings)
+    dev = cols[0].device if cols else torch.device("cuda")
+    F = len(prog.props)
+    lo = torch.empty((max(F, 1), n), dtype=torch.int64, device=dev)
+    hi = torch.empty((max(F, 1), n), dtype=torch.int64, device=dev) if wide else None
+    st = torch.empty(n, dtype=torch.uint8, device=dev)
+    check(lib().kcg_eval_predict(prog.handle, arr, n, None, None, st.data_ptr(), lo.data_ptr(),
+                                 _ptr(hi), 0, _stream(stream)))
+    return BoundBatch(prog, lo[:F], hi[:F] if hi is not None else None, st)
+
+
+def predict(w: ModelWeights, prog: Program, bindings, with_status: bool = False, stream=None):
+    """Batched ``predict`` (model.cpp:95-117) fused with the evaluation:
+    seconds per binding; NaN where the binding is not admissible."""
+    torch = _torch()
+    arr, n, cols = _columns(prog, bindings)
+    dev = cols[0].device if cols else torch.device("cuda")
+    pred = torch.empty(n, dtype=torch.float64, device=dev)
+    st = torch.empty(n, dtype=torch.uint8, device=dev) if with_status else None
+    check(lib().kcg_eval_predict(prog.handle, arr, n, w.alpha_array(), pred.data_ptr(), _ptr(st),
+                                 None, None, 0, _stream(stream)))
+    return (pred, st) if with_status else pred
+
+
+def noiseless_time(alpha149: Sequence[float], prog: Program, bindings, stream=None):
+    """Batched ``noiseless_time`` (simdevice.cpp:76-90): the stored-timing
+    inner product, summed in schema order skipping zero weights."""
+    torch = _torch()
+    arr, n, cols = _columns(prog, bindings)
+    pred = torch.empty(n, dtype=torch.float64, device=cols[0].device)
+    a = (ctypes.c_double * len(alpha149))(*alpha149)
+    check(lib().kcg_eval_predict(prog.handle, arr, n, a, pred.data_ptr(), None, None, None, 1,
+                                 _stream(stream)))
+    return pred
+
+
+def argmin(progs: Sequence[Program], w: ModelWeights, bindings, return_preds: bool = False, stream=None):
+    """Autotuning sweep: fused evaluate + predict over kernel variants with
+    an argmin per problem size (lowest variant index wins ties)."""
+    torch = _torch()
+    arr, n, cols = _columns(progs[0], bindings)
+    dev = cols[0].device
+    best = torch.empty(n, dtype=torch.int32, device=dev)
+    best_t = torch.empty(n, dtype=torch.float64, device=dev)
+    preds = torch.empty((len(progs), n), dtype=torch.float64, device=dev) if return_preds else None
+    handles = (ctypes.c_void_p * len(progs))(*[p.handle.value for p in progs])
+    check(lib().kcg_argmin(handles, len(progs), arr, n, w.alpha_array(), best.data_ptr(),
+                           best_t.data_ptr(), _ptr(preds), _stream(stream)))
+    return (best, best_t, preds) if return_preds else (best, best_t)
+
+
+# ---------------------------------------------------------------------------
+# fit (model.cpp:11-93) via Gram statistics
+
+@dataclass
+class GramStats:
+    G: object       # [F, F] fp64
+    xt1: object     # [F]
+    colmax: object  # [F]
+    n_rows: int = 0
+    bad_rows: int = 0
+
+    @classmethod
+    def zeros(cls, F: int, device="cuda"):
+        torch = _torch()
+        z = lambda *s: torch.zeros(*s, dtype=torch.float64, device=device)
+        return cls(z(F, F), z(F), z(F))
+
+
+def gram_accumulate(X, stats: GramStats | None = None, stream=None) -> GramStats:
+    """G += XᵀX, Xᵀ1, colmax over a materialised design X [N, F] fp64."""
+    N, F = X.shape
+    stats = stats or GramStats.zeros(F, X.device)
+    check(lib().kcg_gram_accumulate(X.data_ptr(), N, F, X.stride(0), stats.G.data_ptr(),
+                                    stats.xt1.data_ptr(), stats.colmax.data_ptr(), _stream(stream)))
+    stats.n_rows += N
+    return stats
+
+
+def gram_fused(prog: Program, bindings, T, stats: GramStats | None = None, stream=None) -> GramStats:
+    """Fused evaluate -> design row (count/T, model.cpp:29) -> Gram."""
+    torch = _torch()
+    arr, n, cols = _columns(prog, bindings)
+    F = len(prog.props)
+    stats = stats or GramStats.zeros(F, cols[0].device)
+    bad = torch.zeros(1, dtype=torch.int64, device=cols[0].device)
+    check(lib().kcg_gram_fused(prog.handle, arr, T.data_ptr(), n, stats.G.data_ptr(),
+                               stats.xt1.data_ptr(), stats.colmax.data_ptr(), bad.data_ptr(),
+                               _stream(stream)))
+    stats.n_rows += n
+    stats.bad_rows += int(bad.item())
+    return stats
+
+
+def solve_gram(stats: GramStats) -> tuple[list[float], int]:
+    """Host minimum-norm solve of the equilibrated normal equations."""
+    G = stats.G.double().cpu().contiguous()
+    F = G.shape[0]
+    dp = lambda t: ctypes.cast(t.data_ptr(), _capi.DP)
+    xt1 = stats.xt1.double().cpu().contiguous()
+    cm = stats.colmax.double().cpu().contiguous()
+    out = (ctypes.c_double * F)()
+    rank = ctypes.c_int()
+    check(lib().kcg_solve_gram(F, dp(G), dp(xt1), dp(cm), out, ctypes.byref(rank)))
+    return list(out), rank.value
+
+
+@dataclass
+class FitResult:
+    alpha: list
+    covered: list
+    objective: float
+    rank: int
+    n_cases: int
+
+
+def fit_weights(X, refine: int = 1, stream=None) -> FitResult:
+    """``fit_weights`` (model.cpp:37-93) over a materialised design X whose
+    rows are p/T (``build_design_matrix``): Gram reduction on the GPU, host
+    min-norm solve, `refine` semi-normal refinement passes, objective from a
+    residual pass (never from the Gram identity)."""
+    torch = _torch()
+    N, F = X.shape
+    if N == 0:
+        raise _capi.KcgError(_capi.E_EMPTY, "empty design matrix")
+    st = gram_accumulate(X, stream=stream)
+    alpha, rank = solve_gram(st)
+    G = st.G.cpu().contiguous()
+    cm = st.colmax.cpu().contiguous()
+    dp = lambda t: ctypes.cast(t.data_ptr(), _capi.DP)
+    for _ in range(refine):
+        a_dev = torch.tensor(alpha, dtype=torch.float64, device=X.device)
+        g = torch.zeros(F, dtype=torch.float64, device=X.device)
+        check(lib().kcg_gram_residual_grad(X.data_ptr(), N, F, X.stride(0), a_dev.data_ptr(),
+                                           g.data_ptr(), _stream(stream)))
+        gh = g.cpu().contiguous()
+        arr = (ctypes.c_double * F)(*alpha)
+        check(lib().kcg_refine_gram(F, dp(G), dp(cm), dp(gh), arr))
+        alpha = list(arr)
+    a_dev = torch.tensor(alpha, dtype=torch.float64, device=X.device)
+    obj = torch.zeros(1, dtype=torch.float64, device=X.device)
+    check(lib().kcg_residual_accumulate(X.data_ptr(), N, F, X.stride(0), a_dev.data_ptr(),
+                                        obj.data_ptr(), _stream(stream)))
+    covered = [bool(c > 0) for c in cm.tolist()]
+    return FitResult(alpha, covered, float(obj.item()), rank, N)
+
+
+def launch_count() -> int:
+    return int(lib().kcg_launch_count())

@@ -1,0 +1,665 @@
+// extern "C" boundary (include/kcg.h): program handles, launch dispatch,
+// host-side solve and weights I/O. No exception crosses this file's
+// functions; failures become KCG_E_* codes plus kcg_last_error().
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/kcg.h"
+#include "json.hpp"
+#include "kcg_codegen.hpp"
+#include "kcg_host.hpp"
+#include "kcg_kernels.hpp"
+
+using kcg::i128;
+using kcg::KcgError;
+
+struct kcg_program {
+  kcg::Symbolic sym;
+  kcg::Lowered low;
+  std::vector<std::string> param_names;
+  int engine = KCG_ENGINE_JIT;
+  KcgDevProg* dprog = nullptr;  // device image (interpreter), lazily uploaded
+  bool dprog_ok = true;         // fits the interpreter's static tables
+  std::string jit_src;
+  void* jit_eval = nullptr;
+  void* jit_gram = nullptr;
+  void* jit_resid = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const KcgError& e) {
+    return fail(e.code, e.what());
+  } catch (const std::invalid_argument& e) {
+    return fail(KCG_E_INVALID_ARGUMENT, e.what());
+  } catch (const std::exception& e) {
+    return fail(KCG_E_CUDA, e.what());
+  }
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw KcgError(KCG_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0)
+    throw KcgError(KCG_E_CUDA, "no CUDA device available (the kcg back end has no CPU fallback)");
+}
+
+// byte-exact image of the generated `struct KcgArgs` (natural C alignment)
+struct ArgBuf {
+  std::vector<unsigned char> b;
+  template <class T>
+  void push(const T& v) {
+    const size_t al = alignof(T);
+    while (b.size() % al) b.push_back(0);
+    const auto* p = reinterpret_cast<const unsigned char*>(&v);
+    b.insert(b.end(), p, p + sizeof(T));
+  }
+  void finish() {
+    while (b.size() % 8) b.push_back(0);
+  }
+};
+
+unsigned grid_for(size_t n, int threads = 256, int per_sm = 8) {
+  const size_t need = (n + threads - 1) / threads;
+  const size_t cap = static_cast<size_t>(kcg::num_sms()) * per_sm;
+  return static_cast<unsigned>(std::max<size_t>(1, std::min(need, cap)));
+}
+
+KcgWide wide(i128 v) { return {static_cast<int64_t>(v), static_cast<int64_t>(v >> 64)}; }
+
+bool build_devprog(const kcg::Lowered& L, KcgDevProg& d) {
+  std::memset(&d, 0, sizeof d);
+  if (L.n_params > KCG_MAX_PARAMS || static_cast<int>(L.ops.size()) > KCG_MAX_OPS ||
+      L.n_atoms > KCG_MAX_ATOMS || L.n_monos > KCG_MAX_MONOS ||
+      static_cast<int>(L.factors.size()) > KCG_MAX_FACTORS ||
+      static_cast<int>(L.terms.size()) > KCG_MAX_TERMS || L.n_exprs > KCG_MAX_EXPRS ||
+      static_cast<int>(L.args.size()) > KCG_MAX_ARGS ||
+      static_cast<int>(L.floordiv_den.size()) > KCG_MAX_FD ||
+      static_cast<int>(L.cons.size()) > KCG_MAX_CONS ||
+      static_cast<int>(L.keys.size()) > KCG_MAX_KEYS)
+    return false;
+  d.n_params = L.n_params;
+  d.n_atoms = L.n_atoms;
+  d.n_monos = L.n_monos;
+  d.n_exprs = L.n_exprs;
+  d.n_ops = static_cast<int32_t>(L.ops.size());
+  d.n_cons = static_cast<int32_t>(L.cons.size());
+  d.n_keys = static_cast<int32_t>(L.keys.size());
+  d.b64 = L.b64;
+  d.b128 = L.b128;
+  for (size_t i = 0; i < L.ops.size(); ++i)
+    d.ops[i] = {L.ops[i].code, L.ops[i].dst, L.ops[i].a, L.ops[i].b, L.ops[i].c};
+  for (size_t i = 0; i < L.factors.size(); ++i) {
+    d.fac_atom[i] = L.factors[i].first;
+    d.fac_exp[i] = L.factors[i].second;
+  }
+  for (size_t i = 0; i < L.terms.size(); ++i) {
+    d.term_coef[i] = wide(L.terms[i].coef);
+    d.term_mono[i] = L.terms[i].mono;
+  }
+  for (size_t i = 0; i < L.exprs.size(); ++i) d.expr_den[i] = wide(L.exprs[i].D);
+  for (size_t i = 0; i < L.args.size(); ++i) {
+    d.arg_expr[i] = L.args[i].expr;
+    d.arg_scale[i] = wide(L.args[i].scale);
+  }
+  for (size_t i = 0; i < L.floordiv_den.size(); ++i) d.fd_den[i] = wide(L.floordiv_den[i]);
+  for (size_t i = 0; i < L.cons.size(); ++i) {
+    d.cons_div[i] = L.cons[i].divisibility;
+    d.cons_op[i] = L.cons[i].op;
+    d.cons_expr[i] = L.cons[i].expr;
+    d.cons_mod[i] = wide(L.cons[i].mod);
+    d.cons_rem[i] = wide(L.cons[i].rem);
+  }
+  for (size_t i = 0; i < L.keys.size(); ++i) {
+    d.key_schema[i] = L.keys[i].schema;
+    d.key_expr[i] = L.keys[i].expr;
+  }
+  return true;
+}
+
+std::vector<int> identity(int n) {
+  std::vector<int> v(n);
+  for (int i = 0; i < n; ++i) v[i] = i;
+  return v;
+}
+
+std::string kname(const char* base, const kcg_program* p) {
+  std::string s = base;
+  for (char c : p->sym.kernel) s.push_back(std::isalnum(static_cast<unsigned char>(c)) ? c : '_');
+  return s;
+}
+
+void compact_alpha(const kcg_program* p, const double* alpha149, double* out) {
+  for (size_t j = 0; j < p->low.keys.size(); ++j)
+    out[j] = alpha149 ? alpha149[p->low.keys[j].schema] : 0.0;
+}
+
+// symmetric eigen-decomposition (cyclic Jacobi), A row-major n x n
+void jacobi_eigen(int n, std::vector<double>& A, std::vector<double>& V, std::vector<double>& w) {
+  V.assign(static_cast<size_t>(n) * n, 0.0);
+  for (int i = 0; i < n; ++i) V[i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0, diag = 0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) (i == j ? diag : off) += A[i * n + j] * A[i * n + j];
+    if (off <= 1e-34 * diag || off == 0) break;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = A[p * n + q];
+        if (apq == 0) continue;
+        const double app = A[p * n + p], aqq = A[q * n + q];
+        const double theta = (aqq - app) / (2 * apq);
+        const double t = (theta >= 0 ? 1 : -1) / (std::fabs(theta) + std::sqrt(theta * theta + 1));
+        const double c = 1 / std::sqrt(t * t + 1), s = t * c;
+        for (int k = 0; k < n; ++k) {
+          const double akp = A[k * n + p], akq = A[k * n + q];
+          A[k * n + p] = c * akp - s * akq;
+          A[k * n + q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double apk = A[p * n + k], aqk = A[q * n + k];
+          A[p * n + k] = c * apk - s * aqk;
+          A[q * n + k] = s * apk + c * aqk;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double vkp = V[k * n + p], vkq = V[k * n + q];
+          V[k * n + p] = c * vkp - s * vkq;
+          V[k * n + q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  w.resize(n);
+  for (int i = 0; i < n; ++i) w[i] = A[i * n + i];
+}
+
+// minimum-norm solution of (D G D) y = D b over covered columns; returns
+// x = D y (unscaled coordinates) and the numerical rank
+int solve_equilibrated(int F, const double* G, const double* colmax, const double* b,
+                       std::vector<double>& x) {
+  std::vector<int> cols;
+  for (int j = 0; j < F; ++j)
+    if (colmax[j] > 0.0) cols.push_back(j);
+  x.assign(F, 0.0);
+  const int n = static_cast<int>(cols.size());
+  if (n == 0) return 0;
+  std::vector<double> s(n), A(static_cast<size_t>(n) * n), rhs(n);
+  for (int i = 0; i < n; ++i) s[i] = 1.0 / colmax[cols[i]];  // model.cpp:71-76
+  for (int i = 0; i < n; ++i) {
+    rhs[i] = b[cols[i]] * s[i];
+    for (int j = 0; j < n; ++j) A[i * n + j] = G[cols[i] * F + cols[j]] * s[i] * s[j];
+  }
+  std::vector<double> V, w;
+  jacobi_eigen(n, A, V, w);
+  double wmax = 0;
+  for (double v : w) wmax = std::max(wmax, std::fabs(v));
+  const double tol = wmax * n * std::numeric_limits<double>::epsilon() * 64;
+  int rank = 0;
+  std::vector<double> y(n, 0.0);
+  for (int k = 0; k < n; ++k) {
+    if (w[k] <= tol) continue;
+    ++rank;
+    double proj = 0;
+    for (int i = 0; i < n; ++i) proj += V[i * n + k] * rhs[i];
+    proj /= w[k];
+    for (int i = 0; i < n; ++i) y[i] += V[i * n + k] * proj;
+  }
+  for (int i = 0; i < n; ++i) x[cols[i]] = y[i] * s[i];  // alpha = x * scale
+  return rank;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kcg_schema_size(void) { return static_cast<int>(kcg::schema_keys().size()); }
+
+const char* kcg_schema_key(int index) {
+  const auto& k = kcg::schema_keys();
+  return index >= 0 && index < static_cast<int>(k.size()) ? k[index].c_str() : nullptr;
+}
+
+int kcg_schema_index(const char* key) { return key ? kcg::schema_index(key) : -1; }
+
+const char* kcg_schema_version(void) { return "v1"; }
+
+int kcg_program_create(const char* text, size_t len, kcg_program** out) {
+  if (!text || !out) return fail(KCG_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    auto p = std::make_unique<kcg_program>();
+    p->sym = kcg::parse_program_text(std::string(text, len));
+    p->low = kcg::lower(p->sym);
+    if (p->low.n_params > KCG_MAX_PARAMS)
+      throw KcgError(KCG_E_UNSUPPORTED, "more than 8 parameters");
+    p->param_names = p->sym.params;
+    if (const char* e = std::getenv("KCG_ENGINE"); e && std::string(e) == "interp")
+      p->engine = KCG_ENGINE_INTERP;
+    *out = p.release();
+    return KCG_OK;
+  });
+}
+
+void kcg_program_destroy(kcg_program* prog) {
+  if (!prog) return;
+  if (prog->dprog) cudaFree(prog->dprog);
+  delete prog;
+}
+
+int kcg_program_num_params(const kcg_program* p) { return p ? p->low.n_params : -1; }
+
+const char* kcg_program_param_name(const kcg_program* p, int i) {
+  return p && i >= 0 && i < p->low.n_params ? p->param_names[i].c_str() : nullptr;
+}
+
+int kcg_program_num_props(const kcg_program* p) {
+  return p ? static_cast<int>(p->low.keys.size()) : -1;
+}
+
+int kcg_program_prop_schema_index(const kcg_program* p, int j) {
+  return p && j >= 0 && j < static_cast<int>(p->low.keys.size()) ? p->low.keys[j].schema : -1;
+}
+
+const char* kcg_program_kernel_name(const kcg_program* p) { return p ? p->sym.kernel.c_str() : nullptr; }
+
+int kcg_program_safe_bounds(const kcg_program* p, int64_t* b64, int64_t* b128) {
+  if (!p) return fail(KCG_E_INVALID_ARGUMENT, "null program");
+  if (b64) *b64 = p->low.b64;
+  if (b128) *b128 = p->low.b128;
+  return KCG_OK;
+}
+
+int kcg_program_set_engine(kcg_program* p, int engine) {
+  if (!p || (engine != KCG_ENGINE_JIT && engine != KCG_ENGINE_INTERP))
+    return fail(KCG_E_INVALID_ARGUMENT, "bad engine");
+  p->engine = engine;
+  return KCG_OK;
+}
+
+const char* kcg_program_jit_source(kcg_program* p) {
+  if (!p) return nullptr;
+  if (p->jit_src.empty())
+    p->jit_src = kcg::codegen({&p->low}, {identity(p->low.n_params)}, p->low.n_params,
+                              kcg::JitKind::eval, kname("kcg_eval_", p));
+  return p->jit_src.c_str();
+}
+
+int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, size_t n,
+                     const double* alpha, double* pred_out, uint8_t* status_out,
+                     int64_t* counts_lo, int64_t* counts_hi, int simulate, void* stream) {
+  kcg_program* p = const_cast<kcg_program*>(cp);
+  if (!p) return fail(KCG_E_INVALID_ARGUMENT, "null program");
+  if (pred_out && !alpha) return fail(KCG_E_INVALID_ARGUMENT, "alpha required for predictions");
+  if (p->low.n_params > 0 && !param_cols) return fail(KCG_E_INVALID_ARGUMENT, "null param_cols");
+  return guarded([&] {
+    require_device();
+    if (n == 0) return KCG_OK;
+    const int np = p->low.n_params;
+    const int F = static_cast<int>(p->low.keys.size());
+    if (p->engine == KCG_ENGINE_INTERP) {
+      if (!p->dprog && p->dprog_ok) {
+        auto img = std::make_unique<KcgDevProg>();
+        p->dprog_ok = build_devprog(p->low, *img);
+        if (p->dprog_ok) {
+          cuda_check(cudaMalloc(&p->dprog, sizeof(KcgDevProg)), "cudaMalloc");
+          cuda_check(cudaMemcpy(p->dprog, img.get(), sizeof(KcgDevProg), cudaMemcpyHostToDevice),
+                     "cudaMemcpy");
+        }
+      }
+      if (!p->dprog_ok)
+        throw KcgError(KCG_E_UNSUPPORTED, "program exceeds the interpreter's static tables");
+      kcg::InterpEvalArgs a{};
+      for (int j = 0; j < np; ++j) a.p[j] = param_cols[j];
+      a.pred = pred_out;
+      a.status = status_out;
+      a.clo = counts_lo;
+      a.chi = counts_hi;
+      a.n = static_cast<int64_t>(n);
+      a.simulate = simulate;
+      compact_alpha(p, alpha, a.alpha);
+      kcg::launch_interp_eval(p->dprog, a, stream);
+      ++g_launches;
+      return KCG_OK;
+    }
+    if (!p->jit_eval) p->jit_eval = kcg::jit_kernel(kcg_program_jit_source(p), kname("kcg_eval_", p));
+    ArgBuf ab;
+    for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
+    ab.push<void*>(pred_out);
+    ab.push<void*>(status_out);
+    ab.push<void*>(counts_lo);
+    ab.push<void*>(counts_hi);
+    ab.push<int64_t>(static_cast<int64_t>(n));
+    ab.push<int32_t>(simulate);
+    std::vector<double> al(std::max(F, 1), 0.0);
+    compact_alpha(p, alpha, al.data());
+    for (double v : al) ab.push<double>(v);
+    ab.finish();
+    kcg::launch_jit(p->jit_eval, ab.b.data(), ab.b.size(), grid_for(n), 256, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_argmin(const kcg_program* const* progs, int V, const int64_t* const* param_cols,
+               size_t n, const double* alpha, int32_t* best_idx, double* best_t,
+               double* preds_out, void* stream) {
+  if (!progs || V < 1 || !alpha || !best_idx || !best_t)
+    return fail(KCG_E_INVALID_ARGUMENT, "bad argmin arguments");
+  return guarded([&] {
+    require_device();
+    if (n == 0) return KCG_OK;
+    const kcg_program* p0 = progs[0];
+    const int np = p0->low.n_params;
+    std::vector<const kcg::Lowered*> lows;
+    std::vector<std::vector<int>> pmaps;
+    std::string name = "kcg_argmin";
+    for (int v = 0; v < V; ++v) {
+      const kcg_program* p = progs[v];
+      if (!p || p->low.n_params != np)
+        throw KcgError(KCG_E_INVALID_ARGUMENT, "argmin variants must share the parameter set");
+      std::vector<int> map(np);
+      for (int j = 0; j < np; ++j) {
+        auto it = std::find(p0->param_names.begin(), p0->param_names.end(), p->param_names[j]);
+        if (it == p0->param_names.end())
+          throw KcgError(KCG_E_INVALID_ARGUMENT, "argmin variants must share the parameter set");
+        map[j] = static_cast<int>(it - p0->param_names.begin());
+      }
+      lows.push_back(&p->low);
+      pmaps.push_back(map);
+    }
+    const std::string src = kcg::codegen(lows, pmaps, np, kcg::JitKind::argmin, name);
+    void* k = kcg::jit_kernel(src, name);
+    // per-variant compact weights live in one device buffer
+    size_t total = 0;
+    for (int v = 0; v < V; ++v) total += std::max<size_t>(1, progs[v]->low.keys.size());
+    std::vector<double> host(total, 0.0);
+    std::vector<size_t> off(V);
+    size_t o = 0;
+    for (int v = 0; v < V; ++v) {
+      off[v] = o;
+      compact_alpha(progs[v], alpha, host.data() + o);
+      o += std::max<size_t>(1, progs[v]->low.keys.size());
+    }
+    // cache the device weights per (variant set, alpha) -- small, reused
+    static std::mutex mu;
+    static std::vector<std::pair<std::vector<double>, double*>> cache;
+    double* dalpha = nullptr;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      for (auto& [h, d] : cache)
+        if (h == host) dalpha = d;
+      if (!dalpha) {
+        cuda_check(cudaMalloc(&dalpha, total * sizeof(double)), "cudaMalloc");
+        cuda_check(cudaMemcpy(dalpha, host.data(), total * sizeof(double), cudaMemcpyHostToDevice),
+                   "cudaMemcpy");
+        cache.emplace_back(host, dalpha);
+      }
+    }
+    ArgBuf ab;
+    for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
+    ab.push<void*>(best_idx);
+    ab.push<void*>(best_t);
+    ab.push<void*>(preds_out);
+    ab.push<int64_t>(static_cast<int64_t>(n));
+    for (int v = 0; v < V; ++v) ab.push<const void*>(dalpha + off[v]);
+    ab.finish();
+    kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid_for(n), 256, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_gram_accumulate(const double* X, size_t n, int F, size_t ld, double* G, double* xt1,
+                        double* colmax, void* stream) {
+  if (!X || !G || !xt1 || !colmax || ld < static_cast<size_t>(F))
+    return fail(KCG_E_INVALID_ARGUMENT, "bad gram arguments");
+  return guarded([&] {
+    require_device();
+    kcg::launch_gram(X, n, F, ld, G, xt1, colmax, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_gram_fused(const kcg_program* cp, const int64_t* const* param_cols, const double* T,
+                   size_t n, double* G, double* xt1, double* colmax,
+                   unsigned long long* bad_rows, void* stream) {
+  kcg_program* p = const_cast<kcg_program*>(cp);
+  if (!p || !T || !G || !xt1 || !colmax) return fail(KCG_E_INVALID_ARGUMENT, "bad gram arguments");
+  return guarded([&] {
+    require_device();
+    if (n == 0) return KCG_OK;
+    const int np = p->low.n_params;
+    if (!p->jit_gram) {
+      const std::string name = kname("kcg_gram_", p);
+      p->jit_gram = kcg::jit_kernel(
+          kcg::codegen({&p->low}, {identity(np)}, np, kcg::JitKind::gram, name), name);
+    }
+    ArgBuf ab;
+    for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
+    ab.push<const void*>(T);
+    ab.push<void*>(G);
+    ab.push<void*>(xt1);
+    ab.push<void*>(colmax);
+    ab.push<void*>(bad_rows);
+    ab.push<int64_t>(static_cast<int64_t>(n));
+    ab.finish();
+    kcg::launch_jit(p->jit_gram, ab.b.data(), ab.b.size(), grid_for(n, 256, 4), 256, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_residual_accumulate(const double* X, size_t n, int F, size_t ld, const double* alpha,
+                            double* obj, void* stream) {
+  if (!X || !alpha || !obj || ld < static_cast<size_t>(F))
+    return fail(KCG_E_INVALID_ARGUMENT, "bad residual arguments");
+  return guarded([&] {
+    require_device();
+    kcg::launch_residual(X, n, F, ld, alpha, obj, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_gram_residual_grad(const double* X, size_t n, int F, size_t ld, const double* alpha,
+                           double* g, void* stream) {
+  if (!X || !alpha || !g || ld < static_cast<size_t>(F))
+    return fail(KCG_E_INVALID_ARGUMENT, "bad residual arguments");
+  return guarded([&] {
+    require_device();
+    kcg::launch_residual_grad(X, n, F, ld, alpha, g, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, const double* T,
+                       size_t n, const double* alpha, double* obj, void* stream) {
+  kcg_program* p = const_cast<kcg_program*>(cp);
+  if (!p || !T || !alpha || !obj) return fail(KCG_E_INVALID_ARGUMENT, "bad residual arguments");
+  return guarded([&] {
+    require_device();
+    if (n == 0) return KCG_OK;
+    const int np = p->low.n_params;
+    const int F = static_cast<int>(p->low.keys.size());
+    if (!p->jit_resid) {
+      const std::string name = kname("kcg_resid_", p);
+      p->jit_resid = kcg::jit_kernel(
+          kcg::codegen({&p->low}, {identity(np)}, np, kcg::JitKind::residual, name), name);
+    }
+    ArgBuf ab;
+    for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
+    ab.push<const void*>(T);
+    ab.push<void*>(obj);
+    ab.push<int64_t>(static_cast<int64_t>(n));
+    std::vector<double> al(std::max(F, 1), 0.0);
+    compact_alpha(p, alpha, al.data());
+    for (double v : al) ab.push<double>(v);
+    ab.finish();
+    kcg::launch_jit(p->jit_resid, ab.b.data(), ab.b.size(), grid_for(n, 256, 8), 256, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_solve_gram(int F, const double* G, const double* xt1, const double* colmax,
+                   double* alpha_out, int* rank_out) {
+  if (F < 1 || !G || !xt1 || !colmax || !alpha_out)
+    return fail(KCG_E_INVALID_ARGUMENT, "bad solve arguments");
+  return guarded([&] {
+    std::vector<double> x;
+    const int r = solve_equilibrated(F, G, colmax, xt1, x);
+    std::copy(x.begin(), x.end(), alpha_out);
+    if (rank_out) *rank_out = r;
+    return KCG_OK;
+  });
+}
+
+int kcg_refine_gram(int F, const double* G, const double* colmax, const double* g,
+                    double* alpha) {
+  if (F < 1 || !G || !colmax || !g || !alpha)
+    return fail(KCG_E_INVALID_ARGUMENT, "bad refine arguments");
+  return guarded([&] {
+    std::vector<double> dx;
+    solve_equilibrated(F, G, colmax, g, dx);
+    for (int j = 0; j < F; ++j)
+      if (colmax[j] > 0.0) alpha[j] += dx[j];
+    return KCG_OK;
+  });
+}
+
+int kcg_weights_read_json(const char* path, double* alpha, uint8_t* covered, double* objective,
+                          uint64_t* n_cases) {
+  if (!path || !alpha || !covered) return fail(KCG_E_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    std::ifstream in(path, std::ios::binary);
+    if (!in) throw KcgError(KCG_E_IO, std::string("cannot open: ") + path);
+    nlohmann::json j;
+    try {
+      j = nlohmann::json::parse(in);
+    } catch (const nlohmann::json::exception& e) {
+      throw KcgError(KCG_E_PARSE, std::string(path) + ": " + e.what());
+    }
+    try {
+      const std::string ver = j.at("schema_version").get<std::string>();
+      if (ver != "v1")
+        throw KcgError(KCG_E_SCHEMA_MISMATCH,
+                       std::string(path) + ": schema '" + ver + "', expected 'v1'");
+      const int K = kcg_schema_size();
+      std::fill(alpha, alpha + K, 0.0);
+      std::fill(covered, covered + K, 0);
+      for (const auto& [key, val] : j.at("weights").items()) {
+        const int i = kcg::schema_index(key);
+        if (i < 0) throw KcgError(KCG_E_SCHEMA_MISMATCH, "unknown property key '" + key + "'");
+        alpha[i] = val.get<double>();
+        covered[i] = 1;
+      }
+      if (j.contains("covered"))
+        for (const auto& [key, val] : j.at("covered").items()) {
+          const int i = kcg::schema_index(key);
+          if (i < 0) throw KcgError(KCG_E_SCHEMA_MISMATCH, "unknown property key '" + key + "'");
+          covered[i] = val.get<bool>() ? 1 : 0;
+        }
+      if (objective) *objective = j.contains("fit") ? j["fit"].value("objective", 0.0) : 0.0;
+      if (n_cases) *n_cases = j.contains("fit") ? j["fit"].value("n_cases", uint64_t{0}) : 0;
+    } catch (const nlohmann::json::exception& e) {
+      throw KcgError(KCG_E_PARSE, std::string(path) + ": " + e.what());
+    }
+    return KCG_OK;
+  });
+}
+
+int kcg_weights_write_json(const char* path, const char* device, const double* alpha,
+                           const uint8_t* covered, double objective, uint64_t n_cases) {
+  if (!path || !alpha || !covered) return fail(KCG_E_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    nlohmann::json weights = nlohmann::json::object(), cov = nlohmann::json::object();
+    const auto& keys = kcg::schema_keys();
+    for (size_t i = 0; i < keys.size(); ++i) {
+      weights[keys[i]] = alpha[i];
+      cov[keys[i]] = static_cast<bool>(covered[i]);
+    }
+    nlohmann::json out;
+    out["device"] = device ? device : "";
+    out["schema_version"] = "v1";
+    out["weights"] = weights;
+    out["covered"] = cov;
+    out["fit"] = {{"objective", objective}, {"n_cases", n_cases}};
+    const std::string tmp = std::string(path) + ".tmp";
+    {
+      std::ofstream o(tmp, std::ios::binary | std::ios::trunc);
+      if (!o) throw KcgError(KCG_E_IO, "cannot open for writing: " + tmp);
+      o << out.dump(2) << "\n";
+      if (!o.flush()) throw KcgError(KCG_E_IO, "write failed: " + tmp);
+    }
+    if (std::rename(tmp.c_str(), path) != 0)
+      throw KcgError(KCG_E_IO, "cannot rename " + tmp + " to " + path);
+    return KCG_OK;
+  });
+}
+
+const char* kcg_status_str(int s) {
+  switch (s) {
+    case KCG_OK: return "OK";
+    case KCG_E_PARSE: return "E_PARSE";
+    case KCG_E_NEEDS_BINDING: return "E_NEEDS_BINDING";
+    case KCG_E_NEEDS_FALLBACK: return "E_NEEDS_FALLBACK";
+    case KCG_E_CAP_EXCEEDED: return "E_CAP_EXCEEDED";
+    case KCG_E_TYPE_CONFLICT: return "E_TYPE_CONFLICT";
+    case KCG_E_ASSUMPTION_VIOLATED: return "E_ASSUMPTION_VIOLATED";
+    case KCG_E_SCHEMA_MISMATCH: return "E_SCHEMA_MISMATCH";
+    case KCG_E_NONPOSITIVE_TIME: return "E_NONPOSITIVE_TIME";
+    case KCG_E_EMPTY: return "E_EMPTY";
+    case KCG_E_IO: return "E_IO";
+    case KCG_E_INVALID_ARGUMENT: return "E_INVALID_ARGUMENT";
+    case KCG_E_CUDA: return "E_CUDA";
+    case KCG_E_JIT: return "E_JIT";
+    case KCG_E_UNSUPPORTED: return "E_UNSUPPORTED";
+    case KCG_E_INTERNAL: return "E_INTERNAL";
+  }
+  return "E_UNKNOWN";
+}
+
+const char* kcg_point_status_str(int s) {
+  switch (s) {
+    case KCG_PT_OK: return "OK";
+    case KCG_PT_ASSUMPTION_VIOLATED: return "E_ASSUMPTION_VIOLATED";
+    case KCG_PT_NONINTEGRAL: return "NONINTEGRAL";
+    case KCG_PT_OVERFLOW: return "OVERFLOW";
+    case KCG_PT_COUNT_WIDE: return "COUNT_WIDE";
+  }
+  return "UNKNOWN";
+}
+
+const char* kcg_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t kcg_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

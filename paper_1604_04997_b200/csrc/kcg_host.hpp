@@ -1,0 +1,165 @@
+// Host-side program representation for the kcg back end.
+//
+// A `Program` is the reference front end's symbolic output for one kernel
+// (parameters, assume constraints, nonzero PropertyVector entries as
+// CountExpr polynomials) lowered to an integer program the GPU evaluates
+// exactly:
+//   * every CountExpr (countexpr.hpp:55-117) becomes an integer-coefficient
+//     polynomial over atom numerators divided by one static denominator D;
+//   * atoms are parameters, floor divisions by constants and n-ary min/max
+//     (countexpr.hpp:20-34), scheduled in dependency order;
+//   * assume constraints (LinCmp, linexpr.hpp:62-77) become integer forms
+//     evaluated per point exactly like AssumeCtx::admits (decide.cpp:153-170).
+// Exactness: evaluation is exact in int64 when every parameter is <= b64
+// and in int128 when <= b128 (static magnitude analysis, `bounds()`);
+// beyond that the point reports KCG_PT_OVERFLOW.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace kcg {
+
+using i128 = __int128;
+using u128 = unsigned __int128;
+
+struct KcgError : std::runtime_error {
+  int code;
+  KcgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+std::string i128_str(i128 v);
+i128 checked_add(i128 a, i128 b);
+i128 checked_mul(i128 a, i128 b);
+i128 gcd128(i128 a, i128 b);
+i128 lcm128(i128 a, i128 b);
+
+/// Exact rational with 128-bit numerator/denominator, normalised; every
+/// operation throws KcgError(KCG_E_UNSUPPORTED) instead of overflowing.
+struct Q {
+  i128 n = 0, d = 1;
+  Q() = default;
+  Q(i128 v) : n(v), d(1) {}
+  Q(i128 num, i128 den);
+  bool is_zero() const { return n == 0; }
+  bool is_int() const { return d == 1; }
+  Q operator+(const Q& o) const;
+  Q operator-(const Q& o) const;
+  Q operator*(const Q& o) const;
+  Q operator-() const { Q r; r.n = -n; r.d = d; return r; }
+  bool operator==(const Q& o) const { return n == o.n && d == o.d; }
+  std::string str() const;
+};
+
+// ---------------------------------------------------------------------------
+// Symbolic layer (parsed text)
+
+enum class AtomKind : int { var = 0, floordiv = 1, min = 2, max = 3 };
+
+struct Mono {
+  std::vector<std::pair<int, int>> f;  // (atom id, exponent), sorted by atom id
+  bool operator<(const Mono& o) const { return f < o.f; }
+  bool operator==(const Mono& o) const { return f == o.f; }
+};
+
+using Poly = std::map<Mono, Q>;
+
+struct AtomDef {
+  AtomKind kind = AtomKind::var;
+  int param = -1;          // var
+  int num = -1;            // floordiv numerator poly id
+  i128 den = 1;            // floordiv denominator (> 0)
+  std::vector<int> args;   // min/max argument poly ids
+  std::string key;         // canonical text (identity)
+};
+
+enum class CmpOp : int { lt = 0, le = 1, gt = 2, ge = 3, eq = 4 };
+
+struct Constraint {
+  bool divisibility = false;
+  CmpOp op = CmpOp::eq;
+  int poly = -1;       // relational: lhs - rhs; divisibility: lhs
+  i128 mod = 0, rem = 0;
+  std::string text;
+};
+
+struct Symbolic {
+  std::string kernel;
+  std::vector<std::string> params;
+  std::vector<AtomDef> atoms;
+  std::vector<Poly> polys;
+  std::vector<Constraint> cons;
+  std::vector<std::pair<int, int>> props;  // (schema index, poly id), schema order
+};
+
+Symbolic parse_program_text(const std::string& text);
+
+// ---------------------------------------------------------------------------
+// Lowered integer program
+
+enum OpCode : int32_t {
+  OP_VAR = 0,       // atom[dst] = param[a]
+  OP_MONO = 1,      // mono[dst] = prod factors[a..b)
+  OP_EXPR = 2,      // expr[dst] = sum terms[a..b)
+  OP_FLOORDIV = 3,  // atom[dst] = floor(expr[a] / big[c])
+  OP_MIN = 4,       // atom[dst] = min over args[a..b) of expr*scale
+  OP_MAX = 5
+};
+
+struct LOp {
+  int32_t code, dst, a, b, c;
+};
+
+struct LTerm {
+  i128 coef;
+  int32_t mono;  // -1: constant term
+};
+
+struct LExpr {
+  int32_t term_begin, term_end;
+  i128 D;  // value = numerator / D
+};
+
+struct LArg {
+  int32_t expr;
+  i128 scale;  // Dm / D_expr
+};
+
+struct LCons {
+  int32_t divisibility, op, expr;
+  i128 mod, rem;
+};
+
+struct LKey {
+  int32_t schema, expr;
+};
+
+struct Lowered {
+  int n_params = 0, n_atoms = 0, n_monos = 0, n_exprs = 0;
+  std::vector<LOp> ops;
+  std::vector<std::pair<int32_t, int32_t>> factors;  // (atom, exp)
+  std::vector<LTerm> terms;
+  std::vector<LExpr> exprs;
+  std::vector<LArg> args;
+  std::vector<i128> floordiv_den;  // per floordiv op (index in op.c)
+  std::vector<LCons> cons;
+  std::vector<LKey> keys;          // schema order
+  std::vector<i128> atom_den;      // value = numerator / atom_den
+  int64_t b64 = 0, b128 = 0;       // safe uniform parameter bounds
+};
+
+Lowered lower(const Symbolic& s);
+
+/// Magnitude bound of the largest intermediate when all |params| <= B.
+long double max_intermediate(const Lowered& L, long double B);
+
+// ---------------------------------------------------------------------------
+// Schema v1 (schema.cpp:16-38)
+
+const std::vector<std::string>& schema_keys();
+int schema_index(const std::string& key);
+
+}  // namespace kcg

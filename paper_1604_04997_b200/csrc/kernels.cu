@@ -1,0 +1,380 @@
+// Ahead-of-time sm_100a kernels:
+//   * kcg_interp_eval   -- table interpreter for evaluate_properties + predict
+//                          (generic engine; the JIT engine specialises the same
+//                          semantics into straight-line code, codegen.cpp)
+//   * kcg_gram_x        -- G += X^T X, X^T 1, column max|x| over a materialised
+//                          fp64 design (the reduction fit_weights needs,
+//                          model.cpp:62-80), register-tiled 4x4 over the upper
+//                          triangle, rows staged through shared memory
+//   * kcg_resid_x / kcg_resid_grad_x -- sum (1 - X a)^2 and X^T (1 - X a)
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "kcg_device.cuh"
+#include "kcg_kernels.hpp"
+
+namespace kcg {
+
+namespace {
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+__device__ __forceinline__ T wide(const KcgWide& w) {
+  return kcg_const<T>(w.lo, w.hi);
+}
+
+// ---------------------------------------------------------------------------
+// interpreter
+
+template <class T>
+__device__ __noinline__ int interp_body(const KcgDevProg* __restrict__ P,
+                                        const kcg_i64* p, T* cnt) {
+  T atom[KCG_MAX_ATOMS];
+  T mono[KCG_MAX_MONOS];
+  T expr[KCG_MAX_EXPRS];
+  const int nops = P->n_ops;
+  for (int k = 0; k < nops; ++k) {
+    const KcgDevOp op = P->ops[k];
+    switch (op.code) {
+      case 0:
+        atom[op.dst] = (T)p[op.a];
+        break;
+      case 1: {
+        T m = (T)1;
+        for (int i = op.a; i < op.b; ++i) {
+          const T v = atom[P->fac_atom[i]];
+          for (int e = 0; e < P->fac_exp[i]; ++e) m *= v;
+        }
+        mono[op.dst] = m;
+        break;
+      }
+      case 2: {
+        T s = (T)0;
+        for (int i = op.a; i < op.b; ++i) {
+          const T c = wide<T>(P->term_coef[i]);
+          const int mi = P->term_mono[i];
+          s += mi < 0 ? c : c * mono[mi];
+        }
+        expr[op.dst] = s;
+        break;
+      }
+      case 3:
+        atom[op.dst] = kcg_floordiv<T>(expr[op.a], wide<T>(P->fd_den[op.c]));
+        break;
+      default: {
+        T best = expr[P->arg_expr[op.a]] * wide<T>(P->arg_scale[op.a]);
+        for (int i = op.a + 1; i < op.b; ++i) {
+          const T v = expr[P->arg_expr[i]] * wide<T>(P->arg_scale[i]);
+          if (op.code == 4 ? v < best : v > best) best = v;
+        }
+        atom[op.dst] = best;
+        break;
+      }
+    }
+  }
+  for (int c = 0; c < P->n_cons; ++c) {
+    const T e = expr[P->cons_expr[c]];
+    if (!P->cons_div[c]) {
+      bool ok;
+      switch (P->cons_op[c]) {
+        case 0: ok = e < (T)0; break;
+        case 1: ok = e <= (T)0; break;
+        case 2: ok = e > (T)0; break;
+        case 3: ok = e >= (T)0; break;
+        default: ok = e == (T)0; break;
+      }
+      if (!ok) return KCG_PT_ASSUMPTION_VIOLATED;
+    } else {
+      const T D = wide<T>(P->expr_den[P->cons_expr[c]]);
+      if (e % D != (T)0) return KCG_PT_NONINTEGRAL;
+      const T v = e / D;
+      if (kcg_posmod<T>(v, wide<T>(P->cons_mod[c])) != wide<T>(P->cons_rem[c]))
+        return KCG_PT_ASSUMPTION_VIOLATED;
+    }
+  }
+  for (int j = 0; j < P->n_keys; ++j) {
+    const T e = expr[P->key_expr[j]];
+    const T D = wide<T>(P->expr_den[P->key_expr[j]]);
+    if (e % D != (T)0) return KCG_PT_NONINTEGRAL;
+    cnt[j] = e / D;
+  }
+  return KCG_PT_OK;
+}
+
+template <class T>
+__device__ __forceinline__ int interp_point(const KcgDevProg* __restrict__ P,
+                                            const kcg_i64* p,
+                                            const InterpEvalArgs& a, kcg_i64 i,
+                                            double& s) {
+  T c[KCG_MAX_KEYS];
+  int st = interp_body<T>(P, p, c);
+  if (st != KCG_PT_OK) return st;
+  for (int j = 0; j < P->n_keys; ++j) s = kcg_accum(s, a.alpha[j], c[j], a.simulate);
+  if (a.clo) {
+    for (int j = 0; j < P->n_keys; ++j) {
+      a.clo[(kcg_i64)j * a.n + i] = (kcg_i64)c[j];
+      if (a.chi)
+        a.chi[(kcg_i64)j * a.n + i] = kcg_hi64(c[j]);
+      else if (!kcg_fits_i64(c[j]))
+        st = KCG_PT_COUNT_WIDE;
+    }
+  }
+  return st;
+}
+
+__global__ void __launch_bounds__(128)
+    kcg_interp_eval(const KcgDevProg* __restrict__ P, const __grid_constant__ InterpEvalArgs a) {
+  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;
+  const int np = P->n_params;
+  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    kcg_i64 p[KCG_MAX_PARAMS];
+    bool neg = false, fast = P->b64 >= 0, wide_ok = P->b128 >= 0;
+    for (int j = 0; j < np; ++j) {
+      p[j] = a.p[j][i];
+      neg |= p[j] < 0;
+      fast &= p[j] <= P->b64;
+      wide_ok &= p[j] <= P->b128;
+    }
+    double s = 0.0;
+    int st;
+    if (neg)
+      st = KCG_PT_ASSUMPTION_VIOLATED;
+    else if (fast)
+      st = interp_point<kcg_i64>(P, p, a, i, s);
+    else if (wide_ok)
+      st = interp_point<kcg_i128>(P, p, a, i, s);
+    else
+      st = KCG_PT_OVERFLOW;
+    if (a.pred) a.pred[i] = (st == KCG_PT_OK || st == KCG_PT_COUNT_WIDE) ? s : kcg_nan();
+    if (a.status) a.status[i] = (uint8_t)st;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// materialised Gram
+
+constexpr int kGramRows = 32;
+constexpr int kGramThreads = 256;
+constexpr int kGramMaxF = 64;
+
+struct GramGeom {
+  int FP, nb, ntiles, slice_threads, S;
+};
+
+__host__ __device__ inline GramGeom gram_geom(int F) {
+  GramGeom g;
+  g.FP = (F + 3) & ~3;
+  g.nb = g.FP / 4;
+  g.ntiles = g.nb * (g.nb + 1) / 2;
+  g.slice_threads = ((g.ntiles + 31) / 32) * 32;
+  g.S = kGramThreads / g.slice_threads;
+  if (g.S < 1) g.S = 1;
+  return g;
+}
+
+__global__ void __launch_bounds__(kGramThreads)
+    kcg_gram_x(const double* __restrict__ X, kcg_i64 n, int F, kcg_i64 ld,
+               kcg_i64 rows_per_cta, double* __restrict__ G,
+               double* __restrict__ xt1, double* __restrict__ cmax) {
+  extern __shared__ double sm[];
+  const GramGeom g = gram_geom(F);
+  double* tile = sm;                           // [kGramRows][FP]
+  double* red = sm + kGramRows * g.FP;         // [ntiles][16] + [FP] + [FP]
+  double* red_s1 = red + g.ntiles * 16;
+  double* red_mx = red_s1 + g.FP;
+
+  const int tid = threadIdx.x;
+  const int slice = tid / g.slice_threads;
+  const int t = tid % g.slice_threads;
+  const bool active = slice < g.S && t < g.ntiles;
+  // tile t -> (bi, bj), bi <= bj, row-major over the upper triangle
+  int bi = 0, bj = 0;
+  {
+    int rem = t;
+    while (bi < g.nb && rem >= g.nb - bi) {
+      rem -= g.nb - bi;
+      ++bi;
+    }
+    bj = bi + rem;
+  }
+  for (int k = tid; k < g.ntiles * 16 + 2 * g.FP; k += blockDim.x) red[k] = 0.0;
+
+  double acc[4][4] = {};
+  double s1[4] = {}, mx[4] = {};
+  const kcg_i64 r0 = (kcg_i64)blockIdx.x * rows_per_cta;
+  kcg_i64 r1 = r0 + rows_per_cta;
+  if (r1 > n) r1 = n;
+  const int warp = tid >> 5, lane = tid & 31;
+  for (kcg_i64 base = r0; base < r1; base += kGramRows) {
+    const int rows = (int)((r1 - base) < kGramRows ? (r1 - base) : kGramRows);
+    __syncthreads();
+    for (int r = warp; r < kGramRows; r += kGramThreads / 32) {
+      const double* src = X + (base + r) * ld;
+      for (int c = lane; c < g.FP; c += 32)
+        tile[r * g.FP + c] = (r < rows && c < F) ? __ldcs(src + c) : 0.0;
+    }
+    __syncthreads();
+    if (active) {
+      for (int r = slice; r < rows; r += g.S) {
+        const double* row = tile + r * g.FP;
+        const double2 a01 = *reinterpret_cast<const double2*>(row + 4 * bi);
+        const double2 a23 = *reinterpret_cast<const double2*>(row + 4 * bi + 2);
+        const double2 b01 = *reinterpret_cast<const double2*>(row + 4 * bj);
+        const double2 b23 = *reinterpret_cast<const double2*>(row + 4 * bj + 2);
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y};
+        const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
+        if (bi == bj) {
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            s1[x] += av[x];
+            mx[x] = fmax(mx[x], fabs(av[x]));
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) atomicAdd(red + t * 16 + x * 4 + y, acc[x][y]);
+    if (bi == bj)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        atomicAdd(red_s1 + 4 * bi + x, s1[x]);
+        atomicMax(reinterpret_cast<unsigned long long*>(red_mx + 4 * bi + x),
+                  (unsigned long long)__double_as_longlong(mx[x]));
+      }
+  }
+  __syncthreads();
+  if (slice == 0 && t < g.ntiles) {
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int r = 4 * bi + x, c = 4 * bj + y;
+        if (r >= F || c >= F) continue;
+        const double v = red[t * 16 + x * 4 + y];
+        atomicAdd(G + r * F + c, v);
+        if (bi != bj) atomicAdd(G + c * F + r, v);
+      }
+    if (bi == bj)
+      for (int x = 0; x < 4; ++x) {
+        const int c = 4 * bi + x;
+        if (c >= F) continue;
+        atomicAdd(xt1 + c, red_s1[c]);
+        atomicMax(reinterpret_cast<unsigned long long*>(cmax + c),
+                  (unsigned long long)__double_as_longlong(red_mx[c]));
+      }
+  }
+}
+
+// warp per row: lanes own columns lane and lane+32
+template <bool GRAD>
+__global__ void __launch_bounds__(256)
+    kcg_resid_x(const double* __restrict__ X, kcg_i64 n, int F, kcg_i64 ld,
+                const double* __restrict__ alpha, double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const kcg_i64 warp = ((kcg_i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const kcg_i64 nwarps = ((kcg_i64)gridDim.x * blockDim.x) >> 5;
+  const double a0 = lane < F ? alpha[lane] : 0.0;
+  const double a1 = lane + 32 < F ? alpha[lane + 32] : 0.0;
+  double acc = 0.0, g0 = 0.0, g1 = 0.0;
+  for (kcg_i64 r = warp; r < n; r += nwarps) {
+    const double* row = X + r * ld;
+    const double x0 = lane < F ? __ldcs(row + lane) : 0.0;
+    const double x1 = lane + 32 < F ? __ldcs(row + lane + 32) : 0.0;
+    double d = fma(x1, a1, x0 * a0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    const double res = 1.0 - d;
+    if (GRAD) {
+      g0 = fma(x0, res, g0);
+      g1 = fma(x1, res, g1);
+    } else {
+      acc = fma(res, res, acc);
+    }
+  }
+  if (GRAD) {
+    if (lane < F) atomicAdd(out + lane, g0);
+    if (lane + 32 < F) atomicAdd(out + lane + 32, g1);
+  } else if (lane == 0) {
+    atomicAdd(out, acc);
+  }
+}
+
+int g_sms = 0;
+
+}  // namespace
+
+int num_sms() {
+  if (g_sms) return g_sms;
+  int dev = 0;
+  check(cudaGetDevice(&dev), "cudaGetDevice");
+  check(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev),
+        "cudaDeviceGetAttribute");
+  return g_sms;
+}
+
+void launch_interp_eval(const KcgDevProg* dprog, const InterpEvalArgs& a, void* stream) {
+  if (a.n == 0) return;
+  const int threads = 128;
+  kcg_i64 blocks = (a.n + threads - 1) / threads;
+  const kcg_i64 cap = (kcg_i64)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  kcg_interp_eval<<<(unsigned)blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(dprog, a);
+  check(cudaGetLastError(), "kcg_interp_eval launch");
+}
+
+void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double* xt1,
+                 double* colmax, void* stream) {
+  if (n == 0) return;
+  if (F < 1 || F > kGramMaxF) throw std::invalid_argument("gram: n_cols must be in [1, 64]");
+  const GramGeom g = gram_geom(F);
+  const size_t smem = (size_t)(kGramRows * g.FP + g.ntiles * 16 + 2 * g.FP) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    check(cudaFuncSetAttribute(kcg_gram_x, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
+          "cudaFuncSetAttribute");
+    attr = true;
+  }
+  const kcg_i64 chunks = ((kcg_i64)n + kGramRows - 1) / kGramRows;
+  kcg_i64 ctas = (kcg_i64)num_sms() * 4;
+  if (ctas > chunks) ctas = chunks;
+  const kcg_i64 chunks_per_cta = (chunks + ctas - 1) / ctas;
+  ctas = (chunks + chunks_per_cta - 1) / chunks_per_cta;
+  kcg_gram_x<<<(unsigned)ctas, kGramThreads, smem, static_cast<cudaStream_t>(stream)>>>(
+      X, (kcg_i64)n, F, (kcg_i64)ld, chunks_per_cta * kGramRows, G, xt1, colmax);
+  check(cudaGetLastError(), "kcg_gram_x launch");
+}
+
+void launch_residual(const double* X, size_t n, int F, size_t ld, const double* alpha,
+                     double* obj, void* stream) {
+  if (n == 0) return;
+  if (F < 1 || F > 64) throw std::invalid_argument("residual: n_cols must be in [1, 64]");
+  kcg_resid_x<false><<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      X, (kcg_i64)n, F, (kcg_i64)ld, alpha, obj);
+  check(cudaGetLastError(), "kcg_resid_x launch");
+}
+
+void launch_residual_grad(const double* X, size_t n, int F, size_t ld, const double* alpha,
+                          double* g, void* stream) {
+  if (n == 0) return;
+  if (F < 1 || F > 64) throw std::invalid_argument("residual grad: n_cols must be in [1, 64]");
+  kcg_resid_x<true><<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      X, (kcg_i64)n, F, (kcg_i64)ld, alpha, g);
+  check(cudaGetLastError(), "kcg_resid_grad_x launch");
+}
+
+}  // namespace kcg

@@ -1,0 +1,285 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the
+reference's golden vectors. Counts bit-exact, predictions bitwise, statuses
+equal. Both engines (NVRTC-specialised and table interpreter) are checked."""
+import math
+import random
+
+import numpy as np
+import pytest
+
+import kc_oracle as ko
+from conftest import PROGRAMS, hexf, load_golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+import paper_1604_04997_b200 as kc  # noqa: E402
+from paper_1604_04997_b200 import _capi  # noqa: E402
+
+ENGINES = ["jit", "interp"]
+ST_NAME = {0: "ok", 1: "E_ASSUMPTION_VIOLATED", 2: "NONINTEGRAL", 3: "OVERFLOW", 4: "COUNT_WIDE"}
+
+
+def _weights(alpha):
+    return kc.ModelWeights(device="t", alpha=list(alpha), covered=[a != 0 for a in alpha])
+
+
+def _cols(prog, bindings):
+    return {p: torch.tensor([b[p] for b in bindings], dtype=torch.int64, device="cuda")
+            for p in prog.params}
+
+
+def _run(prog, bindings, alpha, engine):
+    prog.set_engine(engine)
+    cols = _cols(prog, bindings)
+    bb = kc.evaluate_properties(prog, cols, wide=True)
+    pred, st = kc.predict(_weights(alpha), prog, cols, with_status=True)
+    torch.cuda.synchronize()
+    lo = bb.counts_lo.cpu().numpy()
+    hi = bb.counts_hi.cpu().numpy()
+    return lo, hi, bb.status.cpu().numpy(), pred.cpu().numpy(), st.cpu().numpy()
+
+
+def _as_int(lo, hi):
+    return (int(hi) << 64) | (int(lo) & ((1 << 64) - 1))
+
+
+def _compare(prog, oprog, bindings, alpha, engine, expect=None):
+    lo, hi, st, pred, st2 = _run(prog, bindings, alpha, engine)
+    assert (st == st2).all()
+    for i, b in enumerate(bindings):
+        try:
+            want = oprog.evaluate_properties(b)
+            want_st = 0
+        except ko.AssumptionViolated:
+            want_st = 1
+        except ko.NonIntegral:
+            want_st = 2
+        if expect is not None and expect[i] is not None:
+            assert ST_NAME[want_st] == expect[i] or expect[i] == "ok" and want_st == 0
+        assert st[i] == want_st, (prog.name, engine, b, st[i], want_st)
+        if want_st == 0:
+            for j, k in enumerate(prog.props):
+                assert _as_int(lo[j, i], hi[j, i]) == want[k], (prog.name, b, k)
+            assert pred[i] == ko.predict(alpha, want), (prog.name, b)
+        else:
+            assert math.isnan(pred[i])
+
+
+@pytest.fixture(scope="module")
+def programs():
+    return {p.stem: (kc.Program.from_file(p), ko.Program(p.read_text()))
+            for p in sorted(PROGRAMS.glob("*.kcp"))}
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_suite_manifest_cases(programs, suite_alpha, engine):
+    cases = load_golden("suite_cases.json")["cases"]
+    by_kernel = {}
+    for c in cases:
+        by_kernel.setdefault(c["kernel"], []).append({k: int(v) for k, v in c["binding"].items()})
+    for kid, (prog, oprog) in programs.items():
+        bs = list(by_kernel[kid])
+        # perturbations: inadmissible neighbours and negatives (props.cpp:263-266)
+        bs += [{k: v + 1 for k, v in b.items()} for b in by_kernel[kid][:2]]
+        bs += [{k: -v for k, v in b.items()} for b in by_kernel[kid][:1]]
+        bs += [{k: 0 for k in b} for b in by_kernel[kid][:1]]
+        _compare(prog, oprog, bs, suite_alpha, engine)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_golden_grid_samples(programs, suite_alpha, engine):
+    samples = load_golden("grid_samples.json")["samples"]
+    groups = {}
+    for s in samples:
+        groups.setdefault(s["kernel"], []).append(s)
+    for kid, ss in groups.items():
+        prog, oprog = programs[kid]
+        bs = [{k: int(v) for k, v in s["binding"].items()} for s in ss]
+        prog.set_engine(engine)
+        lo, hi, st, pred, _ = _run(prog, bs, suite_alpha, engine)
+        for i, s in enumerate(ss):
+            if s["status"] == "ok":
+                assert st[i] == 0, (kid, s["binding"])
+                want = {ko.SCHEMA_INDEX[k]: int(v) for k, v in s["counts"].items()}
+                for j, k in enumerate(prog.props):
+                    assert _as_int(lo[j, i], hi[j, i]) == want.get(k, 0)
+                assert pred[i] == hexf(s["predicted_s"][1]), (kid, s["binding"])
+            else:
+                assert st[i] == _capi.PT_ASSUMPTION_VIOLATED
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_extra_programs_atoms(suite_alpha, engine):
+    d = load_golden("extra_programs.json")
+    progs = {p["id"]: (kc.Program(p["program"]), ko.Program(p["program"]))
+             for p in d["programs"] if "program" in p}
+    groups = {}
+    for s in d["samples"]:
+        groups.setdefault(s["kernel"], []).append(s)
+    for kid, ss in groups.items():
+        prog, oprog = progs[kid]
+        bs = [{k: int(v) for k, v in s["binding"].items()} for s in ss]
+        _compare(prog, oprog, bs, suite_alpha, engine,
+                 expect=[s["status"] if s["status"] != "E_ASSUMPTION_VIOLATED" else "E_ASSUMPTION_VIOLATED" for s in ss])
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_wide_and_overflow_paths(suite_alpha, engine):
+    """Counts beyond 2^63 / 2^64 go through the int128 path bit-exactly;
+    bindings beyond the 128-bit safe bound report OVERFLOW, never wrap."""
+    for kid in ("matmul_skinny_g16x16", "matmul_tiled_g16x16", "conv_g16x16"):
+        prog = kc.load_program(kid)
+        oprog = ko.Program((PROGRAMS / f"{kid}.kcp").read_text())
+        b64, b128 = prog.safe_bounds()
+        rng = random.Random(7)
+        bs = []
+        for _ in range(300):
+            n = 16 * rng.randint(1, b128 // 16 // (8 if "skinny" in kid else 1))
+            b = {p: n for p in prog.params}
+            if "skinny" in kid:
+                b["m"] = 8 * n
+            bs.append(b)
+        for edge in (b64 - b64 % 16, b64 - b64 % 16 + 16, b128 - b128 % 16):
+            bs.append({p: edge for p in prog.params})
+        _compare(prog, oprog, [b for b in bs if max(b.values()) <= b128], suite_alpha, engine)
+        over = [{p: b128 - b128 % 16 + 16 * k for p in prog.params} for k in (1, 2, 1000)]
+        _, _, st, pred, _ = _run(prog, over, suite_alpha, engine)
+        assert (st == _capi.PT_OVERFLOW).all() and np.isnan(pred).all()
+
+
+def test_count_wide_status_without_hi_words(suite_alpha):
+    prog = kc.load_program("matmul_skinny_g16x16")
+    n = 1 << 24
+    cols = _cols(prog, [{"n": n, "m": 8 * n, "l": n}, {"n": 16, "m": 128, "l": 16}])
+    bb = kc.evaluate_properties(prog, cols, wide=False)
+    st = bb.status.cpu().tolist()
+    assert st == [_capi.PT_COUNT_WIDE, _capi.PT_OK]
+
+
+def test_simulate_order_matches_noiseless_time(programs):
+    sim = ko.simdev_reference_alpha()
+    cases = load_golden("suite_cases.json")["cases"]
+    for kid, (prog, oprog) in programs.items():
+        bs = [{k: int(v) for k, v in c["binding"].items()} for c in cases if c["kernel"] == kid]
+        t = kc.noiseless_time(sim, prog, _cols(prog, bs)).cpu().numpy()
+        want = [hexf(c["time_s"][1]) for c in cases if c["kernel"] == kid]
+        assert list(t) == want, kid
+
+
+def test_argmin_over_matmul_variants(suite_alpha):
+    ids = ["matmul_tiled_g12x12", "matmul_tiled_g14x14", "matmul_tiled_g16x16",
+           "matmul_naive_g16x12", "matmul_naive_g16x14", "matmul_naive_g16x16"]
+    progs = [kc.load_program(i) for i in ids]
+    oprogs = [ko.Program((PROGRAMS / f"{i}.kcp").read_text()) for i in ids]
+    rng = random.Random(3)
+    bs = [{"n": 336 * rng.randint(1, 551), "m": 336 * rng.randint(1, 551), "l": 336 * rng.randint(1, 551)}
+          for _ in range(500)]
+    bs += [{"n": 16 * rng.randint(1, 200), "m": 16 * rng.randint(1, 200), "l": 16 * rng.randint(1, 200)}
+           for _ in range(500)]  # g12/g14 variants often inadmissible here
+    bs.append({"n": 17, "m": 17, "l": 17})  # nobody admissible
+    cols = _cols(progs[0], bs)
+    best, best_t, preds = kc.argmin(progs, _weights(suite_alpha), cols, return_preds=True)
+    best, best_t, preds = best.cpu().numpy(), best_t.cpu().numpy(), preds.cpu().numpy()
+    for i, b in enumerate(bs):
+        ts = []
+        for v, op in enumerate(oprogs):
+            try:
+                ts.append(ko.predict(suite_alpha, op.evaluate_properties(b)))
+            except ko.AssumptionViolated:
+                ts.append(math.nan)
+        for v in range(len(ids)):
+            assert (math.isnan(ts[v]) and math.isnan(preds[v, i])) or ts[v] == preds[v, i]
+        fin = [(t, v) for v, t in enumerate(ts) if not math.isnan(t)]
+        if fin:
+            t, v = min(fin)
+            assert best[i] == v and best_t[i] == t
+        else:
+            assert best[i] == -1 and math.isinf(best_t[i])
+
+
+def test_gram_accumulate_matches_numpy():
+    rng = np.random.default_rng(0)
+    for F in (1, 3, 18, 40, 64):
+        N = 5000 + F
+        X = rng.uniform(0.5, 2.0, size=(N, F)) * 10.0 ** rng.integers(-3, 3, size=F)
+        X[rng.random((N, F)) < 0.1] = 0.0
+        Xd = torch.tensor(X, device="cuda")
+        st = kc.gram_accumulate(Xd)
+        torch.cuda.synchronize()
+        G = st.G.cpu().numpy()
+        np.testing.assert_allclose(G, X.T @ X, rtol=1e-12, atol=0)
+        np.testing.assert_allclose(st.xt1.cpu().numpy(), X.sum(axis=0), rtol=1e-12)
+        assert (st.colmax.cpu().numpy() == np.abs(X).max(axis=0)).all()
+
+
+def _synthetic_design(fit):
+    keys = fit["keys"]
+    counts = np.array(fit["counts"], dtype=np.float64)
+    times = np.array([hexf(t) for t in fit["times"]])
+    X = counts / times[:, None]
+    return keys, X
+
+
+def test_fit_weights_matches_reference_cod():
+    for fit in load_golden("fit_synthetic.json")["fits"]:
+        keys, X = _synthetic_design(fit)
+        res = kc.fit_weights(torch.tensor(X, device="cuda"), refine=1)
+        ref = [hexf(a) for a in fit["alpha"]]
+        for k, got, r in zip(keys, res.alpha, ref):
+            assert abs(got - r) <= 1e-6 * abs(r), (fit["name"], k, got, r)
+        assert res.objective <= max(1e-18, 10 * hexf(fit["objective"][1])) + 1e-20
+
+
+def test_fit_suite_from_golden_counts(suite_alpha):
+    """config 1: the measurement-suite design (390 x 149) through the GPU
+    Gram + host solve reproduces the reference's fitted weights."""
+    cases = [c for c in load_golden("suite_cases.json")["cases"] if c["role"] == "measurement"]
+    rows = [({ko.SCHEMA_INDEX[k]: int(v) for k, v in c["counts"].items()}, hexf(c["time_s"][1])) for c in cases]
+    X, cov = ko.build_design_matrix(rows)
+    cols = np.flatnonzero(cov)
+    res = kc.fit_weights(torch.tensor(np.ascontiguousarray(X[:, cols]), device="cuda"), refine=2)
+    sim = ko.simdev_reference_alpha()
+    for c, got in zip(cols, res.alpha):
+        ref = suite_alpha[c]
+        if sim[c] != 0.0:
+            assert abs(got - ref) <= 1e-6 * abs(ref), ko.SCHEMA[c]
+        else:
+            assert abs(got) <= 1e-15
+    assert res.objective <= 1e-10
+
+
+def test_gram_fused_matches_oracle_rows():
+    prog = kc.load_program("matmul_tiled_g16x16")
+    oprog = ko.Program((PROGRAMS / "matmul_tiled_g16x16.kcp").read_text())
+    rng = random.Random(11)
+    bs = [{"n": 16 * rng.randint(1, 300), "m": 16 * rng.randint(1, 300), "l": 16 * rng.randint(1, 300)}
+          for _ in range(4000)]
+    bs += [{"n": 17, "m": 16, "l": 16}]  # inadmissible row is skipped and counted
+    sim = ko.simdev_reference_alpha()
+    T = []
+    rows = []
+    for b in bs:
+        try:
+            c = oprog.evaluate_properties(b)
+            t = ko.noiseless_time(sim, c) * (1.0 + 0.01 * rng.random())
+            rows.append([float(c[k]) / t for k in prog.props])
+        except ko.AssumptionViolated:
+            t = 1.0
+        T.append(t)
+    X = np.array(rows)
+    cols = _cols(prog, bs)
+    st = kc.gram_fused(prog, cols, torch.tensor(T, dtype=torch.float64, device="cuda"))
+    torch.cuda.synchronize()
+    assert st.bad_rows == 1
+    np.testing.assert_allclose(st.G.cpu().numpy(), X.T @ X, rtol=1e-11)
+    np.testing.assert_allclose(st.xt1.cpu().numpy(), X.sum(axis=0), rtol=1e-11)
+    assert (st.colmax.cpu().numpy() == np.abs(X).max(axis=0)).all()
+
+
+def test_no_silent_fallback_launches_counted():
+    before = kc.launch_count()
+    prog = kc.load_program("conv_g16x16")
+    kc.evaluate_properties(prog, _cols(prog, [{"n": 16}]))
+    torch.cuda.synchronize()
+    assert kc.launch_count() == before + 1
