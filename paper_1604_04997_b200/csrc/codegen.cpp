@@ -145,10 +145,10 @@ void emit_classify(std::ostringstream& os, const Lowered& L, int v,
                    const std::vector<int>& pmap) {
   os << "__device__ __forceinline__ int kcg_class_" << v
      << "(const kcg_i64* p) {\n";
-  os << "  if (";
+  os << "  if ((";
   for (int j = 0; j < L.n_params; ++j) os << (j ? " | " : "") << "p[" << pmap[j] << "]";
   if (L.n_params == 0) os << "0ll";
-  os << " < 0) return 0;\n";
+  os << ") < 0) return 0;\n";
   if (L.b64 >= 0) {
     os << "  if (";
     for (int j = 0; j < L.n_params; ++j)
