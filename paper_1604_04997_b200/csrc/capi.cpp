@@ -33,6 +33,7 @@ struct kcg_program {
   bool dprog_ok = true;         // fits the interpreter's static tables
   std::string jit_src;
   void* jit_eval = nullptr;
+  void* jit_eval_gen = nullptr;
   void* jit_gram = nullptr;
   void* jit_resid = nullptr;
 };
@@ -136,6 +137,11 @@ bool build_devprog(const kcg::Lowered& L, KcgDevProg& d) {
     d.cons_expr[i] = L.cons[i].expr;
     d.cons_mod[i] = wide(L.cons[i].mod);
     d.cons_rem[i] = wide(L.cons[i].rem);
+  }
+  if (L.quot_mod.size() > KCG_MAX_PARAMS) return false;
+  for (size_t i = 0; i < L.quot_mod.size(); ++i) {
+    d.quot_mod[i] = wide(L.quot_mod[i]);
+    d.quot_rem[i] = wide(L.quot_rem[i]);
   }
   for (size_t i = 0; i < L.keys.size(); ++i) {
     d.key_schema[i] = L.keys[i].schema;
@@ -347,7 +353,11 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
       ++g_launches;
       return KCG_OK;
     }
-    if (!p->jit_eval) p->jit_eval = kcg::jit_kernel(kcg_program_jit_source(p), kname("kcg_eval_", p));
+    if (!p->jit_eval) {
+      const std::string nm = kname("kcg_eval_", p);
+      p->jit_eval = kcg::jit_kernel(kcg_program_jit_source(p), nm);
+      p->jit_eval_gen = kcg::jit_kernel(kcg_program_jit_source(p), nm + "_gen");
+    }
     ArgBuf ab;
     for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
     ab.push<void*>(pred_out);
@@ -356,11 +366,19 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
     ab.push<void*>(counts_hi);
     ab.push<int64_t>(static_cast<int64_t>(n));
     ab.push<int32_t>(simulate);
+    bool vec = (reinterpret_cast<uintptr_t>(pred_out) % 16 == 0) &&
+               (reinterpret_cast<uintptr_t>(status_out) % 4 == 0);
+    for (int j = 0; j < np; ++j) vec = vec && reinterpret_cast<uintptr_t>(param_cols[j]) % 16 == 0;
+    ab.push<int32_t>(vec ? 1 : 0);
     std::vector<double> al(std::max(F, 1), 0.0);
     compact_alpha(p, alpha, al.data());
     for (double v : al) ab.push<double>(v);
     ab.finish();
-    kcg::launch_jit(p->jit_eval, ab.b.data(), ab.b.size(), grid_for(n), 256, stream);
+    // finite weights: the skip rules cannot change the sum (GEN = 0 kernel)
+    bool finite = true;
+    for (double v : al) finite = finite && std::isfinite(v);
+    kcg::launch_jit(finite ? p->jit_eval : p->jit_eval_gen, ab.b.data(), ab.b.size(),
+                    grid_for((n + 3) / 4), 256, stream);
     ++g_launches;
     return KCG_OK;
   });

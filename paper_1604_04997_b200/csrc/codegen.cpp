@@ -1,12 +1,20 @@
 // JIT specialisation: lowered programs -> straight-line CUDA source.
 //
-// Each program becomes `kcg_body_<v><T>()`, the exact evaluation of its
-// admissibility (AssumeCtx::admits, decide.cpp:153-170) and nonzero property
-// entries (evaluate_properties, props.cpp:259-271) with every coefficient,
-// denominator and modulus a compile-time constant, instantiated for
-// T = int64 (fast path) and T = int128 (wide path). The kernels around the
-// bodies implement fused evaluate+predict, argmin over variants, and the
-// fused design-row Gram / residual reductions.
+// Each program v becomes two exact evaluators of its admissibility
+// (AssumeCtx::admits, decide.cpp:153-170) and nonzero property entries
+// (evaluate_properties, props.cpp:259-271) with every coefficient,
+// denominator and modulus a compile-time constant:
+//   kcg_fast_<v>  int64, used when every parameter is in [0, b64]. When
+//                 b64 < 2^32 parameters and congruence quotients are handled
+//                 as 32-bit unsigned values (one IMAD.WIDE per first product,
+//                 32-bit quotients instead of 64-bit division sequences).
+//   kcg_wide_<v>  int128, out of line (__noinline__) so it does not inflate
+//                 the fast path's register allocation; parameters in
+//                 (b64, b128].
+// The kernels around them: fused evaluate+predict (4 points per thread,
+// 16-byte vector loads/stores), argmin over variants, and the fused
+// design-row Gram / residual reductions.
+#include <cstdlib>
 #include <sstream>
 
 #include "kcg_codegen.hpp"
@@ -29,8 +37,7 @@ std::string lit(i128 v) {
     else
       os << "((T)" << lo << "ll)";
   } else {
-    os << "kcg_const<T>((kcg_i64)" << static_cast<uint64_t>(lo) << "ull, "
-       << hi << "ll)";
+    os << "kcg_const<T>((kcg_i64)" << static_cast<uint64_t>(lo) << "ull, " << hi << "ll)";
   }
   return os.str();
 }
@@ -45,22 +52,55 @@ const char* cmp_str(int op) {
   }
 }
 
-void emit_body(std::ostringstream& os, const Lowered& L, int v) {
-  os << "template <class T>\n__device__ __forceinline__ int kcg_body_" << v
-     << "(const kcg_i64* __restrict__ p, T* __restrict__ cnt) {\n";
+constexpr int64_t kU32 = 0xffffffffll;
+
+// fast: T = kcg_i64; small: every parameter <= b64 < 2^32
+void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast) {
+  const bool small = fast && L.b64 >= 0 && L.b64 <= kU32;
+  std::vector<bool> atom_u32(L.n_atoms, false);  // value known in [0, 2^32)
+  if (fast)
+    os << "__device__ __forceinline__ int kcg_fast_" << v
+       << "(const kcg_i64* __restrict__ p, kcg_i64* __restrict__ cnt) {\n  typedef kcg_i64 T;\n";
+  else
+    os << "__device__ __noinline__ int kcg_wide_" << v
+       << "(const kcg_i64* __restrict__ p, kcg_i128* __restrict__ cnt) {\n  typedef kcg_i128 T;\n";
   for (const LOp& op : L.ops) {
     switch (op.code) {
       case OP_VAR:
+        if (small) {
+          os << "  const unsigned u" << op.dst << " = (unsigned)p[" << op.a << "];\n";
+          atom_u32[op.dst] = true;
+        }
         os << "  const T a" << op.dst << " = (T)p[" << op.a << "];\n";
         break;
+      case OP_QUOT: {
+        const i128 M = L.quot_mod[op.c], R = L.quot_rem[op.c];
+        if (small && M <= kU32) {
+          // admissible points have p = M q + R with 0 <= R <= p < 2^32
+          os << "  const unsigned u" << op.dst << " = ((unsigned)p[" << op.a << "] - "
+             << static_cast<uint64_t>(R) << "u) / " << static_cast<uint64_t>(M) << "u;\n";
+          os << "  const T a" << op.dst << " = (T)u" << op.dst << ";\n";
+          atom_u32[op.dst] = true;
+        } else {
+          os << "  const T a" << op.dst << " = kcg_floordiv<T>((T)p[" << op.a << "] - " << lit(R)
+             << ", " << lit(M) << ");\n";
+        }
+        break;
+      }
       case OP_MONO: {
-        os << "  const T m" << op.dst << " = ";
-        bool first = true;
+        std::vector<int> f;
         for (int i = op.a; i < op.b; ++i)
-          for (int k = 0; k < L.factors[i].second; ++k) {
-            os << (first ? "" : " * ") << "a" << L.factors[i].first;
-            first = false;
-          }
+          for (int k = 0; k < L.factors[i].second; ++k) f.push_back(L.factors[i].first);
+        os << "  const T m" << op.dst << " = ";
+        size_t start = 0;
+        if (f.size() >= 2 && atom_u32[f[0]] && atom_u32[f[1]]) {
+          os << "(T)((kcg_u64)u" << f[0] << " * u" << f[1] << ")";
+          start = 2;
+        } else {
+          os << "a" << f[0];
+          start = 1;
+        }
+        for (size_t k = start; k < f.size(); ++k) os << " * a" << f[k];
         os << ";\n";
         break;
       }
@@ -70,15 +110,14 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v) {
         for (int i = op.a; i < op.b; ++i) {
           const LTerm& t = L.terms[i];
           if (i != op.a) os << " + ";
-          if (t.mono < 0) {
+          if (t.mono < 0)
             os << lit(t.coef);
-          } else if (t.coef == 1) {
+          else if (t.coef == 1)
             os << "m" << t.mono;
-          } else if (t.coef == -1) {
+          else if (t.coef == -1)
             os << "(-m" << t.mono << ")";
-          } else {
+          else
             os << lit(t.coef) << " * m" << t.mono;
-          }
         }
         os << ";\n";
         break;
@@ -98,8 +137,8 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v) {
         }
         os << "    a" << op.dst << " = v0;\n";
         for (int i = op.a + 1; i < op.b; ++i)
-          os << "    if (v" << (i - op.a) << (op.code == OP_MIN ? " < " : " > ")
-             << "a" << op.dst << ") a" << op.dst << " = v" << (i - op.a) << ";\n";
+          os << "    if (v" << (i - op.a) << (op.code == OP_MIN ? " < " : " > ") << "a" << op.dst
+             << ") a" << op.dst << " = v" << (i - op.a) << ";\n";
         os << "  }\n";
         break;
       }
@@ -107,6 +146,16 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v) {
   }
   // admissibility
   for (const LCons& c : L.cons) {
+    if (c.divisibility == 2) {
+      // congruence facts folded into p = M q + R
+      if (small && atom_u32[c.expr] && c.rem == 0 && c.mod <= kU32)
+        os << "  if ((unsigned)p[" << c.op << "] != " << static_cast<uint64_t>(c.mod) << "u * u"
+           << c.expr << ") return KCG_PT_ASSUMPTION_VIOLATED;\n";
+      else
+        os << "  if ((T)p[" << c.op << "] - " << lit(c.rem) << " != " << lit(c.mod) << " * a"
+           << c.expr << ") return KCG_PT_ASSUMPTION_VIOLATED;\n";
+      continue;
+    }
     const LExpr& ex = L.exprs[c.expr];
     if (!c.divisibility) {
       os << "  if (!(e" << c.expr << " " << cmp_str(c.op)
@@ -114,8 +163,7 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v) {
     } else {
       os << "  {\n";
       if (ex.D != 1) {
-        os << "    if (e" << c.expr << " % " << lit(ex.D)
-           << " != (T)0) return KCG_PT_NONINTEGRAL;\n";
+        os << "    if (e" << c.expr << " % " << lit(ex.D) << " != (T)0) return KCG_PT_NONINTEGRAL;\n";
         os << "    const T v = e" << c.expr << " / " << lit(ex.D) << ";\n";
       } else {
         os << "    const T v = e" << c.expr << ";\n";
@@ -129,8 +177,7 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v) {
     const LExpr& ex = L.exprs[L.keys[j].expr];
     const int e = L.keys[j].expr;
     if (ex.D != 1) {
-      os << "  if (e" << e << " % " << lit(ex.D)
-         << " != (T)0) return KCG_PT_NONINTEGRAL;\n";
+      os << "  if (e" << e << " % " << lit(ex.D) << " != (T)0) return KCG_PT_NONINTEGRAL;\n";
       os << "  cnt[" << j << "] = e" << e << " / " << lit(ex.D) << ";\n";
     } else {
       os << "  cnt[" << j << "] = e" << e << ";\n";
@@ -139,50 +186,147 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v) {
   os << "  return KCG_PT_OK;\n}\n\n";
 }
 
-// param range classification: 0 = negative (inadmissible), 1 = fast int64,
-// 2 = wide int128, 3 = beyond the wide bound
-void emit_classify(std::ostringstream& os, const Lowered& L, int v,
-                   const std::vector<int>& pmap) {
-  os << "__device__ __forceinline__ int kcg_class_" << v
-     << "(const kcg_i64* p) {\n";
-  os << "  if ((";
+// parameter range class: 0 negative (inadmissible), 1 fast, 2 wide, 3 overflow
+void emit_classify(std::ostringstream& os, const Lowered& L, int v, const std::vector<int>& pmap) {
+  os << "__device__ __forceinline__ int kcg_class_" << v << "(const kcg_i64* p) {\n  if ((";
   for (int j = 0; j < L.n_params; ++j) os << (j ? " | " : "") << "p[" << pmap[j] << "]";
   if (L.n_params == 0) os << "0ll";
   os << ") < 0) return 0;\n";
-  if (L.b64 >= 0) {
+  for (int pass = 0; pass < 2; ++pass) {
+    const int64_t b = pass == 0 ? L.b64 : L.b128;
+    if (b < 0) continue;
     os << "  if (";
-    for (int j = 0; j < L.n_params; ++j)
-      os << (j ? " && " : "") << "p[" << pmap[j] << "] <= " << L.b64 << "ll";
+    for (int j = 0; j < L.n_params; ++j) os << (j ? " && " : "") << "p[" << pmap[j] << "] <= " << b << "ll";
     if (L.n_params == 0) os << "true";
-    os << ") return 1;\n";
-  }
-  if (L.b128 >= 0) {
-    os << "  if (";
-    for (int j = 0; j < L.n_params; ++j)
-      os << (j ? " && " : "") << "p[" << pmap[j] << "] <= " << L.b128 << "ll";
-    if (L.n_params == 0) os << "true";
-    os << ") return 2;\n";
+    os << ") return " << (pass + 1) << ";\n";
   }
   os << "  return 3;\n}\n\n";
 }
 
-void emit_gather(std::ostringstream& os, int v, const Lowered& L,
-                 const std::vector<int>& pmap) {
-  // variant parameter vector in its own declaration order
-  os << "    kcg_i64 q" << v << "[" << (L.n_params ? L.n_params : 1) << "];\n";
+// gather program v's parameters (its declaration order) from the launch's columns
+void emit_gather(std::ostringstream& os, const char* dst, const char* src, const Lowered& L,
+                 const std::vector<int>& pmap, const char* indent) {
+  os << indent << "kcg_i64 " << dst << "[" << (L.n_params ? L.n_params : 1) << "];\n";
   for (int j = 0; j < L.n_params; ++j)
-    os << "    q" << v << "[" << j << "] = p[" << pmap[j] << "];\n";
+    os << indent << dst << "[" << j << "] = " << src << "[" << pmap[j] << "];\n";
+}
+
+// point evaluator for the eval kernel: status + prediction (+ counts).
+// GEN = 0: every compact weight is finite, so skipping zero counts
+//          (model.cpp:106-111) or zero weights (simdevice.cpp:84-88) cannot
+//          change the sum (adding +-0.0 to a sum that starts at +0.0 is an
+//          identity) and the accumulation is unconditional.
+// GEN = 1: general case, the skip rule is applied per key.
+void emit_eval_point(std::ostringstream& os, const Lowered& L) {
+  const int F = static_cast<int>(L.keys.size());
+  const int FA = F > 0 ? F : 1;
+  os << "struct KcgRes { double s; int st; };\n";
+  // out-of-line wide path: reloads its parameters, writes counts
+  os << "__device__ __noinline__ KcgRes kcg_point_slow(const KcgArgs& a, kcg_i64 i) {\n"
+        "  kcg_i64 p["
+     << (L.n_params ? L.n_params : 1) << "];\n";
+  for (int j = 0; j < L.n_params; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
+  os << "  KcgRes r; r.s = kcg_nan();\n"
+        "  const int cls = kcg_class_0(p);\n"
+        "  if (cls != 2) { r.st = cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW; return r; }\n"
+        "  kcg_i128 c["
+     << FA << "];\n  r.st = kcg_wide_0(p, c);\n  if (r.st != KCG_PT_OK) return r;\n  double s = 0.0;\n";
+  for (int j = 0; j < F; ++j) os << "  s = kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim);\n";
+  os << "  r.s = s;\n  if (a.clo) {\n";
+  for (int j = 0; j < F; ++j)
+    os << "    a.clo[(kcg_i64)" << j << " * a.n + i] = (kcg_i64)c[" << j << "];\n"
+       << "    if (a.chi) a.chi[(kcg_i64)" << j << " * a.n + i] = kcg_hi64(c[" << j
+       << "]); else if (!kcg_fits_i64(c[" << j << "])) r.st = KCG_PT_COUNT_WIDE;\n";
+  os << "  }\n  return r;\n}\n";
+  // fast path only; returns -1 when the point needs kcg_point_slow
+  os << "template <int GEN>\n__device__ __forceinline__ int kcg_point_fast(const kcg_i64* p, const KcgArgs& a, kcg_i64 i, double& out) {\n"
+        "  if (kcg_class_0(p) != 1) return -1;\n"
+        "  kcg_i64 c["
+     << FA << "];\n  const int st = kcg_fast_0(p, c);\n  if (st != KCG_PT_OK) return st;\n"
+              "  double s = 0.0;\n";
+  for (int j = 0; j < F; ++j)
+    os << "  s = GEN ? kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim) : "
+       << "__dadd_rn(s, __dmul_rn(a.alpha[" << j << "], kcg_to_double(c[" << j << "])));\n";
+  os << "  out = s;\n  if (a.clo) {\n";
+  for (int j = 0; j < F; ++j) {
+    os << "    __stcs(a.clo + (kcg_i64)" << j << " * a.n + i, c[" << j << "]);\n";
+    os << "    if (a.chi) __stcs(a.chi + (kcg_i64)" << j << " * a.n + i, kcg_hi64(c[" << j << "]));\n";
+  }
+  os << "  }\n  return KCG_PT_OK;\n}\n";
+}
+
+int min_blocks() {
+  // occupancy target of the eval kernels (blocks of 256 per SM); the
+  // register cap it implies is the main tuning knob (KCG_MIN_BLOCKS)
+  const char* e = std::getenv("KCG_MIN_BLOCKS");
+  const int v = e ? std::atoi(e) : 3;
+  return v >= 1 && v <= 8 ? v : 3;
+}
+
+void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& name, int gen) {
+  const int NP = n_cols > 0 ? n_cols : 1;
+  os << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks() << ") " << name
+     << "(const __grid_constant__ KcgArgs a) {\n"
+        "  const kcg_i64 tid = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x;\n"
+        "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
+        "  kcg_i64 done = 0;\n"
+        "  if (a.vec) {\n"
+        "    // 4 consecutive points per thread: two 16-byte loads per column,\n"
+        "    // two 16-byte streaming stores of predictions, one 4-byte status store\n"
+        "    const kcg_i64 nv = a.n >> 2;\n"
+        "    for (kcg_i64 v = tid; v < nv; v += stride) {\n"
+        "      kcg_i64 q[4]["
+     << NP << "];\n";
+  for (int j = 0; j < n_cols; ++j)
+    os << "      { const longlong2 x = __ldcs(reinterpret_cast<const longlong2*>(a.p[" << j
+       << "]) + 2 * v); const longlong2 y = __ldcs(reinterpret_cast<const longlong2*>(a.p[" << j
+       << "]) + 2 * v + 1);\n"
+          "        q[0]["
+       << j << "] = x.x; q[1][" << j << "] = x.y; q[2][" << j << "] = y.x; q[3][" << j << "] = y.y; }\n";
+  os << "      double s[4]; int st[4];\n"
+        "      #pragma unroll\n"
+        "      for (int u = 0; u < 4; ++u) { s[u] = kcg_nan(); st[u] = kcg_point_fast<"
+     << gen << ">(q[u], a, 4 * v + u, s[u]); }\n"
+               "      if ((st[0] | st[1] | st[2] | st[3]) < 0) {\n"
+               "        #pragma unroll\n"
+               "        for (int u = 0; u < 4; ++u)\n"
+               "          if (st[u] < 0) { const KcgRes r = kcg_point_slow(a, 4 * v + u); s[u] = r.s; st[u] = r.st; }\n"
+               "      }\n"
+               "      #pragma unroll\n"
+               "      for (int u = 0; u < 4; ++u)\n"
+               "        if (st[u] != KCG_PT_OK && st[u] != KCG_PT_COUNT_WIDE) s[u] = kcg_nan();\n"
+               "      if (a.pred) {\n"
+               "        __stcs(reinterpret_cast<double2*>(a.pred) + 2 * v, make_double2(s[0], s[1]));\n"
+               "        __stcs(reinterpret_cast<double2*>(a.pred) + 2 * v + 1, make_double2(s[2], s[3]));\n"
+               "      }\n"
+               "      if (a.status) reinterpret_cast<unsigned*>(a.status)[v] =\n"
+               "          (unsigned)st[0] | ((unsigned)st[1] << 8) | ((unsigned)st[2] << 16) | ((unsigned)st[3] << 24);\n"
+               "    }\n"
+               "    done = nv << 2;\n"
+               "  }\n"
+               "  for (kcg_i64 i = done + tid; i < a.n; i += stride) {\n"
+               "    kcg_i64 p["
+     << NP << "];\n";
+  for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
+  os << "    double s = kcg_nan();\n    int st = kcg_point_fast<" << gen
+     << ">(p, a, i, s);\n"
+        "    if (st < 0) { const KcgRes r = kcg_point_slow(a, i); s = r.s; st = r.st; }\n"
+        "    if (st != KCG_PT_OK && st != KCG_PT_COUNT_WIDE) s = kcg_nan();\n"
+        "    if (a.pred) __stcs(a.pred + i, s);\n"
+        "    if (a.status) a.status[i] = (unsigned char)st;\n"
+        "  }\n}\n";
 }
 
 }  // namespace
 
 std::string codegen(const std::vector<const Lowered*>& progs,
-                    const std::vector<std::vector<int>>& pmaps, int n_cols,
-                    JitKind kind, const std::string& name) {
+                    const std::vector<std::vector<int>>& pmaps, int n_cols, JitKind kind,
+                    const std::string& name) {
   std::ostringstream os;
   os << "// generated by kcg codegen\n" << kDeviceHelpers << "\n";
   for (size_t v = 0; v < progs.size(); ++v) {
-    emit_body(os, *progs[v], static_cast<int>(v));
+    emit_body(os, *progs[v], static_cast<int>(v), true);
+    emit_body(os, *progs[v], static_cast<int>(v), false);
     emit_classify(os, *progs[v], static_cast<int>(v), pmaps[v]);
   }
   const int NP = n_cols > 0 ? n_cols : 1;
@@ -192,50 +336,44 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     const int F = static_cast<int>(L.keys.size());
     const int FA = F > 0 ? F : 1;
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; double* pred; "
-          "unsigned char* status; kcg_i64* clo; kcg_i64* chi; kcg_i64 n; int sim; "
+          "unsigned char* status; kcg_i64* clo; kcg_i64* chi; kcg_i64 n; int sim; int vec; "
           "double alpha["
        << FA << "]; };\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(256) " << name
-       << "(const __grid_constant__ KcgArgs a) {\n"
-          "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
-          "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {\n"
-          "    kcg_i64 p["
-       << NP << "];\n";
-    for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
-    os << "    int st; double s = 0.0;\n"
-          "    const int cls = kcg_class_0(p);\n"
-          "    if (cls == 0) { st = KCG_PT_ASSUMPTION_VIOLATED; }\n"
-          "    else if (cls == 1) {\n"
-          "      kcg_i64 c["
-       << FA << "];\n      st = kcg_body_0<kcg_i64>(p, c);\n"
-          "      if (st == KCG_PT_OK) {\n";
-    for (int j = 0; j < F; ++j) os << "        s = kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim);\n";
-    os << "        if (a.clo) {\n";
-    for (int j = 0; j < F; ++j) os << "          __stcs(a.clo + (kcg_i64)" << j << " * a.n + i, c[" << j << "]);\n";
-    os << "          if (a.chi) {\n";
-    for (int j = 0; j < F; ++j) os << "            __stcs(a.chi + (kcg_i64)" << j << " * a.n + i, kcg_hi64(c[" << j << "]));\n";
-    os << "          }\n        }\n      }\n    } else if (cls == 2) {\n"
-          "      kcg_i128 c["
-       << FA << "];\n      st = kcg_body_0<kcg_i128>(p, c);\n"
-          "      if (st == KCG_PT_OK) {\n";
-    for (int j = 0; j < F; ++j) os << "        s = kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim);\n";
-    os << "        if (a.clo) {\n";
-    for (int j = 0; j < F; ++j) {
-      os << "          a.clo[(kcg_i64)" << j << " * a.n + i] = (kcg_i64)c[" << j << "];\n";
-      os << "          if (a.chi) a.chi[(kcg_i64)" << j << " * a.n + i] = kcg_hi64(c[" << j
-         << "]); else if (!kcg_fits_i64(c[" << j << "])) st = KCG_PT_COUNT_WIDE;\n";
-    }
-    os << "        }\n      }\n    } else { st = KCG_PT_OVERFLOW; }\n"
-          "    if (a.pred) __stcs(a.pred + i, (st == KCG_PT_OK || st == KCG_PT_COUNT_WIDE) ? s : kcg_nan());\n"
-          "    if (a.status) a.status[i] = (unsigned char)st;\n"
-          "  }\n}\n";
+    emit_eval_point(os, L);
+    emit_eval_kernel(os, n_cols, name, 0);
+    emit_eval_kernel(os, n_cols, name + "_gen", 1);
     return os.str();
   }
 
   if (kind == JitKind::argmin) {
     const int V = static_cast<int>(progs.size());
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; int* best; double* best_t; "
-          "double* preds; kcg_i64 n; const double* alpha[" << V << "]; };\n";
+          "double* preds; kcg_i64 n; const double* alpha["
+       << V << "]; };\n";
+    for (int v = 0; v < V; ++v) {
+      const Lowered& L = *progs[v];
+      const int F = static_cast<int>(L.keys.size());
+      const int FA = F > 0 ? F : 1;
+      os << "__device__ __noinline__ int kcg_wide_pred_" << v
+         << "(const kcg_i64* q, const double* __restrict__ al, double* out) {\n  kcg_i128 c[" << FA
+         << "];\n  const int st = kcg_wide_" << v
+         << "(q, c);\n  if (st != KCG_PT_OK) return st;\n  double s = 0.0;\n";
+      for (int j = 0; j < F; ++j) os << "  s = kcg_accum(s, al[" << j << "], c[" << j << "], 0);\n";
+      os << "  *out = s;\n  return KCG_PT_OK;\n}\n";
+      os << "__device__ __forceinline__ int kcg_pred_" << v
+         << "(const kcg_i64* p, const double* __restrict__ al, double* out) {\n"
+            "  const int cls = kcg_class_"
+         << v << "(p);\n";
+      emit_gather(os, "q", "p", L, pmaps[v], "  ");
+      os << "  if (cls == 1) {\n    kcg_i64 c[" << FA << "];\n    const int st = kcg_fast_" << v
+         << "(q, c);\n    if (st != KCG_PT_OK) return st;\n    double s = 0.0;\n";
+      for (int j = 0; j < F; ++j) os << "    s = kcg_accum(s, al[" << j << "], c[" << j << "], 0);\n";
+      os << "    *out = s;\n    return KCG_PT_OK;\n  }\n"
+            "  if (cls == 2) return kcg_wide_pred_"
+         << v
+         << "(q, al, out);\n"
+            "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
+    }
     os << "extern \"C\" __global__ void __launch_bounds__(256) " << name
        << "(const __grid_constant__ KcgArgs a) {\n"
           "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
@@ -245,25 +383,12 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
     os << "    int best = -1; double best_t = __longlong_as_double(0x7ff0000000000000ll);\n";
     for (int v = 0; v < V; ++v) {
-      const Lowered& L = *progs[v];
-      const int F = static_cast<int>(L.keys.size());
-      const int FA = F > 0 ? F : 1;
-      os << "    {\n      double s = 0.0; int st;\n"
-            "      const int cls = kcg_class_"
-         << v << "(p);\n";
-      emit_gather(os, v, L, pmaps[v]);
-      os << "      if (cls == 0) st = KCG_PT_ASSUMPTION_VIOLATED;\n"
-            "      else if (cls == 1) { kcg_i64 c["
-         << FA << "]; st = kcg_body_" << v << "<kcg_i64>(q" << v
-         << ", c); if (st == KCG_PT_OK) {\n";
-      for (int j = 0; j < F; ++j) os << "        s = kcg_accum(s, a.alpha[" << v << "][" << j << "], c[" << j << "], 0);\n";
-      os << "      } }\n      else if (cls == 2) { kcg_i128 c[" << FA << "]; st = kcg_body_" << v
-         << "<kcg_i128>(q" << v << ", c); if (st == KCG_PT_OK) {\n";
-      for (int j = 0; j < F; ++j) os << "        s = kcg_accum(s, a.alpha[" << v << "][" << j << "], c[" << j << "], 0);\n";
-      os << "      } }\n      else st = KCG_PT_OVERFLOW;\n"
+      os << "    {\n      double s = kcg_nan();\n      const int st = kcg_pred_" << v << "(p, a.alpha[" << v
+         << "], &s);\n"
             "      if (st == KCG_PT_OK && s < best_t) { best_t = s; best = "
-         << v << "; }\n"
-                 "      if (a.preds) __stcs(a.preds + (kcg_i64)"
+         << v
+         << "; }\n"
+            "      if (a.preds) __stcs(a.preds + (kcg_i64)"
          << v << " * a.n + i, st == KCG_PT_OK ? s : kcg_nan());\n    }\n";
     }
     os << "    __stcs(a.best + i, best);\n    __stcs(a.best_t + i, best_t);\n  }\n}\n";
@@ -275,19 +400,20 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   const int F = static_cast<int>(L.keys.size());
   const int FA = F > 0 ? F : 1;
   const int NG = F * (F + 1) / 2;
-  os << "template <class T> __device__ __forceinline__ int kcg_row(const kcg_i64* p, double t, double* x) {\n"
-        "  T c["
-     << FA << "];\n  const int st = kcg_body_0<T>(p, c);\n  if (st != KCG_PT_OK) return st;\n";
+  os << "template <class T> __device__ __forceinline__ void kcg_xrow(const T* c, double t, double* x) {\n";
   for (int j = 0; j < F; ++j)
-    os << "  x[" << j << "] = (c[" << j << "] != 0) ? __ddiv_rn(kcg_to_double(c[" << j
-       << "]), t) : 0.0;\n";
-  os << "  return KCG_PT_OK;\n}\n";
+    os << "  x[" << j << "] = (c[" << j << "] != 0) ? __ddiv_rn(kcg_to_double(c[" << j << "]), t) : 0.0;\n";
+  os << "}\n";
+  os << "__device__ __noinline__ int kcg_row_wide(const kcg_i64* p, double t, double* x) {\n"
+        "  kcg_i128 c["
+     << FA << "];\n  const int st = kcg_wide_0(p, c);\n  if (st == KCG_PT_OK) kcg_xrow(c, t, x);\n  return st;\n}\n";
   os << "__device__ __forceinline__ int kcg_row_any(const kcg_i64* p, double t, double* x) {\n"
         "  if (!(t > 0.0)) return KCG_PT_ASSUMPTION_VIOLATED;\n"
         "  const int cls = kcg_class_0(p);\n"
-        "  if (cls == 1) return kcg_row<kcg_i64>(p, t, x);\n"
-        "  if (cls == 2) return kcg_row<kcg_i128>(p, t, x);\n"
-        "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
+        "  if (cls == 1) { kcg_i64 c["
+     << FA << "]; const int st = kcg_fast_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n"
+              "  if (cls == 2) return kcg_row_wide(p, t, x);\n"
+              "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
   if (kind == JitKind::gram) {
     os << "struct KcgArgs { const kcg_i64* p[" << NP
        << "]; const double* t; double* G; double* xt1; double* cmax; "
@@ -295,8 +421,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     os << "extern \"C\" __global__ void __launch_bounds__(256) " << name
        << "(const __grid_constant__ KcgArgs a) {\n"
           "  double g["
-       << (NG ? NG : 1) << "], s1[" << FA << "], mx[" << FA << "];\n"
-          "  #pragma unroll\n  for (int k = 0; k < "
+       << (NG ? NG : 1) << "], s1[" << FA << "], mx[" << FA << "];\n  #pragma unroll\n  for (int k = 0; k < "
        << NG << "; ++k) g[k] = 0.0;\n  #pragma unroll\n  for (int k = 0; k < " << F
        << "; ++k) { s1[k] = 0.0; mx[k] = 0.0; }\n"
           "  unsigned long long bad = 0;\n"
@@ -309,13 +434,12 @@ std::string codegen(const std::vector<const Lowered*>& progs,
           "    if (kcg_row_any(p, __ldcs(a.t + i), x) != KCG_PT_OK) { ++bad; continue; }\n";
     int k = 0;
     for (int r = 0; r < F; ++r) {
-      os << "    s1[" << r << "] += x[" << r << "]; mx[" << r << "] = fmax(mx[" << r
-         << "], fabs(x[" << r << "]));\n";
+      os << "    s1[" << r << "] += x[" << r << "]; mx[" << r << "] = fmax(mx[" << r << "], fabs(x[" << r
+         << "]));\n";
       for (int c = r; c < F; ++c, ++k)
         os << "    g[" << k << "] = fma(x[" << r << "], x[" << c << "], g[" << k << "]);\n";
     }
     os << "  }\n"
-          "  // warp reduce, then one atomic per warp and value\n"
           "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) {\n"
           "    #pragma unroll\n    for (int k = 0; k < "
        << NG << "; ++k) g[k] += __shfl_down_sync(0xffffffffu, g[k], o);\n"
@@ -327,7 +451,8 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     k = 0;
     for (int r = 0; r < F; ++r) {
       os << "    atomicAdd(a.xt1 + " << r << ", s1[" << r << "]);\n";
-      os << "    atomicMax((unsigned long long*)(a.cmax + " << r << "), (unsigned long long)__double_as_longlong(mx[" << r << "]));\n";
+      os << "    atomicMax((unsigned long long*)(a.cmax + " << r
+         << "), (unsigned long long)__double_as_longlong(mx[" << r << "]));\n";
       for (int c = r; c < F; ++c, ++k) {
         os << "    atomicAdd(a.G + " << (r * F + c) << ", g[" << k << "]);\n";
         if (c != r) os << "    atomicAdd(a.G + " << (c * F + r) << ", g[" << k << "]);\n";
@@ -338,8 +463,8 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   }
 
   // residual: obj += (1 - x . alpha)^2
-  os << "struct KcgArgs { const kcg_i64* p[" << NP
-     << "]; const double* t; double* obj; kcg_i64 n; double alpha[" << FA << "]; };\n";
+  os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* obj; kcg_i64 n; double alpha["
+     << FA << "]; };\n";
   os << "extern \"C\" __global__ void __launch_bounds__(256) " << name
      << "(const __grid_constant__ KcgArgs a) {\n"
         "  double acc = 0.0;\n"

@@ -23,7 +23,8 @@ namespace kcg {
 namespace {
 
 std::mutex g_mu;
-std::unordered_map<std::string, void*> g_kernels;  // key: name + source hash
+std::unordered_map<std::string, void*> g_kernels;  // key: source hash + name
+std::unordered_map<std::string, cudaLibrary_t> g_libs;  // key: source hash
 
 uint64_t fnv1a64(const std::string& s) {
   uint64_t h = 1469598103934665603ull;
@@ -76,33 +77,39 @@ void* jit_kernel(const std::string& src, const std::string& name) {
   char hex[32];
   std::snprintf(hex, sizeof hex, "%016llx",
                 static_cast<unsigned long long>(fnv1a64(src)));
-  const std::string key = name + "_" + hex;
+  const std::string key = std::string(hex) + ":" + name;
   std::lock_guard<std::mutex> lock(g_mu);
   auto it = g_kernels.find(key);
   if (it != g_kernels.end()) return it->second;
 
-  const std::string dir = cache_dir();
-  const std::string path = dir + "/" + key + ".cubin";
-  std::vector<char> cubin;
-  if (!read_file(path, cubin)) {
-    cubin = compile(src, name);
-    mkdir(dir.c_str(), 0777);
-    const std::string tmp = path + ".tmp." + std::to_string(getpid());
-    {
-      std::ofstream out(tmp, std::ios::binary);
-      out.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
-    }
-    std::rename(tmp.c_str(), path.c_str());
-  }
   cudaLibrary_t lib;
-  cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0,
-                                      nullptr, nullptr, 0);
-  if (e != cudaSuccess)
-    throw KcgError(KCG_E_CUDA, std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e));
+  auto lit = g_libs.find(hex);
+  if (lit != g_libs.end()) {
+    lib = lit->second;
+  } else {
+    const std::string dir = cache_dir();
+    const std::string path = dir + "/kcg_" + hex + ".cubin";
+    std::vector<char> cubin;
+    if (!read_file(path, cubin)) {
+      cubin = compile(src, name);
+      mkdir(dir.c_str(), 0777);
+      const std::string tmp = path + ".tmp." + std::to_string(getpid());
+      {
+        std::ofstream out(tmp, std::ios::binary);
+        out.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
+      }
+      std::rename(tmp.c_str(), path.c_str());
+    }
+    const cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0,
+                                              nullptr, nullptr, 0);
+    if (e != cudaSuccess)
+      throw KcgError(KCG_E_CUDA, std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e));
+    g_libs.emplace(hex, lib);
+  }
   cudaKernel_t k;
-  e = cudaLibraryGetKernel(&k, lib, name.c_str());
+  const cudaError_t e = cudaLibraryGetKernel(&k, lib, name.c_str());
   if (e != cudaSuccess)
-    throw KcgError(KCG_E_CUDA, std::string("cudaLibraryGetKernel: ") + cudaGetErrorString(e));
+    throw KcgError(KCG_E_CUDA, std::string("cudaLibraryGetKernel(") + name + "): " + cudaGetErrorString(e));
   g_kernels.emplace(key, reinterpret_cast<void*>(k));
   return reinterpret_cast<void*>(k);
 }

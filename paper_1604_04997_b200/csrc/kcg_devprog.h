@@ -42,4 +42,5 @@ struct KcgDevProg {
   int32_t cons_div[KCG_MAX_CONS], cons_op[KCG_MAX_CONS], cons_expr[KCG_MAX_CONS];
   KcgWide cons_mod[KCG_MAX_CONS], cons_rem[KCG_MAX_CONS];
   int32_t key_schema[KCG_MAX_KEYS], key_expr[KCG_MAX_KEYS];
+  KcgWide quot_mod[KCG_MAX_PARAMS], quot_rem[KCG_MAX_PARAMS];
 };

@@ -57,7 +57,7 @@ struct Q {
 // ---------------------------------------------------------------------------
 // Symbolic layer (parsed text)
 
-enum class AtomKind : int { var = 0, floordiv = 1, min = 2, max = 3 };
+enum class AtomKind : int { var = 0, floordiv = 1, min = 2, max = 3, quot = 4 };
 
 struct Mono {
   std::vector<std::pair<int, int>> f;  // (atom id, exponent), sorted by atom id
@@ -73,6 +73,7 @@ struct AtomDef {
   int num = -1;            // floordiv numerator poly id
   i128 den = 1;            // floordiv denominator (> 0)
   std::vector<int> args;   // min/max argument poly ids
+  i128 qmod = 1, qrem = 0; // quot: (param - qrem) / qmod
   std::string key;         // canonical text (identity)
 };
 
@@ -83,6 +84,7 @@ struct Constraint {
   CmpOp op = CmpOp::eq;
   int poly = -1;       // relational: lhs - rhs; divisibility: lhs
   i128 mod = 0, rem = 0;
+  bool absorbed = false;  // folded into a quot atom's exactness check
   std::string text;
 };
 
@@ -106,7 +108,8 @@ enum OpCode : int32_t {
   OP_EXPR = 2,      // expr[dst] = sum terms[a..b)
   OP_FLOORDIV = 3,  // atom[dst] = floor(expr[a] / big[c])
   OP_MIN = 4,       // atom[dst] = min over args[a..b) of expr*scale
-  OP_MAX = 5
+  OP_MAX = 5,
+  OP_QUOT = 6       // atom[dst] = floor((param[a] - quot_rem[c]) / quot_mod[c])
 };
 
 struct LOp {
@@ -129,7 +132,9 @@ struct LArg {
 };
 
 struct LCons {
-  int32_t divisibility, op, expr;
+  int32_t divisibility;  // 0 relational, 1 divisibility, 2 quot exactness
+  int32_t op;            // relational: CmpOp; quot: parameter index
+  int32_t expr;          // relational/divisibility: expr; quot: atom id
   i128 mod, rem;
 };
 
@@ -148,6 +153,7 @@ struct Lowered {
   std::vector<LCons> cons;
   std::vector<LKey> keys;          // schema order
   std::vector<i128> atom_den;      // value = numerator / atom_den
+  std::vector<i128> quot_mod, quot_rem;  // per OP_QUOT (index in op.c)
   int64_t b64 = 0, b128 = 0;       // safe uniform parameter bounds
 };
 

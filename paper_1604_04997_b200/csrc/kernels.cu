@@ -67,6 +67,10 @@ __device__ __noinline__ int interp_body(const KcgDevProg* __restrict__ P,
       case 3:
         atom[op.dst] = kcg_floordiv<T>(expr[op.a], wide<T>(P->fd_den[op.c]));
         break;
+      case 6:
+        atom[op.dst] = kcg_floordiv<T>((T)p[op.a] - wide<T>(P->quot_rem[op.c]),
+                                       wide<T>(P->quot_mod[op.c]));
+        break;
       default: {
         T best = expr[P->arg_expr[op.a]] * wide<T>(P->arg_scale[op.a]);
         for (int i = op.a + 1; i < op.b; ++i) {
@@ -79,6 +83,12 @@ __device__ __noinline__ int interp_body(const KcgDevProg* __restrict__ P,
     }
   }
   for (int c = 0; c < P->n_cons; ++c) {
+    if (P->cons_div[c] == 2) {  // p == M * quot + R
+      const T q = atom[P->cons_expr[c]];
+      if ((T)p[P->cons_op[c]] - wide<T>(P->cons_rem[c]) != wide<T>(P->cons_mod[c]) * q)
+        return KCG_PT_ASSUMPTION_VIOLATED;
+      continue;
+    }
     const T e = expr[P->cons_expr[c]];
     if (!P->cons_div[c]) {
       bool ok;

@@ -568,9 +568,127 @@ Symbolic parse_program_text(const std::string& text) {
 }
 
 // ---------------------------------------------------------------------------
+// Congruence substitution
+//
+// A parameter with divisibility facts p % m_i == r_i (AssumeCtx::add_constraint
+// distils the same facts, decide.cpp:33-45) satisfies p = M*q + R at every
+// admissible binding, with (M, R) their CRT combination. Substituting that
+// into every property polynomial is an exact identity on the admissible set
+// and typically clears all denominators (9/8 l m n with l,m,n = 16 q_*
+// becomes 4608 q_l q_m q_n), so the GPU evaluates the counts with no
+// division at all. Constraints keep the original parameters; inadmissible
+// points are rejected before any count is formed.
+
+namespace {
+
+bool ext_crt(i128 m1, i128 r1, i128 m2, i128 r2, i128& M, i128& R) {
+  // x = r1 (m1), x = r2 (m2)
+  i128 a = m1, b = m2, x0 = 1, x1 = 0;
+  while (b) {
+    const i128 q = a / b;
+    i128 t = a - q * b; a = b; b = t;
+    t = x0 - q * x1; x0 = x1; x1 = t;
+  }
+  const i128 g = a;  // m1 * x0 = g (mod m2)
+  if ((r2 - r1) % g != 0) return false;
+  const i128 m2g = m2 / g;
+  i128 k = ((r2 - r1) / g) % m2g;
+  k = (k * (x0 % m2g)) % m2g;
+  if (k < 0) k += m2g;
+  M = checked_mul(m1 / g, m2);
+  R = ((r1 + checked_mul(m1, k)) % M + M) % M;
+  return true;
+}
+
+Poly poly_subst_atom(const Poly& p, int atom, const Poly& repl) {
+  Poly out;
+  for (const auto& [m, c] : p) {
+    Poly term = poly_const(c);
+    Mono rest;
+    int e_sub = 0;
+    for (const auto& [a, e] : m.f) {
+      if (a == atom)
+        e_sub = e;
+      else
+        rest.f.push_back({a, e});
+    }
+    Poly restp;
+    restp.emplace(rest, Q(1));
+    term = poly_mul(term, restp);
+    for (int k = 0; k < e_sub; ++k) term = poly_mul(term, repl);
+    out = poly_add(out, term);
+  }
+  return out;
+}
+
+Symbolic substitute_congruences(const Symbolic& in) {
+  Symbolic s = in;
+  const int np = static_cast<int>(s.params.size());
+  std::vector<i128> M(np, 1), R(np, 0);
+  std::vector<bool> ok(np, true);
+  std::vector<std::vector<size_t>> used(np);
+  for (size_t ci = 0; ci < s.cons.size(); ++ci) {
+    const Constraint& c = s.cons[ci];
+    if (!c.divisibility) continue;
+    const Poly& p = s.polys[c.poly];
+    int var_atom = -1;
+    i128 k = 0;
+    bool shape = true;
+    for (const auto& [m, q] : p) {
+      if (!q.is_int()) { shape = false; break; }
+      if (m.f.empty()) { k = q.n; continue; }
+      if (m.f.size() != 1 || m.f[0].second != 1 || q.n != 1 ||
+          s.atoms[m.f[0].first].kind != AtomKind::var || var_atom >= 0) {
+        shape = false;
+        break;
+      }
+      var_atom = m.f[0].first;
+    }
+    if (!shape || var_atom < 0) continue;
+    const int par = s.atoms[var_atom].param;
+    const i128 r = ((c.rem - k) % c.mod + c.mod) % c.mod;
+    i128 nm, nr;
+    if (!ext_crt(M[par], R[par], c.mod, r, nm, nr)) {
+      ok[par] = false;  // never admissible; leave the checks to reject it
+      continue;
+    }
+    M[par] = nm;
+    R[par] = nr;
+    used[par].push_back(ci);
+  }
+  for (int par = 0; par < np; ++par) {
+    if (!ok[par] || M[par] <= 1) continue;
+    int var_atom = -1;
+    for (size_t a = 0; a < s.atoms.size(); ++a)
+      if (s.atoms[a].kind == AtomKind::var && s.atoms[a].param == par) var_atom = static_cast<int>(a);
+    if (var_atom < 0) continue;
+    AtomDef q;
+    q.kind = AtomKind::quot;
+    q.param = par;
+    q.qmod = M[par];
+    q.qrem = R[par];
+    q.key = "(quot " + s.params[par] + " " + i128_str(M[par]) + " " + i128_str(R[par]) + ")";
+    const int qid = static_cast<int>(s.atoms.size());
+    s.atoms.push_back(q);
+    for (size_t ci : used[par]) s.cons[ci].absorbed = true;
+    Poly repl;
+    repl.emplace(Mono{{{qid, 1}}}, Q(M[par]));
+    if (R[par] != 0) repl.emplace(Mono{}, Q(R[par]));
+    std::vector<bool> is_cons(s.polys.size(), false);
+    for (const Constraint& c : s.cons) is_cons[c.poly] = true;
+    for (size_t i = 0; i < s.polys.size(); ++i)
+      if (!is_cons[i]) s.polys[i] = poly_subst_atom(s.polys[i], var_atom, repl);
+  }
+  return s;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
 // Lowering
 
-Lowered lower(const Symbolic& s) {
+Lowered lower(const Symbolic& s_in) {
+  const Symbolic s = substitute_congruences(s_in);
   Lowered L;
   L.n_params = static_cast<int>(s.params.size());
   L.n_atoms = static_cast<int>(s.atoms.size());
@@ -608,6 +726,12 @@ Lowered lower(const Symbolic& s) {
       case AtomKind::var:
         L.atom_den[a] = 1;
         L.ops.push_back({OP_VAR, a, ad.param, 0, 0});
+        break;
+      case AtomKind::quot:
+        L.atom_den[a] = 1;
+        L.quot_mod.push_back(ad.qmod);
+        L.quot_rem.push_back(ad.qrem);
+        L.ops.push_back({OP_QUOT, a, ad.param, 0, static_cast<int32_t>(L.quot_mod.size() - 1)});
         break;
       case AtomKind::floordiv: {
         const int e = visit_poly(ad.num);
@@ -665,7 +789,13 @@ Lowered lower(const Symbolic& s) {
     return id;
   };
 
+  for (size_t a = 0; a < s.atoms.size(); ++a) {
+    if (s.atoms[a].kind != AtomKind::quot) continue;
+    visit_atom(static_cast<int>(a));
+    L.cons.push_back({2, s.atoms[a].param, static_cast<int32_t>(a), s.atoms[a].qmod, s.atoms[a].qrem});
+  }
   for (const auto& c : s.cons) {
+    if (c.absorbed) continue;
     const int e = visit_poly(c.poly);
     L.cons.push_back({c.divisibility ? 1 : 0, static_cast<int32_t>(c.op), e, c.mod, c.rem});
   }
@@ -732,6 +862,10 @@ long double max_intermediate(const Lowered& L, long double B) {
         expr[op.dst] = sum;
         break;
       }
+      case OP_QUOT:
+        atom[op.dst] = (B + absq(L.quot_rem[op.c])) / absq(L.quot_mod[op.c]) + 1;
+        see(B + absq(L.quot_rem[op.c]));
+        break;
       case OP_FLOORDIV:
         atom[op.dst] = expr[op.a] / absq(L.floordiv_den[op.c]) + 1;
         see(absq(L.floordiv_den[op.c]));
