@@ -34,6 +34,7 @@ struct kcg_program {
   std::string jit_src;
   void* jit_eval = nullptr;
   void* jit_eval_gen = nullptr;
+  void* jit_eval_tma = nullptr;
   void* jit_gram = nullptr;
   void* jit_resid = nullptr;
 };
@@ -357,6 +358,7 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
       const std::string nm = kname("kcg_eval_", p);
       p->jit_eval = kcg::jit_kernel(kcg_program_jit_source(p), nm);
       p->jit_eval_gen = kcg::jit_kernel(kcg_program_jit_source(p), nm + "_gen");
+      p->jit_eval_tma = kcg::jit_kernel(kcg_program_jit_source(p), nm + "_tma");
     }
     ArgBuf ab;
     for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
@@ -377,8 +379,17 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
     // finite weights: the skip rules cannot change the sum (GEN = 0 kernel)
     bool finite = true;
     for (double v : al) finite = finite && std::isfinite(v);
-    kcg::launch_jit(finite ? p->jit_eval : p->jit_eval_gen, ab.b.data(), ab.b.size(),
-                    grid_for((n + 3) / 4), 256, stream);
+    static const bool no_tma = std::getenv("KCG_NO_TMA") != nullptr;
+    const size_t tiles = n / kcg::kTmaPointsPerTile;
+    if (finite && vec && !no_tma && tiles >= static_cast<size_t>(kcg::num_sms())) {
+      // TMA-staged persistent kernel: 2 CTAs per SM
+      const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, kcg::num_sms() * 2));
+      kcg::launch_jit(p->jit_eval_tma, ab.b.data(), ab.b.size(), grid, 256, stream,
+                      kcg::tma_smem_bytes(np));
+    } else {
+      kcg::launch_jit(finite ? p->jit_eval : p->jit_eval_gen, ab.b.data(), ab.b.size(),
+                      grid_for((n + 3) / 4), 256, stream);
+    }
     ++g_launches;
     return KCG_OK;
   });
@@ -424,6 +435,9 @@ int kcg_argmin(const kcg_program* const* progs, int V, const int64_t* const* par
       compact_alpha(progs[v], alpha, host.data() + o);
       o += std::max<size_t>(1, progs[v]->low.keys.size());
     }
+    for (double a : host)
+      if (!std::isfinite(a))
+        throw KcgError(KCG_E_INVALID_ARGUMENT, "argmin requires finite weights");
     // cache the device weights per (variant set, alpha) -- small, reused
     static std::mutex mu;
     static std::vector<std::pair<std::vector<double>, double*>> cache;

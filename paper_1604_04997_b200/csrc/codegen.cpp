@@ -14,6 +14,7 @@
 // The kernels around them: fused evaluate+predict (4 points per thread,
 // 16-byte vector loads/stores), argmin over variants, and the fused
 // design-row Gram / residual reductions.
+#include <cmath>
 #include <cstdlib>
 #include <sstream>
 
@@ -186,9 +187,182 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast) {
   os << "  return KCG_PT_OK;\n}\n\n";
 }
 
+// Fast path (every parameter in [0, b64]), branch-free: admissibility and
+// integrality are folded into flags, the status is selected at the end.
+//   dbl = false: kcg_fasti_<v> writes the exact int64 counts;
+//   dbl = true : kcg_fastd_<v> writes RN(double(count)) only (predict). A key
+//                that is one monomial times a constant C with |C| and the
+//                monomial's bound below 2^53 gets C (x) double(mono): both
+//                factors are exact doubles, so the single rounding of their
+//                product equals RN(C * mono) -- no 64-bit constant multiply.
+void emit_fast(std::ostringstream& os, const Lowered& L, int v, bool dbl) {
+  const bool small = L.b64 >= 0 && L.b64 <= kU32;
+  const long double two53 = std::ldexp(1.0L, 53);
+  std::vector<bool> atom_u32(L.n_atoms, false);
+  os << "__device__ __forceinline__ int kcg_fast" << (dbl ? "d_" : "i_") << v
+     << "(const kcg_i64* __restrict__ p, " << (dbl ? "double" : "kcg_i64")
+     << "* __restrict__ cnt) {\n  typedef kcg_i64 T;\n  bool ok = true, integral = true;\n";
+  // which exprs are needed as integers
+  std::vector<bool> need_expr(L.n_exprs, false), need_mono_d(L.n_monos, false);
+  std::vector<int> key_fast(L.keys.size(), -1);  // mono id for the DMUL trick
+  for (size_t j = 0; j < L.keys.size(); ++j) {
+    const LExpr& ex = L.exprs[L.keys[j].expr];
+    bool trick = dbl && ex.D == 1 && ex.term_end - ex.term_begin == 1;
+    if (trick) {
+      const LTerm& t = L.terms[ex.term_begin];
+      const i128 ac = t.coef < 0 ? -t.coef : t.coef;
+      trick = t.mono >= 0 && static_cast<long double>(ac) < two53 &&
+              t.mono < static_cast<int>(L.mono_bound64.size()) && L.mono_bound64[t.mono] < two53;
+      if (trick) {
+        key_fast[j] = t.mono;
+        need_mono_d[t.mono] = true;
+      }
+    }
+    if (!trick) need_expr[L.keys[j].expr] = true;
+  }
+  for (const LCons& c : L.cons)
+    if (c.divisibility != 2) need_expr[c.expr] = true;
+  for (const LOp& op : L.ops)
+    if (op.code == OP_FLOORDIV) need_expr[op.a] = true;
+    else if (op.code == OP_MIN || op.code == OP_MAX)
+      for (int i = op.a; i < op.b; ++i) need_expr[L.args[i].expr] = true;
+  for (const LOp& op : L.ops) {
+    switch (op.code) {
+      case OP_VAR:
+        if (small) {
+          os << "  const unsigned u" << op.dst << " = (unsigned)p[" << op.a << "];\n";
+          atom_u32[op.dst] = true;
+        }
+        os << "  const T a" << op.dst << " = (T)p[" << op.a << "];\n";
+        break;
+      case OP_QUOT: {
+        const i128 M = L.quot_mod[op.c], R = L.quot_rem[op.c];
+        if (small && M <= kU32) {
+          os << "  const unsigned u" << op.dst << " = ((unsigned)p[" << op.a << "] - "
+             << static_cast<uint64_t>(R) << "u) / " << static_cast<uint64_t>(M) << "u;\n";
+          os << "  const T a" << op.dst << " = (T)u" << op.dst << ";\n";
+          atom_u32[op.dst] = true;
+        } else {
+          os << "  const T a" << op.dst << " = kcg_floordiv<T>((T)p[" << op.a << "] - " << lit(R)
+             << ", " << lit(M) << ");\n";
+        }
+        break;
+      }
+      case OP_MONO: {
+        std::vector<int> f;
+        for (int i = op.a; i < op.b; ++i)
+          for (int k = 0; k < L.factors[i].second; ++k) f.push_back(L.factors[i].first);
+        os << "  const T m" << op.dst << " = ";
+        size_t start;
+        if (f.size() >= 2 && atom_u32[f[0]] && atom_u32[f[1]]) {
+          os << "(T)((kcg_u64)u" << f[0] << " * u" << f[1] << ")";
+          start = 2;
+        } else {
+          os << "a" << f[0];
+          start = 1;
+        }
+        for (size_t k = start; k < f.size(); ++k) os << " * a" << f[k];
+        os << ";\n";
+        if (need_mono_d[op.dst]) os << "  const double dm" << op.dst << " = __ll2double_rn(m" << op.dst << ");\n";
+        break;
+      }
+      case OP_EXPR: {
+        if (!need_expr[op.dst]) break;
+        os << "  const T e" << op.dst << " = ";
+        if (op.a == op.b) os << "(T)0";
+        for (int i = op.a; i < op.b; ++i) {
+          const LTerm& t = L.terms[i];
+          if (i != op.a) os << " + ";
+          if (t.mono < 0)
+            os << lit(t.coef);
+          else if (t.coef == 1)
+            os << "m" << t.mono;
+          else if (t.coef == -1)
+            os << "(-m" << t.mono << ")";
+          else
+            os << lit(t.coef) << " * m" << t.mono;
+        }
+        os << ";\n";
+        break;
+      }
+      case OP_FLOORDIV:
+        os << "  const T a" << op.dst << " = kcg_floordiv<T>(e" << op.a << ", "
+           << lit(L.floordiv_den[op.c]) << ");\n";
+        break;
+      case OP_MIN:
+      case OP_MAX: {
+        os << "  T a" << op.dst << ";\n  {\n";
+        for (int i = op.a; i < op.b; ++i) {
+          const LArg& g = L.args[i];
+          os << "    const T v" << (i - op.a) << " = e" << g.expr;
+          if (g.scale != 1) os << " * " << lit(g.scale);
+          os << ";\n";
+        }
+        os << "    a" << op.dst << " = v0;\n";
+        for (int i = op.a + 1; i < op.b; ++i)
+          os << "    a" << op.dst << " = (v" << (i - op.a) << (op.code == OP_MIN ? " < " : " > ") << "a"
+             << op.dst << ") ? v" << (i - op.a) << " : a" << op.dst << ";\n";
+        os << "  }\n";
+        break;
+      }
+    }
+  }
+  for (const LCons& c : L.cons) {
+    if (c.divisibility == 2) {
+      if (small && atom_u32[c.expr] && c.rem == 0 && c.mod <= kU32)
+        os << "  ok &= (unsigned)p[" << c.op << "] == " << static_cast<uint64_t>(c.mod) << "u * u" << c.expr << ";\n";
+      else
+        os << "  ok &= (T)p[" << c.op << "] - " << lit(c.rem) << " == " << lit(c.mod) << " * a" << c.expr << ";\n";
+      continue;
+    }
+    const LExpr& ex = L.exprs[c.expr];
+    if (!c.divisibility) {
+      os << "  ok &= e" << c.expr << " " << cmp_str(c.op) << " (T)0;\n";
+    } else if (ex.D != 1) {
+      os << "  { const bool di = (e" << c.expr << " % " << lit(ex.D) << ") == (T)0; integral &= di;"
+         << " ok &= !di || kcg_posmod<T>(e" << c.expr << " / " << lit(ex.D) << ", " << lit(c.mod)
+         << ") == " << lit(c.rem) << "; }\n";
+    } else {
+      os << "  ok &= kcg_posmod<T>(e" << c.expr << ", " << lit(c.mod) << ") == " << lit(c.rem) << ";\n";
+    }
+  }
+  for (size_t j = 0; j < L.keys.size(); ++j) {
+    const int e = L.keys[j].expr;
+    const LExpr& ex = L.exprs[e];
+    if (key_fast[j] >= 0) {
+      const i128 C = L.terms[ex.term_begin].coef;
+      if (C == 1)
+        os << "  cnt[" << j << "] = dm" << key_fast[j] << ";\n";
+      else
+        os << "  cnt[" << j << "] = __dmul_rn(" << static_cast<long long>(C) << ".0, dm" << key_fast[j] << ");\n";
+      continue;
+    }
+    std::string val = "e" + std::to_string(e);
+    if (ex.D != 1) {
+      os << "  integral &= (e" << e << " % " << lit(ex.D) << ") == (T)0;\n";
+      val = "(e" + std::to_string(e) + " / " + lit(ex.D) + ")";
+    }
+    if (dbl)
+      os << "  cnt[" << j << "] = __ll2double_rn(" << val << ");\n";
+    else
+      os << "  cnt[" << j << "] = " << val << ";\n";
+  }
+  os << "  return ok ? (integral ? KCG_PT_OK : KCG_PT_NONINTEGRAL) : KCG_PT_ASSUMPTION_VIOLATED;\n}\n\n";
+}
+
 // parameter range class: 0 negative (inadmissible), 1 fast, 2 wide, 3 overflow
 void emit_classify(std::ostringstream& os, const Lowered& L, int v, const std::vector<int>& pmap) {
-  os << "__device__ __forceinline__ int kcg_class_" << v << "(const kcg_i64* p) {\n  if ((";
+  os << "__device__ __forceinline__ int kcg_class_" << v << "(const kcg_i64* p) {\n";
+  if (L.b64 >= 0 && L.b64 <= kU32 && L.n_params > 0) {
+    // class 1 <=> all high words zero and every low word <= b64
+    os << "  if (((";
+    for (int j = 0; j < L.n_params; ++j) os << (j ? " | " : "") << "p[" << pmap[j] << "]";
+    os << ") >> 32) == 0 && ";
+    for (int j = 0; j < L.n_params; ++j)
+      os << (j ? " && " : "") << "(unsigned)p[" << pmap[j] << "] <= " << L.b64 << "u";
+    os << ") return 1;\n";
+  }
+  os << "  if ((";
   for (int j = 0; j < L.n_params; ++j) os << (j ? " | " : "") << "p[" << pmap[j] << "]";
   if (L.n_params == 0) os << "0ll";
   os << ") < 0) return 0;\n";
@@ -241,26 +415,132 @@ void emit_eval_point(std::ostringstream& os, const Lowered& L) {
   // fast path only; returns -1 when the point needs kcg_point_slow
   os << "template <int GEN>\n__device__ __forceinline__ int kcg_point_fast(const kcg_i64* p, const KcgArgs& a, kcg_i64 i, double& out) {\n"
         "  if (kcg_class_0(p) != 1) return -1;\n"
-        "  kcg_i64 c["
-     << FA << "];\n  const int st = kcg_fast_0(p, c);\n  if (st != KCG_PT_OK) return st;\n"
-              "  double s = 0.0;\n";
+        "  if (a.clo) {\n    kcg_i64 c["
+     << FA << "];\n    const int st = kcg_fasti_0(p, c);\n    if (st != KCG_PT_OK) return st;\n"
+              "    double s = 0.0;\n";
   for (int j = 0; j < F; ++j)
-    os << "  s = GEN ? kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim) : "
+    os << "    s = GEN ? kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim) : "
        << "__dadd_rn(s, __dmul_rn(a.alpha[" << j << "], kcg_to_double(c[" << j << "])));\n";
-  os << "  out = s;\n  if (a.clo) {\n";
+  os << "    out = s;\n";
   for (int j = 0; j < F; ++j) {
     os << "    __stcs(a.clo + (kcg_i64)" << j << " * a.n + i, c[" << j << "]);\n";
     os << "    if (a.chi) __stcs(a.chi + (kcg_i64)" << j << " * a.n + i, kcg_hi64(c[" << j << "]));\n";
   }
-  os << "  }\n  return KCG_PT_OK;\n}\n";
+  os << "    return KCG_PT_OK;\n  }\n  double c[" << FA << "];\n  const int st = kcg_fastd_0(p, c);\n"
+        "  double s = 0.0;\n";
+  for (int j = 0; j < F; ++j)
+    os << "  s = GEN ? kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim) : "
+       << "__dadd_rn(s, __dmul_rn(a.alpha[" << j << "], c[" << j << "]));\n";
+  os << "  out = s;\n  return st;\n}\n";
 }
 
 int min_blocks() {
   // occupancy target of the eval kernels (blocks of 256 per SM); the
   // register cap it implies is the main tuning knob (KCG_MIN_BLOCKS)
   const char* e = std::getenv("KCG_MIN_BLOCKS");
-  const int v = e ? std::atoi(e) : 3;
-  return v >= 1 && v <= 8 ? v : 3;
+  const int v = e ? std::atoi(e) : 4;
+  return v >= 1 && v <= 8 ? v : 4;
+}
+
+// TMA-staged eval kernel (persistent, 2 CTAs/SM): one elected thread streams
+// tiles of 1024 points per parameter column into a ring of shared-memory
+// stages with cp.async.bulk (SASS UBLKCP) completing on an mbarrier; the
+// 256 threads evaluate 4 points each from shared memory while the next
+// stages are in flight, so the bytes in flight no longer depend on the
+// register budget of the exact integer evaluation.
+constexpr int kTmaTile = 1024;
+
+int tma_stages(int n_cols) {
+  const int per = (n_cols > 0 ? n_cols : 1) * kTmaTile * 8;
+  int s = (96 * 1024) / per;
+  return s < 2 ? 2 : (s > 8 ? 8 : s);
+}
+
+void emit_tma_kernel(std::ostringstream& os, int n_cols, const std::string& name) {
+  const int NP = n_cols > 0 ? n_cols : 1;
+  const int S = tma_stages(n_cols);
+  os << "extern \"C\" __global__ void __launch_bounds__(256, 2) " << name
+     << "(const __grid_constant__ KcgArgs a) {\n"
+        "  constexpr int TP = "
+     << kTmaTile << ", S = " << S << ", NP = " << NP
+     << ";\n"
+        "  extern __shared__ __align__(128) unsigned char kcg_smem[];\n"
+        "  kcg_i64* buf = reinterpret_cast<kcg_i64*>(kcg_smem);\n"
+        "  __shared__ __align__(8) unsigned long long full[S];\n"
+        "  const kcg_i64 ntiles = a.n / TP;\n"
+        "  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);\n"
+        "  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);\n"
+        "  if (threadIdx.x == 0) {\n"
+        "    for (int s = 0; s < S; ++s)\n"
+        "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(fb + 8 * s));\n"
+        "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+        "  }\n"
+        "  __syncthreads();\n"
+        "  auto issue = [&](int s, kcg_i64 tile) {\n"
+        "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+        "    asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(fb + 8 * s), \"r\"(NP * TP * 8) : \"memory\");\n"
+        "    for (int j = 0; j < NP; ++j)\n"
+        "      asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\"\n"
+        "                   :: \"r\"(bb + (unsigned)((s * NP + j) * TP * 8)), \"l\"(a.p[j] + tile * TP), \"r\"(TP * 8), \"r\"(fb + 8 * s) : \"memory\");\n"
+        "  };\n"
+        "  if (threadIdx.x == 0)\n"
+        "    for (int s = 0; s < S; ++s) {\n"
+        "      const kcg_i64 t = blockIdx.x + (kcg_i64)s * gridDim.x;\n"
+        "      if (t < ntiles) issue(s, t);\n"
+        "    }\n"
+        "  for (kcg_i64 k = 0;; ++k) {\n"
+        "    const kcg_i64 tile = blockIdx.x + k * gridDim.x;\n"
+        "    if (tile >= ntiles) break;\n"
+        "    const int s = (int)(k % S);\n"
+        "    const unsigned parity = (unsigned)((k / S) & 1);\n"
+        "    {\n"
+        "      unsigned done = 0;\n"
+        "      while (!done)\n"
+        "        asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\"\n"
+        "                     : \"=r\"(done) : \"r\"(fb + 8 * s), \"r\"(parity) : \"memory\");\n"
+        "    }\n"
+        "    kcg_i64 q[4][NP];\n"
+        "    #pragma unroll\n"
+        "    for (int j = 0; j < NP; ++j) {\n"
+        "      const longlong2* src = reinterpret_cast<const longlong2*>(buf + (s * NP + j) * TP) + 2 * threadIdx.x;\n"
+        "      const longlong2 x = src[0], y = src[1];\n"
+        "      q[0][j] = x.x; q[1][j] = x.y; q[2][j] = y.x; q[3][j] = y.y;\n"
+        "    }\n"
+        "    __syncthreads();  // stage s fully read: refill it\n"
+        "    if (threadIdx.x == 0) {\n"
+        "      const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+        "      if (nt < ntiles) issue(s, nt);\n"
+        "    }\n"
+        "    const kcg_i64 base = tile * TP + 4 * threadIdx.x;\n"
+        "    double r[4]; int st[4];\n"
+        "    #pragma unroll\n"
+        "    for (int u = 0; u < 4; ++u) { r[u] = kcg_nan(); st[u] = kcg_point_fast<0>(q[u], a, base + u, r[u]); }\n"
+        "    if ((st[0] | st[1] | st[2] | st[3]) < 0) {\n"
+        "      #pragma unroll\n"
+        "      for (int u = 0; u < 4; ++u)\n"
+        "        if (st[u] < 0) { const KcgRes x = kcg_point_slow(a, base + u); r[u] = x.s; st[u] = x.st; }\n"
+        "    }\n"
+        "    #pragma unroll\n"
+        "    for (int u = 0; u < 4; ++u)\n"
+        "      if (st[u] != KCG_PT_OK && st[u] != KCG_PT_COUNT_WIDE) r[u] = kcg_nan();\n"
+        "    if (a.pred) {\n"
+        "      __stcs(reinterpret_cast<double2*>(a.pred + base), make_double2(r[0], r[1]));\n"
+        "      __stcs(reinterpret_cast<double2*>(a.pred + base) + 1, make_double2(r[2], r[3]));\n"
+        "    }\n"
+        "    if (a.status) reinterpret_cast<unsigned*>(a.status)[base >> 2] =\n"
+        "        (unsigned)st[0] | ((unsigned)st[1] << 8) | ((unsigned)st[2] << 16) | ((unsigned)st[3] << 24);\n"
+        "  }\n"
+        "  // tail (n % TP points): scalar\n"
+        "  for (kcg_i64 i = ntiles * TP + (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;\n"
+        "       i += (kcg_i64)gridDim.x * blockDim.x) {\n"
+        "    kcg_i64 p[NP];\n";
+  for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = a.p[" << j << "][i];\n";
+  os << "    double r = kcg_nan();\n    int st = kcg_point_fast<0>(p, a, i, r);\n"
+        "    if (st < 0) { const KcgRes x = kcg_point_slow(a, i); r = x.s; st = x.st; }\n"
+        "    if (st != KCG_PT_OK && st != KCG_PT_COUNT_WIDE) r = kcg_nan();\n"
+        "    if (a.pred) a.pred[i] = r;\n"
+        "    if (a.status) a.status[i] = (unsigned char)st;\n"
+        "  }\n}\n";
 }
 
 void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& name, int gen) {
@@ -319,13 +599,18 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 
 }  // namespace
 
+size_t tma_smem_bytes(int n_cols) {
+  return static_cast<size_t>(tma_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * kTmaTile * 8;
+}
+
 std::string codegen(const std::vector<const Lowered*>& progs,
                     const std::vector<std::vector<int>>& pmaps, int n_cols, JitKind kind,
                     const std::string& name) {
   std::ostringstream os;
   os << "// generated by kcg codegen\n" << kDeviceHelpers << "\n";
   for (size_t v = 0; v < progs.size(); ++v) {
-    emit_body(os, *progs[v], static_cast<int>(v), true);
+    emit_fast(os, *progs[v], static_cast<int>(v), false);
+    emit_fast(os, *progs[v], static_cast<int>(v), true);
     emit_body(os, *progs[v], static_cast<int>(v), false);
     emit_classify(os, *progs[v], static_cast<int>(v), pmaps[v]);
   }
@@ -342,6 +627,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     emit_eval_point(os, L);
     emit_eval_kernel(os, n_cols, name, 0);
     emit_eval_kernel(os, n_cols, name + "_gen", 1);
+    emit_tma_kernel(os, n_cols, name + "_tma");
     return os.str();
   }
 
@@ -365,9 +651,9 @@ std::string codegen(const std::vector<const Lowered*>& progs,
             "  const int cls = kcg_class_"
          << v << "(p);\n";
       emit_gather(os, "q", "p", L, pmaps[v], "  ");
-      os << "  if (cls == 1) {\n    kcg_i64 c[" << FA << "];\n    const int st = kcg_fast_" << v
+      os << "  if (cls == 1) {\n    double c[" << FA << "];\n    const int st = kcg_fastd_" << v
          << "(q, c);\n    if (st != KCG_PT_OK) return st;\n    double s = 0.0;\n";
-      for (int j = 0; j < F; ++j) os << "    s = kcg_accum(s, al[" << j << "], c[" << j << "], 0);\n";
+      for (int j = 0; j < F; ++j) os << "    s = __dadd_rn(s, __dmul_rn(al[" << j << "], c[" << j << "]));\n";
       os << "    *out = s;\n    return KCG_PT_OK;\n  }\n"
             "  if (cls == 2) return kcg_wide_pred_"
          << v
@@ -411,7 +697,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
         "  if (!(t > 0.0)) return KCG_PT_ASSUMPTION_VIOLATED;\n"
         "  const int cls = kcg_class_0(p);\n"
         "  if (cls == 1) { kcg_i64 c["
-     << FA << "]; const int st = kcg_fast_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n"
+     << FA << "]; const int st = kcg_fasti_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n"
               "  if (cls == 2) return kcg_row_wide(p, t, x);\n"
               "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
   if (kind == JitKind::gram) {

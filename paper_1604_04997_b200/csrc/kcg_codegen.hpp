@@ -23,6 +23,10 @@ void* jit_kernel(const std::string& src, const std::string& name);
 
 /// Launches a JIT kernel with a single by-value argument struct.
 void launch_jit(void* kernel, const void* args, size_t args_size,
-                unsigned grid, unsigned block, void* stream);
+                unsigned grid, unsigned block, void* stream, size_t smem = 0);
+
+/// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.
+size_t tma_smem_bytes(int n_cols);
+constexpr int kTmaPointsPerTile = 1024;
 
 }  // namespace kcg

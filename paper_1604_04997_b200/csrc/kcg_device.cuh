@@ -92,6 +92,13 @@ __device__ __forceinline__ double kcg_accum(double s, double alpha, T count, int
   return s;
 }
 
+// same rule when the count is already RN(double(count)) (count == 0 <=> 0.0)
+__device__ __forceinline__ double kcg_accum(double s, double alpha, double count, int simulate) {
+  const bool take = simulate ? (alpha != 0.0) : (count != 0.0);
+  if (take) s = __dadd_rn(s, __dmul_rn(alpha, count));
+  return s;
+}
+
 __device__ __forceinline__ double kcg_nan() { return __longlong_as_double(0x7ff8000000000000ll); }
 
 #endif  // KCG_DEVICE_HELPERS

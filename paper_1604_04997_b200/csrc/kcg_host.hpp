@@ -155,12 +155,14 @@ struct Lowered {
   std::vector<i128> atom_den;      // value = numerator / atom_den
   std::vector<i128> quot_mod, quot_rem;  // per OP_QUOT (index in op.c)
   int64_t b64 = 0, b128 = 0;       // safe uniform parameter bounds
+  std::vector<long double> mono_bound64;  // |monomial| bound when params <= b64
 };
 
 Lowered lower(const Symbolic& s);
 
 /// Magnitude bound of the largest intermediate when all |params| <= B.
-long double max_intermediate(const Lowered& L, long double B);
+long double max_intermediate(const Lowered& L, long double B,
+                             std::vector<long double>* mono_bounds = nullptr);
 
 // ---------------------------------------------------------------------------
 // Schema v1 (schema.cpp:16-38)

@@ -822,10 +822,12 @@ Lowered lower(const Symbolic& s_in) {
   };
   L.b64 = search(std::ldexp(1.0L, 62));
   L.b128 = search(std::ldexp(1.0L, 125));
+  if (L.b64 >= 0) max_intermediate(L, static_cast<long double>(L.b64), &L.mono_bound64);
   return L;
 }
 
-long double max_intermediate(const Lowered& L, long double B) {
+long double max_intermediate(const Lowered& L, long double B,
+                             std::vector<long double>* mono_bounds) {
   auto absq = [](i128 v) -> long double {
     return static_cast<long double>(v < 0 ? -v : v);
   };
@@ -883,10 +885,8 @@ long double max_intermediate(const Lowered& L, long double B) {
       }
     }
   }
-  for (const LCons& c : L.cons) {
-    see(2 * absq(c.mod) + absq(c.rem));
-    (void)c;
-  }
+  for (const LCons& c : L.cons) see(2 * absq(c.mod) + absq(c.rem));
+  if (mono_bounds) *mono_bounds = mono;
   return worst;
 }
 

@@ -283,3 +283,39 @@ def test_no_silent_fallback_launches_counted():
     kc.evaluate_properties(prog, _cols(prog, [{"n": 16}]))
     torch.cuda.synchronize()
     assert kc.launch_count() == before + 1
+
+
+@pytest.mark.parametrize("kid", ["matmul_tiled_g12x12", "conv_g16x16", "matmul_skinny_g16x16"])
+def test_large_launch_tma_path_matches_interpreter(kid, suite_alpha):
+    """Launches large enough for the TMA-staged persistent kernel (>= 148
+    tiles of 1024 points, ragged tail) agree bitwise with the table
+    interpreter and with the oracle on a sample, including inadmissible and
+    wide-path points mixed into the stream."""
+    prog = kc.load_program(kid)
+    oprog = ko.Program((PROGRAMS / f"{kid}.kcp").read_text())
+    g = torch.Generator(device="cpu").manual_seed(5)
+    n = 148 * 1024 * 2 + 777
+    unit = 12 if "g12" in kid else 16
+    u = torch.randint(1, 20000, (len(prog.params), n), generator=g)
+    cols = {p: (u[j] * unit).to(torch.int64) for j, p in enumerate(prog.params)}
+    if "skinny" in kid:
+        cols["m"] = cols["n"] * 8
+    cols[prog.params[0]][::97] += 1                  # inadmissible
+    cols[prog.params[0]][5::1013] = 16 * 3_000_000   # wide path
+    cols = {k: v.cuda().contiguous() for k, v in cols.items()}
+    w = _weights(suite_alpha)
+    prog.set_engine("jit")
+    pj, sj = kc.predict(w, prog, cols, with_status=True)
+    prog.set_engine("interp")
+    pi, si = kc.predict(w, prog, cols, with_status=True)
+    torch.cuda.synchronize()
+    assert torch.equal(sj, si)
+    same = (pj == pi) | (torch.isnan(pj) & torch.isnan(pi))
+    assert bool(same.all())
+    for i in list(range(0, n, n // 97)) + [n - 1, n - 2, 5, 97]:
+        b = {p: int(cols[p][i]) for p in prog.params}
+        try:
+            want = ko.predict(suite_alpha, oprog.evaluate_properties(b))
+            assert float(pj[i]) == want and int(sj[i]) == 0
+        except ko.AssumptionViolated:
+            assert int(sj[i]) == 1
