@@ -186,7 +186,10 @@ def main():
             "l": (idx % args.side + 1) * UNIT}
     del idx
     cols = {k: v.contiguous() for k, v in cols.items()}
-    preds = torch.empty((len(VARIANTS), n), dtype=torch.float64, device=dev)
+    # rows padded to a 16-byte multiple so every variant's output row is
+    # aligned for the vector stores (the kernels also accept unaligned rows)
+    ld = (n + 1) // 2 * 2
+    preds = torch.empty((len(VARIANTS), ld), dtype=torch.float64, device=dev)[:, :n]
     stream = torch.cuda.current_stream(dev)
 
     def step(ev=None):

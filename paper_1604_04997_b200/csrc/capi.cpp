@@ -368,10 +368,14 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
     ab.push<void*>(counts_hi);
     ab.push<int64_t>(static_cast<int64_t>(n));
     ab.push<int32_t>(simulate);
-    bool vec = (reinterpret_cast<uintptr_t>(pred_out) % 16 == 0) &&
-               (reinterpret_cast<uintptr_t>(status_out) % 4 == 0);
+    // inputs 16-byte aligned: TMA bulk copies / vector loads; outputs
+    // aligned: 16-byte prediction stores and 4-byte status stores
+    bool vec = true;
     for (int j = 0; j < np; ++j) vec = vec && reinterpret_cast<uintptr_t>(param_cols[j]) % 16 == 0;
+    const bool vout = (reinterpret_cast<uintptr_t>(pred_out) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(status_out) % 4 == 0);
     ab.push<int32_t>(vec ? 1 : 0);
+    ab.push<int32_t>(vout ? 1 : 0);
     std::vector<double> al(std::max(F, 1), 0.0);
     compact_alpha(p, alpha, al.data());
     for (double v : al) ab.push<double>(v);
@@ -383,7 +387,8 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
     const size_t tiles = n / kcg::kTmaPointsPerTile;
     if (finite && vec && !no_tma && tiles >= static_cast<size_t>(kcg::num_sms())) {
       // TMA-staged persistent kernel: 2 CTAs per SM
-      const unsigned grid = static_cast<unsigned>(std::min<size_t>(tiles, kcg::num_sms() * 2));
+      const unsigned grid = static_cast<unsigned>(
+          std::min<size_t>(tiles, static_cast<size_t>(kcg::num_sms()) * kcg::tma_ctas_per_sm()));
       kcg::launch_jit(p->jit_eval_tma, ab.b.data(), ab.b.size(), grid, 256, stream,
                       kcg::tma_smem_bytes(np));
     } else {

@@ -450,16 +450,26 @@ int min_blocks() {
 // register budget of the exact integer evaluation.
 constexpr int kTmaTile = 1024;
 
+int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = std::getenv(name);
+  const int v = e ? std::atoi(e) : dflt;
+  return v >= lo && v <= hi ? v : dflt;
+}
+
+// per-CTA ring size (KB) and CTAs per SM of the TMA kernel (tuning knobs)
+int tma_ring_kb() { return env_int("KCG_TMA_RING_KB", 96, 16, 200); }
+int tma_ctas() { return env_int("KCG_TMA_CTAS", 2, 1, 4); }
+
 int tma_stages(int n_cols) {
   const int per = (n_cols > 0 ? n_cols : 1) * kTmaTile * 8;
-  int s = (96 * 1024) / per;
+  int s = (tma_ring_kb() * 1024) / per;
   return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
 void emit_tma_kernel(std::ostringstream& os, int n_cols, const std::string& name) {
   const int NP = n_cols > 0 ? n_cols : 1;
   const int S = tma_stages(n_cols);
-  os << "extern \"C\" __global__ void __launch_bounds__(256, 2) " << name
+  os << "extern \"C\" __global__ void __launch_bounds__(256, " << tma_ctas() << ") " << name
      << "(const __grid_constant__ KcgArgs a) {\n"
         "  constexpr int TP = "
      << kTmaTile << ", S = " << S << ", NP = " << NP
@@ -523,12 +533,20 @@ void emit_tma_kernel(std::ostringstream& os, int n_cols, const std::string& name
         "    #pragma unroll\n"
         "    for (int u = 0; u < 4; ++u)\n"
         "      if (st[u] != KCG_PT_OK && st[u] != KCG_PT_COUNT_WIDE) r[u] = kcg_nan();\n"
-        "    if (a.pred) {\n"
-        "      __stcs(reinterpret_cast<double2*>(a.pred + base), make_double2(r[0], r[1]));\n"
-        "      __stcs(reinterpret_cast<double2*>(a.pred + base) + 1, make_double2(r[2], r[3]));\n"
+        "    if (a.vout) {\n"
+        "      if (a.pred) {\n"
+        "        __stcs(reinterpret_cast<double2*>(a.pred + base), make_double2(r[0], r[1]));\n"
+        "        __stcs(reinterpret_cast<double2*>(a.pred + base) + 1, make_double2(r[2], r[3]));\n"
+        "      }\n"
+        "      if (a.status) reinterpret_cast<unsigned*>(a.status)[base >> 2] =\n"
+        "          (unsigned)st[0] | ((unsigned)st[1] << 8) | ((unsigned)st[2] << 16) | ((unsigned)st[3] << 24);\n"
+        "    } else {\n"
+        "      #pragma unroll\n"
+        "      for (int u = 0; u < 4; ++u) {\n"
+        "        if (a.pred) __stcs(a.pred + base + u, r[u]);\n"
+        "        if (a.status) a.status[base + u] = (unsigned char)st[u];\n"
+        "      }\n"
         "    }\n"
-        "    if (a.status) reinterpret_cast<unsigned*>(a.status)[base >> 2] =\n"
-        "        (unsigned)st[0] | ((unsigned)st[1] << 8) | ((unsigned)st[2] << 16) | ((unsigned)st[3] << 24);\n"
         "  }\n"
         "  // tail (n % TP points): scalar\n"
         "  for (kcg_i64 i = ntiles * TP + (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;\n"
@@ -550,7 +568,7 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
         "  const kcg_i64 tid = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x;\n"
         "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
         "  kcg_i64 done = 0;\n"
-        "  if (a.vec) {\n"
+        "  if (a.vec && a.vout) {\n"
         "    // 4 consecutive points per thread: two 16-byte loads per column,\n"
         "    // two 16-byte streaming stores of predictions, one 4-byte status store\n"
         "    const kcg_i64 nv = a.n >> 2;\n"
@@ -599,6 +617,8 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 
 }  // namespace
 
+int tma_ctas_per_sm() { return tma_ctas(); }
+
 size_t tma_smem_bytes(int n_cols) {
   return static_cast<size_t>(tma_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * kTmaTile * 8;
 }
@@ -621,7 +641,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     const int F = static_cast<int>(L.keys.size());
     const int FA = F > 0 ? F : 1;
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; double* pred; "
-          "unsigned char* status; kcg_i64* clo; kcg_i64* chi; kcg_i64 n; int sim; int vec; "
+          "unsigned char* status; kcg_i64* clo; kcg_i64* chi; kcg_i64 n; int sim; int vec; int vout; "
           "double alpha["
        << FA << "]; };\n";
     emit_eval_point(os, L);

@@ -27,6 +27,7 @@ void launch_jit(void* kernel, const void* args, size_t args_size,
 
 /// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.
 size_t tma_smem_bytes(int n_cols);
+int tma_ctas_per_sm();
 constexpr int kTmaPointsPerTile = 1024;
 
 }  // namespace kcg

@@ -319,3 +319,30 @@ def test_large_launch_tma_path_matches_interpreter(kid, suite_alpha):
             assert float(pj[i]) == want and int(sj[i]) == 0
         except ko.AssumptionViolated:
             assert int(sj[i]) == 1
+
+
+@pytest.mark.parametrize("in_off,out_off", [(0, 1), (1, 0), (1, 1)])
+def test_unaligned_buffers_through_c_abi(suite_alpha, in_off, out_off):
+    """Odd element offsets (8-byte but not 16-byte aligned) for the binding
+    columns and/or the outputs select the scalar paths; results are
+    identical to the aligned launch."""
+    import ctypes
+    prog = kc.load_program("matmul_tiled_g16x16")
+    n = 148 * 1024 + 333
+    g = torch.Generator(device="cpu").manual_seed(9)
+    base = {p: (torch.randint(1, 5000, (n + 1,), generator=g) * 16).cuda() for p in prog.params}
+    base["n"][::31] += 3
+    w = _weights(suite_alpha)
+    ref, ref_st = kc.predict(w, prog, {p: base[p][:n].contiguous() for p in prog.params}, with_status=True)
+    cols = [base[p][in_off:in_off + n] for p in prog.params]
+    arr = (ctypes.c_void_p * 3)(*[c.data_ptr() for c in cols])
+    pred = torch.empty(n + 1, dtype=torch.float64, device="cuda")[out_off:out_off + n]
+    st = torch.empty(n + 1, dtype=torch.uint8, device="cuda")[out_off:out_off + n]
+    if in_off:
+        ref, ref_st = kc.predict(w, prog, {p: base[p][1:n + 1].contiguous() for p in prog.params}, with_status=True)
+    _capi.check(_capi.lib().kcg_eval_predict(prog.handle, arr, n, w.alpha_array(), pred.data_ptr(),
+                                             st.data_ptr(), None, None, 0,
+                                             torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    assert torch.equal(st, ref_st)
+    assert bool(((pred == ref) | (torch.isnan(pred) & torch.isnan(ref))).all())
