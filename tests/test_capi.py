@@ -1,0 +1,168 @@
+"""CPU-side checks of the C ABI (no kernel launches): the library loads and
+exports every symbol include/kcg.h declares, programs parse and lower like
+the reference front end printed them, errors map to the reference's Errc
+codes, the weights file round-trips byte-identically, the host solve
+reproduces the reference fit, and launches fail loudly without a GPU."""
+import ctypes
+import json
+import math
+
+import numpy as np
+import pytest
+
+import kc_oracle as ko
+from conftest import GOLDEN, PROGRAMS, hexf, load_golden
+import paper_1604_04997_b200 as kc
+from paper_1604_04997_b200 import _capi
+
+
+def test_library_exports_every_header_symbol():
+    L = _capi.lib()
+    names = _capi.header_functions()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(L, n), n
+
+
+def test_schema_matches_reference_order():
+    assert kc.schema_keys() == ko.SCHEMA
+    assert kc.schema_index("launch.const") == 148
+    with pytest.raises(kc.KcgError) as e:
+        kc.schema_index("mem.bogus")
+    assert e.value.code == _capi.E_SCHEMA_MISMATCH
+
+
+def test_every_suite_program_lowers():
+    idx = {k["id"]: k for k in kc.suite_index()}
+    n = 0
+    for path in sorted(PROGRAMS.glob("*.kcp")):
+        p = kc.Program.from_file(path)
+        o = ko.Program(path.read_text())
+        assert p.params == idx[path.stem]["params"] == o.params
+        assert p.props == [k for k, _ in o.props]
+        b64, b128 = p.safe_bounds()
+        assert 0 < b64 <= b128
+        n += 1
+    assert n == 59
+    assert not idx["fd_stencil_g16x16"]["symbolic"] and not idx["nbody_g256"]["symbolic"]
+
+
+def test_safe_bounds_are_sound_for_matmul():
+    p = kc.load_program("matmul_tiled_g16x16")
+    b64, b128 = p.safe_bounds()
+    # largest count 4608 q^3 (q = n/16) must fit int63 at the bound
+    assert 4608 * (b64 // 16) ** 3 < 2**63
+    assert (b128 // 16) ** 3 * 4608 < 2**127
+
+
+@pytest.mark.parametrize("text,code", [
+    ("", _capi.E_PARSE),
+    ("kernelcost-program v1\nkernel k\nparam n\nprop launch.const 1\n", _capi.E_PARSE),
+    ("kernelcost-program v1\nkernel k\nparam n\nprop bogus.key n\nend\n", _capi.E_SCHEMA_MISMATCH),
+    ("kernelcost-program v1\nkernel k\nparam n\nprop launch.const (* m 2)\nend\n", _capi.E_PARSE),
+    ("kernelcost-program v1\nkernel k\nparam n\nassume n ~ 3\nend\n", _capi.E_PARSE),
+    ("kernelcost-program v1\nkernel k\nparam n\nprop launch.const (floordiv n 0)\nend\n", _capi.E_PARSE),
+])
+def test_parse_errors(text, code):
+    with pytest.raises(kc.KcgError) as e:
+        kc.Program(text)
+    assert e.value.code == code
+
+
+def test_program_with_atoms_and_rationals_lowers():
+    d = load_golden("extra_programs.json")
+    for p in d["programs"]:
+        if "program" in p:
+            prog = kc.Program(p["program"])
+            src = prog.jit_source()
+            assert "kcg_fasti_0" in src and "kcg_wide_0" in src and "_tma" in src
+
+
+def test_jit_source_has_no_divisions_after_congruence_substitution():
+    src = kc.load_program("matmul_tiled_g16x16").jit_source()
+    fast = src[src.index("kcg_fastd_0"):src.index("kcg_wide_0")]
+    assert " % " not in fast and "4608" in fast
+
+
+def test_launches_fail_loudly_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    p = kc.load_program("conv_g16x16")
+    rc = _capi.lib().kcg_eval_predict(p.handle, (ctypes.c_void_p * 1)(0), 4, None, None, None,
+                                      None, None, 0, None)
+    assert rc == _capi.E_CUDA
+    assert b"no CUDA device" in _capi.lib().kcg_last_error()
+
+
+def test_weights_json_round_trip_is_byte_identical(tmp_path):
+    src = GOLDEN / "weights_suite.json"
+    w = kc.read_weights_json(src)
+    fit = load_golden("fit_suite.json")
+    for k, v in fit["alpha"].items():
+        assert w.alpha[ko.SCHEMA_INDEX[k]] == hexf(v[1])
+    assert w.device == "simdev-v1" and w.n_cases == 390
+    out = tmp_path / "w.json"
+    kc.write_weights_json(out, w)
+    assert out.read_bytes() == src.read_bytes()
+
+
+def test_weights_json_errors(tmp_path):
+    with pytest.raises(kc.KcgError) as e:
+        kc.read_weights_json(tmp_path / "missing.json")
+    assert e.value.code == _capi.E_IO
+    bad = tmp_path / "bad.json"
+    bad.write_text(json.dumps({"schema_version": "v0", "weights": {}}))
+    with pytest.raises(kc.KcgError) as e:
+        kc.read_weights_json(bad)
+    assert e.value.code == _capi.E_SCHEMA_MISMATCH
+    bad.write_text("{not json")
+    with pytest.raises(kc.KcgError) as e:
+        kc.read_weights_json(bad)
+    assert e.value.code == _capi.E_PARSE
+
+
+def _solve(X):
+    F = X.shape[1]
+    G = np.ascontiguousarray(X.T @ X)
+    s1 = np.ascontiguousarray(X.sum(0))
+    cm = np.ascontiguousarray(np.abs(X).max(0))
+    out = (ctypes.c_double * F)()
+    rank = ctypes.c_int()
+    dp = lambda a: a.ctypes.data_as(_capi.DP)
+    _capi.check(_capi.lib().kcg_solve_gram(F, dp(G), dp(s1), dp(cm), out, ctypes.byref(rank)))
+    alpha = np.array(list(out))
+    # one semi-normal refinement step, as fit_weights() does on the GPU
+    g = np.ascontiguousarray(X.T @ (1.0 - X @ alpha))
+    arr = (ctypes.c_double * F)(*alpha)
+    _capi.check(_capi.lib().kcg_refine_gram(F, dp(G), dp(cm), dp(g), arr))
+    return np.array(list(arr)), rank.value
+
+
+def test_host_solve_reproduces_reference_fits():
+    for fit in load_golden("fit_synthetic.json")["fits"]:
+        counts = np.array(fit["counts"], dtype=np.float64)
+        times = np.array([hexf(t) for t in fit["times"]])
+        X = counts / times[:, None]
+        alpha, rank = _solve(X)
+        ref = [hexf(a) for a in fit["alpha"]]
+        for k, got, r in zip(fit["keys"], alpha, ref):
+            assert abs(got - r) <= 1e-6 * abs(r), (fit["name"], k, got, r)
+        if fit["name"] == "duplicate_columns":
+            assert rank == 2  # min-norm split of the two identical columns
+        r = 1.0 - X @ alpha
+        assert float(r @ r) <= max(1e-18, 10 * hexf(fit["objective"][1]))
+
+
+def test_host_solve_suite_design_matches_reference(suite_alpha):
+    cases = [c for c in load_golden("suite_cases.json")["cases"] if c["role"] == "measurement"]
+    rows = [({ko.SCHEMA_INDEX[k]: int(v) for k, v in c["counts"].items()}, hexf(c["time_s"][1])) for c in cases]
+    X, cov = ko.build_design_matrix(rows)
+    cols = np.flatnonzero(cov)
+    alpha, rank = _solve(np.ascontiguousarray(X[:, cols]))
+    sim = ko.simdev_reference_alpha()
+    for c, got in zip(cols, alpha):
+        if sim[c] != 0.0:
+            assert abs(got - suite_alpha[c]) <= 1e-6 * abs(suite_alpha[c]), ko.SCHEMA[c]
+        else:
+            assert abs(got) <= 1e-15
