@@ -9,6 +9,8 @@
 //   * kcg_resid_x / kcg_resid_grad_x -- sum (1 - X a)^2 and X^T (1 - X a)
 #include <cuda_runtime.h>
 
+#include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -290,6 +292,171 @@ __global__ void __launch_bounds__(kGramThreads)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Gram on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64) fed by a TMA ring
+//
+// G = X^T X is a GEMM with M = N = F (<= 48 here) and K = rows. For a 4-row
+// k-step, lane (gid = lane/4, tig = lane%4) loads v_b = X[k0+tig][8b+gid]
+// for every 8-column block b; that one register is simultaneously the A
+// fragment (row-major 8x4, A[i][k] = X[k][8I+i]) and the B fragment
+// (col-major 4x8, B[k][j] = X[k][8J+j]) of the m8n8k4 DMMA, so each k-step
+// costs NB shared loads and NB(NB+1)/2 tensor instructions for the upper
+// block triangle. Rows stream through a 4-stage cp.async.bulk ring.
+
+constexpr int kDmmaRows = 64;
+
+__device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <int NB>
+__global__ void __launch_bounds__(256, 2)
+    kcg_gram_dmma(const double* __restrict__ X, kcg_i64 n, int F, int stages,
+                  double* __restrict__ G, double* __restrict__ xt1, double* __restrict__ cmax) {
+  constexpr int NT = NB * (NB + 1) / 2;
+  constexpr int FP = NB * 8;
+  extern __shared__ __align__(128) unsigned char kcg_smem[];
+  double* buf = reinterpret_cast<double*>(kcg_smem);
+  const int stage_d = kDmmaRows * F;
+  double* red = buf + stages * stage_d;  // [FP][FP] + s1[FP] + mx[FP]
+  double* red_s1 = red + FP * FP;
+  double* red_mx = red_s1 + FP;
+  __shared__ __align__(8) unsigned long long full[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  for (int k = tid; k < FP * FP + 2 * FP; k += blockDim.x) red[k] = 0.0;
+  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);
+  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fb + 8 * s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const kcg_i64 ntiles = n / kDmmaRows;
+  const unsigned bytes = (unsigned)(stage_d * 8);
+  auto issue = [&](int s, kcg_i64 tile) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb + 8 * s), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     bb + (unsigned)(s * stage_d * 8)),
+                 "l"(X + tile * stage_d), "r"(bytes), "r"(fb + 8 * s)
+                 : "memory");
+  };
+  if (tid == 0)
+    for (int s = 0; s < stages; ++s) {
+      const kcg_i64 t = blockIdx.x + (kcg_i64)s * gridDim.x;
+      if (t < ntiles) issue(s, t);
+    }
+  double acc[NT][2];
+#pragma unroll
+  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
+  double s1[NB], mx[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) s1[b] = mx[b] = 0.0;
+
+  auto kstep = [&](const double* rowp, bool valid) {
+    double v[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int col = 8 * b + gid;
+      v[b] = (valid && col < F) ? rowp[col] : 0.0;
+      s1[b] += v[b];
+      mx[b] = fmax(mx[b], fabs(v[b]));
+    }
+    int t = 0;
+#pragma unroll
+    for (int I = 0; I < NB; ++I)
+#pragma unroll
+      for (int J = I; J < NB; ++J, ++t) dmma_8x8x4(acc[t][0], acc[t][1], v[I], v[J]);
+  };
+
+  for (kcg_i64 k = 0;; ++k) {
+    const kcg_i64 tile = blockIdx.x + k * gridDim.x;
+    if (tile >= ntiles) break;
+    const int s = (int)(k % stages);
+    const unsigned parity = (unsigned)((k / stages) & 1);
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(fb + 8 * s), "r"(parity)
+                   : "memory");
+    const double* st = buf + s * stage_d;
+    // 8 warps x 2 k-steps x 4 rows = 64 rows
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) kstep(st + (warp * 8 + ks * 4 + tig) * F, true);
+    __syncthreads();
+    if (tid == 0) {
+      const kcg_i64 nt = blockIdx.x + (k + stages) * gridDim.x;
+      if (nt < ntiles) issue(s, nt);
+    }
+  }
+  // tail rows straight from global (block 0 only)
+  if (blockIdx.x == 0)
+    for (kcg_i64 r0 = ntiles * kDmmaRows + warp * 4; r0 < n; r0 += 32) {
+      const kcg_i64 r = r0 + tig;
+      kstep(X + (r < n ? r : 0) * F, r < n);
+    }
+  // reduce warps through shared memory, then one atomic per entry
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    double a = s1[b], m = mx[b];
+    a += __shfl_xor_sync(0xffffffffu, a, 1);
+    a += __shfl_xor_sync(0xffffffffu, a, 2);
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
+    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+    if (tig == 0) {
+      atomicAdd(red_s1 + 8 * b + gid, a);
+      atomicMax(reinterpret_cast<unsigned long long*>(red_mx + 8 * b + gid),
+                (unsigned long long)__double_as_longlong(m));
+    }
+  }
+  {
+    int t = 0;
+#pragma unroll
+    for (int I = 0; I < NB; ++I)
+#pragma unroll
+      for (int J = I; J < NB; ++J, ++t) {
+        atomicAdd(red + (8 * I + gid) * FP + 8 * J + 2 * tig, acc[t][0]);
+        atomicAdd(red + (8 * I + gid) * FP + 8 * J + 2 * tig + 1, acc[t][1]);
+      }
+  }
+  __syncthreads();
+  for (int e = tid; e < FP * FP; e += blockDim.x) {
+    const int r = e / FP, c = e % FP;
+    if (r >= F || c >= F || (c / 8) < (r / 8)) continue;  // upper block triangle holds the data
+    const double v = red[e];
+    atomicAdd(G + r * F + c, v);
+    if (c / 8 != r / 8) atomicAdd(G + c * F + r, v);
+  }
+  for (int c = tid; c < F; c += blockDim.x) {
+    atomicAdd(xt1 + c, red_s1[c]);
+    atomicMax(reinterpret_cast<unsigned long long*>(cmax + c),
+              (unsigned long long)__double_as_longlong(red_mx[c]));
+  }
+}
+
+template <int NB>
+void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, double* colmax,
+                      cudaStream_t stream) {
+  const int stages = F <= 40 ? 4 : 3;
+  const size_t smem = (size_t)(stages * kDmmaRows * F + NB * 8 * NB * 8 + 2 * NB * 8) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    check(cudaFuncSetAttribute(kcg_gram_dmma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem + 4096),
+          "cudaFuncSetAttribute");
+    attr = true;
+  }
+  const kcg_i64 tiles = (kcg_i64)n / kDmmaRows;
+  kcg_i64 grid = (kcg_i64)num_sms() * 2;
+  if (grid > tiles) grid = tiles > 0 ? tiles : 1;
+  kcg_gram_dmma<NB><<<(unsigned)grid, 256, smem, stream>>>(X, (kcg_i64)n, F, stages, G, xt1, colmax);
+  check(cudaGetLastError(), "kcg_gram_dmma launch");
+}
+
 // warp per row: lanes own columns lane and lane+32
 template <bool GRAD>
 __global__ void __launch_bounds__(256)
@@ -351,6 +518,19 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
                  double* colmax, void* stream) {
   if (n == 0) return;
   if (F < 1 || F > kGramMaxF) throw std::invalid_argument("gram: n_cols must be in [1, 64]");
+  static const bool no_dmma = std::getenv("KCG_NO_DMMA") != nullptr;
+  if (!no_dmma && ld == (size_t)F && F <= 48 && F % 2 == 0 &&
+      reinterpret_cast<uintptr_t>(X) % 16 == 0) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    switch ((F + 7) / 8) {
+      case 1: return launch_gram_dmma<1>(X, n, F, G, xt1, colmax, st);
+      case 2: return launch_gram_dmma<2>(X, n, F, G, xt1, colmax, st);
+      case 3: return launch_gram_dmma<3>(X, n, F, G, xt1, colmax, st);
+      case 4: return launch_gram_dmma<4>(X, n, F, G, xt1, colmax, st);
+      case 5: return launch_gram_dmma<5>(X, n, F, G, xt1, colmax, st);
+      default: return launch_gram_dmma<6>(X, n, F, G, xt1, colmax, st);
+    }
+  }
   const GramGeom g = gram_geom(F);
   const size_t smem = (size_t)(kGramRows * g.FP + g.ntiles * 16 + 2 * g.FP) * sizeof(double);
   static bool attr = false;
