@@ -109,6 +109,12 @@ int kcg_program_set_engine(kcg_program* prog, int engine);
 /* CUDA source the JIT path compiles for this program (NUL-terminated,
  * owned by the program) -- for inspection and tests                       */
 const char* kcg_program_jit_source(kcg_program* prog);
+/* source of the other specialised kernels: kind 0 eval, 1 fused Gram,
+ * 2 fused residual (owned by the program, valid until the next call)     */
+const char* kcg_program_jit_source_kind(kcg_program* prog, int kind);
+/* NVRTC-compiles `src` for sm_100a without loading it (no GPU needed);
+ * KCG_OK or KCG_E_JIT with the compiler log in kcg_last_error()          */
+int kcg_jit_compile_check(const char* src, const char* name);
 
 /* ---- fused evaluate_properties + predict -------------------------------
  * param_cols: host array of n_params DEVICE pointers, each n_points int64

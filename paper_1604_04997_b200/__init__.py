@@ -21,6 +21,7 @@ from .api import (  # noqa: F401
     noiseless_time,
     predict,
     read_weights_json,
+    residual_fused,
     schema_index,
     schema_keys,
     schema_size,

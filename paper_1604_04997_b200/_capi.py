@@ -55,6 +55,8 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_program_safe_bounds": (ctypes.c_int, [P, I64P, I64P]),
         "kcg_program_set_engine": (ctypes.c_int, [P, ctypes.c_int]),
         "kcg_program_jit_source": (ctypes.c_char_p, [P]),
+        "kcg_program_jit_source_kind": (ctypes.c_char_p, [P, ctypes.c_int]),
+        "kcg_jit_compile_check": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p]),
         "kcg_eval_predict": (ctypes.c_int, [P, P, ctypes.c_size_t, DP, P, P, P, P, ctypes.c_int, P]),
         "kcg_argmin": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_size_t, DP, P, P, P, P]),
         "kcg_gram_accumulate": (ctypes.c_int, [P, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t, P, P, P, P]),

@@ -308,6 +308,17 @@ def gram_fused(prog: Program, bindings, T, stats: GramStats | None = None, strea
     return stats
 
 
+def residual_fused(prog: Program, bindings, T, alpha149: Sequence[float], stream=None) -> float:
+    """Objective sum_r (1 - x_r . alpha)^2 of the fit (model.cpp:81-92) with
+    rows x_r = count/T formed from the bindings on the fly."""
+    torch = _torch()
+    arr, n, cols = _columns(prog, bindings)
+    obj = torch.zeros(1, dtype=torch.float64, device=cols[0].device)
+    a = (ctypes.c_double * len(alpha149))(*alpha149)
+    check(lib().kcg_residual_fused(prog.handle, arr, T.data_ptr(), n, a, obj.data_ptr(), _stream(stream)))
+    return float(obj.item())
+
+
 def solve_gram(stats: GramStats) -> tuple[list[float], int]:
     """Host minimum-norm solve of the equilibrated normal equations."""
     G = stats.G.double().cpu().contiguous()

@@ -32,6 +32,7 @@ struct kcg_program {
   KcgDevProg* dprog = nullptr;  // device image (interpreter), lazily uploaded
   bool dprog_ok = true;         // fits the interpreter's static tables
   std::string jit_src;
+  std::string jit_src_kind;
   void* jit_eval = nullptr;
   void* jit_eval_gen = nullptr;
   void* jit_eval_tma = nullptr;
@@ -315,6 +316,24 @@ const char* kcg_program_jit_source(kcg_program* p) {
     p->jit_src = kcg::codegen({&p->low}, {identity(p->low.n_params)}, p->low.n_params,
                               kcg::JitKind::eval, kname("kcg_eval_", p));
   return p->jit_src.c_str();
+}
+
+const char* kcg_program_jit_source_kind(kcg_program* p, int kind) {
+  if (!p || kind < 0 || kind > 2) return nullptr;
+  if (kind == 0) return kcg_program_jit_source(p);
+  const int np = p->low.n_params;
+  p->jit_src_kind = kcg::codegen({&p->low}, {identity(np)}, np,
+                                 kind == 1 ? kcg::JitKind::gram : kcg::JitKind::residual,
+                                 kname(kind == 1 ? "kcg_gram_" : "kcg_resid_", p));
+  return p->jit_src_kind.c_str();
+}
+
+int kcg_jit_compile_check(const char* src, const char* name) {
+  if (!src || !name) return fail(KCG_E_INVALID_ARGUMENT, "null argument");
+  return guarded([&] {
+    kcg::jit_compile_only(src, name);
+    return KCG_OK;
+  });
 }
 
 int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, size_t n,

@@ -720,6 +720,89 @@ std::string codegen(const std::vector<const Lowered*>& progs,
      << FA << "]; const int st = kcg_fasti_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n"
               "  if (cls == 2) return kcg_row_wide(p, t, x);\n"
               "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
+  if (kind == JitKind::gram && F >= 1 && F <= 48) {
+    // rows formed in registers (fast path: RN(count) doubles, x = c / T with
+    // a correctly rounded Markstein division sharing one reciprocal), staged
+    // per warp in shared memory in the DMMA fragment layout, reduced on the
+    // FP64 tensor cores (mma.sync m8n8k4 f64) over the upper block triangle.
+    const int NB = (F + 7) / 8, NT = NB * (NB + 1) / 2, FP = NB * 8, LDX = FP + 1;
+    os << "struct KcgArgs { const kcg_i64* p[" << NP
+       << "]; const double* t; double* G; double* xt1; double* cmax; "
+          "unsigned long long* bad; kcg_i64 n; };\n";
+    os << "__device__ __forceinline__ double kcg_div(double c, double t, double r) {\n"
+          "  const double q = __dmul_rn(c, r);\n  const double e = fma(-q, t, c);\n  return fma(e, r, q);\n}\n";
+    os << "__device__ __noinline__ int kcg_row_slow(const kcg_i64* p, double t, double* x) { return kcg_row_any(p, t, x); }\n";
+    os << "extern \"C\" __global__ void __launch_bounds__(256) " << name
+       << "(const __grid_constant__ KcgArgs a) {\n"
+          "  constexpr int F = " << F << ", NB = " << NB << ", NT = " << NT << ", FP = " << FP << ", LDX = " << LDX << ";\n"
+          "  __shared__ double xs[8][32 * LDX];\n"
+          "  __shared__ double red[FP * FP + 2 * FP];\n"
+          "  __shared__ unsigned long long red_bad;\n"
+          "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gid = lane >> 2, tig = lane & 3;\n"
+          "  for (int k = tid; k < FP * FP + 2 * FP; k += blockDim.x) red[k] = 0.0;\n"
+          "  if (tid == 0) red_bad = 0;\n"
+          "  double acc[NT][2];\n  #pragma unroll\n  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;\n"
+          "  double s1[NB], mx[NB];\n  #pragma unroll\n  for (int b = 0; b < NB; ++b) s1[b] = mx[b] = 0.0;\n"
+          "  unsigned long long bad = 0;\n"
+          "  double* xw = xs[warp];\n"
+          "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
+          "  const kcg_i64 nr = (a.n + 31) / 32 * 32;\n"
+          "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + tid; i < nr; i += stride) {\n"
+          "    double x[FP];\n    #pragma unroll\n    for (int j = 0; j < FP; ++j) x[j] = 0.0;\n"
+          "    if (i < a.n) {\n"
+          "      kcg_i64 p[" << NP << "];\n";
+    for (int j = 0; j < n_cols; ++j) os << "      p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
+    os << "      const double t = __ldcs(a.t + i);\n"
+          "      int st;\n"
+          "      if (t > 0.0 && kcg_class_0(p) == 1) {\n"
+          "        double c[F];\n        st = kcg_fastd_0(p, c);\n"
+          "        const double r = __drcp_rn(t);\n"
+          "        #pragma unroll\n        for (int j = 0; j < F; ++j) x[j] = kcg_div(c[j], t, r);\n"
+          "      } else {\n        st = kcg_row_slow(p, t, x);\n      }\n"
+          "      if (st != KCG_PT_OK) {\n        ++bad;\n        #pragma unroll\n        for (int j = 0; j < FP; ++j) x[j] = 0.0;\n      }\n"
+          "    }\n"
+          "    #pragma unroll\n    for (int j = 0; j < FP; ++j) xw[lane * LDX + j] = x[j];\n"
+          "    __syncwarp();\n"
+          "    #pragma unroll\n    for (int ks = 0; ks < 8; ++ks) {\n"
+          "      const double* row = xw + (4 * ks + tig) * LDX;\n"
+          "      double v[NB];\n"
+          "      #pragma unroll\n      for (int b = 0; b < NB; ++b) { v[b] = row[8 * b + gid]; s1[b] += v[b]; mx[b] = fmax(mx[b], fabs(v[b])); }\n"
+          "      int t = 0;\n"
+          "      #pragma unroll\n      for (int I = 0; I < NB; ++I)\n"
+          "        #pragma unroll\n        for (int J = I; J < NB; ++J, ++t)\n"
+          "          asm volatile(\"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\"\n"
+          "                       : \"+d\"(acc[t][0]), \"+d\"(acc[t][1]) : \"d\"(v[I]), \"d\"(v[J]));\n"
+          "    }\n"
+          "    __syncwarp();\n"
+          "  }\n"
+          "  __syncthreads();\n"
+          "  #pragma unroll\n  for (int b = 0; b < NB; ++b) {\n"
+          "    double s = s1[b], m = mx[b];\n"
+          "    s += __shfl_xor_sync(0xffffffffu, s, 1); s += __shfl_xor_sync(0xffffffffu, s, 2);\n"
+          "    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1)); m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));\n"
+          "    if (tig == 0) { atomicAdd(red + FP * FP + 8 * b + gid, s);\n"
+          "      atomicMax((unsigned long long*)(red + FP * FP + FP + 8 * b + gid), (unsigned long long)__double_as_longlong(m)); }\n"
+          "  }\n"
+          "  { int t = 0;\n    #pragma unroll\n    for (int I = 0; I < NB; ++I)\n      #pragma unroll\n      for (int J = I; J < NB; ++J, ++t) {\n"
+          "        atomicAdd(red + (8 * I + gid) * FP + 8 * J + 2 * tig, acc[t][0]);\n"
+          "        atomicAdd(red + (8 * I + gid) * FP + 8 * J + 2 * tig + 1, acc[t][1]); } }\n"
+          "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);\n"
+          "  if (lane == 0 && bad) atomicAdd(&red_bad, bad);\n"
+          "  __syncthreads();\n"
+          "  for (int e = tid; e < FP * FP; e += blockDim.x) {\n"
+          "    const int r = e / FP, c = e % FP;\n"
+          "    if (r >= F || c >= F || (c / 8) < (r / 8)) continue;\n"
+          "    atomicAdd(a.G + r * F + c, red[e]);\n"
+          "    if (c / 8 != r / 8) atomicAdd(a.G + c * F + r, red[e]);\n"
+          "  }\n"
+          "  for (int c = tid; c < F; c += blockDim.x) {\n"
+          "    atomicAdd(a.xt1 + c, red[FP * FP + c]);\n"
+          "    atomicMax((unsigned long long*)(a.cmax + c), (unsigned long long)__double_as_longlong(red[FP * FP + FP + c]));\n"
+          "  }\n"
+          "  if (tid == 0 && a.bad && red_bad) atomicAdd(a.bad, red_bad);\n"
+          "}\n";
+    return os.str();
+  }
   if (kind == JitKind::gram) {
     os << "struct KcgArgs { const kcg_i64* p[" << NP
        << "]; const double* t; double* G; double* xt1; double* cmax; "

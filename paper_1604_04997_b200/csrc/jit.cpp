@@ -73,6 +73,8 @@ std::vector<char> compile(const std::string& src, const std::string& name) {
 
 }  // namespace
 
+void jit_compile_only(const std::string& src, const std::string& name) { compile(src, name); }
+
 void* jit_kernel(const std::string& src, const std::string& name) {
   char hex[32];
   std::snprintf(hex, sizeof hex, "%016llx",

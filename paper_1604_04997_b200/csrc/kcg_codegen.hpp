@@ -21,6 +21,9 @@ std::string codegen(const std::vector<const Lowered*>& progs,
 /// returns an opaque kernel handle usable with launch_jit(). Throws KcgError.
 void* jit_kernel(const std::string& src, const std::string& name);
 
+/// NVRTC compile only (no module load, no GPU needed); throws KcgError.
+void jit_compile_only(const std::string& src, const std::string& name);
+
 /// Launches a JIT kernel with a single by-value argument struct.
 void launch_jit(void* kernel, const void* args, size_t args_size,
                 unsigned grid, unsigned block, void* stream, size_t smem = 0);

@@ -166,3 +166,28 @@ def test_host_solve_suite_design_matches_reference(suite_alpha):
             assert abs(got - suite_alpha[c]) <= 1e-6 * abs(suite_alpha[c]), ko.SCHEMA[c]
         else:
             assert abs(got) <= 1e-15
+
+
+@pytest.mark.parametrize("kid", ["matmul_tiled_g16x16", "matmul_skinny_g16x16", "conv_g16x16",
+                                 "arith_div_g16x12", "stride2_fill_g192", "transpose_tile_g16x16"])
+def test_generated_kernels_compile_for_sm100a(kid):
+    """NVRTC (sm_100a) accepts every specialised kernel family for the
+    program -- eval (+ _gen, _tma), fused Gram (DMMA), fused residual."""
+    p = kc.load_program(kid)
+    L = _capi.lib()
+    for kind, base in ((0, "kcg_eval_"), (1, "kcg_gram_"), (2, "kcg_resid_")):
+        src = L.kcg_program_jit_source_kind(p.handle, kind)
+        rc = L.kcg_jit_compile_check(src, (base + kid).encode())
+        assert rc == 0, L.kcg_last_error().decode()[:3000]
+
+
+def test_generated_kernels_compile_for_atom_programs():
+    d = load_golden("extra_programs.json")
+    L = _capi.lib()
+    for q in d["programs"]:
+        if "program" not in q:
+            continue
+        p = kc.Program(q["program"])
+        for kind in (0, 1):
+            rc = L.kcg_jit_compile_check(L.kcg_program_jit_source_kind(p.handle, kind), b"k")
+            assert rc == 0, L.kcg_last_error().decode()[:3000]

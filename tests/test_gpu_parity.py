@@ -269,12 +269,22 @@ def test_gram_fused_matches_oracle_rows():
         T.append(t)
     X = np.array(rows)
     cols = _cols(prog, bs)
-    st = kc.gram_fused(prog, cols, torch.tensor(T, dtype=torch.float64, device="cuda"))
+    Td = torch.tensor(T, dtype=torch.float64, device="cuda")
+    st = kc.gram_fused(prog, cols, Td)
     torch.cuda.synchronize()
     assert st.bad_rows == 1
     np.testing.assert_allclose(st.G.cpu().numpy(), X.T @ X, rtol=1e-11)
     np.testing.assert_allclose(st.xt1.cpu().numpy(), X.sum(axis=0), rtol=1e-11)
+    # rows are c/T correctly rounded (Markstein division) -> colmax bitwise
     assert (st.colmax.cpu().numpy() == np.abs(X).max(axis=0)).all()
+    # fused residual pass == numpy objective at some weights
+    alpha = [0.0] * 149
+    for j, k in enumerate(prog.props):
+        alpha[k] = sim[k] * 1.001 + 1e-15
+    got = kc.residual_fused(prog, cols, Td, alpha)
+    a = np.array([alpha[k] for k in prog.props])
+    r = 1.0 - X @ a
+    assert got == pytest.approx(float(r @ r), rel=1e-9)
 
 
 def test_no_silent_fallback_launches_counted():
