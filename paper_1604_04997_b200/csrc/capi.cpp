@@ -525,8 +525,15 @@ int kcg_gram_fused(const kcg_program* cp, const int64_t* const* param_cols, cons
     ab.push<void*>(colmax);
     ab.push<void*>(bad_rows);
     ab.push<int64_t>(static_cast<int64_t>(n));
+    bool vec = reinterpret_cast<uintptr_t>(T) % 16 == 0;
+    for (int j = 0; j < np; ++j) vec = vec && reinterpret_cast<uintptr_t>(param_cols[j]) % 16 == 0;
+    ab.push<int32_t>(vec ? 1 : 0);
     ab.finish();
-    kcg::launch_jit(p->jit_gram, ab.b.data(), ab.b.size(), grid_for(n, 256, 4), 256, stream);
+    // persistent TMA-streamed kernel (2 CTAs/SM for the DMMA variant)
+    const size_t F = p->low.keys.size();
+    const unsigned per_sm = (F >= 1 && F <= 48) ? 2 : 1;
+    kcg::launch_jit(p->jit_gram, ab.b.data(), ab.b.size(), kcg::num_sms() * per_sm, 256, stream,
+                    kcg::fused_smem_bytes(np));
     ++g_launches;
     return KCG_OK;
   });
@@ -575,11 +582,15 @@ int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, 
     ab.push<const void*>(T);
     ab.push<void*>(obj);
     ab.push<int64_t>(static_cast<int64_t>(n));
+    bool vec = reinterpret_cast<uintptr_t>(T) % 16 == 0;
+    for (int j = 0; j < np; ++j) vec = vec && reinterpret_cast<uintptr_t>(param_cols[j]) % 16 == 0;
+    ab.push<int32_t>(vec ? 1 : 0);
     std::vector<double> al(std::max(F, 1), 0.0);
     compact_alpha(p, alpha, al.data());
     for (double v : al) ab.push<double>(v);
     ab.finish();
-    kcg::launch_jit(p->jit_resid, ab.b.data(), ab.b.size(), grid_for(n, 256, 8), 256, stream);
+    kcg::launch_jit(p->jit_resid, ab.b.data(), ab.b.size(), kcg::num_sms(), 256, stream,
+                    kcg::fused_smem_bytes(np));
     ++g_launches;
     return KCG_OK;
   });

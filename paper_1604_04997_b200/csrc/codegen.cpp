@@ -14,6 +14,7 @@
 // The kernels around them: fused evaluate+predict (4 points per thread,
 // 16-byte vector loads/stores), argmin over variants, and the fused
 // design-row Gram / residual reductions.
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <sstream>
@@ -619,6 +620,12 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 
 int tma_ctas_per_sm() { return tma_ctas(); }
 
+size_t fused_smem_bytes(int n_cols) {
+  const int NC = n_cols + 1;
+  const int S = std::max(2, std::min(8, (tma_ring_kb() * 1024) / (NC * kTmaTile * 8)));
+  return static_cast<size_t>(S) * NC * kTmaTile * 8;
+}
+
 size_t tma_smem_bytes(int n_cols) {
   return static_cast<size_t>(tma_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * kTmaTile * 8;
 }
@@ -705,170 +712,227 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   const Lowered& L = *progs[0];
   const int F = static_cast<int>(L.keys.size());
   const int FA = F > 0 ? F : 1;
-  const int NG = F * (F + 1) / 2;
+  const bool gram = kind == JitKind::gram;
+  const bool dmma = gram && F >= 1 && F <= 48;
+  const int NB = (F + 7) / 8, NT = NB * (NB + 1) / 2, FP = NB * 8, LDX = FP + 1;
+  const int NC = n_cols + 1;  // parameter columns + T
+  const int S = std::max(2, std::min(8, (tma_ring_kb() * 1024) / (NC * kTmaTile * 8)));
+  if (gram)
+    os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* G; double* xt1; "
+          "double* cmax; unsigned long long* bad; kcg_i64 n; int vec; };\n";
+  else
+    os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* obj; kcg_i64 n; "
+          "int vec; double alpha[" << FA << "]; };\n";
+  // x = c / t correctly rounded (Markstein: one reciprocal per row, exact
+  // residual by FMA, final FMA correction)
+  os << "__device__ __forceinline__ double kcg_div(double c, double t, double r) {\n"
+        "  const double q = __dmul_rn(c, r);\n  const double e = fma(-q, t, c);\n  return fma(e, r, q);\n}\n";
   os << "template <class T> __device__ __forceinline__ void kcg_xrow(const T* c, double t, double* x) {\n";
   for (int j = 0; j < F; ++j)
     os << "  x[" << j << "] = (c[" << j << "] != 0) ? __ddiv_rn(kcg_to_double(c[" << j << "]), t) : 0.0;\n";
   os << "}\n";
-  os << "__device__ __noinline__ int kcg_row_wide(const kcg_i64* p, double t, double* x) {\n"
-        "  kcg_i128 c["
-     << FA << "];\n  const int st = kcg_wide_0(p, c);\n  if (st == KCG_PT_OK) kcg_xrow(c, t, x);\n  return st;\n}\n";
-  os << "__device__ __forceinline__ int kcg_row_any(const kcg_i64* p, double t, double* x) {\n"
+  // out-of-line row: reloads its inputs (no address-taken locals in callers)
+  os << "__device__ __noinline__ int kcg_row_i(const KcgArgs& a, kcg_i64 i, double* x) {\n"
+        "  kcg_i64 p["
+     << NP << "];\n";
+  for (int j = 0; j < n_cols; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
+  os << "  const double t = a.t[i];\n"
         "  if (!(t > 0.0)) return KCG_PT_ASSUMPTION_VIOLATED;\n"
         "  const int cls = kcg_class_0(p);\n"
         "  if (cls == 1) { kcg_i64 c["
      << FA << "]; const int st = kcg_fasti_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n"
-              "  if (cls == 2) return kcg_row_wide(p, t, x);\n"
+              "  if (cls == 2) { kcg_i128 c["
+     << FA << "]; const int st = kcg_wide_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n"
               "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
-  if (kind == JitKind::gram && F >= 1 && F <= 48) {
-    // rows formed in registers (fast path: RN(count) doubles, x = c / T with
-    // a correctly rounded Markstein division sharing one reciprocal), staged
-    // per warp in shared memory in the DMMA fragment layout, reduced on the
-    // FP64 tensor cores (mma.sync m8n8k4 f64) over the upper block triangle.
-    const int NB = (F + 7) / 8, NT = NB * (NB + 1) / 2, FP = NB * 8, LDX = FP + 1;
-    os << "struct KcgArgs { const kcg_i64* p[" << NP
-       << "]; const double* t; double* G; double* xt1; double* cmax; "
-          "unsigned long long* bad; kcg_i64 n; };\n";
-    os << "__device__ __forceinline__ double kcg_div(double c, double t, double r) {\n"
-          "  const double q = __dmul_rn(c, r);\n  const double e = fma(-q, t, c);\n  return fma(e, r, q);\n}\n";
-    os << "__device__ __noinline__ int kcg_row_slow(const kcg_i64* p, double t, double* x) { return kcg_row_any(p, t, x); }\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(256) " << name
-       << "(const __grid_constant__ KcgArgs a) {\n"
-          "  constexpr int F = " << F << ", NB = " << NB << ", NT = " << NT << ", FP = " << FP << ", LDX = " << LDX << ";\n"
-          "  __shared__ double xs[8][32 * LDX];\n"
-          "  __shared__ double red[FP * FP + 2 * FP];\n"
-          "  __shared__ unsigned long long red_bad;\n"
-          "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, gid = lane >> 2, tig = lane & 3;\n"
-          "  for (int k = tid; k < FP * FP + 2 * FP; k += blockDim.x) red[k] = 0.0;\n"
-          "  if (tid == 0) red_bad = 0;\n"
-          "  double acc[NT][2];\n  #pragma unroll\n  for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;\n"
-          "  double s1[NB], mx[NB];\n  #pragma unroll\n  for (int b = 0; b < NB; ++b) s1[b] = mx[b] = 0.0;\n"
-          "  unsigned long long bad = 0;\n"
-          "  double* xw = xs[warp];\n"
-          "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
-          "  const kcg_i64 nr = (a.n + 31) / 32 * 32;\n"
-          "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + tid; i < nr; i += stride) {\n"
-          "    double x[FP];\n    #pragma unroll\n    for (int j = 0; j < FP; ++j) x[j] = 0.0;\n"
-          "    if (i < a.n) {\n"
-          "      kcg_i64 p[" << NP << "];\n";
-    for (int j = 0; j < n_cols; ++j) os << "      p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
-    os << "      const double t = __ldcs(a.t + i);\n"
-          "      int st;\n"
-          "      if (t > 0.0 && kcg_class_0(p) == 1) {\n"
-          "        double c[F];\n        st = kcg_fastd_0(p, c);\n"
-          "        const double r = __drcp_rn(t);\n"
-          "        #pragma unroll\n        for (int j = 0; j < F; ++j) x[j] = kcg_div(c[j], t, r);\n"
-          "      } else {\n        st = kcg_row_slow(p, t, x);\n      }\n"
-          "      if (st != KCG_PT_OK) {\n        ++bad;\n        #pragma unroll\n        for (int j = 0; j < FP; ++j) x[j] = 0.0;\n      }\n"
-          "    }\n"
-          "    #pragma unroll\n    for (int j = 0; j < FP; ++j) xw[lane * LDX + j] = x[j];\n"
-          "    __syncwarp();\n"
-          "    #pragma unroll\n    for (int ks = 0; ks < 8; ++ks) {\n"
-          "      const double* row = xw + (4 * ks + tig) * LDX;\n"
-          "      double v[NB];\n"
-          "      #pragma unroll\n      for (int b = 0; b < NB; ++b) { v[b] = row[8 * b + gid]; s1[b] += v[b]; mx[b] = fmax(mx[b], fabs(v[b])); }\n"
-          "      int t = 0;\n"
-          "      #pragma unroll\n      for (int I = 0; I < NB; ++I)\n"
-          "        #pragma unroll\n        for (int J = I; J < NB; ++J, ++t)\n"
-          "          asm volatile(\"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\"\n"
-          "                       : \"+d\"(acc[t][0]), \"+d\"(acc[t][1]) : \"d\"(v[I]), \"d\"(v[J]));\n"
-          "    }\n"
-          "    __syncwarp();\n"
-          "  }\n"
-          "  __syncthreads();\n"
-          "  #pragma unroll\n  for (int b = 0; b < NB; ++b) {\n"
-          "    double s = s1[b], m = mx[b];\n"
-          "    s += __shfl_xor_sync(0xffffffffu, s, 1); s += __shfl_xor_sync(0xffffffffu, s, 2);\n"
-          "    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1)); m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));\n"
-          "    if (tig == 0) { atomicAdd(red + FP * FP + 8 * b + gid, s);\n"
-          "      atomicMax((unsigned long long*)(red + FP * FP + FP + 8 * b + gid), (unsigned long long)__double_as_longlong(m)); }\n"
-          "  }\n"
-          "  { int t = 0;\n    #pragma unroll\n    for (int I = 0; I < NB; ++I)\n      #pragma unroll\n      for (int J = I; J < NB; ++J, ++t) {\n"
-          "        atomicAdd(red + (8 * I + gid) * FP + 8 * J + 2 * tig, acc[t][0]);\n"
-          "        atomicAdd(red + (8 * I + gid) * FP + 8 * J + 2 * tig + 1, acc[t][1]); } }\n"
-          "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);\n"
-          "  if (lane == 0 && bad) atomicAdd(&red_bad, bad);\n"
-          "  __syncthreads();\n"
-          "  for (int e = tid; e < FP * FP; e += blockDim.x) {\n"
-          "    const int r = e / FP, c = e % FP;\n"
-          "    if (r >= F || c >= F || (c / 8) < (r / 8)) continue;\n"
-          "    atomicAdd(a.G + r * F + c, red[e]);\n"
-          "    if (c / 8 != r / 8) atomicAdd(a.G + c * F + r, red[e]);\n"
-          "  }\n"
-          "  for (int c = tid; c < F; c += blockDim.x) {\n"
-          "    atomicAdd(a.xt1 + c, red[FP * FP + c]);\n"
-          "    atomicMax((unsigned long long*)(a.cmax + c), (unsigned long long)__double_as_longlong(red[FP * FP + FP + c]));\n"
-          "  }\n"
-          "  if (tid == 0 && a.bad && red_bad) atomicAdd(a.bad, red_bad);\n"
-          "}\n";
-    return os.str();
-  }
-  if (kind == JitKind::gram) {
-    os << "struct KcgArgs { const kcg_i64* p[" << NP
-       << "]; const double* t; double* G; double* xt1; double* cmax; "
-          "unsigned long long* bad; kcg_i64 n; };\n";
-    os << "extern \"C\" __global__ void __launch_bounds__(256) " << name
-       << "(const __grid_constant__ KcgArgs a) {\n"
-          "  double g["
-       << (NG ? NG : 1) << "], s1[" << FA << "], mx[" << FA << "];\n  #pragma unroll\n  for (int k = 0; k < "
-       << NG << "; ++k) g[k] = 0.0;\n  #pragma unroll\n  for (int k = 0; k < " << F
-       << "; ++k) { s1[k] = 0.0; mx[k] = 0.0; }\n"
-          "  unsigned long long bad = 0;\n"
-          "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
-          "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {\n"
-          "    kcg_i64 p["
-       << NP << "];\n";
-    for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
-    os << "    double x[" << FA << "];\n"
-          "    if (kcg_row_any(p, __ldcs(a.t + i), x) != KCG_PT_OK) { ++bad; continue; }\n";
+  // fast row from registers; -1 -> caller uses kcg_row_i
+  os << "__device__ __forceinline__ int kcg_row_fast(const kcg_i64* p, double t, double* x) {\n"
+        "  if (!(t > 0.0) || kcg_class_0(p) != 1) return -1;\n"
+        "  double c["
+     << FA << "];\n  const int st = kcg_fastd_0(p, c);\n  const double r = __drcp_rn(t);\n"
+              "  #pragma unroll\n  for (int j = 0; j < "
+     << F << "; ++j) x[j] = kcg_div(c[j], t, r);\n  return st;\n}\n";
+
+  // ---- per-row consumer ---------------------------------------------------
+  std::ostringstream cons_decl, cons_row, cons_end;
+  if (dmma) {
+    cons_decl << "  __shared__ double xs[8][32 * " << LDX << "];\n"
+              << "  __shared__ double red[" << FP * FP + 2 * FP << "];\n"
+              << "  __shared__ unsigned long long red_bad;\n"
+              << "  for (int k = threadIdx.x; k < " << FP * FP + 2 * FP << "; k += blockDim.x) red[k] = 0.0;\n"
+              << "  if (threadIdx.x == 0) red_bad = 0;\n"
+              << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;\n"
+              << "  double acc[" << NT << "][2];\n  #pragma unroll\n  for (int t = 0; t < " << NT
+              << "; ++t) acc[t][0] = acc[t][1] = 0.0;\n"
+              << "  double s1[" << NB << "], mx[" << NB << "];\n  #pragma unroll\n  for (int b = 0; b < " << NB
+              << "; ++b) s1[b] = mx[b] = 0.0;\n"
+              << "  unsigned long long bad = 0;\n  double* xw = xs[warp];\n";
+    // consume x[FP] (zeros for skipped rows); warp-synchronous
+    cons_row << "      #pragma unroll\n      for (int j = 0; j < " << FP << "; ++j) xw[lane * " << LDX
+             << " + j] = x[j];\n"
+             << "      __syncwarp();\n"
+             << "      #pragma unroll\n      for (int ks = 0; ks < 8; ++ks) {\n"
+             << "        const double* row = xw + (4 * ks + tig) * " << LDX << ";\n"
+             << "        double v[" << NB << "];\n"
+             << "        #pragma unroll\n        for (int b = 0; b < " << NB
+             << "; ++b) { v[b] = row[8 * b + gid]; s1[b] += v[b]; mx[b] = fmax(mx[b], fabs(v[b])); }\n"
+             << "        int t = 0;\n"
+             << "        #pragma unroll\n        for (int I = 0; I < " << NB << "; ++I)\n"
+             << "          #pragma unroll\n          for (int J = I; J < " << NB << "; ++J, ++t)\n"
+             << "            asm volatile(\"mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\"\n"
+             << "                         : \"+d\"(acc[t][0]), \"+d\"(acc[t][1]) : \"d\"(v[I]), \"d\"(v[J]));\n"
+             << "      }\n      __syncwarp();\n";
+    cons_end << "  __syncthreads();\n"
+             << "  #pragma unroll\n  for (int b = 0; b < " << NB << "; ++b) {\n"
+             << "    double s = s1[b], m = mx[b];\n"
+             << "    s += __shfl_xor_sync(0xffffffffu, s, 1); s += __shfl_xor_sync(0xffffffffu, s, 2);\n"
+             << "    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1)); m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));\n"
+             << "    if (tig == 0) { atomicAdd(red + " << FP * FP << " + 8 * b + gid, s);\n"
+             << "      atomicMax((unsigned long long*)(red + " << FP * FP + FP
+             << " + 8 * b + gid), (unsigned long long)__double_as_longlong(m)); }\n  }\n"
+             << "  { int t = 0;\n    #pragma unroll\n    for (int I = 0; I < " << NB
+             << "; ++I)\n      #pragma unroll\n      for (int J = I; J < " << NB << "; ++J, ++t) {\n"
+             << "        atomicAdd(red + (8 * I + gid) * " << FP << " + 8 * J + 2 * tig, acc[t][0]);\n"
+             << "        atomicAdd(red + (8 * I + gid) * " << FP << " + 8 * J + 2 * tig + 1, acc[t][1]); } }\n"
+             << "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);\n"
+             << "  if (lane == 0 && bad) atomicAdd(&red_bad, bad);\n"
+             << "  __syncthreads();\n"
+             << "  for (int e = threadIdx.x; e < " << FP * FP << "; e += blockDim.x) {\n"
+             << "    const int r = e / " << FP << ", c = e % " << FP << ";\n"
+             << "    if (r >= " << F << " || c >= " << F << " || (c / 8) < (r / 8)) continue;\n"
+             << "    atomicAdd(a.G + r * " << F << " + c, red[e]);\n"
+             << "    if (c / 8 != r / 8) atomicAdd(a.G + c * " << F << " + r, red[e]);\n  }\n"
+             << "  for (int c = threadIdx.x; c < " << F << "; c += blockDim.x) {\n"
+             << "    atomicAdd(a.xt1 + c, red[" << FP * FP << " + c]);\n"
+             << "    atomicMax((unsigned long long*)(a.cmax + c), (unsigned long long)__double_as_longlong(red["
+             << FP * FP + FP << " + c]));\n  }\n"
+             << "  if (threadIdx.x == 0 && a.bad && red_bad) atomicAdd(a.bad, red_bad);\n";
+  } else if (gram) {
+    const int NG = F * (F + 1) / 2;
+    cons_decl << "  double g[" << (NG ? NG : 1) << "], s1[" << FA << "], mx[" << FA << "];\n"
+              << "  #pragma unroll\n  for (int k = 0; k < " << NG << "; ++k) g[k] = 0.0;\n"
+              << "  #pragma unroll\n  for (int k = 0; k < " << F << "; ++k) { s1[k] = 0.0; mx[k] = 0.0; }\n"
+              << "  unsigned long long bad = 0;\n";
     int k = 0;
     for (int r = 0; r < F; ++r) {
-      os << "    s1[" << r << "] += x[" << r << "]; mx[" << r << "] = fmax(mx[" << r << "], fabs(x[" << r
-         << "]));\n";
+      cons_row << "      s1[" << r << "] += x[" << r << "]; mx[" << r << "] = fmax(mx[" << r << "], fabs(x[" << r << "]));\n";
       for (int c = r; c < F; ++c, ++k)
-        os << "    g[" << k << "] = fma(x[" << r << "], x[" << c << "], g[" << k << "]);\n";
+        cons_row << "      g[" << k << "] = fma(x[" << r << "], x[" << c << "], g[" << k << "]);\n";
     }
-    os << "  }\n"
-          "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) {\n"
-          "    #pragma unroll\n    for (int k = 0; k < "
-       << NG << "; ++k) g[k] += __shfl_down_sync(0xffffffffu, g[k], o);\n"
-          "    #pragma unroll\n    for (int k = 0; k < "
-       << F << "; ++k) { s1[k] += __shfl_down_sync(0xffffffffu, s1[k], o); "
-          "mx[k] = fmax(mx[k], __shfl_down_sync(0xffffffffu, mx[k], o)); }\n"
-          "    bad += __shfl_down_sync(0xffffffffu, bad, o);\n  }\n"
-          "  if ((threadIdx.x & 31) == 0) {\n";
+    cons_end << "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) {\n"
+             << "    #pragma unroll\n    for (int k = 0; k < " << NG << "; ++k) g[k] += __shfl_down_sync(0xffffffffu, g[k], o);\n"
+             << "    #pragma unroll\n    for (int k = 0; k < " << F
+             << "; ++k) { s1[k] += __shfl_down_sync(0xffffffffu, s1[k], o); mx[k] = fmax(mx[k], __shfl_down_sync(0xffffffffu, mx[k], o)); }\n"
+             << "    bad += __shfl_down_sync(0xffffffffu, bad, o);\n  }\n"
+             << "  if ((threadIdx.x & 31) == 0) {\n";
     k = 0;
     for (int r = 0; r < F; ++r) {
-      os << "    atomicAdd(a.xt1 + " << r << ", s1[" << r << "]);\n";
-      os << "    atomicMax((unsigned long long*)(a.cmax + " << r
-         << "), (unsigned long long)__double_as_longlong(mx[" << r << "]));\n";
+      cons_end << "    atomicAdd(a.xt1 + " << r << ", s1[" << r << "]);\n"
+               << "    atomicMax((unsigned long long*)(a.cmax + " << r
+               << "), (unsigned long long)__double_as_longlong(mx[" << r << "]));\n";
       for (int c = r; c < F; ++c, ++k) {
-        os << "    atomicAdd(a.G + " << (r * F + c) << ", g[" << k << "]);\n";
-        if (c != r) os << "    atomicAdd(a.G + " << (c * F + r) << ", g[" << k << "]);\n";
+        cons_end << "    atomicAdd(a.G + " << (r * F + c) << ", g[" << k << "]);\n";
+        if (c != r) cons_end << "    atomicAdd(a.G + " << (c * F + r) << ", g[" << k << "]);\n";
       }
     }
-    os << "    if (a.bad && bad) atomicAdd(a.bad, bad);\n  }\n}\n";
-    return os.str();
+    cons_end << "    if (a.bad && bad) atomicAdd(a.bad, bad);\n  }\n";
+  } else {
+    cons_decl << "  double acc = 0.0;\n";
+    cons_row << "      if (ok) {\n        double pr = 0.0;\n";
+    for (int j = 0; j < F; ++j) cons_row << "        pr = fma(x[" << j << "], a.alpha[" << j << "], pr);\n";
+    cons_row << "        const double r = 1.0 - pr;\n        acc = fma(r, r, acc);\n      }\n";
+    cons_end << "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);\n"
+             << "  if ((threadIdx.x & 31) == 0) atomicAdd(a.obj, acc);\n";
   }
+  const int XW = dmma ? FP : FA;  // x row width
+  // produce row x for global index i from registers q/t (or out of line)
+  auto emit_make_row = [&](const char* qexpr, const char* texpr, const char* iexpr, const char* valid) {
+    os << "      double x[" << XW << "];\n      #pragma unroll\n      for (int j = 0; j < " << XW
+       << "; ++j) x[j] = 0.0;\n"
+       << "      bool ok = false;\n"
+       << "      if (" << valid << ") {\n"
+       << "        int st = kcg_row_fast(" << qexpr << ", " << texpr << ", x);\n"
+       << "        if (st < 0) st = kcg_row_i(a, " << iexpr << ", x);\n"
+       << "        ok = st == KCG_PT_OK;\n"
+       << "        if (!ok) {\n          #pragma unroll\n          for (int j = 0; j < " << XW
+       << "; ++j) x[j] = 0.0;\n";
+    if (gram) os << "          ++bad;\n";
+    os << "        }\n      }\n";
+  };
 
-  // residual: obj += (1 - x . alpha)^2
-  os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* obj; kcg_i64 n; double alpha["
-     << FA << "]; };\n";
-  os << "extern \"C\" __global__ void __launch_bounds__(256) " << name
+  os << "extern \"C\" __global__ void __launch_bounds__(256, " << (dmma ? 2 : 1) << ") " << name
      << "(const __grid_constant__ KcgArgs a) {\n"
-        "  double acc = 0.0;\n"
-        "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
-        "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {\n"
-        "    kcg_i64 p["
+        "  constexpr int TP = "
+     << kTmaTile << ", S = " << S << ", NC = " << NC
+     << ";\n"
+        "  extern __shared__ __align__(128) unsigned char kcg_smem[];\n"
+        "  kcg_i64* buf = reinterpret_cast<kcg_i64*>(kcg_smem);\n"
+        "  __shared__ __align__(8) unsigned long long full[S];\n"
+     << cons_decl.str()
+     << "  const kcg_i64 ntiles = a.vec ? a.n / TP : 0;\n"
+        "  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);\n"
+        "  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);\n"
+        "  if (threadIdx.x == 0) {\n"
+        "    for (int s = 0; s < S; ++s) asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(fb + 8 * s));\n"
+        "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+        "  }\n"
+        "  __syncthreads();\n"
+        "  auto issue = [&](int s, kcg_i64 tile) {\n"
+        "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+        "    asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(fb + 8 * s), \"r\"(NC * TP * 8) : \"memory\");\n"
+        "    for (int j = 0; j < NC; ++j) {\n"
+        "      const void* src = j < NC - 1 ? (const void*)(a.p[j] + tile * TP) : (const void*)(a.t + tile * TP);\n"
+        "      asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\"\n"
+        "                   :: \"r\"(bb + (unsigned)((s * NC + j) * TP * 8)), \"l\"(src), \"r\"(TP * 8), \"r\"(fb + 8 * s) : \"memory\");\n"
+        "    }\n"
+        "  };\n"
+        "  if (threadIdx.x == 0)\n"
+        "    for (int s = 0; s < S; ++s) {\n"
+        "      const kcg_i64 t = blockIdx.x + (kcg_i64)s * gridDim.x;\n"
+        "      if (t < ntiles) issue(s, t);\n"
+        "    }\n"
+        "  for (kcg_i64 k = 0;; ++k) {\n"
+        "    const kcg_i64 tile = blockIdx.x + k * gridDim.x;\n"
+        "    if (tile >= ntiles) break;\n"
+        "    const int s = (int)(k % S);\n"
+        "    const unsigned parity = (unsigned)((k / S) & 1);\n"
+        "    { unsigned done = 0;\n"
+        "      while (!done)\n"
+        "        asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\"\n"
+        "                     : \"=r\"(done) : \"r\"(fb + 8 * s), \"r\"(parity) : \"memory\"); }\n"
+        "    kcg_i64 q[4]["
+     << NP << "]; double tq[4];\n"
+              "    #pragma unroll\n"
+              "    for (int j = 0; j < NC; ++j) {\n"
+              "      const longlong2* src = reinterpret_cast<const longlong2*>(buf + (s * NC + j) * TP) + 2 * threadIdx.x;\n"
+              "      const longlong2 x0 = src[0], x1 = src[1];\n"
+              "      if (j < NC - 1) { q[0][j] = x0.x; q[1][j] = x0.y; q[2][j] = x1.x; q[3][j] = x1.y; }\n"
+              "      else { tq[0] = __longlong_as_double(x0.x); tq[1] = __longlong_as_double(x0.y);\n"
+              "             tq[2] = __longlong_as_double(x1.x); tq[3] = __longlong_as_double(x1.y); }\n"
+              "    }\n"
+              "    __syncthreads();\n"
+              "    if (threadIdx.x == 0) {\n"
+              "      const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+              "      if (nt < ntiles) issue(s, nt);\n"
+              "    }\n"
+              "    const kcg_i64 base = tile * TP + 4 * threadIdx.x;\n"
+              "    #pragma unroll\n"
+              "    for (int u = 0; u < 4; ++u) {\n";
+  emit_make_row("q[u]", "tq[u]", "base + u", "true");
+  os << cons_row.str() << "    }\n  }\n";
+  // tail (and the whole range when not aligned): warp-uniform trip counts
+  os << "  {\n"
+        "    const kcg_i64 t0 = ntiles * TP;\n"
+        "    const kcg_i64 rem = a.n - t0;\n"
+        "    const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
+        "    const kcg_i64 span = (rem + 31) / 32 * 32;\n"
+        "    for (kcg_i64 r = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; r < span; r += stride) {\n"
+        "      const kcg_i64 i = t0 + r;\n"
+        "      kcg_i64 p["
      << NP << "];\n";
-  for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
-  os << "    double x[" << FA << "];\n"
-        "    if (kcg_row_any(p, __ldcs(a.t + i), x) != KCG_PT_OK) continue;\n"
-        "    double pr = 0.0;\n";
-  for (int j = 0; j < F; ++j) os << "    pr = fma(x[" << j << "], a.alpha[" << j << "], pr);\n";
-  os << "    const double r = 1.0 - pr;\n    acc = fma(r, r, acc);\n  }\n"
-        "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);\n"
-        "  if ((threadIdx.x & 31) == 0) atomicAdd(a.obj, acc);\n}\n";
+  for (int j = 0; j < n_cols; ++j) os << "      p[" << j << "] = i < a.n ? a.p[" << j << "][i] : 0;\n";
+  os << "      const double tv = i < a.n ? a.t[i] : 0.0;\n";
+  emit_make_row("p", "tv", "i", "i < a.n");
+  os << cons_row.str() << "    }\n  }\n" << cons_end.str() << "}\n";
   return os.str();
 }
 

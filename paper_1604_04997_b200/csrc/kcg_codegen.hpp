@@ -31,6 +31,8 @@ void launch_jit(void* kernel, const void* args, size_t args_size,
 /// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.
 size_t tma_smem_bytes(int n_cols);
 int tma_ctas_per_sm();
+/// Shared-memory ring of the fused (bindings + T) Gram / residual kernels.
+size_t fused_smem_bytes(int n_cols);
 constexpr int kTmaPointsPerTile = 1024;
 
 }  // namespace kcg

@@ -356,3 +356,32 @@ def test_unaligned_buffers_through_c_abi(suite_alpha, in_off, out_off):
     torch.cuda.synchronize()
     assert torch.equal(st, ref_st)
     assert bool(((pred == ref) | (torch.isnan(pred) & torch.isnan(ref))).all())
+
+
+def test_fused_gram_large_matches_materialised_path():
+    """>= 148 TMA tiles plus a ragged tail: the fused evaluate -> row -> Gram
+    (DMMA) equals the Gram of rows materialised from evaluate_properties
+    counts, and the fused residual equals the materialised residual."""
+    prog = kc.load_program("matmul_tiled_g16x16")
+    sim = ko.simdev_reference_alpha()
+    n = 148 * 1024 * 2 + 555
+    g = torch.Generator(device="cpu").manual_seed(21)
+    cols = {p: (torch.randint(1, 3000, (n,), generator=g) * 16).cuda() for p in prog.params}
+    cols["n"][::101] += 1  # inadmissible rows are skipped and counted
+    T = kc.noiseless_time(sim, prog, cols) * (1.0 + 0.01 * torch.rand(n, generator=g, dtype=torch.float64).cuda())
+    st = kc.gram_fused(prog, cols, T)
+    bb = kc.evaluate_properties(prog, cols)
+    ok = bb.status == 0
+    X = (bb.counts_lo.to(torch.float64) / T).T[ok].contiguous()
+    ref = kc.gram_accumulate(X)
+    torch.cuda.synchronize()
+    assert st.bad_rows == int((~ok).sum())
+    torch.testing.assert_close(st.G, ref.G, rtol=1e-11, atol=0)
+    torch.testing.assert_close(st.xt1, ref.xt1, rtol=1e-11, atol=0)
+    assert torch.equal(st.colmax, ref.colmax)
+    alpha = [0.0] * 149
+    for k in prog.props:
+        alpha[k] = sim[k] * 0.999
+    a = torch.tensor([alpha[k] for k in prog.props], dtype=torch.float64, device="cuda")
+    want = float(((1.0 - X @ a) ** 2).sum())
+    assert kc.residual_fused(prog, cols, T, alpha) == pytest.approx(want, rel=1e-9)
