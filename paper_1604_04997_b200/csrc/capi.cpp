@@ -530,10 +530,8 @@ int kcg_gram_fused(const kcg_program* cp, const int64_t* const* param_cols, cons
     ab.push<int32_t>(vec ? 1 : 0);
     ab.finish();
     // persistent TMA-streamed kernel (2 CTAs/SM for the DMMA variant)
-    const size_t F = p->low.keys.size();
-    const unsigned per_sm = (F >= 1 && F <= 48) ? 2 : 1;
-    kcg::launch_jit(p->jit_gram, ab.b.data(), ab.b.size(), kcg::num_sms() * per_sm, 256, stream,
-                    kcg::fused_smem_bytes(np));
+    kcg::launch_jit(p->jit_gram, ab.b.data(), ab.b.size(), kcg::num_sms() * 2, 256, stream,
+                    kcg::fused_smem_bytes(np, static_cast<int>(p->low.keys.size()), true));
     ++g_launches;
     return KCG_OK;
   });
@@ -589,8 +587,8 @@ int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, 
     compact_alpha(p, alpha, al.data());
     for (double v : al) ab.push<double>(v);
     ab.finish();
-    kcg::launch_jit(p->jit_resid, ab.b.data(), ab.b.size(), kcg::num_sms(), 256, stream,
-                    kcg::fused_smem_bytes(np));
+    kcg::launch_jit(p->jit_resid, ab.b.data(), ab.b.size(), kcg::num_sms() * 2, 256, stream,
+                    kcg::fused_smem_bytes(np, F, false));
     ++g_launches;
     return KCG_OK;
   });

@@ -451,6 +451,16 @@ int min_blocks() {
 // register budget of the exact integer evaluation.
 constexpr int kTmaTile = 1024;
 
+int env_int(const char* name, int dflt, int lo, int hi);
+
+// ring depth of the fused (bindings + T) kernels: 64 KB so that two CTAs
+// (each with 35 KB of DMMA row buffers) fit one SM
+int fused_stages(int n_cols) {
+  const int per = (n_cols + 1) * 1024 * 8;
+  const int s = (env_int("KCG_FUSED_RING_KB", 64, 16, 200) * 1024) / per;
+  return s < 2 ? 2 : (s > 8 ? 8 : s);
+}
+
 int env_int(const char* name, int dflt, int lo, int hi) {
   const char* e = std::getenv(name);
   const int v = e ? std::atoi(e) : dflt;
@@ -620,10 +630,15 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 
 int tma_ctas_per_sm() { return tma_ctas(); }
 
-size_t fused_smem_bytes(int n_cols) {
-  const int NC = n_cols + 1;
-  const int S = std::max(2, std::min(8, (tma_ring_kb() * 1024) / (NC * kTmaTile * 8)));
-  return static_cast<size_t>(S) * NC * kTmaTile * 8;
+size_t fused_smem_bytes(int n_cols, int F, bool gram) {
+  const int FA = F > 0 ? F : 1;
+  const int NB = (F + 7) / 8, LDX = NB * 8 + 1;
+  size_t b = static_cast<size_t>(fused_stages(n_cols)) * (n_cols + 1) * kTmaTile * 8;
+  if (gram && F >= 1 && F <= 48)
+    b += static_cast<size_t>(8) * 32 * LDX * 8;  // DMMA row buffers (also the slow-path rows)
+  else
+    b += static_cast<size_t>(256) * FA * 8;      // slow-path rows
+  return b;
 }
 
 size_t tma_smem_bytes(int n_cols) {
@@ -716,7 +731,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   const bool dmma = gram && F >= 1 && F <= 48;
   const int NB = (F + 7) / 8, NT = NB * (NB + 1) / 2, FP = NB * 8, LDX = FP + 1;
   const int NC = n_cols + 1;  // parameter columns + T
-  const int S = std::max(2, std::min(8, (tma_ring_kb() * 1024) / (NC * kTmaTile * 8)));
+  const int S = fused_stages(n_cols);
   if (gram)
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* G; double* xt1; "
           "double* cmax; unsigned long long* bad; kcg_i64 n; int vec; };\n";
@@ -732,7 +747,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     os << "  x[" << j << "] = (c[" << j << "] != 0) ? __ddiv_rn(kcg_to_double(c[" << j << "]), t) : 0.0;\n";
   os << "}\n";
   // out-of-line row: reloads its inputs (no address-taken locals in callers)
-  os << "__device__ __noinline__ int kcg_row_i(const KcgArgs& a, kcg_i64 i, double* x) {\n"
+  os << "__device__ __noinline__ int kcg_row_i(const KcgArgs& a, kcg_i64 i, double* __restrict__ x) {\n"
         "  kcg_i64 p["
      << NP << "];\n";
   for (int j = 0; j < n_cols; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
@@ -755,7 +770,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   // ---- per-row consumer ---------------------------------------------------
   std::ostringstream cons_decl, cons_row, cons_end;
   if (dmma) {
-    cons_decl << "  __shared__ double xs[8][32 * " << LDX << "];\n"
+    cons_decl << "  double* xs_base = reinterpret_cast<double*>(kcg_smem) + S * NC * TP;\n"
               << "  __shared__ double red[" << FP * FP + 2 * FP << "];\n"
               << "  __shared__ unsigned long long red_bad;\n"
               << "  for (int k = threadIdx.x; k < " << FP * FP + 2 * FP << "; k += blockDim.x) red[k] = 0.0;\n"
@@ -765,7 +780,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
               << "; ++t) acc[t][0] = acc[t][1] = 0.0;\n"
               << "  double s1[" << NB << "], mx[" << NB << "];\n  #pragma unroll\n  for (int b = 0; b < " << NB
               << "; ++b) s1[b] = mx[b] = 0.0;\n"
-              << "  unsigned long long bad = 0;\n  double* xw = xs[warp];\n";
+              << "  unsigned long long bad = 0;\n  double* xw = xs_base + warp * 32 * " << LDX << ";\n";
     // consume x[FP] (zeros for skipped rows); warp-synchronous
     cons_row << "      #pragma unroll\n      for (int j = 0; j < " << FP << "; ++j) xw[lane * " << LDX
              << " + j] = x[j];\n"
@@ -845,13 +860,21 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   }
   const int XW = dmma ? FP : FA;  // x row width
   // produce row x for global index i from registers q/t (or out of line)
+  // The out-of-line path writes its row to a scratch row (shared memory for
+  // the DMMA variant) and the fast path's registers are copied there too, so
+  // no per-thread array ever has its address taken (no local memory).
   auto emit_make_row = [&](const char* qexpr, const char* texpr, const char* iexpr, const char* valid) {
     os << "      double x[" << XW << "];\n      #pragma unroll\n      for (int j = 0; j < " << XW
        << "; ++j) x[j] = 0.0;\n"
        << "      bool ok = false;\n"
        << "      if (" << valid << ") {\n"
        << "        int st = kcg_row_fast(" << qexpr << ", " << texpr << ", x);\n"
-       << "        if (st < 0) st = kcg_row_i(a, " << iexpr << ", x);\n"
+       << "        if (st < 0) {\n"
+       << "          double* sx = slow_row;\n"
+       << "          st = kcg_row_i(a, " << iexpr << ", sx);\n"
+       << "          if (st == KCG_PT_OK) {\n            #pragma unroll\n            for (int j = 0; j < " << F
+       << "; ++j) x[j] = sx[j];\n          }\n"
+       << "        }\n"
        << "        ok = st == KCG_PT_OK;\n"
        << "        if (!ok) {\n          #pragma unroll\n          for (int j = 0; j < " << XW
        << "; ++j) x[j] = 0.0;\n";
@@ -859,7 +882,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     os << "        }\n      }\n";
   };
 
-  os << "extern \"C\" __global__ void __launch_bounds__(256, " << (dmma ? 2 : 1) << ") " << name
+  os << "extern \"C\" __global__ void __launch_bounds__(256, 2) " << name
      << "(const __grid_constant__ KcgArgs a) {\n"
         "  constexpr int TP = "
      << kTmaTile << ", S = " << S << ", NC = " << NC
@@ -868,6 +891,9 @@ std::string codegen(const std::vector<const Lowered*>& progs,
         "  kcg_i64* buf = reinterpret_cast<kcg_i64*>(kcg_smem);\n"
         "  __shared__ __align__(8) unsigned long long full[S];\n"
      << cons_decl.str()
+     << (dmma ? std::string("  double* slow_row = xw + lane * ") + std::to_string(LDX) + ";\n"
+              : std::string("  double* slow_row = reinterpret_cast<double*>(kcg_smem) + S * NC * TP + threadIdx.x * ") +
+                    std::to_string(FA) + ";\n")
      << "  const kcg_i64 ntiles = a.vec ? a.n / TP : 0;\n"
         "  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);\n"
         "  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);\n"

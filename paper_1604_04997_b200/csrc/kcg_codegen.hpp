@@ -32,7 +32,7 @@ void launch_jit(void* kernel, const void* args, size_t args_size,
 size_t tma_smem_bytes(int n_cols);
 int tma_ctas_per_sm();
 /// Shared-memory ring of the fused (bindings + T) Gram / residual kernels.
-size_t fused_smem_bytes(int n_cols);
+size_t fused_smem_bytes(int n_cols, int F, bool gram);
 constexpr int kTmaPointsPerTile = 1024;
 
 }  // namespace kcg
