@@ -236,6 +236,12 @@ def main():
     checked = _spot_check(kc, progs, cols, preds, sim_alpha, r0, args.side) if rank == 0 else 0
 
     hbm, peak_kind = peaks()
+    traffic = None
+    try:  # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (profiles/)
+        traffic = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())["traffic_bytes_per_launch"]
+        traffic *= n / 167284151  # the capture is of the full-size launch
+    except Exception:
+        pass
     avg_launch = statistics.mean(kern_ms) / 1e3
     bytes_per_launch = 32.0 * n  # 8*P + 8 with P = 3
     achieved = bytes_per_launch / avg_launch / 1e9
@@ -251,7 +257,8 @@ def main():
                    "l2": "inputs 4.0 GB + outputs 8.0 GB per step exceed the 126 MB L2 (no flush)",
                    "parallelism": f"dp{world} (contiguous size shards)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                     "traffic_source": "profiles/r01_launches_eval.csv (ncu, per launch)",
                      "kernel": "kcg_eval_<variant> (NVRTC sm_100a)",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "avg_launch_ms": avg_launch * 1e3},
