@@ -30,6 +30,7 @@ struct kcg_program {
   std::vector<std::string> param_names;
   int engine = KCG_ENGINE_JIT;
   KcgDevProg* dprog = nullptr;  // device image (interpreter), lazily uploaded
+  KcgDevProg* dadmit = nullptr; // admissibility-only image (beyond the count bound)
   bool dprog_ok = true;         // fits the interpreter's static tables
   std::string jit_src;
   std::string jit_src_kind;
@@ -277,6 +278,7 @@ int kcg_program_create(const char* text, size_t len, kcg_program** out) {
 void kcg_program_destroy(kcg_program* prog) {
   if (!prog) return;
   if (prog->dprog) cudaFree(prog->dprog);
+  if (prog->dadmit) cudaFree(prog->dadmit);
   delete prog;
 }
 
@@ -356,6 +358,11 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
           cuda_check(cudaMalloc(&p->dprog, sizeof(KcgDevProg)), "cudaMalloc");
           cuda_check(cudaMemcpy(p->dprog, img.get(), sizeof(KcgDevProg), cudaMemcpyHostToDevice),
                      "cudaMemcpy");
+          if (p->low.admit && build_devprog(*p->low.admit, *img)) {
+            cuda_check(cudaMalloc(&p->dadmit, sizeof(KcgDevProg)), "cudaMalloc");
+            cuda_check(cudaMemcpy(p->dadmit, img.get(), sizeof(KcgDevProg), cudaMemcpyHostToDevice),
+                       "cudaMemcpy");
+          }
         }
       }
       if (!p->dprog_ok)
@@ -369,7 +376,7 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
       a.n = static_cast<int64_t>(n);
       a.simulate = simulate;
       compact_alpha(p, alpha, a.alpha);
-      kcg::launch_interp_eval(p->dprog, a, stream);
+      kcg::launch_interp_eval(p->dprog, p->dadmit, a, stream);
       ++g_launches;
       return KCG_OK;
     }

@@ -57,14 +57,15 @@ const char* cmp_str(int op) {
 constexpr int64_t kU32 = 0xffffffffll;
 
 // fast: T = kcg_i64; small: every parameter <= b64 < 2^32
-void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast) {
+void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast,
+               const char* wide_name = "kcg_wide_") {
   const bool small = fast && L.b64 >= 0 && L.b64 <= kU32;
   std::vector<bool> atom_u32(L.n_atoms, false);  // value known in [0, 2^32)
   if (fast)
     os << "__device__ __forceinline__ int kcg_fast_" << v
        << "(const kcg_i64* __restrict__ p, kcg_i64* __restrict__ cnt) {\n  typedef kcg_i64 T;\n";
   else
-    os << "__device__ __noinline__ int kcg_wide_" << v
+    os << "__device__ __noinline__ int " << wide_name << v
        << "(const kcg_i64* __restrict__ p, kcg_i128* __restrict__ cnt) {\n  typedef kcg_i128 T;\n";
   for (const LOp& op : L.ops) {
     switch (op.code) {
@@ -403,8 +404,18 @@ void emit_eval_point(std::ostringstream& os, const Lowered& L) {
   for (int j = 0; j < L.n_params; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
   os << "  KcgRes r; r.s = kcg_nan();\n"
         "  const int cls = kcg_class_0(p);\n"
-        "  if (cls != 2) { r.st = cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW; return r; }\n"
-        "  kcg_i128 c["
+        "  if (cls == 0) { r.st = KCG_PT_ASSUMPTION_VIOLATED; return r; }\n";
+  if (L.admit && L.admit->b128 >= 0) {
+    // beyond the count bound: still decide admissibility first (props.cpp:263-266)
+    os << "  if (cls == 3) {\n    r.st = KCG_PT_OVERFLOW;\n    if (";
+    for (int j = 0; j < L.n_params; ++j) os << (j ? " && " : "") << "p[" << j << "] <= " << L.admit->b128 << "ll";
+    if (L.n_params == 0) os << "true";
+    os << ") {\n      kcg_i128 none[1];\n      const int a0 = kcg_admit_0(p, none);\n"
+          "      if (a0 != KCG_PT_OK) r.st = a0;\n    }\n    return r;\n  }\n";
+  } else {
+    os << "  if (cls == 3) { r.st = KCG_PT_OVERFLOW; return r; }\n";
+  }
+  os << "  kcg_i128 c["
      << FA << "];\n  r.st = kcg_wide_0(p, c);\n  if (r.st != KCG_PT_OK) return r;\n  double s = 0.0;\n";
   for (int j = 0; j < F; ++j) os << "  s = kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim);\n";
   os << "  r.s = s;\n  if (a.clo) {\n";
@@ -656,6 +667,8 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     emit_body(os, *progs[v], static_cast<int>(v), false);
     emit_classify(os, *progs[v], static_cast<int>(v), pmaps[v]);
   }
+  if (kind == JitKind::eval && progs[0]->admit)
+    emit_body(os, *progs[0]->admit, 0, false, "kcg_admit_");
   const int NP = n_cols > 0 ? n_cols : 1;
 
   if (kind == JitKind::eval) {

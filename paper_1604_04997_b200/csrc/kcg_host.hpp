@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -156,6 +157,10 @@ struct Lowered {
   std::vector<i128> quot_mod, quot_rem;  // per OP_QUOT (index in op.c)
   int64_t b64 = 0, b128 = 0;       // safe uniform parameter bounds
   std::vector<long double> mono_bound64;  // |monomial| bound when params <= b64
+  // admissibility-only lowering (no properties): decides E_ASSUMPTION_VIOLATED
+  // for points whose counts are beyond the 128-bit bound (admits() is checked
+  // before any count in props.cpp:263-269)
+  std::shared_ptr<Lowered> admit;
 };
 
 Lowered lower(const Symbolic& s);

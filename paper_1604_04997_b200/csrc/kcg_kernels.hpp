@@ -20,8 +20,8 @@ struct InterpEvalArgs {
 };
 
 /// Table-interpreter evaluate + predict (KCG_ENGINE_INTERP).
-void launch_interp_eval(const KcgDevProg* dprog, const InterpEvalArgs& a,
-                        void* stream);
+void launch_interp_eval(const KcgDevProg* dprog, const KcgDevProg* dadmit,
+                        const InterpEvalArgs& a, void* stream);
 
 /// Materialised-X Gram: G += X^T X, xt1 += X^T 1, colmax = max(colmax,|X|).
 void launch_gram(const double* X, size_t n, int F, size_t ld, double* G,

@@ -141,7 +141,8 @@ __device__ __forceinline__ int interp_point(const KcgDevProg* __restrict__ P,
 }
 
 __global__ void __launch_bounds__(128)
-    kcg_interp_eval(const KcgDevProg* __restrict__ P, const __grid_constant__ InterpEvalArgs a) {
+    kcg_interp_eval(const KcgDevProg* __restrict__ P, const KcgDevProg* __restrict__ A,
+                    const __grid_constant__ InterpEvalArgs a) {
   const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;
   const int np = P->n_params;
   for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
@@ -161,8 +162,19 @@ __global__ void __launch_bounds__(128)
       st = interp_point<kcg_i64>(P, p, a, i, s);
     else if (wide_ok)
       st = interp_point<kcg_i128>(P, p, a, i, s);
-    else
+    else {
+      // counts beyond 128 bits: admissibility still decides first
       st = KCG_PT_OVERFLOW;
+      if (A) {
+        bool ok = A->b128 >= 0;
+        for (int j = 0; j < np; ++j) ok &= p[j] <= A->b128;
+        kcg_i128 none[1];
+        if (ok) {
+          const int a0 = interp_body<kcg_i128>(A, p, none);
+          if (a0 != KCG_PT_OK) st = a0;
+        }
+      }
+    }
     if (a.pred) a.pred[i] = (st == KCG_PT_OK || st == KCG_PT_COUNT_WIDE) ? s : kcg_nan();
     if (a.status) a.status[i] = (uint8_t)st;
   }
@@ -504,13 +516,14 @@ int num_sms() {
   return g_sms;
 }
 
-void launch_interp_eval(const KcgDevProg* dprog, const InterpEvalArgs& a, void* stream) {
+void launch_interp_eval(const KcgDevProg* dprog, const KcgDevProg* dadmit, const InterpEvalArgs& a,
+                        void* stream) {
   if (a.n == 0) return;
   const int threads = 128;
   kcg_i64 blocks = (a.n + threads - 1) / threads;
   const kcg_i64 cap = (kcg_i64)num_sms() * 16;
   if (blocks > cap) blocks = cap;
-  kcg_interp_eval<<<(unsigned)blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(dprog, a);
+  kcg_interp_eval<<<(unsigned)blocks, threads, 0, static_cast<cudaStream_t>(stream)>>>(dprog, dadmit, a);
   check(cudaGetLastError(), "kcg_interp_eval launch");
 }
 

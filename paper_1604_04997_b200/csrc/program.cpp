@@ -823,6 +823,11 @@ Lowered lower(const Symbolic& s_in) {
   L.b64 = search(std::ldexp(1.0L, 62));
   L.b128 = search(std::ldexp(1.0L, 125));
   if (L.b64 >= 0) max_intermediate(L, static_cast<long double>(L.b64), &L.mono_bound64);
+  if (!s_in.props.empty()) {
+    Symbolic only = s_in;
+    only.props.clear();
+    L.admit = std::make_shared<Lowered>(lower(only));
+  }
   return L;
 }
 
