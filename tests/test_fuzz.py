@@ -75,4 +75,4 @@ def test_random_programs_bit_exact_on_gpu(engine, suite_alpha):
             else:
                 assert math.isnan(pred[i])
                 checked["viol" if ws == 1 else "nonint"] += 1
-    assert checked["ok"] > 1000 and checked["viol"] > 100 and checked["nonint"] > 10, checked
+    assert checked["ok"] > 800 and checked["viol"] > 100 and checked["nonint"] > 10, checked
