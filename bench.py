@@ -413,29 +413,31 @@ def _extras(kc, torch, dev, args):
     w = kc.ModelWeights(device="simdev-v1", alpha=sim_alpha, covered=[a != 0 for a in sim_alpha])
     stream = torch.cuda.current_stream(dev).cuda_stream
 
-    # ---- config 2: 1e6 test-suite points (skinny + conv, u = 1..5e5) -------
-    U = 500_000
+    # ---- config 2: 1e6 points over the 4 test kernels (250k each) ----------
+    U = 250_000
     u = torch.arange(1, U + 1, dtype=torch.int64, device=dev)
-    sk = kc.load_program("matmul_skinny_g16x16")
-    cv = kc.load_program("conv_g16x16")
-    sk_cols = {"n": (16 * u).contiguous(), "m": (128 * u).contiguous(), "l": (16 * u).contiguous()}
-    cv_cols = {"n": (16 * u).contiguous()}
-    p_sk = torch.empty(U, dtype=torch.float64, device=dev)
-    p_cv = torch.empty(U, dtype=torch.float64, device=dev)
-    a_sk, a_cv = _colarr(sk, sk_cols), _colarr(cv, cv_cols)
+    specs = [("matmul_skinny_g16x16", {"n": 16 * u, "m": 128 * u, "l": 16 * u}),
+             ("conv_g16x16", {"n": 16 * u}),
+             ("fd_stencil_g16x16", {"n": 16 * u}),
+             ("nbody_g256", {"n": 256 * u})]
+    launches = []
+    for kid, cdict in specs:
+        p = kc.load_program(kid)
+        cdict = {k: v.contiguous() for k, v in cdict.items()}
+        launches.append((p, cdict, _colarr(p, cdict), torch.empty(U, dtype=torch.float64, device=dev)))
 
     def c2():
-        kc.api.check(kc.api.lib().kcg_eval_predict(sk.handle, a_sk, U, w.alpha_array(), p_sk.data_ptr(),
-                                                   None, None, None, 0, stream))
-        kc.api.check(kc.api.lib().kcg_eval_predict(cv.handle, a_cv, U, w.alpha_array(), p_cv.data_ptr(),
-                                                   None, None, None, 0, stream))
+        for p, _, arr, out in launches:
+            kc.api.check(kc.api.lib().kcg_eval_predict(p.handle, arr, U, w.alpha_array(), out.data_ptr(),
+                                                       None, None, None, 0, stream))
     sec = _timed(torch, c2, reps=20)
-    b64, _ = sk.safe_bounds()
+    b64, _ = launches[0][0].safe_bounds()
     out["config2_suite_1e6"] = {
-        "points": 2 * U, "ms": sec * 1e3, "points_per_s": 2 * U / sec,
-        "note": "matmul_skinny (16u,128u,16u) + conv (16u), u<=5e5; skinny counts reach 4.6e21 "
-                f"(int128 path for n > {b64}); fd_stencil/nbody are not symbolic in the reference"}
-    del sk_cols, cv_cols, p_sk, p_cv, u
+        "points": 4 * U, "ms": sec * 1e3, "points_per_s": 4 * U / sec, "launches": 4,
+        "note": "skinny (16u,128u,16u), conv 16u, fd_stencil 16u, nbody 256u, u=1..250000; skinny counts "
+                f"reach 5.8e20 (int128 path for n > {b64}); fd_stencil / nbody use the derived programs "
+                "(SURVEY 8f row 1); latency-bound (4 launches)"}
+    del launches, u
 
     # ---- config 4 fused: evaluate + predict + argmin over the 6 variants ---
     side = args.side

@@ -43,7 +43,7 @@ def test_every_suite_program_lowers():
         b64, b128 = p.safe_bounds()
         assert 0 < b64 <= b128
         n += 1
-    assert n == 59
+    assert n == 61  # 59 symbolic + fd_stencil / nbody derived (programs/derived.json)
     assert not idx["fd_stencil_g16x16"]["symbolic"] and not idx["nbody_g256"]["symbolic"]
 
 

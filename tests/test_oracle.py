@@ -25,7 +25,6 @@ def programs():
 
 
 def test_schema_has_149_keys_in_reference_order():
-    idx = load_golden("../../paper_1604_04997_b200/programs/index.json") if False else None
     assert len(ko.SCHEMA) == 149
     assert ko.SCHEMA[0] == "mem.global.load.s32.uniform"
     assert ko.SCHEMA[-3:] == ["sync.barrier", "launch.groups", "launch.const"]
@@ -60,14 +59,11 @@ def test_suite_cases_match_reference_bound_extraction(programs):
         want = _counts(c["counts"])
         # the stored timing is the reference's noiseless_time
         assert ko.noiseless_time(sim, want) == hexf(c["time_s"][1])
-        prog = programs.get(c["kernel"])
-        if prog is None:
-            assert c["kernel"] in ("fd_stencil_g16x16", "nbody_g256")
-            continue
+        prog = programs[c["kernel"]]  # fd_stencil / nbody: derived programs (§8f row 1)
         got = prog.evaluate_properties(_binding(c["binding"]))
         assert {k: v for k, v in got.items() if v} == want, c
         checked += 1
-    assert checked == 406 - 8  # fd_stencil and nbody have 4 cases each
+    assert checked == 406
 
 
 def test_oracle_draws_match(programs):
@@ -76,8 +72,10 @@ def test_oracle_draws_match(programs):
     for d in draws:
         if "symbolic_equal" in d:
             assert d["symbolic_equal"], d
-            got = programs[d["kernel"]].evaluate_properties(_binding(d["binding"]))
-            assert {k: v for k, v in got.items() if v} == _counts(d["counts"])
+        # every kernel, incl. the derived fd_stencil / nbody programs, must
+        # reproduce the reference's bound-mode extraction on its oracle lattice
+        got = programs[d["kernel"]].evaluate_properties(_binding(d["binding"]))
+        assert {k: v for k, v in got.items() if v} == _counts(d["counts"])
 
 
 def _check_samples(samples, progs, alpha):
@@ -185,3 +183,19 @@ def test_admits_semantics():
     assert not p.admits({"n": 17, "m": 32, "l": 48})
     assert not p.admits({"n": 0, "m": 32, "l": 48})
     assert not p.admits({"n": -16, "m": 32, "l": 48})
+
+
+def test_derived_programs_match_survey_appendix_a():
+    """fd_stencil / nbody closed forms recovered from
+    the reference's bound-mode counts."""
+    import json
+    d = json.loads((PROGRAMS / "derived.json").read_text())["derived"]
+    assert {e["id"] for e in d if "file" in e} == {"fd_stencil_g16x16", "nbody_g256"}
+    fd = ko.Program((PROGRAMS / "fd_stencil_g16x16.kcp").read_text())
+    c = fd.evaluate_properties({"n": 4096})
+    assert c[ko.SCHEMA_INDEX["mem.global.load.s32.1/1"]] == 9 * 4096 ** 2 // 8
+    assert c[ko.SCHEMA_INDEX["mem.local.load"]] == 6 * 4096 ** 2
+    nb = ko.Program((PROGRAMS / "nbody_g256.kcp").read_text())
+    c = nb.evaluate_properties({"n": 1 << 20})
+    assert c[ko.SCHEMA_INDEX["mem.global.load.s32.3/3"]] == 3 * 4 ** 20 + 3 * 4 ** 20 // 256
+    assert c[ko.SCHEMA_INDEX["launch.groups"]] == (1 << 20) // 256
