@@ -153,6 +153,8 @@ def main():
     ap.add_argument("--side", type=int, default=SIDE, help="u,v,w in [1, side]")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fit", action="store_true", help="skip the sharded fit (config 5)")
+    ap.add_argument("--fit-rows", type=int, default=10**9, help="fit rows per rank")
     ap.add_argument("--extras", action="store_true", help="also time configs 2/3/5 and argmin")
     args = ap.parse_args()
 
@@ -266,6 +268,9 @@ def main():
         "clocks": clk.summary(),
         "spot_checked_points": checked,
     }
+    if not args.no_fit:
+        del preds, cols
+        line["fit"] = _sharded_fit(kc, torch, dev, world, rank, args.fit_rows)
     if rank == 0 and not args.no_e2e:
         line["e2e"] = _e2e(kc, progs, w, args, torch, dev, world, rank)
     if rank == 0 and not args.no_cpu:
@@ -379,6 +384,68 @@ def _e2e(kc, progs, w, args, torch, dev, world, rank):
             "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3,
             "note": "pinned host SoA bindings -> kcg_eval_predict (6 variants) -> pinned host predictions; "
                     "2 streams, 8M-size chunks; wall clock incl. all copies"}
+
+
+def _sharded_fit(kc, torch, dev, world, rank, rows):
+    """Config 5: every rank forms `rows` design rows (matmul_tiled_g16x16 at
+    its own block of sizes, T = noiseless_time on the GPU) and reduces them
+    through the fused evaluate -> row -> Gram kernel; G / Xᵀ1 / colmax are
+    all-reduced over NCCL, every rank solves the same small system, then
+    re-predicts its shard in the fused residual pass (objective all-reduced).
+    Timed on the device from the Gram launch to the reduced objective, max
+    over ranks (host solve included)."""
+    import torch.distributed as dist
+
+    from paper_1604_04997_b200.dist import allreduce_gram
+    prog = kc.load_program("matmul_tiled_g16x16")
+    alpha = _simdev_alpha(kc)
+    g = torch.arange(0, rows, dtype=torch.int64, device=dev)
+    cols = {"n": (16 * (g // 1_000_000 % 1000 + 1 + 1000 * rank)).contiguous(),
+            "m": (16 * (g // 1000 % 1000 + 1)).contiguous(),
+            "l": (16 * (g % 1000 + 1)).contiguous()}
+    del g
+    T = kc.noiseless_time(alpha, prog, cols)
+    arr = _colarr(prog, cols)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+
+    def once():
+        st = kc.GramStats.zeros(len(prog.props), dev)
+        kc.api.check(kc.api.lib().kcg_gram_fused(prog.handle, arr, T.data_ptr(), rows, st.G.data_ptr(),
+                                                 st.xt1.data_ptr(), st.colmax.data_ptr(), None, stream))
+        st.n_rows = rows
+        allreduce_gram(st)
+        a, rank_ = kc.solve_gram(st)
+        full = [0.0] * kc.schema_size()
+        for j, k in enumerate(prog.props):
+            full[k] = a[j]
+        obj = torch.zeros(1, dtype=torch.float64, device=dev)
+        import ctypes
+        kc.api.check(kc.api.lib().kcg_residual_fused(prog.handle, arr, T.data_ptr(), rows,
+                                                     (ctypes.c_double * len(full))(*full), obj.data_ptr(), stream))
+        if world > 1:
+            dist.all_reduce(obj)
+        return rank_, float(obj.item()), st.n_rows
+
+    once()  # JIT + warm-up
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    rk, obj, total_rows = once()
+    t1.record()
+    torch.cuda.synchronize()
+    sec = t0.elapsed_time(t1) / 1e3
+    if world > 1:
+        t = torch.tensor([sec], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    return {"metric": "fit rows/sec", "rows": total_rows, "value": total_rows / sec, "ms": sec * 1e3,
+            "rank": rk, "objective": obj, "scaling": "weak",
+            "workload": f"config5: {rows} rows/rank (matmul_tiled_g16x16, T = noiseless_time), fused "
+                        "evaluate->row->Gram (DMMA) + NCCL all-reduce + host min-norm solve + fused residual",
+            "hbm_frac_gram_input": 32.0 * rows / sec / 1e9 / peaks()[0]}
 
 
 def _timed(torch, fn, reps=5, warm=2):
