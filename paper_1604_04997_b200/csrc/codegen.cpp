@@ -783,6 +783,10 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   // ---- per-row consumer ---------------------------------------------------
   std::ostringstream cons_decl, cons_row, cons_end;
   if (dmma) {
+    // Xᵀ1 rides on the tensor cores as a constant-one column F (when the
+    // padded width leaves room): G[j][F] = sum_r x_rj. colmax is kept per
+    // thread at row production, so the k-step loop is loads + DMMA only.
+    const bool ones = FP > F;
     cons_decl << "  double* xs_base = reinterpret_cast<double*>(kcg_smem) + S * NC * TP;\n"
               << "  __shared__ double red[" << FP * FP + 2 * FP << "];\n"
               << "  __shared__ unsigned long long red_bad;\n"
@@ -791,18 +795,21 @@ std::string codegen(const std::vector<const Lowered*>& progs,
               << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;\n"
               << "  double acc[" << NT << "][2];\n  #pragma unroll\n  for (int t = 0; t < " << NT
               << "; ++t) acc[t][0] = acc[t][1] = 0.0;\n"
-              << "  double s1[" << NB << "], mx[" << NB << "];\n  #pragma unroll\n  for (int b = 0; b < " << NB
-              << "; ++b) s1[b] = mx[b] = 0.0;\n"
-              << "  unsigned long long bad = 0;\n  double* xw = xs_base + warp * 32 * " << LDX << ";\n";
-    // consume x[FP] (zeros for skipped rows); warp-synchronous
-    cons_row << "      #pragma unroll\n      for (int j = 0; j < " << FP << "; ++j) xw[lane * " << LDX
-             << " + j] = x[j];\n"
-             << "      __syncwarp();\n"
+              << "  double mxr[" << F << "]" << (ones ? "" : std::string(", s1r[") + std::to_string(F) + "]") << ";\n"
+              << "  #pragma unroll\n  for (int j = 0; j < " << F << "; ++j) { mxr[j] = 0.0;"
+              << (ones ? "" : " s1r[j] = 0.0;") << " }\n"
+              << "  unsigned long long bad = 0;\n  double* xw = xs_base + warp * 32 * " << LDX << ";\n"
+              << "  for (int e = lane; e < 32 * " << LDX << "; e += 32) xw[e] = 0.0;  // padding stays zero\n"
+              << "  __syncwarp();\n";
+    cons_row << "      #pragma unroll\n      for (int j = 0; j < " << F << "; ++j) { xw[lane * " << LDX
+             << " + j] = x[j]; mxr[j] = fmax(mxr[j], fabs(x[j]));"
+             << (ones ? "" : " s1r[j] += x[j];") << " }\n";
+    if (ones) cons_row << "      xw[lane * " << LDX << " + " << F << "] = ok ? 1.0 : 0.0;\n";
+    cons_row << "      __syncwarp();\n"
              << "      #pragma unroll\n      for (int ks = 0; ks < 8; ++ks) {\n"
              << "        const double* row = xw + (4 * ks + tig) * " << LDX << ";\n"
              << "        double v[" << NB << "];\n"
-             << "        #pragma unroll\n        for (int b = 0; b < " << NB
-             << "; ++b) { v[b] = row[8 * b + gid]; s1[b] += v[b]; mx[b] = fmax(mx[b], fabs(v[b])); }\n"
+             << "        #pragma unroll\n        for (int b = 0; b < " << NB << "; ++b) v[b] = row[8 * b + gid];\n"
              << "        int t = 0;\n"
              << "        #pragma unroll\n        for (int I = 0; I < " << NB << "; ++I)\n"
              << "          #pragma unroll\n          for (int J = I; J < " << NB << "; ++J, ++t)\n"
@@ -810,13 +817,16 @@ std::string codegen(const std::vector<const Lowered*>& progs,
              << "                         : \"+d\"(acc[t][0]), \"+d\"(acc[t][1]) : \"d\"(v[I]), \"d\"(v[J]));\n"
              << "      }\n      __syncwarp();\n";
     cons_end << "  __syncthreads();\n"
-             << "  #pragma unroll\n  for (int b = 0; b < " << NB << "; ++b) {\n"
-             << "    double s = s1[b], m = mx[b];\n"
-             << "    s += __shfl_xor_sync(0xffffffffu, s, 1); s += __shfl_xor_sync(0xffffffffu, s, 2);\n"
-             << "    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1)); m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));\n"
-             << "    if (tig == 0) { atomicAdd(red + " << FP * FP << " + 8 * b + gid, s);\n"
-             << "      atomicMax((unsigned long long*)(red + " << FP * FP + FP
-             << " + 8 * b + gid), (unsigned long long)__double_as_longlong(m)); }\n  }\n"
+             << "  #pragma unroll\n  for (int j = 0; j < " << F << "; ++j) {\n"
+             << "    double m = mxr[j];\n"
+             << "    #pragma unroll\n    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));\n"
+             << "    if (lane == 0) atomicMax((unsigned long long*)(red + " << FP * FP + FP
+             << " + j), (unsigned long long)__double_as_longlong(m));\n";
+    if (!ones)
+      cons_end << "    double sj = s1r[j];\n"
+               << "    #pragma unroll\n    for (int o = 16; o > 0; o >>= 1) sj += __shfl_xor_sync(0xffffffffu, sj, o);\n"
+               << "    if (lane == 0) atomicAdd(red + " << FP * FP << " + j, sj);\n";
+    cons_end << "  }\n"
              << "  { int t = 0;\n    #pragma unroll\n    for (int I = 0; I < " << NB
              << "; ++I)\n      #pragma unroll\n      for (int J = I; J < " << NB << "; ++J, ++t) {\n"
              << "        atomicAdd(red + (8 * I + gid) * " << FP << " + 8 * J + 2 * tig, acc[t][0]);\n"
@@ -830,7 +840,8 @@ std::string codegen(const std::vector<const Lowered*>& progs,
              << "    atomicAdd(a.G + r * " << F << " + c, red[e]);\n"
              << "    if (c / 8 != r / 8) atomicAdd(a.G + c * " << F << " + r, red[e]);\n  }\n"
              << "  for (int c = threadIdx.x; c < " << F << "; c += blockDim.x) {\n"
-             << "    atomicAdd(a.xt1 + c, red[" << FP * FP << " + c]);\n"
+             << "    atomicAdd(a.xt1 + c, red[" << (ones ? std::string("c * ") + std::to_string(FP) + " + " + std::to_string(F)
+                                                    : std::to_string(FP * FP) + " + c") << "]);\n"
              << "    atomicMax((unsigned long long*)(a.cmax + c), (unsigned long long)__double_as_longlong(red["
              << FP * FP + FP << " + c]));\n  }\n"
              << "  if (threadIdx.x == 0 && a.bad && red_bad) atomicAdd(a.bad, red_bad);\n";
@@ -871,7 +882,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     cons_end << "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);\n"
              << "  if ((threadIdx.x & 31) == 0) atomicAdd(a.obj, acc);\n";
   }
-  const int XW = dmma ? FP : FA;  // x row width
+  const int XW = FA;  // x row width
   // produce row x for global index i from registers q/t (or out of line)
   // The out-of-line path writes its row to a scratch row (shared memory for
   // the DMMA variant) and the fast path's registers are copied there too, so
