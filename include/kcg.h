@@ -196,6 +196,25 @@ int kcg_gram_residual_grad(const double* X, size_t n_rows, int n_cols,
                            size_t ld, const double* alpha, double* g,
                            void* stream);
 
+/* ---- synthetic device: stored timings (simdevice.cpp:76-127) ----------
+ * times_out[i] = noiseless_time * exp(sigma * keyed_gaussian(seed,
+ * "<kernel>|<binding_str>", run)) -- simulate_time for run 0 and the run-th
+ * entry of simulate_runs otherwise. sigma == 0 returns the noiseless time
+ * bit-exactly; with noise, exp/log/cos are CUDA's (<= 2 ulp from glibc).
+ * NaN where the binding is not admissible (status_out, nullable, says why).
+ * alpha: HOST, 149 schema-indexed device weights (SimDevice::alpha).       */
+int kcg_simulate_time(const kcg_program* prog, const int64_t* const* param_cols,
+                      size_t n_points, const double* alpha, double sigma,
+                      uint64_t seed, uint64_t run, double* times_out,
+                      uint8_t* status_out, void* stream);
+
+/* geometric_mean_error (model.cpp:119-133), accumulated: log_sum +=
+ * sum log(max(|p-a|/a, 1e-12)), count += valid pairs, bad += pairs with
+ * a <= 0 (E_NONPOSITIVE_TIME). The mean is exp(log_sum / count).          */
+int kcg_geomean_accumulate(const double* pred, const double* actual, size_t n,
+                           double* log_sum, unsigned long long* count,
+                           unsigned long long* bad, void* stream);
+
 /* ---- weights file (jsonio.cpp:96-143) ---------------------------------- */
 int kcg_weights_read_json(const char* path, double* alpha149,
                           uint8_t* covered149, double* objective,

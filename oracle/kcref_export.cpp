@@ -413,6 +413,35 @@ int main(int argc, char** argv) {
           json{{"programs", xprogs}, {"samples", xsamples}});
   }
 
+  // ---- simulate_time with noise (simdevice.cpp:13-46, 96-127) --------------
+  {
+    kc::SimDevice dev = ref;
+    dev.sigma = 0.02;
+    dev.seed = 7;
+    json sims = json::array();
+    for (const auto& c : lib.measurement_cases()) {
+      if (!sym.count(c.kernel_id)) continue;
+      const kc::PropertyVector pv = kc::extract_properties(irs.at(c.kernel_id), c.binding, kCap);
+      const auto runs = kc::simulate_runs(dev, c.kernel_id, c.binding, pv, 3);
+      json r = json::array();
+      for (double t : runs) r.push_back(hexd(t));
+      sims.push_back({{"kernel", c.kernel_id}, {"binding", binding_json(c.binding)},
+                      {"key", c.kernel_id + "|" + kc::binding_str(c.binding)},
+                      {"noiseless", hexd(kc::noiseless_time(dev, pv))},
+                      {"simulate_time", hexd(kc::simulate_time(dev, c.kernel_id, c.binding, pv))},
+                      {"runs", r},
+                      {"gaussian", hexd(kc::keyed_gaussian(dev.seed, c.kernel_id + "|" + kc::binding_str(c.binding), 0))}});
+    }
+    json gm = json::array();
+    for (const auto& pairs : std::vector<std::vector<std::pair<double, double>>>{
+             {{1.1, 1.0}, {0.9, 1.0}}, {{1.0, 1.0}, {2.0, 1.0}}, {{3.0, 2.0}, {2.5, 2.0}, {1e-3, 1e-3}}}) {
+      json pj = json::array();
+      for (const auto& [p, a] : pairs) pj.push_back({p, a});
+      gm.push_back({{"pairs", pj}, {"geomean", hexd(kc::geometric_mean_error(pairs))}});
+    }
+    write(gdir + "/simulate.json", json{{"sigma", dev.sigma}, {"seed", dev.seed}, {"cases", sims}, {"geomean", gm}});
+  }
+
   // ---- fd_stencil / nbody made grid-evaluable ---------
   // Symbolic extraction throws E_NEEDS_BINDING for these two kernels only
   // because array_stat() computes a footprint before classifying

@@ -14,6 +14,7 @@ from .api import (  # noqa: F401
     argmin,
     evaluate_properties,
     fit_weights,
+    geometric_mean_error,
     gram_accumulate,
     gram_fused,
     launch_count,
@@ -25,6 +26,7 @@ from .api import (  # noqa: F401
     schema_index,
     schema_keys,
     schema_size,
+    simulate_time,
     solve_gram,
     suite_index,
     write_weights_json,

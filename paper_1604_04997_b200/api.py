@@ -250,6 +250,36 @@ def noiseless_time(alpha149: Sequence[float], prog: Program, bindings, stream=No
     return pred
 
 
+def simulate_time(alpha149: Sequence[float], prog: Program, bindings, sigma: float = 0.0, seed: int = 0,
+                  run: int = 0, with_status: bool = False, stream=None):
+    """Batched ``simulate_time`` / ``simulate_runs`` (simdevice.cpp:96-127):
+    the synthetic device's stored timings, noise keyed by
+    "<kernel>|<binding_str>" exactly as the reference keys it."""
+    torch = _torch()
+    arr, n, cols = _columns(prog, bindings)
+    out = torch.empty(n, dtype=torch.float64, device=cols[0].device)
+    st = torch.empty(n, dtype=torch.uint8, device=cols[0].device) if with_status else None
+    a = (ctypes.c_double * len(alpha149))(*alpha149)
+    check(lib().kcg_simulate_time(prog.handle, arr, n, a, float(sigma), int(seed), int(run), out.data_ptr(),
+                                  _ptr(st), _stream(stream)))
+    return (out, st) if with_status else out
+
+
+def geometric_mean_error(pred, actual, stream=None) -> float:
+    """``geometric_mean_error`` (model.cpp:119-133) over device tensors."""
+    torch = _torch()
+    if pred.numel() == 0:
+        raise _capi.KcgError(_capi.E_EMPTY, "no error pairs")
+    ls = torch.zeros(1, dtype=torch.float64, device=pred.device)
+    cnt = torch.zeros(1, dtype=torch.int64, device=pred.device)
+    bad = torch.zeros(1, dtype=torch.int64, device=pred.device)
+    check(lib().kcg_geomean_accumulate(pred.data_ptr(), actual.data_ptr(), pred.numel(), ls.data_ptr(),
+                                       cnt.data_ptr(), bad.data_ptr(), _stream(stream)))
+    if int(bad.item()):
+        raise _capi.KcgError(_capi.E_NONPOSITIVE_TIME, "actual time must be positive")
+    return math.exp(float(ls.item()) / int(cnt.item()))
+
+
 def argmin(progs: Sequence[Program], w: ModelWeights, bindings, return_preds: bool = False, stream=None):
     """Autotuning sweep: fused evaluate + predict over kernel variants with
     an argmin per problem size (lowest variant index wins ties)."""

@@ -601,6 +601,58 @@ int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, 
   });
 }
 
+int kcg_simulate_time(const kcg_program* cp, const int64_t* const* param_cols, size_t n,
+                      const double* alpha, double sigma, uint64_t seed, uint64_t run,
+                      double* times_out, uint8_t* status_out, void* stream) {
+  kcg_program* p = const_cast<kcg_program*>(cp);
+  if (!p || !alpha || !times_out) return fail(KCG_E_INVALID_ARGUMENT, "bad simulate arguments");
+  const int rc = kcg_eval_predict(cp, param_cols, n, alpha, times_out, status_out, nullptr, nullptr,
+                                  /*simulate=*/1, stream);
+  if (rc != KCG_OK || sigma == 0.0 || n == 0) return rc;  // simdevice.cpp:99
+  return guarded([&] {
+    kcg::NoiseArgs a{};
+    const int np = p->low.n_params;
+    std::vector<int> order(np);
+    for (int j = 0; j < np; ++j) order[j] = j;
+    std::sort(order.begin(), order.end(),
+              [&](int x, int y) { return p->param_names[x] < p->param_names[y]; });
+    for (int k = 0; k < np; ++k) {
+      const std::string seg = (k ? ";" : "") + p->param_names[order[k]] + "=";
+      if (seg.size() > sizeof(a.seg[0])) throw KcgError(KCG_E_UNSUPPORTED, "parameter name too long");
+      std::memcpy(a.seg[k], seg.data(), seg.size());
+      a.seg_len[k] = static_cast<int>(seg.size());
+      a.cols[k] = param_cols[order[k]];
+    }
+    a.n_params = np;
+    uint64_t h = 1469598103934665603ull;  // fnv1a(kernel + "|"), simdevice.cpp:23-30
+    for (unsigned char c : p->sym.kernel + "|") {
+      h ^= c;
+      h *= 1099511628211ull;
+    }
+    a.prefix_hash = h;
+    a.seed = seed;
+    a.counter = run;
+    a.sigma = sigma;
+    a.t = times_out;
+    a.n = static_cast<int64_t>(n);
+    kcg::launch_noise(a, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_geomean_accumulate(const double* pred, const double* actual, size_t n, double* log_sum,
+                           unsigned long long* count, unsigned long long* bad, void* stream) {
+  if (!pred || !actual || !log_sum || !count || !bad)
+    return fail(KCG_E_INVALID_ARGUMENT, "bad geomean arguments");
+  return guarded([&] {
+    require_device();
+    kcg::launch_geomean(pred, actual, n, log_sum, count, bad, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
 int kcg_solve_gram(int F, const double* G, const double* xt1, const double* colmax,
                    double* alpha_out, int* rank_out) {
   if (F < 1 || !G || !xt1 || !colmax || !alpha_out)

@@ -35,6 +35,25 @@ void launch_residual(const double* X, size_t n, int F, size_t ld,
 void launch_residual_grad(const double* X, size_t n, int F, size_t ld,
                           const double* alpha, double* g, void* stream);
 
+struct NoiseArgs {
+  const int64_t* cols[KCG_MAX_PARAMS];  // parameter columns, sorted by name
+  int n_params;
+  int seg_len[KCG_MAX_PARAMS];
+  unsigned char seg[KCG_MAX_PARAMS][48];  // "name=" (";name=" after the first)
+  uint64_t prefix_hash;                   // FNV-1a state after "kernel|"
+  uint64_t seed, counter;
+  double sigma;
+  double* t;                              // in: noiseless, out: noisy
+  int64_t n;
+};
+
+/// simulate_time's multiplicative noise (simdevice.cpp:13-46, 96-102)
+void launch_noise(const NoiseArgs& a, void* stream);
+
+/// geometric_mean_error accumulation (model.cpp:119-133)
+void launch_geomean(const double* pred, const double* actual, size_t n, double* log_sum,
+                    unsigned long long* count, unsigned long long* bad, void* stream);
+
 int num_sms();
 
 }  // namespace kcg

@@ -503,6 +503,80 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ---------------------------------------------------------------------------
+// simulate_time noise and geometric_mean_error
+
+__device__ __forceinline__ kcg_u64 fnv_byte(kcg_u64 h, unsigned char c) {
+  return (h ^ c) * 1099511628211ull;
+}
+
+__device__ __forceinline__ kcg_u64 splitmix64(kcg_u64& x) {
+  x += 0x9e3779b97f4a7c15ull;
+  kcg_u64 z = x;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+__global__ void __launch_bounds__(256) kcg_noise(const __grid_constant__ NoiseArgs a) {
+  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;
+  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {
+    const double t0 = a.t[i];
+    if (t0 != t0) continue;  // inadmissible point (NaN) stays NaN
+    // key = kernel + "|" + binding_str(b): "p=v;q=w" in std::map (name) order
+    kcg_u64 h = a.prefix_hash;
+    for (int j = 0; j < a.n_params; ++j) {
+      for (int c = 0; c < a.seg_len[j]; ++c) h = fnv_byte(h, a.seg[j][c]);
+      const kcg_i64 v = a.cols[j][i];
+      kcg_u64 u = v < 0 ? (kcg_u64)0 - (kcg_u64)v : (kcg_u64)v;
+      if (v < 0) h = fnv_byte(h, '-');
+      unsigned char d[20];
+      int nd = 0;
+      do {
+        d[nd++] = (unsigned char)('0' + u % 10);
+        u /= 10;
+      } while (u);
+      while (nd) h = fnv_byte(h, d[--nd]);
+    }
+    kcg_u64 st = h ^ (a.seed * 0x9e3779b97f4a7c15ull) ^ (a.counter * 0xd1342543de82ef95ull);
+    double u1 = (double)(splitmix64(st) >> 11) * 0x1.0p-53;
+    const double u2 = (double)(splitmix64(st) >> 11) * 0x1.0p-53;
+    if (u1 <= 0.0) u1 = 0x1.0p-53;
+    const double g = sqrt(-2.0 * log(u1)) * cos(2.0 * 3.14159265358979323846 * u2);
+    a.t[i] = t0 * exp(a.sigma * g);
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    kcg_geomean(const double* __restrict__ pred, const double* __restrict__ actual, kcg_i64 n,
+                double* log_sum, unsigned long long* count, unsigned long long* bad) {
+  double acc = 0.0;
+  unsigned long long c = 0, b = 0;
+  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;
+  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double p = pred[i], y = actual[i];
+    if (!(y > 0.0)) {
+      ++b;
+      continue;
+    }
+    double rel = fabs(p - y) / y;
+    if (rel < 1e-12) rel = 1e-12;
+    acc += log(rel);
+    ++c;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_down_sync(0xffffffffu, acc, o);
+    c += __shfl_down_sync(0xffffffffu, c, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(log_sum, acc);
+    atomicAdd(count, c);
+    if (b) atomicAdd(bad, b);
+  }
+}
+
 int g_sms = 0;
 
 }  // namespace
@@ -560,6 +634,20 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
   kcg_gram_x<<<(unsigned)ctas, kGramThreads, smem, static_cast<cudaStream_t>(stream)>>>(
       X, (kcg_i64)n, F, (kcg_i64)ld, chunks_per_cta * kGramRows, G, xt1, colmax);
   check(cudaGetLastError(), "kcg_gram_x launch");
+}
+
+void launch_noise(const NoiseArgs& a, void* stream) {
+  if (a.n == 0) return;
+  kcg_noise<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  check(cudaGetLastError(), "kcg_noise launch");
+}
+
+void launch_geomean(const double* pred, const double* actual, size_t n, double* log_sum,
+                    unsigned long long* count, unsigned long long* bad, void* stream) {
+  if (n == 0) return;
+  kcg_geomean<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(pred, actual, (kcg_i64)n,
+                                                                           log_sum, count, bad);
+  check(cudaGetLastError(), "kcg_geomean launch");
 }
 
 void launch_residual(const double* X, size_t n, int F, size_t ld, const double* alpha,

@@ -385,3 +385,38 @@ def test_fused_gram_large_matches_materialised_path():
     a = torch.tensor([alpha[k] for k in prog.props], dtype=torch.float64, device="cuda")
     want = float(((1.0 - X @ a) ** 2).sum())
     assert kc.residual_fused(prog, cols, T, alpha) == pytest.approx(want, rel=1e-9)
+
+
+def test_simulate_time_with_noise_matches_reference(programs):
+    """simulate_time / simulate_runs with sigma = 0.02, seed 7 for every
+    measurement case of a symbolic kernel: the noise key "<kernel>|<binding>"
+    is hashed on the GPU exactly like simdevice.cpp; exp/log/cos are CUDA's,
+    so times agree to a few ulps (sigma = 0 is bitwise, see
+    test_simulate_order_matches_noiseless_time)."""
+    d = load_golden("simulate.json")
+    sim = ko.simdev_reference_alpha()
+    groups = {}
+    for c in d["cases"]:
+        groups.setdefault(c["kernel"], []).append(c)
+    worst = 0.0
+    for kid, cs in groups.items():
+        prog, _ = programs[kid]
+        cols = _cols(prog, [{k: int(v) for k, v in c["binding"].items()} for c in cs])
+        for run in range(3):
+            t = kc.simulate_time(sim, prog, cols, sigma=d["sigma"], seed=d["seed"], run=run).cpu().numpy()
+            for i, c in enumerate(cs):
+                want = hexf(c["runs"][run])
+                worst = max(worst, abs(t[i] - want) / want)
+        t0 = kc.simulate_time(sim, prog, cols, sigma=0.0).cpu().numpy()
+        assert list(t0) == [hexf(c["noiseless"]) for c in cs]
+    assert worst < 1e-14, worst
+
+
+def test_geometric_mean_error_fixtures():
+    for g in load_golden("simulate.json")["geomean"]:
+        p = torch.tensor([x[0] for x in g["pairs"]], dtype=torch.float64, device="cuda")
+        a = torch.tensor([x[1] for x in g["pairs"]], dtype=torch.float64, device="cuda")
+        assert kc.geometric_mean_error(p, a) == pytest.approx(hexf(g["geomean"]), rel=1e-14)
+    with pytest.raises(kc.KcgError):
+        kc.geometric_mean_error(torch.ones(2, dtype=torch.float64, device="cuda"),
+                                torch.zeros(2, dtype=torch.float64, device="cuda"))

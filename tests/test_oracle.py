@@ -199,3 +199,19 @@ def test_derived_programs_match_survey_appendix_a():
     c = nb.evaluate_properties({"n": 1 << 20})
     assert c[ko.SCHEMA_INDEX["mem.global.load.s32.3/3"]] == 3 * 4 ** 20 + 3 * 4 ** 20 // 256
     assert c[ko.SCHEMA_INDEX["launch.groups"]] == (1 << 20) // 256
+
+
+def test_keyed_gaussian_and_simulate_match_reference_bitwise():
+    """The Python restatement of simdevice.cpp:13-46 / 96-127 reproduces the
+    reference's noisy stored timings bit for bit (same libm)."""
+    import math
+    d = load_golden("simulate.json")
+    sim = ko.simdev_reference_alpha()
+    for c in d["cases"][:120]:
+        g = ko.keyed_gaussian(d["seed"], c["key"], 0)
+        assert g == hexf(c["gaussian"])
+        t0 = hexf(c["noiseless"])
+        for run, r in enumerate(c["runs"]):
+            assert t0 * math.exp(d["sigma"] * ko.keyed_gaussian(d["seed"], c["key"], run)) == hexf(r)
+    for gm in d["geomean"]:
+        assert ko.geometric_mean_error(gm["pairs"]) == hexf(gm["geomean"])
