@@ -795,14 +795,15 @@ std::string codegen(const std::vector<const Lowered*>& progs,
               << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;\n"
               << "  double acc[" << NT << "][2];\n  #pragma unroll\n  for (int t = 0; t < " << NT
               << "; ++t) acc[t][0] = acc[t][1] = 0.0;\n"
-              << "  double mxr[" << F << "]" << (ones ? "" : std::string(", s1r[") + std::to_string(F) + "]") << ";\n"
-              << "  #pragma unroll\n  for (int j = 0; j < " << F << "; ++j) { mxr[j] = 0.0;"
+              << "  unsigned long long mxr[" << F << "];\n"
+              << (ones ? "" : std::string("  double s1r[") + std::to_string(F) + "];\n")
+              << "  #pragma unroll\n  for (int j = 0; j < " << F << "; ++j) { mxr[j] = 0ull;"
               << (ones ? "" : " s1r[j] = 0.0;") << " }\n"
               << "  unsigned long long bad = 0;\n  double* xw = xs_base + warp * 32 * " << LDX << ";\n"
               << "  for (int e = lane; e < 32 * " << LDX << "; e += 32) xw[e] = 0.0;  // padding stays zero\n"
               << "  __syncwarp();\n";
     cons_row << "      #pragma unroll\n      for (int j = 0; j < " << F << "; ++j) { xw[lane * " << LDX
-             << " + j] = x[j]; mxr[j] = fmax(mxr[j], fabs(x[j]));"
+             << " + j] = x[j]; { const unsigned long long b = (unsigned long long)__double_as_longlong(x[j]) & 0x7fffffffffffffffull; mxr[j] = b > mxr[j] ? b : mxr[j]; }"
              << (ones ? "" : " s1r[j] += x[j];") << " }\n";
     if (ones) cons_row << "      xw[lane * " << LDX << " + " << F << "] = ok ? 1.0 : 0.0;\n";
     cons_row << "      __syncwarp();\n"
@@ -818,10 +819,9 @@ std::string codegen(const std::vector<const Lowered*>& progs,
              << "      }\n      __syncwarp();\n";
     cons_end << "  __syncthreads();\n"
              << "  #pragma unroll\n  for (int j = 0; j < " << F << "; ++j) {\n"
-             << "    double m = mxr[j];\n"
-             << "    #pragma unroll\n    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));\n"
-             << "    if (lane == 0) atomicMax((unsigned long long*)(red + " << FP * FP + FP
-             << " + j), (unsigned long long)__double_as_longlong(m));\n";
+             << "    unsigned long long m = mxr[j];\n"
+             << "    #pragma unroll\n    for (int o = 16; o > 0; o >>= 1) { const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o); m = y > m ? y : m; }\n"
+             << "    if (lane == 0) atomicMax((unsigned long long*)(red + " << FP * FP + FP << " + j), m);\n";
     if (!ones)
       cons_end << "    double sj = s1r[j];\n"
                << "    #pragma unroll\n    for (int o = 16; o > 0; o >>= 1) sj += __shfl_xor_sync(0xffffffffu, sj, o);\n"
@@ -914,6 +914,8 @@ std::string codegen(const std::vector<const Lowered*>& progs,
         "  extern __shared__ __align__(128) unsigned char kcg_smem[];\n"
         "  kcg_i64* buf = reinterpret_cast<kcg_i64*>(kcg_smem);\n"
         "  __shared__ __align__(8) unsigned long long full[S];\n"
+        "  __shared__ unsigned reads[S];\n"
+        "  if (threadIdx.x < S) reads[threadIdx.x] = 0;\n"
      << cons_decl.str()
      << (dmma ? std::string("  double* slow_row = xw + lane * ") + std::to_string(LDX) + ";\n"
               : std::string("  double* slow_row = reinterpret_cast<double*>(kcg_smem) + S * NC * TP + threadIdx.x * ") +
@@ -959,10 +961,16 @@ std::string codegen(const std::vector<const Lowered*>& progs,
               "      else { tq[0] = __longlong_as_double(x0.x); tq[1] = __longlong_as_double(x0.y);\n"
               "             tq[2] = __longlong_as_double(x1.x); tq[3] = __longlong_as_double(x1.y); }\n"
               "    }\n"
-              "    __syncthreads();\n"
-              "    if (threadIdx.x == 0) {\n"
-              "      const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
-              "      if (nt < ntiles) issue(s, nt);\n"
+              "    // last warp to finish reading stage s refills it (no CTA-wide barrier:\n"
+              "    // warps drift apart freely between tiles)\n"
+              "    __syncwarp();\n"
+              "    if ((threadIdx.x & 31) == 0) {\n"
+              "      __threadfence_block();\n"
+              "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
+              "        reads[s] = 0;\n"
+              "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+              "        if (nt < ntiles) issue(s, nt);\n"
+              "      }\n"
               "    }\n"
               "    const kcg_i64 base = tile * TP + 4 * threadIdx.x;\n"
               "    #pragma unroll\n"
