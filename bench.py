@@ -170,9 +170,16 @@ def main():
 
     import paper_1604_04997_b200 as kc
 
+    # one process per GPU; KCG_DIST_BACKEND=gloo lets several ranks share
+    # one device for a functional dry run of the multi-rank path
+    backend = os.environ.get("KCG_DIST_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     progs = [kc.load_program(v) for v in VARIANTS]
