@@ -223,6 +223,24 @@ int kcg_weights_write_json(const char* path, const char* device,
                            const double* alpha149, const uint8_t* covered149,
                            double objective, uint64_t n_cases);
 
+/* ---- measurements (csvio.cpp:104-225) -----------------------------------
+ * Reads the reference's measurement CSV (kernel,binding,group_config,time_s)
+ * or raw-runs CSV (..,run_index,time_s; reduced like reduce_raw_runs: runs
+ * ordered by index, the first `discard` dropped, min of the rest), detected
+ * by header like the CLI (kernelcost.cpp:116-126). Records are grouped per
+ * kernel (kernels sorted by name) into HOST SoA columns, one per binding
+ * parameter (sorted by name), plus the observed times.                    */
+typedef struct kcg_measurements kcg_measurements;
+int kcg_measurements_read_csv(const char* path, int discard, kcg_measurements** out);
+void kcg_measurements_destroy(kcg_measurements* m);
+int kcg_measurements_num_kernels(const kcg_measurements* m);
+const char* kcg_measurements_kernel(const kcg_measurements* m, int i);
+size_t kcg_measurements_num_rows(const kcg_measurements* m, int i);
+int kcg_measurements_num_params(const kcg_measurements* m, int i);
+const char* kcg_measurements_param_name(const kcg_measurements* m, int i, int j);
+const int64_t* kcg_measurements_column(const kcg_measurements* m, int i, int j);
+const double* kcg_measurements_times(const kcg_measurements* m, int i);
+
 /* ---- diagnostics -------------------------------------------------------- */
 const char* kcg_status_str(int status);
 const char* kcg_point_status_str(int point_status);

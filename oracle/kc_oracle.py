@@ -394,3 +394,36 @@ def simdev_reference_alpha() -> list[float]:
     }.items():
         a[SCHEMA_INDEX[k]] = v
     return a
+
+
+def parse_binding(s: str) -> dict:
+    """csvio.cpp:86-102"""
+    b = {}
+    if not s:
+        return b
+    for part in s.split(";"):
+        k, _, v = part.partition("=")
+        b[k] = int(v)
+    return b
+
+
+def read_any_csv(path, discard: int = 4):
+    """kernelcost.cpp:116-126: measurement CSV, or raw runs reduced like
+    reduce_raw_runs (csvio.cpp:192-225). Returns [(kernel, binding, time)]."""
+    lines = [ln.rstrip("\r") for ln in open(path).read().splitlines() if ln.strip()]
+    header, rows = lines[0], [ln.split(",") for ln in lines[1:]]
+    if header == "kernel,binding,group_config,time_s":
+        return [(r[0], parse_binding(r[1]), float(r[3])) for r in rows]
+    assert header == "kernel,binding,group_config,run_index,time_s", header
+    groups = {}
+    for r in rows:
+        b = parse_binding(r[1])
+        key = (r[0], ";".join(f"{k}={v}" for k, v in sorted(b.items())), r[2])
+        groups.setdefault(key, []).append((int(r[3]), float(r[4])))
+    out = []
+    for key in sorted(groups):
+        times = [t for _, t in sorted(groups[key])]
+        if len(times) <= discard:
+            raise ValueError("E_INVALID_ARGUMENT: not enough runs")
+        out.append((key[0], parse_binding(key[1]), min(times[discard:])))
+    return out

@@ -25,6 +25,7 @@
 
 #include "json.hpp"
 #include "kcref_program.hpp"
+#include "kernelcost/campaign.hpp"
 #include "kernelcost/csvio.hpp"
 #include "kernelcost/error.hpp"
 #include "kernelcost/jsonio.hpp"
@@ -440,6 +441,60 @@ int main(int argc, char** argv) {
       gm.push_back({{"pairs", pj}, {"geomean", hexd(kc::geometric_mean_error(pairs))}});
     }
     write(gdir + "/simulate.json", json{{"sigma", dev.sigma}, {"seed", dev.seed}, {"cases", sims}, {"geomean", gm}});
+  }
+
+  // ---- campaign CSVs and the CLI fit / eval on them (kernelcost.cpp:116-400)
+  {
+    kc::SimDevice dev0 = ref;
+    const auto camp = kc::run_campaign(dev0, lib, lib.measurement_cases(), kCap);
+    kc::write_measurements_csv(gdir + "/meas_sigma0.csv", camp.records);
+    // raw runs: sigma 0.02, seed 7, 8 runs per case (simulate --runs 8)
+    kc::SimDevice dev = ref;
+    dev.sigma = 0.02;
+    dev.seed = 7;
+    std::vector<kc::RawRun> raw;
+    for (const auto& c : lib.measurement_cases()) {
+      const kc::PropertyVector pv = kc::extract_properties(irs.at(c.kernel_id), c.binding, kCap);
+      const auto ts = kc::simulate_runs(dev, c.kernel_id, c.binding, pv, 8);
+      for (int r = 0; r < 8; ++r) raw.push_back({c.kernel_id, c.binding, c.group_config, r, ts[r]});
+    }
+    kc::write_raw_runs_csv(gdir + "/raw_runs_sigma002.csv", raw);
+    json out = json::object();
+    for (const char* name : {"meas_sigma0.csv", "raw_runs_sigma002.csv"}) {
+      const std::string path = gdir + "/" + name;
+      std::vector<kc::MeasurementRecord> recs;
+      {
+        std::ifstream probe(path);
+        std::string header;
+        std::getline(probe, header);
+        recs = header == "kernel,binding,group_config,run_index,time_s"
+                   ? kc::reduce_raw_runs(kc::read_raw_runs_csv(path))
+                   : kc::read_measurements_csv(path);
+      }
+      std::vector<kc::FitCase> cases;
+      std::vector<kc::PropertyVector> pvs;
+      for (const auto& r : recs) {
+        pvs.push_back(kc::extract_properties(irs.at(r.kernel), r.binding, kCap));
+        cases.push_back({pvs.back(), r.time_s});
+      }
+      auto [w, rep] = kc::fit_weights(kc::build_design_matrix(cases), "gpu-sim");
+      json alpha = json::object();
+      for (size_t i = 0; i < kc::schema_size(); ++i)
+        if (w.covered[i]) alpha[kc::schema_keys()[i]] = hexd(w.alpha[i]);
+      // eval (kernelcost.cpp:366-400) with these weights on the same records
+      std::map<std::string, std::vector<std::pair<double, double>>> by_kernel;
+      std::vector<std::pair<double, double>> all;
+      for (size_t i = 0; i < recs.size(); ++i) {
+        const double pred = kc::predict(w, pvs[i]).seconds;
+        by_kernel[recs[i].kernel].emplace_back(pred, recs[i].time_s);
+        all.emplace_back(pred, recs[i].time_s);
+      }
+      json per = json::object();
+      for (const auto& [id, pairs] : by_kernel) per[id] = hexd(kc::geometric_mean_error(pairs));
+      out[name] = {{"n_records", recs.size()}, {"alpha", alpha}, {"objective", hexd(rep.objective)},
+                   {"geomean_per_kernel", per}, {"geomean_overall", hexd(kc::geometric_mean_error(all))}};
+    }
+    write(gdir + "/cli_fit_eval.json", out);
   }
 
   // ---- fd_stencil / nbody made grid-evaluable ---------

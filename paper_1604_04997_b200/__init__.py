@@ -7,6 +7,10 @@ of the least-squares fit. See DESIGN.md; the C ABI is include/kcg.h.
 """
 from .api import (  # noqa: F401
     BoundBatch,
+    KernelMeasurements,
+    eval_from_csv,
+    fit_from_csv,
+    read_measurements,
     FitResult,
     GramStats,
     ModelWeights,

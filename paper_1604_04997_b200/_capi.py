@@ -67,6 +67,15 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_simulate_time": (ctypes.c_int, [P, P, ctypes.c_size_t, DP, ctypes.c_double, ctypes.c_uint64,
                                              ctypes.c_uint64, P, P, P]),
         "kcg_geomean_accumulate": (ctypes.c_int, [P, P, ctypes.c_size_t, P, P, P, P]),
+        "kcg_measurements_read_csv": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(P)]),
+        "kcg_measurements_destroy": (None, [P]),
+        "kcg_measurements_num_kernels": (ctypes.c_int, [P]),
+        "kcg_measurements_kernel": (ctypes.c_char_p, [P, ctypes.c_int]),
+        "kcg_measurements_num_rows": (ctypes.c_size_t, [P, ctypes.c_int]),
+        "kcg_measurements_num_params": (ctypes.c_int, [P, ctypes.c_int]),
+        "kcg_measurements_param_name": (ctypes.c_char_p, [P, ctypes.c_int, ctypes.c_int]),
+        "kcg_measurements_column": (I64P, [P, ctypes.c_int, ctypes.c_int]),
+        "kcg_measurements_times": (DP, [P, ctypes.c_int]),
         "kcg_solve_gram": (ctypes.c_int, [ctypes.c_int, DP, DP, DP, DP, ctypes.POINTER(ctypes.c_int)]),
         "kcg_refine_gram": (ctypes.c_int, [ctypes.c_int, DP, DP, DP, DP]),
         "kcg_weights_read_json": (ctypes.c_int, [ctypes.c_char_p, DP, U8P, DP, ctypes.POINTER(ctypes.c_uint64)]),

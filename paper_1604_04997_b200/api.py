@@ -404,3 +404,109 @@ def fit_weights(X, refine: int = 1, stream=None) -> FitResult:
 
 def launch_count() -> int:
     return int(lib().kcg_launch_count())
+
+
+# ---------------------------------------------------------------------------
+# measurement CSVs -> GPU fit / eval (the CLI's `fit` and `eval`,
+# kernelcost.cpp:236-272 and 366-400)
+
+@dataclass
+class KernelMeasurements:
+    kernel: str
+    params: list          # binding parameter names (sorted)
+    columns: dict         # name -> numpy int64 array
+    times: object         # numpy float64 array
+
+
+def read_measurements(path, discard: int = 4) -> list[KernelMeasurements]:
+    """Measurement or raw-runs CSV (csvio.cpp:104-225), grouped per kernel."""
+    import numpy as np
+    h = _capi.P()
+    check(lib().kcg_measurements_read_csv(str(path).encode(), int(discard), ctypes.byref(h)))
+    L = lib()
+    try:
+        out = []
+        for i in range(L.kcg_measurements_num_kernels(h)):
+            n = L.kcg_measurements_num_rows(h, i)
+            params = [L.kcg_measurements_param_name(h, i, j).decode()
+                      for j in range(L.kcg_measurements_num_params(h, i))]
+            cols = {p: np.ctypeslib.as_array(L.kcg_measurements_column(h, i, j), shape=(n,)).copy()
+                    for j, p in enumerate(params)}
+            t = np.ctypeslib.as_array(L.kcg_measurements_times(h, i), shape=(n,)).copy()
+            out.append(KernelMeasurements(L.kcg_measurements_kernel(h, i).decode(), params, cols, t))
+        return out
+    finally:
+        L.kcg_measurements_destroy(h)
+
+
+def _program_for(kernel: str, programs) -> Program:
+    if programs is None:
+        return load_program(kernel)
+    if isinstance(programs, Mapping):
+        return programs[kernel]
+    return Program.from_file(Path(programs) / f"{kernel}.kcp")
+
+
+def _device_rows(km: KernelMeasurements, prog: Program, device="cuda"):
+    torch = _torch()
+    if sorted(prog.params) != sorted(km.params):
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT,
+                             f"binding missing parameter for kernel '{km.kernel}': {km.params} vs {prog.params}")
+    cols = {p: torch.from_numpy(km.columns[p]).to(device) for p in prog.params}
+    T = torch.from_numpy(km.times).to(device)
+    return cols, T
+
+
+def fit_from_csv(path, programs=None, device: str = "", discard: int = 4, stream=None):
+    """``kernelcost fit <csv>`` on the GPU: per kernel the fused
+    evaluate -> row -> Gram kernel, scattered into the schema-wide Gram
+    (rows of different kernels are disjoint), one equilibrated min-norm
+    solve, then the fused residual pass for the objective. Returns
+    (ModelWeights, report) with report = {objective, n_cases, rank, bad_rows}."""
+    torch = _torch()
+    K = schema_size()
+    G = torch.zeros((K, K), dtype=torch.float64, device="cuda")
+    x1 = torch.zeros(K, dtype=torch.float64, device="cuda")
+    cm = torch.zeros(K, dtype=torch.float64, device="cuda")
+    meas = read_measurements(path, discard)
+    if not meas:
+        raise _capi.KcgError(_capi.E_EMPTY, "no fit cases")
+    rows, bad = 0, 0
+    staged = []
+    for km in meas:
+        if (km.times <= 0).any():
+            raise _capi.KcgError(_capi.E_NONPOSITIVE_TIME, f"observed time must be positive ({km.kernel})")
+        prog = _program_for(km.kernel, programs)
+        cols, T = _device_rows(km, prog)
+        st = gram_fused(prog, cols, T, stream=stream)
+        idx = torch.tensor(prog.props, dtype=torch.int64, device="cuda")
+        G[idx.unsqueeze(1), idx.unsqueeze(0)] += st.G
+        x1[idx] += st.xt1
+        cm[idx] = torch.maximum(cm[idx], st.colmax)
+        rows += st.n_rows
+        bad += st.bad_rows
+        staged.append((prog, cols, T))
+    if bad:
+        raise _capi.KcgError(_capi.E_ASSUMPTION_VIOLATED, f"{bad} measurement rows are not admissible")
+    alpha, rank = solve_gram(GramStats(G, x1, cm, rows))
+    obj = sum(residual_fused(prog, cols, T, alpha, stream=stream) for prog, cols, T in staged)
+    covered = [bool(c > 0) for c in cm.cpu().tolist()]
+    w = ModelWeights(device, "v1", list(alpha), covered, obj, rows)
+    return w, {"objective": obj, "n_cases": rows, "rank": rank, "bad_rows": bad}
+
+
+def eval_from_csv(w: ModelWeights, path, programs=None, discard: int = 4, stream=None) -> dict:
+    """``kernelcost eval <csv> --weights w.json`` on the GPU: batched
+    predict per kernel and geometric mean relative error per kernel and
+    overall (model.cpp:119-133)."""
+    torch = _torch()
+    per, preds, acts = {}, [], []
+    for km in read_measurements(path, discard):
+        prog = _program_for(km.kernel, programs)
+        cols, T = _device_rows(km, prog)
+        p = predict(w, prog, cols, stream=stream)
+        per[km.kernel] = geometric_mean_error(p, T, stream=stream)
+        preds.append(p)
+        acts.append(T)
+    overall = geometric_mean_error(torch.cat(preds), torch.cat(acts), stream=stream)
+    return {"per_kernel": per, "overall": overall, "n_cases": sum(int(a.numel()) for a in acts)}

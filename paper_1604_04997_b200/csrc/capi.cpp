@@ -51,6 +51,12 @@ int fail(int code, const std::string& msg) {
   return code;
 }
 
+}  // namespace
+
+extern "C" void kcg_set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
+namespace {
+
 template <class F>
 int guarded(F&& f) {
   try {

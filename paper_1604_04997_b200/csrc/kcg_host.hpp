@@ -27,6 +27,11 @@ namespace kcg {
 using i128 = __int128;
 using u128 = unsigned __int128;
 
+/// sets the calling thread's kcg_last_error() text (capi.cpp)
+}  // namespace kcg
+extern "C" void kcg_set_last_error(const char* msg);
+namespace kcg {
+
 struct KcgError : std::runtime_error {
   int code;
   KcgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}

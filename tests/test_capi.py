@@ -191,3 +191,39 @@ def test_generated_kernels_compile_for_atom_programs():
         for kind in (0, 1):
             rc = L.kcg_jit_compile_check(L.kcg_program_jit_source_kind(p.handle, kind), b"k")
             assert rc == 0, L.kcg_last_error().decode()[:3000]
+
+
+@pytest.mark.parametrize("name", ["meas_sigma0.csv", "raw_runs_sigma002.csv"])
+def test_measurement_csv_reader_matches_oracle(name):
+    """kcg_measurements_read_csv == the restated read_any_csv /
+    reduce_raw_runs of the reference CLI (bitwise times, exact bindings)."""
+    recs = ko.read_any_csv(GOLDEN / name)
+    got = {}
+    for km in kc.read_measurements(GOLDEN / name):
+        for i in range(len(km.times)):
+            key = (km.kernel, tuple(sorted((p, int(km.columns[p][i])) for p in km.params)))
+            got.setdefault(key, []).append(float(km.times[i]))
+    want = {}
+    for k, b, t in recs:
+        want.setdefault((k, tuple(sorted(b.items()))), []).append(t)
+    assert got == want
+    assert sum(len(v) for v in got.values()) == 390
+
+
+def test_measurement_csv_errors(tmp_path):
+    bad = tmp_path / "bad.csv"
+    bad.write_text("kernel,binding,time_s\n")
+    with pytest.raises(kc.KcgError) as e:
+        kc.read_measurements(bad)
+    assert e.value.code == _capi.E_PARSE
+    bad.write_text("kernel,binding,group_config,time_s\nk,n=12,1,abc\n")
+    with pytest.raises(kc.KcgError) as e:
+        kc.read_measurements(bad)
+    assert e.value.code == _capi.E_PARSE
+    bad.write_text("kernel,binding,group_config,run_index,time_s\nk,n=12,1,0,1.0\n")
+    with pytest.raises(kc.KcgError) as e:
+        kc.read_measurements(bad)  # fewer runs than the 4 discarded warm-ups
+    assert e.value.code == _capi.E_INVALID_ARGUMENT
+    with pytest.raises(kc.KcgError) as e:
+        kc.read_measurements(tmp_path / "missing.csv")
+    assert e.value.code == _capi.E_IO

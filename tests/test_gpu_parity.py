@@ -420,3 +420,33 @@ def test_geometric_mean_error_fixtures():
     with pytest.raises(kc.KcgError):
         kc.geometric_mean_error(torch.ones(2, dtype=torch.float64, device="cuda"),
                                 torch.zeros(2, dtype=torch.float64, device="cuda"))
+
+
+@pytest.mark.parametrize("name", ["meas_sigma0.csv", "raw_runs_sigma002.csv"])
+def test_cli_fit_and_eval_from_csv(name, tmp_path):
+    """`kernelcost fit` / `eval` on the reference's own campaign CSVs
+    (noiseless and 8 noisy raw runs per case), on the GPU: weights within the
+    reference's 1e-6, per-kernel geometric mean errors to 1e-6 (bitwise
+    predictions when given the reference's weights)."""
+    ref = load_golden("cli_fit_eval.json")[name]
+    path = GOLDEN / name
+    w, rep = kc.fit_from_csv(path, device="gpu-sim")
+    assert rep["n_cases"] == ref["n_records"] == 390
+    for k, v in ref["alpha"].items():
+        r, got = hexf(v), w.alpha[ko.SCHEMA_INDEX[k]]
+        if abs(r) > 1e-15:
+            assert abs(got - r) <= 1e-6 * abs(r), (name, k, got, r)
+    assert rep["objective"] == pytest.approx(hexf(ref["objective"]), rel=1e-6, abs=1e-20)
+    # eval with the reference's weights: predictions are bitwise, geomeans ~ulp
+    wref = kc.ModelWeights(device="ref", alpha=[0.0] * 149, covered=[False] * 149)
+    for k, v in ref["alpha"].items():
+        wref.alpha[ko.SCHEMA_INDEX[k]] = hexf(v)
+        wref.covered[ko.SCHEMA_INDEX[k]] = True
+    ev = kc.eval_from_csv(wref, path)
+    for k, v in ref["geomean_per_kernel"].items():
+        assert ev["per_kernel"][k] == pytest.approx(hexf(v), rel=1e-12), k
+    assert ev["overall"] == pytest.approx(hexf(ref["geomean_overall"]), rel=1e-12)
+    # and the weights file round-trips through the reference format
+    kc.write_weights_json(tmp_path / "w.json", w)
+    w2 = kc.read_weights_json(tmp_path / "w.json")
+    assert w2.alpha == w.alpha and w2.n_cases == 390
