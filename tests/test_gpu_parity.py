@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import kc_oracle as ko
-from conftest import PROGRAMS, hexf, load_golden
+from conftest import GOLDEN, PROGRAMS, hexf, load_golden
 
 pytestmark = pytest.mark.gpu
 
