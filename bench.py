@@ -451,8 +451,12 @@ def _sharded_fit(kc, torch, dev, world, rank, rows):
     return {"metric": "fit rows/sec", "rows": total_rows, "value": total_rows / sec, "ms": sec * 1e3,
             "rank": rk, "objective": obj, "scaling": "weak",
             "workload": f"config5: {rows} rows/rank (matmul_tiled_g16x16, T = noiseless_time), fused "
-                        "evaluate->row->Gram (DMMA) + NCCL all-reduce + host min-norm solve + fused residual",
-            "hbm_frac_gram_input": 32.0 * rows / sec / 1e9 / peaks()[0]}
+                        "evaluate->row->Gram (monomial basis) + NCCL all-reduce + host min-norm solve + "
+                        "fused residual",
+            # two streaming passes over the rows (Gram, then residual at the
+            # solved weights), 8*P + 8 = 32 B per row each
+            "bytes_per_row": 64,
+            "hbm_frac": 64.0 * rows / sec / 1e9 / peaks()[0]}
 
 
 def _timed(torch, fn, reps=5, warm=2):

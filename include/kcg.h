@@ -106,6 +106,11 @@ const char* kcg_program_kernel_name(const kcg_program* prog);
  * (fast path) and int128 (wide path); diagnostics for tests/DESIGN.md     */
 int kcg_program_safe_bounds(const kcg_program* prog, int64_t* b64, int64_t* b128);
 int kcg_program_set_engine(kcg_program* prog, int engine);
+/* Fused Gram / residual rows over the monomial basis of the program's keys
+ * (default 1: used whenever it is narrower than the key set; G, xt1 and
+ * colmax are the same statistics up to fp64 rounding). 0 = one column per
+ * key, every x_j = double(count_j) / T correctly rounded.                  */
+int kcg_program_set_gram_basis(kcg_program* prog, int enable);
 /* CUDA source the JIT path compiles for this program (NUL-terminated,
  * owned by the program) -- for inspection and tests                       */
 const char* kcg_program_jit_source(kcg_program* prog);

@@ -54,6 +54,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_program_kernel_name": (ctypes.c_char_p, [P]),
         "kcg_program_safe_bounds": (ctypes.c_int, [P, I64P, I64P]),
         "kcg_program_set_engine": (ctypes.c_int, [P, ctypes.c_int]),
+        "kcg_program_set_gram_basis": (ctypes.c_int, [P, ctypes.c_int]),
         "kcg_program_jit_source": (ctypes.c_char_p, [P]),
         "kcg_program_jit_source_kind": (ctypes.c_char_p, [P, ctypes.c_int]),
         "kcg_jit_compile_check": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p]),

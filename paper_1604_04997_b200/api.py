@@ -84,6 +84,11 @@ class Program:
         code = {"jit": _capi.ENGINE_JIT, "interp": _capi.ENGINE_INTERP}[engine]
         check(lib().kcg_program_set_engine(self._h, code))
 
+    def set_gram_basis(self, enable: bool) -> None:
+        """Fused Gram / residual rows over the keys' monomial basis (default)
+        or one correctly rounded column per key (include/kcg.h)."""
+        check(lib().kcg_program_set_gram_basis(self._h, 1 if enable else 0))
+
     def jit_source(self) -> str:
         return lib().kcg_program_jit_source(self._h).decode()
 

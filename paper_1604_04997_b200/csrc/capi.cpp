@@ -318,6 +318,15 @@ int kcg_program_set_engine(kcg_program* p, int engine) {
   return KCG_OK;
 }
 
+int kcg_program_set_gram_basis(kcg_program* p, int enable) {
+  if (!p) return fail(KCG_E_INVALID_ARGUMENT, "null program");
+  if (p->low.gram_basis != (enable != 0)) {
+    p->low.gram_basis = enable != 0;
+    p->jit_gram = p->jit_resid = nullptr;  // respecialise on next use (modules stay cached)
+  }
+  return KCG_OK;
+}
+
 const char* kcg_program_jit_source(kcg_program* p) {
   if (!p) return nullptr;
   if (p->jit_src.empty())
@@ -544,7 +553,7 @@ int kcg_gram_fused(const kcg_program* cp, const int64_t* const* param_cols, cons
     ab.finish();
     // persistent TMA-streamed kernel (2 CTAs/SM for the DMMA variant)
     kcg::launch_jit(p->jit_gram, ab.b.data(), ab.b.size(), kcg::num_sms() * 2, 256, stream,
-                    kcg::fused_smem_bytes(np, static_cast<int>(p->low.keys.size()), true));
+                    kcg::fused_smem_bytes(np, p->low, true));
     ++g_launches;
     return KCG_OK;
   });
@@ -598,10 +607,19 @@ int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, 
     ab.push<int32_t>(vec ? 1 : 0);
     std::vector<double> al(std::max(F, 1), 0.0);
     compact_alpha(p, alpha, al.data());
+    const kcg::GramBasis gb = kcg::gram_basis(p->low);
+    if (gb.reduced) {
+      // x . alpha = sum_b u_b * beta_b with beta_b = sum_j alpha_j A_jb
+      std::vector<double> beta(gb.monos.size(), 0.0);
+      for (int j = 0; j < F; ++j)
+        for (const auto& [b, c] : gb.terms[j]) beta[b] += al[j] * c;
+      al.assign(std::max(F, 1), 0.0);
+      std::copy(beta.begin(), beta.end(), al.begin());
+    }
     for (double v : al) ab.push<double>(v);
     ab.finish();
     kcg::launch_jit(p->jit_resid, ab.b.data(), ab.b.size(), kcg::num_sms() * 2, 256, stream,
-                    kcg::fused_smem_bytes(np, F, false));
+                    kcg::fused_smem_bytes(np, p->low, false));
     ++g_launches;
     return KCG_OK;
   });

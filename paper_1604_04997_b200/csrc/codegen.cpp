@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
 #include <sstream>
 
 #include "kcg_codegen.hpp"
@@ -57,11 +58,16 @@ const char* cmp_str(int op) {
 constexpr int64_t kU32 = 0xffffffffll;
 
 // fast: T = kcg_i64; small: every parameter <= b64 < 2^32
+// gb != nullptr: kcg_widem_<v> -- same checks, but writes the basis values
+// u[b] = double(mono_b) (gram_basis) instead of the counts.
 void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast,
-               const char* wide_name = "kcg_wide_") {
+               const char* wide_name = "kcg_wide_", const GramBasis* gb = nullptr) {
   const bool small = fast && L.b64 >= 0 && L.b64 <= kU32;
   std::vector<bool> atom_u32(L.n_atoms, false);  // value known in [0, 2^32)
-  if (fast)
+  if (gb)
+    os << "__device__ __noinline__ int kcg_widem_" << v
+       << "(const kcg_i64* __restrict__ p, double* __restrict__ u) {\n  typedef kcg_i128 T;\n";
+  else if (fast)
     os << "__device__ __forceinline__ int kcg_fast_" << v
        << "(const kcg_i64* __restrict__ p, kcg_i64* __restrict__ cnt) {\n  typedef kcg_i64 T;\n";
   else
@@ -179,6 +185,11 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast,
   for (size_t j = 0; j < L.keys.size(); ++j) {
     const LExpr& ex = L.exprs[L.keys[j].expr];
     const int e = L.keys[j].expr;
+    if (gb) {
+      if (ex.D != 1)
+        os << "  if (e" << e << " % " << lit(ex.D) << " != (T)0) return KCG_PT_NONINTEGRAL;\n";
+      continue;
+    }
     if (ex.D != 1) {
       os << "  if (e" << e << " % " << lit(ex.D) << " != (T)0) return KCG_PT_NONINTEGRAL;\n";
       os << "  cnt[" << j << "] = e" << e << " / " << lit(ex.D) << ";\n";
@@ -186,6 +197,10 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast,
       os << "  cnt[" << j << "] = e" << e << ";\n";
     }
   }
+  if (gb)
+    for (size_t b = 0; b < gb->monos.size(); ++b)
+      os << "  u[" << b << "] = " << (gb->monos[b] < 0 ? std::string("1.0") : "kcg_to_double(m" + std::to_string(gb->monos[b]) + ")")
+         << ";\n";
   os << "  return KCG_PT_OK;\n}\n\n";
 }
 
@@ -197,18 +212,29 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast,
 //                monomial's bound below 2^53 gets C (x) double(mono): both
 //                factors are exact doubles, so the single rounding of their
 //                product equals RN(C * mono) -- no 64-bit constant multiply.
-void emit_fast(std::ostringstream& os, const Lowered& L, int v, bool dbl) {
+//   gb != null: kcg_fastm_<v> writes the basis values double(mono_b) (the
+//                fused Gram / residual rows) and checks key integrality only.
+void emit_fast(std::ostringstream& os, const Lowered& L, int v, bool dbl,
+               const GramBasis* gb = nullptr) {
   const bool small = L.b64 >= 0 && L.b64 <= kU32;
   const long double two53 = std::ldexp(1.0L, 53);
   std::vector<bool> atom_u32(L.n_atoms, false);
-  os << "__device__ __forceinline__ int kcg_fast" << (dbl ? "d_" : "i_") << v
+  if (gb) dbl = true;
+  os << "__device__ __forceinline__ int kcg_fast" << (gb ? "m_" : dbl ? "d_" : "i_") << v
      << "(const kcg_i64* __restrict__ p, " << (dbl ? "double" : "kcg_i64")
      << "* __restrict__ cnt) {\n  typedef kcg_i64 T;\n  bool ok = true, integral = true;\n";
   // which exprs are needed as integers
   std::vector<bool> need_expr(L.n_exprs, false), need_mono_d(L.n_monos, false);
   std::vector<int> key_fast(L.keys.size(), -1);  // mono id for the DMUL trick
+  if (gb)
+    for (int m : gb->monos)
+      if (m >= 0) need_mono_d[m] = true;
   for (size_t j = 0; j < L.keys.size(); ++j) {
     const LExpr& ex = L.exprs[L.keys[j].expr];
+    if (gb) {
+      if (ex.D != 1) need_expr[L.keys[j].expr] = true;
+      continue;
+    }
     bool trick = dbl && ex.D == 1 && ex.term_end - ex.term_begin == 1;
     if (trick) {
       const LTerm& t = L.terms[ex.term_begin];
@@ -328,7 +354,16 @@ void emit_fast(std::ostringstream& os, const Lowered& L, int v, bool dbl) {
       os << "  ok &= kcg_posmod<T>(e" << c.expr << ", " << lit(c.mod) << ") == " << lit(c.rem) << ";\n";
     }
   }
-  for (size_t j = 0; j < L.keys.size(); ++j) {
+  if (gb) {
+    for (size_t j = 0; j < L.keys.size(); ++j) {
+      const int e = L.keys[j].expr;
+      if (L.exprs[e].D != 1) os << "  integral &= (e" << e << " % " << lit(L.exprs[e].D) << ") == (T)0;\n";
+    }
+    for (size_t b = 0; b < gb->monos.size(); ++b)
+      os << "  cnt[" << b << "] = " << (gb->monos[b] < 0 ? std::string("1.0") : "dm" + std::to_string(gb->monos[b]))
+         << ";\n";
+  }
+  for (size_t j = 0; j < (gb ? 0 : L.keys.size()); ++j) {
     const int e = L.keys[j].expr;
     const LExpr& ex = L.exprs[e];
     if (key_fast[j] >= 0) {
@@ -464,11 +499,11 @@ constexpr int kTmaTile = 1024;
 
 int env_int(const char* name, int dflt, int lo, int hi);
 
-// ring depth of the fused (bindings + T) kernels: 64 KB so that two CTAs
-// (each with 35 KB of DMMA row buffers) fit one SM
-int fused_stages(int n_cols) {
+// ring depth of the fused (bindings + T) kernels: 64 KB when two CTAs also
+// hold 35 KB of DMMA row buffers each, 96 KB otherwise (3 stages for P = 3)
+int fused_stages(int n_cols, bool dmma) {
   const int per = (n_cols + 1) * 1024 * 8;
-  const int s = (env_int("KCG_FUSED_RING_KB", 64, 16, 200) * 1024) / per;
+  const int s = (env_int("KCG_FUSED_RING_KB", dmma ? 64 : 96, 16, 200) * 1024) / per;
   return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
@@ -641,14 +676,67 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 
 int tma_ctas_per_sm() { return tma_ctas(); }
 
-size_t fused_smem_bytes(int n_cols, int F, bool gram) {
-  const int FA = F > 0 ? F : 1;
-  const int NB = (F + 7) / 8, LDX = NB * 8 + 1;
-  size_t b = static_cast<size_t>(fused_stages(n_cols)) * (n_cols + 1) * kTmaTile * 8;
-  if (gram && F >= 1 && F <= 48)
+GramBasis gram_basis(const Lowered& L) {
+  GramBasis g;
+  std::map<int, int> idx;
+  const int F = static_cast<int>(L.keys.size());
+  g.terms.resize(F);
+  for (int j = 0; j < F; ++j) {
+    const LExpr& ex = L.exprs[L.keys[j].expr];
+    for (int t = ex.term_begin; t < ex.term_end; ++t) {
+      const LTerm& lt = L.terms[t];
+      auto it = idx.find(lt.mono);
+      if (it == idx.end()) {
+        it = idx.emplace(lt.mono, static_cast<int>(g.monos.size())).first;
+        g.monos.push_back(lt.mono);
+      }
+      const long double c = static_cast<long double>(lt.coef) / static_cast<long double>(ex.D);
+      g.terms[j].emplace_back(it->second, static_cast<double>(c));
+    }
+    if (g.terms[j].size() != 1) g.compound.push_back(j);
+  }
+  // A key with several terms is expanded without cancellation only when
+  // every term is a positive coefficient times a monomial of parameters /
+  // congruence quotients (both >= 0 at admissible points): then every
+  // product in A Gu A^T is non-negative and the expansion is as accurate as
+  // the direct sum. Otherwise (e.g. n^3/6 - n^2/2 + n/3) keep one column per key.
+  std::vector<bool> nonneg_atom(L.n_atoms, false), nonneg_mono(L.n_monos, false);
+  for (const LOp& op : L.ops) {
+    if (op.code == OP_VAR || op.code == OP_QUOT) nonneg_atom[op.dst] = true;
+    if (op.code == OP_MONO) {
+      bool nn = true;
+      for (int i = op.a; i < op.b; ++i) nn = nn && nonneg_atom[L.factors[i].first];
+      nonneg_mono[op.dst] = nn;
+    }
+  }
+  bool safe = true;
+  for (int j : g.compound) {
+    const LExpr& ex = L.exprs[L.keys[j].expr];
+    for (int t = ex.term_begin; t < ex.term_end; ++t)
+      safe = safe && L.terms[t].coef > 0 && (L.terms[t].mono < 0 || nonneg_mono[L.terms[t].mono]);
+  }
+  // the basis pays when it is narrower than the key set; the expansion
+  // tables stay small (F <= 64) and the compound-key maxima few
+  g.reduced = L.gram_basis && safe && g.monos.size() < static_cast<size_t>(F) && F <= 64 &&
+              g.compound.size() <= 8;
+  return g;
+}
+
+namespace {
+// register-accumulator fused Gram for narrow rows, DMMA otherwise
+constexpr int kRegGramMax = 6;
+bool gram_dmma(int W) { return W > kRegGramMax && W <= 48; }
+}  // namespace
+
+size_t fused_smem_bytes(int n_cols, const Lowered& L, bool gram) {
+  const int W = gram_basis(L).width(static_cast<int>(L.keys.size()));
+  const int WA = W > 0 ? W : 1;
+  const int NB = (W + 7) / 8, LDX = NB * 8 + 1;
+  size_t b = static_cast<size_t>(fused_stages(n_cols, gram && gram_dmma(W))) * (n_cols + 1) * kTmaTile * 8;
+  if (gram && gram_dmma(W))
     b += static_cast<size_t>(8) * 32 * LDX * 8;  // DMMA row buffers (also the slow-path rows)
   else
-    b += static_cast<size_t>(256) * FA * 8;      // slow-path rows
+    b += static_cast<size_t>(256) * WA * 8;      // slow-path rows
   return b;
 }
 
@@ -739,18 +827,58 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   // fused design-row reductions (gram / residual)
   const Lowered& L = *progs[0];
   const int F = static_cast<int>(L.keys.size());
-  const int FA = F > 0 ? F : 1;
+  const GramBasis gb = gram_basis(L);
+  const bool red_basis = gb.reduced;
+  // row width: the F design columns, or the W < F basis values u_b = mono_b / T
+  const int W = gb.width(F);
+  const int WA = W > 0 ? W : 1;
   const bool gram = kind == JitKind::gram;
-  const bool dmma = gram && F >= 1 && F <= 48;
-  const int NB = (F + 7) / 8, NT = NB * (NB + 1) / 2, FP = NB * 8, LDX = FP + 1;
+  const bool dmma = gram && gram_dmma(W);
+  const bool regsm = gram && !dmma && W <= 48;  // register accumulators, CTA totals in smem
+  const int NCMP = red_basis ? static_cast<int>(gb.compound.size()) : 0;
+  const int NB = (W + 7) / 8, NT = NB * (NB + 1) / 2, FP = NB * 8, LDX = FP + 1;
   const int NC = n_cols + 1;  // parameter columns + T
-  const int S = fused_stages(n_cols);
+  const int S = fused_stages(n_cols, dmma);
+  if (red_basis) {
+    emit_fast(os, L, 0, true, &gb);
+    emit_body(os, L, 0, false, "kcg_wide_", &gb);
+  }
   if (gram)
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* G; double* xt1; "
           "double* cmax; unsigned long long* bad; kcg_i64 n; int vec; };\n";
   else
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* obj; kcg_i64 n; "
-          "int vec; double alpha[" << FA << "]; };\n";
+          "int vec; double alpha[" << (F > 0 ? F : 1) << "]; };\n";
+  if (red_basis) {
+    // expansion tables: key j = sum over kcg_kt[off[j]..off[j+1]) of coef * u_b
+    std::vector<int> off{0}, tb;
+    std::vector<double> tc;
+    for (int j = 0; j < F; ++j) {
+      for (const auto& [b, c] : gb.terms[j]) {
+        tb.push_back(b);
+        tc.push_back(c);
+      }
+      off.push_back(static_cast<int>(tb.size()));
+    }
+    std::vector<int> cidx(F, -1);
+    for (int k = 0; k < NCMP; ++k) cidx[gb.compound[k]] = k;
+    auto arr = [&](const char* ty, const char* nm, auto& v) {
+      os << "__constant__ " << ty << " " << nm << "[" << v.size() << "] = {";
+      for (size_t i = 0; i < v.size(); ++i) os << (i ? ", " : "") << v[i];
+      os << "};\n";
+    };
+    os.precision(17);
+    arr("int", "kcg_kt_off", off);
+    arr("int", "kcg_kt_b", tb);
+    std::vector<std::string> tcs;
+    for (double c : tc) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%a", c);
+      tcs.push_back(buf);
+    }
+    arr("double", "kcg_kt_c", tcs);
+    arr("int", "kcg_kt_cmp", cidx);
+  }
   // x = c / t correctly rounded (Markstein: one reciprocal per row, exact
   // residual by FMA, final FMA correction)
   os << "__device__ __forceinline__ double kcg_div(double c, double t, double r) {\n"
@@ -766,46 +894,124 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   for (int j = 0; j < n_cols; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
   os << "  const double t = a.t[i];\n"
         "  if (!(t > 0.0)) return KCG_PT_ASSUMPTION_VIOLATED;\n"
-        "  const int cls = kcg_class_0(p);\n"
-        "  if (cls == 1) { kcg_i64 c["
-     << FA << "]; const int st = kcg_fasti_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n"
-              "  if (cls == 2) { kcg_i128 c["
-     << FA << "]; const int st = kcg_wide_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n"
-              "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
+        "  const int cls = kcg_class_0(p);\n";
+  if (red_basis) {
+    os << "  if (cls == 1 || cls == 2) {\n    double u[" << WA << "];\n"
+       << "    const int st = cls == 1 ? kcg_fastm_0(p, u) : kcg_widem_0(p, u);\n"
+       << "    if (st == KCG_PT_OK) {\n      #pragma unroll\n      for (int b = 0; b < " << W
+       << "; ++b) x[b] = __ddiv_rn(u[b], t);\n    }\n    return st;\n  }\n";
+  } else {
+    os << "  if (cls == 1) { kcg_i64 c[" << (F > 0 ? F : 1)
+       << "]; const int st = kcg_fasti_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n"
+          "  if (cls == 2) { kcg_i128 c["
+       << (F > 0 ? F : 1) << "]; const int st = kcg_wide_0(p, c); if (st == KCG_PT_OK) kcg_xrow(c, t, x); return st; }\n";
+  }
+  os << "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
   // fast row from registers; -1 -> caller uses kcg_row_i
   os << "__device__ __forceinline__ int kcg_row_fast(const kcg_i64* p, double t, double* x) {\n"
         "  if (!(t > 0.0) || kcg_class_0(p) != 1) return -1;\n"
         "  double c["
-     << FA << "];\n  const int st = kcg_fastd_0(p, c);\n  const double r = __drcp_rn(t);\n"
-              "  #pragma unroll\n  for (int j = 0; j < "
-     << F << "; ++j) x[j] = kcg_div(c[j], t, r);\n  return st;\n}\n";
+     << WA << "];\n  const int st = " << (red_basis ? "kcg_fastm_0" : "kcg_fastd_0")
+     << "(p, c);\n  const double r = __drcp_rn(t);\n"
+        "  #pragma unroll\n  for (int j = 0; j < "
+     << W << "; ++j) x[j] = " << (red_basis ? "__dmul_rn(c[j], r)" : "kcg_div(c[j], t, r)")
+     << ";\n  return st;\n}\n";
+
+  // compound keys (basis mode): x_j = sum_t coef * u_b, max |x_j| per row
+  std::ostringstream cmp_row;
+  for (int k = 0; k < NCMP; ++k) {
+    const int j = gb.compound[k];
+    cmp_row << "      { double xc = 0.0;";
+    for (const auto& [b, c] : gb.terms[j]) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, "%a", c);
+      cmp_row << " xc = fma(" << buf << ", x[" << b << "], xc);";
+    }
+    cmp_row << " mxc[" << k << "] = fmax(mxc[" << k << "], fabs(xc)); }\n";
+  }
+
+  // CTA totals in shared memory (dmma / regsm): G block (upper, stride LD),
+  // sum of rows, max |x| bits, compound maxima bits
+  const bool ones = dmma && FP > W;
+  const int LD = dmma ? FP : W;
+  const int GSZ = dmma ? FP * FP : W * W;
+  const int S1OFF = GSZ, MXOFF = GSZ + (dmma ? FP : W), MCOFF = MXOFF + (dmma ? FP : W);
+  const int REDN = MCOFF + (NCMP ? NCMP : 1);
+  std::string s1_at = ones ? "red[(b) * " + std::to_string(FP) + " + " + std::to_string(W) + "]"
+                           : "red[" + std::to_string(S1OFF) + " + (b)]";
+  std::ostringstream epi;  // CTA totals -> global statistics
+  if (dmma || regsm) {
+    epi << "  __syncthreads();\n";
+    if (red_basis) {
+      epi << "  for (int e = threadIdx.x; e < " << F * F << "; e += blockDim.x) {\n"
+          << "    const int j = e / " << F << ", k = e % " << F << ";\n"
+          << "    if (k < j) continue;\n"
+          << "    double v = 0.0;\n"
+          << "    for (int ta = kcg_kt_off[j]; ta < kcg_kt_off[j + 1]; ++ta)\n"
+          << "      for (int tb = kcg_kt_off[k]; tb < kcg_kt_off[k + 1]; ++tb) {\n"
+          << "        const int x = kcg_kt_b[ta], y = kcg_kt_b[tb];\n"
+          << "        const int lo = x < y ? x : y, hi = x < y ? y : x;\n"
+          << "        v = fma(kcg_kt_c[ta] * kcg_kt_c[tb], red[lo * " << LD << " + hi], v);\n"
+          << "      }\n"
+          << "    atomicAdd(a.G + j * " << F << " + k, v);\n"
+          << "    if (j != k) atomicAdd(a.G + k * " << F << " + j, v);\n  }\n"
+          << "  for (int j = threadIdx.x; j < " << F << "; j += blockDim.x) {\n"
+          << "    double s = 0.0;\n"
+          << "    for (int t = kcg_kt_off[j]; t < kcg_kt_off[j + 1]; ++t) { const int b = kcg_kt_b[t]; s = fma(kcg_kt_c[t], "
+          << s1_at << ", s); }\n"
+          << "    atomicAdd(a.xt1 + j, s);\n"
+          << "    const int ci = kcg_kt_cmp[j];\n"
+          << "    const double m = ci >= 0 ? __longlong_as_double((long long)reinterpret_cast<unsigned long long*>(red)["
+          << MCOFF << " + ci])\n"
+          << "        : fabs(kcg_kt_c[kcg_kt_off[j]]) * __longlong_as_double((long long)reinterpret_cast<unsigned long long*>(red)["
+          << MXOFF << " + kcg_kt_b[kcg_kt_off[j]]]);\n"
+          << "    atomicMax((unsigned long long*)(a.cmax + j), (unsigned long long)__double_as_longlong(m));\n  }\n";
+    } else {
+      epi << "  for (int e = threadIdx.x; e < " << LD * LD << "; e += blockDim.x) {\n"
+          << "    const int r = e / " << LD << ", c = e % " << LD << ";\n"
+          << "    if (r >= " << F << " || c >= " << F << " || c < r) continue;\n"
+          << "    atomicAdd(a.G + r * " << F << " + c, red[e]);\n"
+          << "    if (c != r) atomicAdd(a.G + c * " << F << " + r, red[e]);\n  }\n"
+          << "  for (int b = threadIdx.x; b < " << F << "; b += blockDim.x) {\n"
+          << "    atomicAdd(a.xt1 + b, " << s1_at << ");\n"
+          << "    atomicMax((unsigned long long*)(a.cmax + b), reinterpret_cast<unsigned long long*>(red)[" << MXOFF
+          << " + b]);\n  }\n";
+    }
+    epi << "  if (threadIdx.x == 0 && a.bad && red_bad) atomicAdd(a.bad, red_bad);\n";
+  }
+  const std::string red_decl = "  __shared__ double red[" + std::to_string(REDN) + "];\n"
+                               "  __shared__ unsigned long long red_bad;\n"
+                               "  for (int k = threadIdx.x; k < " + std::to_string(REDN) +
+                               "; k += blockDim.x) red[k] = 0.0;\n"
+                               "  if (threadIdx.x == 0) red_bad = 0;\n";
+  const std::string mxc_decl = NCMP ? "  double mxc[" + std::to_string(NCMP) + "];\n  #pragma unroll\n  for (int k = 0; k < " +
+                                          std::to_string(NCMP) + "; ++k) mxc[k] = 0.0;\n"
+                                    : "";
 
   // ---- per-row consumer ---------------------------------------------------
   std::ostringstream cons_decl, cons_row, cons_end;
   if (dmma) {
-    // Xᵀ1 rides on the tensor cores as a constant-one column F (when the
-    // padded width leaves room): G[j][F] = sum_r x_rj. colmax is kept per
+    // Xᵀ1 rides on the tensor cores as a constant-one column W (when the
+    // padded width leaves room): G[j][W] = sum_r x_rj. colmax is kept per
     // thread at row production, so the k-step loop is loads + DMMA only.
-    const bool ones = FP > F;
     cons_decl << "  double* xs_base = reinterpret_cast<double*>(kcg_smem) + S * NC * TP;\n"
-              << "  __shared__ double red[" << FP * FP + 2 * FP << "];\n"
-              << "  __shared__ unsigned long long red_bad;\n"
-              << "  for (int k = threadIdx.x; k < " << FP * FP + 2 * FP << "; k += blockDim.x) red[k] = 0.0;\n"
-              << "  if (threadIdx.x == 0) red_bad = 0;\n"
+              << red_decl
               << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;\n"
               << "  double acc[" << NT << "][2];\n  #pragma unroll\n  for (int t = 0; t < " << NT
               << "; ++t) acc[t][0] = acc[t][1] = 0.0;\n"
-              << "  unsigned long long mxr[" << F << "];\n"
-              << (ones ? "" : std::string("  double s1r[") + std::to_string(F) + "];\n")
-              << "  #pragma unroll\n  for (int j = 0; j < " << F << "; ++j) { mxr[j] = 0ull;"
+              << "  unsigned long long mxr[" << W << "];\n"
+              << (ones ? "" : std::string("  double s1r[") + std::to_string(W) + "];\n")
+              << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) { mxr[j] = 0ull;"
               << (ones ? "" : " s1r[j] = 0.0;") << " }\n"
+              << mxc_decl
               << "  unsigned long long bad = 0;\n  double* xw = xs_base + warp * 32 * " << LDX << ";\n"
               << "  for (int e = lane; e < 32 * " << LDX << "; e += 32) xw[e] = 0.0;  // padding stays zero\n"
               << "  __syncwarp();\n";
-    cons_row << "      #pragma unroll\n      for (int j = 0; j < " << F << "; ++j) { xw[lane * " << LDX
+    cons_row << "      #pragma unroll\n      for (int j = 0; j < " << W << "; ++j) { xw[lane * " << LDX
              << " + j] = x[j]; { const unsigned long long b = (unsigned long long)__double_as_longlong(x[j]) & 0x7fffffffffffffffull; mxr[j] = b > mxr[j] ? b : mxr[j]; }"
-             << (ones ? "" : " s1r[j] += x[j];") << " }\n";
-    if (ones) cons_row << "      xw[lane * " << LDX << " + " << F << "] = ok ? 1.0 : 0.0;\n";
+             << (ones ? "" : " s1r[j] += x[j];") << " }\n"
+             << cmp_row.str();
+    if (ones) cons_row << "      xw[lane * " << LDX << " + " << W << "] = ok ? 1.0 : 0.0;\n";
     cons_row << "      __syncwarp();\n"
              << "      #pragma unroll\n      for (int ks = 0; ks < 8; ++ks) {\n"
              << "        const double* row = xw + (4 * ks + tig) * " << LDX << ";\n"
@@ -818,36 +1024,65 @@ std::string codegen(const std::vector<const Lowered*>& progs,
              << "                         : \"+d\"(acc[t][0]), \"+d\"(acc[t][1]) : \"d\"(v[I]), \"d\"(v[J]));\n"
              << "      }\n      __syncwarp();\n";
     cons_end << "  __syncthreads();\n"
-             << "  #pragma unroll\n  for (int j = 0; j < " << F << "; ++j) {\n"
+             << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j) {\n"
              << "    unsigned long long m = mxr[j];\n"
              << "    #pragma unroll\n    for (int o = 16; o > 0; o >>= 1) { const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o); m = y > m ? y : m; }\n"
-             << "    if (lane == 0) atomicMax((unsigned long long*)(red + " << FP * FP + FP << " + j), m);\n";
+             << "    if (lane == 0) atomicMax((unsigned long long*)(red + " << MXOFF << " + j), m);\n";
     if (!ones)
       cons_end << "    double sj = s1r[j];\n"
                << "    #pragma unroll\n    for (int o = 16; o > 0; o >>= 1) sj += __shfl_xor_sync(0xffffffffu, sj, o);\n"
-               << "    if (lane == 0) atomicAdd(red + " << FP * FP << " + j, sj);\n";
-    cons_end << "  }\n"
-             << "  { int t = 0;\n    #pragma unroll\n    for (int I = 0; I < " << NB
+               << "    if (lane == 0) atomicAdd(red + " << S1OFF << " + j, sj);\n";
+    cons_end << "  }\n";
+    for (int k = 0; k < NCMP; ++k)
+      cons_end << "  { double m = mxc[" << k << "];\n    #pragma unroll\n    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));\n"
+               << "    if (lane == 0) atomicMax((unsigned long long*)(red + " << MCOFF + k
+               << "), (unsigned long long)__double_as_longlong(m)); }\n";
+    // each (I, J) block of the upper block triangle; diagonal blocks are full
+    cons_end << "  { int t = 0;\n    #pragma unroll\n    for (int I = 0; I < " << NB
              << "; ++I)\n      #pragma unroll\n      for (int J = I; J < " << NB << "; ++J, ++t) {\n"
              << "        atomicAdd(red + (8 * I + gid) * " << FP << " + 8 * J + 2 * tig, acc[t][0]);\n"
              << "        atomicAdd(red + (8 * I + gid) * " << FP << " + 8 * J + 2 * tig + 1, acc[t][1]); } }\n"
              << "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, o);\n"
              << "  if (lane == 0 && bad) atomicAdd(&red_bad, bad);\n"
-             << "  __syncthreads();\n"
-             << "  for (int e = threadIdx.x; e < " << FP * FP << "; e += blockDim.x) {\n"
-             << "    const int r = e / " << FP << ", c = e % " << FP << ";\n"
-             << "    if (r >= " << F << " || c >= " << F << " || (c / 8) < (r / 8)) continue;\n"
-             << "    atomicAdd(a.G + r * " << F << " + c, red[e]);\n"
-             << "    if (c / 8 != r / 8) atomicAdd(a.G + c * " << F << " + r, red[e]);\n  }\n"
-             << "  for (int c = threadIdx.x; c < " << F << "; c += blockDim.x) {\n"
-             << "    atomicAdd(a.xt1 + c, red[" << (ones ? std::string("c * ") + std::to_string(FP) + " + " + std::to_string(F)
-                                                    : std::to_string(FP * FP) + " + c") << "]);\n"
-             << "    atomicMax((unsigned long long*)(a.cmax + c), (unsigned long long)__double_as_longlong(red["
-             << FP * FP + FP << " + c]));\n  }\n"
-             << "  if (threadIdx.x == 0 && a.bad && red_bad) atomicAdd(a.bad, red_bad);\n";
+             << epi.str();
+  } else if (regsm) {
+    const int NG = W * (W + 1) / 2;
+    cons_decl << red_decl
+              << "  double g[" << (NG ? NG : 1) << "], s1[" << WA << "], mx[" << WA << "];\n"
+              << "  #pragma unroll\n  for (int k = 0; k < " << NG << "; ++k) g[k] = 0.0;\n"
+              << "  #pragma unroll\n  for (int k = 0; k < " << W << "; ++k) { s1[k] = 0.0; mx[k] = 0.0; }\n"
+              << mxc_decl << "  unsigned long long bad = 0;\n";
+    int k = 0;
+    for (int r = 0; r < W; ++r) {
+      cons_row << "      s1[" << r << "] += x[" << r << "]; mx[" << r << "] = fmax(mx[" << r << "], fabs(x[" << r << "]));\n";
+      for (int c = r; c < W; ++c, ++k)
+        cons_row << "      g[" << k << "] = fma(x[" << r << "], x[" << c << "], g[" << k << "]);\n";
+    }
+    cons_row << cmp_row.str();
+    cons_end << "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) {\n"
+             << "    #pragma unroll\n    for (int k = 0; k < " << NG << "; ++k) g[k] += __shfl_down_sync(0xffffffffu, g[k], o);\n"
+             << "    #pragma unroll\n    for (int k = 0; k < " << W
+             << "; ++k) { s1[k] += __shfl_down_sync(0xffffffffu, s1[k], o); mx[k] = fmax(mx[k], __shfl_down_sync(0xffffffffu, mx[k], o)); }\n";
+    if (NCMP)
+      cons_end << "    #pragma unroll\n    for (int k = 0; k < " << NCMP
+               << "; ++k) mxc[k] = fmax(mxc[k], __shfl_down_sync(0xffffffffu, mxc[k], o));\n";
+    cons_end << "    bad += __shfl_down_sync(0xffffffffu, bad, o);\n  }\n"
+             << "  if ((threadIdx.x & 31) == 0) {\n";
+    k = 0;
+    for (int r = 0; r < W; ++r) {
+      cons_end << "    atomicAdd(red + " << S1OFF + r << ", s1[" << r << "]);\n"
+               << "    atomicMax((unsigned long long*)(red + " << MXOFF + r
+               << "), (unsigned long long)__double_as_longlong(mx[" << r << "]));\n";
+      for (int c = r; c < W; ++c, ++k) cons_end << "    atomicAdd(red + " << (r * W + c) << ", g[" << k << "]);\n";
+    }
+    for (int q = 0; q < NCMP; ++q)
+      cons_end << "    atomicMax((unsigned long long*)(red + " << MCOFF + q
+               << "), (unsigned long long)__double_as_longlong(mxc[" << q << "]));\n";
+    cons_end << "    if (bad) atomicAdd(&red_bad, bad);\n  }\n" << epi.str();
   } else if (gram) {
+    // wide rows (W > 48): warp totals straight to global
     const int NG = F * (F + 1) / 2;
-    cons_decl << "  double g[" << (NG ? NG : 1) << "], s1[" << FA << "], mx[" << FA << "];\n"
+    cons_decl << "  double g[" << (NG ? NG : 1) << "], s1[" << WA << "], mx[" << WA << "];\n"
               << "  #pragma unroll\n  for (int k = 0; k < " << NG << "; ++k) g[k] = 0.0;\n"
               << "  #pragma unroll\n  for (int k = 0; k < " << F << "; ++k) { s1[k] = 0.0; mx[k] = 0.0; }\n"
               << "  unsigned long long bad = 0;\n";
@@ -875,14 +1110,15 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     }
     cons_end << "    if (a.bad && bad) atomicAdd(a.bad, bad);\n  }\n";
   } else {
+    // residual: alpha holds the compact weights, or beta = A^T alpha in basis mode
     cons_decl << "  double acc = 0.0;\n";
     cons_row << "      if (ok) {\n        double pr = 0.0;\n";
-    for (int j = 0; j < F; ++j) cons_row << "        pr = fma(x[" << j << "], a.alpha[" << j << "], pr);\n";
+    for (int j = 0; j < W; ++j) cons_row << "        pr = fma(x[" << j << "], a.alpha[" << j << "], pr);\n";
     cons_row << "        const double r = 1.0 - pr;\n        acc = fma(r, r, acc);\n      }\n";
     cons_end << "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);\n"
              << "  if ((threadIdx.x & 31) == 0) atomicAdd(a.obj, acc);\n";
   }
-  const int XW = FA;  // x row width
+  const int XW = WA;  // x row width
   // produce row x for global index i from registers q/t (or out of line)
   // The out-of-line path writes its row to a scratch row (shared memory for
   // the DMMA variant) and the fast path's registers are copied there too, so
@@ -896,7 +1132,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
        << "        if (st < 0) {\n"
        << "          double* sx = slow_row;\n"
        << "          st = kcg_row_i(a, " << iexpr << ", sx);\n"
-       << "          if (st == KCG_PT_OK) {\n            #pragma unroll\n            for (int j = 0; j < " << F
+       << "          if (st == KCG_PT_OK) {\n            #pragma unroll\n            for (int j = 0; j < " << W
        << "; ++j) x[j] = sx[j];\n          }\n"
        << "        }\n"
        << "        ok = st == KCG_PT_OK;\n"
@@ -919,7 +1155,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
      << cons_decl.str()
      << (dmma ? std::string("  double* slow_row = xw + lane * ") + std::to_string(LDX) + ";\n"
               : std::string("  double* slow_row = reinterpret_cast<double*>(kcg_smem) + S * NC * TP + threadIdx.x * ") +
-                    std::to_string(FA) + ";\n")
+                    std::to_string(WA) + ";\n")
      << "  const kcg_i64 ntiles = a.vec ? a.n / TP : 0;\n"
         "  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);\n"
         "  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);\n"

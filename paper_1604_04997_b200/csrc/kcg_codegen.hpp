@@ -31,8 +31,23 @@ void launch_jit(void* kernel, const void* args, size_t args_size,
 /// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.
 size_t tma_smem_bytes(int n_cols);
 int tma_ctas_per_sm();
+/// Monomial basis of a program's property columns for the fused design-row
+/// reductions. Every key is count_j = sum_t coef_t * mono_t / D_j, so a
+/// design row x_j = count_j / T is A_j . u with u_b = mono_b / T. When the
+/// keys share monomials (tiled matmul: 9 keys over {lmn, ln, 1}) the kernels
+/// accumulate the W x W Gram of u and expand G = A Gu A^T per CTA, which is
+/// exactly the same statistic with W^2 instead of F^2 work per row.
+struct GramBasis {
+  std::vector<int> monos;                                   // basis b: mono id, -1 = constant 1
+  std::vector<std::vector<std::pair<int, double>>> terms;  // per key: (b, coef / D)
+  std::vector<int> compound;                                // keys with more than one term
+  bool reduced = false;                                     // W < F: use the basis
+  int width(int F) const { return reduced ? static_cast<int>(monos.size()) : F; }
+};
+GramBasis gram_basis(const Lowered& L);
+
 /// Shared-memory ring of the fused (bindings + T) Gram / residual kernels.
-size_t fused_smem_bytes(int n_cols, int F, bool gram);
+size_t fused_smem_bytes(int n_cols, const Lowered& L, bool gram);
 constexpr int kTmaPointsPerTile = 1024;
 
 }  // namespace kcg

@@ -161,6 +161,7 @@ struct Lowered {
   std::vector<i128> atom_den;      // value = numerator / atom_den
   std::vector<i128> quot_mod, quot_rem;  // per OP_QUOT (index in op.c)
   int64_t b64 = 0, b128 = 0;       // safe uniform parameter bounds
+  bool gram_basis = true;          // fused Gram/residual over the monomial basis when narrower
   std::vector<long double> mono_bound64;  // |monomial| bound when params <= b64
   // admissibility-only lowering (no properties): decides E_ASSUMPTION_VIOLATED
   // for points whose counts are beyond the 128-bit bound (admits() is checked

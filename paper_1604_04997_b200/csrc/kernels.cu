@@ -7,6 +7,7 @@
 //                          model.cpp:62-80), register-tiled 4x4 over the upper
 //                          triangle, rows staged through shared memory
 //   * kcg_resid_x / kcg_resid_grad_x -- sum (1 - X a)^2 and X^T (1 - X a)
+#include <mutex>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -455,12 +456,20 @@ void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, 
                       cudaStream_t stream) {
   const int stages = F <= 40 ? 4 : 3;
   const size_t smem = (size_t)(stages * kDmmaRows * F + NB * 8 * NB * 8 + 2 * NB * 8) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    check(cudaFuncSetAttribute(kcg_gram_dmma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem + 4096),
-          "cudaFuncSetAttribute");
-    attr = true;
+  // the opt-in size grows with F within one NB (per device, process-wide)
+  static std::mutex mu;
+  static size_t attr_smem[64] = {};
+  int dev = 0;
+  check(cudaGetDevice(&dev), "cudaGetDevice");
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = attr_smem[dev & 63];
+    if (smem + 4096 > cur) {
+      check(cudaFuncSetAttribute(kcg_gram_dmma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem + 4096),
+            "cudaFuncSetAttribute");
+      cur = smem + 4096;
+    }
   }
   const kcg_i64 tiles = (kcg_i64)n / kDmmaRows;
   kcg_i64 grid = (kcg_i64)num_sms() * 2;
