@@ -246,6 +246,24 @@ const char* kcg_measurements_param_name(const kcg_measurements* m, int i, int j)
 const int64_t* kcg_measurements_column(const kcg_measurements* m, int i, int j);
 const double* kcg_measurements_times(const kcg_measurements* m, int i);
 
+/* ---- GPU enumeration oracle (enumerate.cpp:371-456) ---------------------
+ * A "kernelcost-enum v1" text (oracle/kcref_program.hpp enum_text, printed
+ * by the reference front end) describes every assign / barrier statement's
+ * domain, guards, accesses and per-point op counts. kcg_enumerate_points
+ * walks every domain on the GPU at one binding (host array, one int64 per
+ * parameter in declaration order) and tallies like enumerate_points:
+ * counts_lo/hi (HOST, 149 each) receive the bound property vector as
+ * two's-complement int128, points (nullable) the visited lattice points.
+ * cap = 0: unlimited; otherwise KCG_E_CAP_EXCEEDED beyond cap visited
+ * points (Errc::cap_exceeded). Synchronous on `stream`.                     */
+typedef struct kcg_enum_program kcg_enum_program;
+int kcg_enum_program_create(const char* text, size_t len, kcg_enum_program** out);
+void kcg_enum_program_destroy(kcg_enum_program* prog);
+int kcg_enum_program_num_params(const kcg_enum_program* prog);
+const char* kcg_enum_program_param_name(const kcg_enum_program* prog, int i);
+int kcg_enumerate_points(const kcg_enum_program* prog, const int64_t* binding, uint64_t cap,
+                         int64_t* counts_lo, int64_t* counts_hi, uint64_t* points, void* stream);
+
 /* ---- diagnostics -------------------------------------------------------- */
 const char* kcg_status_str(int status);
 const char* kcg_point_status_str(int point_status);

@@ -27,6 +27,7 @@
 #include "kcref_program.hpp"
 #include "kernelcost/campaign.hpp"
 #include "kernelcost/csvio.hpp"
+#include "kernelcost/enumerate.hpp"
 #include "kernelcost/error.hpp"
 #include "kernelcost/jsonio.hpp"
 #include "kernelcost/model.hpp"
@@ -573,6 +574,72 @@ int main(int argc, char** argv) {
                 << " points\n";
     }
     write(pdir + "/derived.json", json{{"derived", derived}});
+  }
+
+  // ---- enumeration programs + enumerate_points goldens (enumerate.cpp:371-456)
+  {
+    std::filesystem::create_directories(pdir + "/enum");
+    const std::vector<std::pair<std::string, std::string>> xk = {
+        {"x_triangle",
+         "kernel x_triangle\nparam n\nassume n >= 1\n"
+         "array o : f32 [n] global row_major out\n"
+         "axis g0 = group(0) extent 1\naxis l0 = local(0) extent 1\n"
+         "loop i = 0 .. n\nloop j = 0 .. i + 1\n"
+         "o[i] = o[i] + 1.0\nend\nend\n"},
+        {"x_guarded",
+         "kernel x_guarded\nparam n, m\nassume n >= 1 and m >= 1\n"
+         "array o : f32 [n] global row_major out\n"
+         "axis g0 = group(0) extent 1\naxis l0 = local(0) extent 1\n"
+         "loop i = 0 .. n\nloop j = 0 .. m\nguard j < i\n"
+         "o[i] = 2.0\nend\nend\nend\n"},
+        {"x_divguard",
+         "kernel x_divguard\nparam n\nassume n % 4 == 0 and n >= 4\n"
+         "array a : f32 [n, n] global column_major in\n"
+         "array o : f32 [n] global row_major out\n"
+         "axis g0 = group(0) extent n // 4\naxis l0 = local(0) extent 4\n"
+         "loop j = 0 .. n\nguard j % 3 == 1\n"
+         "o[4*g0 + l0] = o[4*g0 + l0] + a[4*g0 + l0, j] * 2.0\nend\nend\n"},
+        {"x_halfstride",
+         "kernel x_halfstride\nparam n\nassume n % 8 == 0 and n >= 8\n"
+         "array a : f64 [2*n + 1] global row_major in\n"
+         "array t : f64 [8] local row_major temp\n"
+         "array o : f64 [n] global row_major out\n"
+         "axis g0 = group(0) extent n // 8\naxis l0 = local(0) extent 8\n"
+         "t[l0] = a[16*g0 + 2*l0 + 1]\nbarrier\n"
+         "guard l0 <= 3\no[8*g0 + l0] = t[l0] / t[7 - l0]\nend\n"},
+    };
+    json enums = json::array();
+    std::mt19937_64 er(0xe17);
+    auto tally = [&](const std::string& id, const kc::KernelIR& k, const kc::Binding& b) {
+      json e{{"kernel", id}, {"binding", binding_json(b)}};
+      try {
+        const kc::EnumTally t = kc::enumerate_points(k, b, kCap);
+        e["status"] = "ok";
+        e["counts"] = pv_json(t.props);
+        e["points"] = t.points.str();
+      } catch (const kc::Error& err) {
+        e["status"] = kc::errc_name(err.code());
+      }
+      enums.push_back(e);
+    };
+    for (const auto& sk : lib.kernels) {
+      const kc::KernelIR& k = irs.at(sk.id);
+      std::ofstream(pdir + "/enum/" + sk.id + ".kce") << kcref::enum_text(k);
+      for (int d = 0; d < 3; ++d) tally(sk.id, k, kc::sample_oracle_binding(sk, er));
+    }
+    for (const auto& [id, text] : xk) {
+      const kc::KernelIR k = kc::parse_kernel(text);
+      std::ofstream(pdir + "/enum/" + id + ".kce") << kcref::enum_text(k);
+      const bool two = k.params.size() == 2;
+      for (long n : {0L, 1L, 2L, 3L, 4L, 5L, 8L, 12L, 13L, 16L, 40L, 64L, 100L})
+        for (long m : two ? std::vector<long>{0L, 1L, 3L, 7L, 50L} : std::vector<long>{0L}) {
+          kc::Binding b{{"n", kc::Int(n)}};
+          if (two) b["m"] = kc::Int(m);
+          tally(id, k, b);
+        }
+    }
+    write(gdir + "/enum_points.json", json{{"cap", kCap.str()}, {"cases", enums}});
+    std::cerr << "enumeration goldens: " << enums.size() << "\n";
   }
   return 0;
 }

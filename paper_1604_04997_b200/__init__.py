@@ -7,6 +7,8 @@ of the least-squares fit. See DESIGN.md; the C ABI is include/kcg.h.
 """
 from .api import (  # noqa: F401
     BoundBatch,
+    EnumProgram,
+    load_enum_program,
     KernelMeasurements,
     eval_from_csv,
     fit_from_csv,

@@ -81,6 +81,12 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_refine_gram": (ctypes.c_int, [ctypes.c_int, DP, DP, DP, DP]),
         "kcg_weights_read_json": (ctypes.c_int, [ctypes.c_char_p, DP, U8P, DP, ctypes.POINTER(ctypes.c_uint64)]),
         "kcg_weights_write_json": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, DP, U8P, ctypes.c_double, ctypes.c_uint64]),
+        "kcg_enum_program_create": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(P)]),
+        "kcg_enum_program_destroy": (None, [P]),
+        "kcg_enum_program_num_params": (ctypes.c_int, [P]),
+        "kcg_enum_program_param_name": (ctypes.c_char_p, [P, ctypes.c_int]),
+        "kcg_enumerate_points": (ctypes.c_int, [P, I64P, ctypes.c_uint64, I64P, I64P,
+                                                ctypes.POINTER(ctypes.c_uint64), P]),
         "kcg_status_str": (ctypes.c_char_p, [ctypes.c_int]),
         "kcg_point_status_str": (ctypes.c_char_p, [ctypes.c_int]),
         "kcg_last_error": (ctypes.c_char_p, []),
@@ -114,6 +120,7 @@ def check(rc: int) -> None:
 # status codes (kcg.h)
 OK = 0
 E_PARSE = 1
+E_CAP_EXCEEDED = 4
 E_ASSUMPTION_VIOLATED = 6
 E_SCHEMA_MISMATCH = 7
 E_NONPOSITIVE_TIME = 8

@@ -515,3 +515,57 @@ def eval_from_csv(w: ModelWeights, path, programs=None, discard: int = 4, stream
         acts.append(T)
     overall = geometric_mean_error(torch.cat(preds), torch.cat(acts), stream=stream)
     return {"per_kernel": per, "overall": overall, "n_cases": sum(int(a.numel()) for a in acts)}
+
+
+# ---- GPU enumeration oracle (enumerate.cpp:371-456) -------------------------
+
+ENUM_DIR = PROGRAM_DIR / "enum"
+
+
+class EnumProgram:
+    """A kernel's enumeration program ("kernelcost-enum v1", printed by the
+    reference front end with oracle/kcref_program.hpp enum_text): every
+    statement domain, guard, access and per-point op count that
+    ``enumerate_points`` walks."""
+
+    def __init__(self, text: str):
+        h = ctypes.c_void_p()
+        b = text.encode()
+        check(lib().kcg_enum_program_create(b, len(b), ctypes.byref(h)))
+        self._h = h
+        L = lib()
+        self.params = [L.kcg_enum_program_param_name(h, i).decode()
+                       for i in range(L.kcg_enum_program_num_params(h))]
+
+    @classmethod
+    def from_file(cls, path) -> "EnumProgram":
+        return cls(Path(path).read_text())
+
+    def enumerate_points(self, binding: dict, cap: int = 0, stream=None) -> tuple[dict, int]:
+        """Brute-force bound property vector at one binding, walked on the
+        GPU: ({schema key: exact int} for the nonzero keys, visited points).
+        Raises KcgError E_ASSUMPTION_VIOLATED / E_CAP_EXCEEDED like the
+        reference."""
+        b = (ctypes.c_int64 * max(1, len(self.params)))(*[int(binding[p]) for p in self.params])
+        n = schema_size()
+        lo, hi = (ctypes.c_int64 * n)(), (ctypes.c_int64 * n)()
+        pts = ctypes.c_uint64()
+        check(lib().kcg_enumerate_points(self._h, b, cap, lo, hi, ctypes.byref(pts), _stream(stream)))
+        keys = schema_keys()
+        out = {}
+        for i in range(n):
+            v = (hi[i] << 64) | (lo[i] & ((1 << 64) - 1))
+            if v:
+                out[keys[i]] = v
+        return out, pts.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _capi._lib is not None:
+            _capi._lib.kcg_enum_program_destroy(h)
+            self._h = None
+
+
+def load_enum_program(kernel_id: str) -> EnumProgram:
+    """Enumeration program of one bundled suite kernel (programs/enum/<id>.kce)."""
+    return EnumProgram.from_file(ENUM_DIR / f"{kernel_id}.kce")

@@ -811,3 +811,49 @@ const char* kcg_last_error(void) { return g_last_error.c_str(); }
 uint64_t kcg_launch_count(void) { return g_launches.load(); }
 
 }  // extern "C"
+
+// ---- GPU enumeration oracle --------------------------------------------------
+
+struct kcg_enum_program {
+  kcg::EnumSymbolic e;
+};
+
+extern "C" {
+
+int kcg_enum_program_create(const char* text, size_t len, kcg_enum_program** out) {
+  if (!text || !out) return fail(KCG_E_INVALID_ARGUMENT, "null argument");
+  *out = nullptr;
+  return guarded([&] {
+    auto p = std::make_unique<kcg_enum_program>();
+    p->e = kcg::parse_enum_text(std::string(text, len));
+    *out = p.release();
+    return KCG_OK;
+  });
+}
+
+void kcg_enum_program_destroy(kcg_enum_program* p) { delete p; }
+
+int kcg_enum_program_num_params(const kcg_enum_program* p) { return p ? p->e.n_params : -1; }
+
+const char* kcg_enum_program_param_name(const kcg_enum_program* p, int i) {
+  return p && i >= 0 && i < p->e.n_params ? p->e.sym.params[i].c_str() : nullptr;
+}
+
+int kcg_enumerate_points(const kcg_enum_program* p, const int64_t* binding, uint64_t cap, int64_t* lo,
+                         int64_t* hi, uint64_t* points, void* stream) {
+  if (!p || (!binding && p->e.n_params > 0) || !lo || !hi)
+    return fail(KCG_E_INVALID_ARGUMENT, "bad enumerate arguments");
+  return guarded([&] {
+    require_device();
+    std::vector<i128> c(kcg::schema_keys().size(), 0);
+    const int launches = kcg::enumerate_points(p->e, binding, cap, c.data(), points, stream);
+    for (size_t i = 0; i < c.size(); ++i) {
+      lo[i] = static_cast<int64_t>(c[i]);
+      hi[i] = static_cast<int64_t>(c[i] >> 64);
+    }
+    g_launches += static_cast<uint64_t>(launches);
+    return KCG_OK;
+  });
+}
+
+}  // extern "C"

@@ -106,6 +106,56 @@ struct Symbolic {
 Symbolic parse_program_text(const std::string& text);
 
 // ---------------------------------------------------------------------------
+// Enumeration program ("kernelcost-enum v1", oracle/kcref_program.hpp
+// enum_text): what enumerate_points (enumerate.cpp:371-456) walks. Variables
+// of `sym` are the kernel parameters followed by every domain variable name;
+// polys are LinExpr / CountExpr texts parsed by the same front end.
+
+struct EnumVar {
+  std::string name;
+  int lo = -1, hi = -1;  // poly ids; hi exclusive
+};
+
+struct EnumAccess {
+  int array = -1;
+  bool store = false;
+  int stride = -1;  // lane_stride_signed poly (global arrays), -1 for local
+  std::vector<int> idx;  // poly ids
+};
+
+struct EnumStmt {
+  bool barrier = false;
+  std::vector<EnumVar> vars;
+  std::vector<int> guards;  // indices into sym.cons
+  std::vector<EnumAccess> acc;
+  std::vector<std::pair<int, i128>> ops;  // (schema index, count per point)
+};
+
+struct EnumArray {
+  std::string name;
+  bool global = true;
+  int bits = 32, nd = 1, fast = 0;
+};
+
+struct EnumSymbolic {
+  Symbolic sym;     // sym.params = kernel params + domain variables
+  int n_params = 0; // the kernel's own parameters (binding order)
+  std::vector<int> assumes;  // indices into sym.cons
+  std::vector<EnumArray> arrays;
+  std::vector<int> groups;   // group-axis extent polys
+  std::vector<EnumStmt> stmts;
+};
+
+EnumSymbolic parse_enum_text(const std::string& text);
+
+/// enumerate_points at one binding (enumerate.cpp): counts149 gets the bound
+/// property vector, points_out the visited points. Synchronous on `stream`
+/// (a cudaStream_t). Throws KcgError (E_ASSUMPTION_VIOLATED, E_CAP_EXCEEDED,
+/// E_UNSUPPORTED, E_CUDA ...). Returns the number of kernels launched.
+int enumerate_points(const EnumSymbolic& E, const int64_t* binding, uint64_t cap, i128* counts149,
+                      uint64_t* points_out, void* stream);
+
+// ---------------------------------------------------------------------------
 // Lowered integer program
 
 enum OpCode : int32_t {

@@ -4,7 +4,11 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 #include "kcg_devprog.h"
+
+struct KeStmt;  // kcg_enum_dev.h
 
 namespace kcg {
 
@@ -53,6 +57,12 @@ void launch_noise(const NoiseArgs& a, void* stream);
 /// geometric_mean_error accumulation (model.cpp:119-133)
 void launch_geomean(const double* pred, const double* actual, size_t n, double* log_sum,
                     unsigned long long* count, unsigned long long* bad, void* stream);
+
+/// GPU enumeration oracle (enum_kernels.cu): one statement walk, and the
+/// popcount / min / max set bit of a bitmap (out[0] +=, out[1] min=, out[2] max=)
+void launch_enum_walk(const KeStmt* dev_stmt, unsigned long long box_total, cudaStream_t stream);
+void launch_enum_bits(const unsigned long long* bm, unsigned long long words, unsigned long long* out,
+                      cudaStream_t stream);
 
 int num_sms();
 

@@ -568,6 +568,146 @@ Symbolic parse_program_text(const std::string& text) {
 }
 
 // ---------------------------------------------------------------------------
+// Enumeration program text (oracle/kcref_program.hpp enum_text)
+
+namespace {
+
+std::vector<std::string> split_bar(const std::string& s) {
+  std::vector<std::string> out;
+  size_t b = 0;
+  while (true) {
+    const size_t e = s.find(" | ", b);
+    out.push_back(trim(s.substr(b, e == std::string::npos ? std::string::npos : e - b)));
+    if (e == std::string::npos) break;
+    b = e + 3;
+  }
+  return out;
+}
+
+}  // namespace
+
+EnumSymbolic parse_enum_text(const std::string& text) {
+  std::vector<std::string> lines;
+  {
+    std::istringstream in(text);
+    std::string line;
+    while (std::getline(in, line)) {
+      line = trim(line);
+      if (!line.empty() && line[0] != '#') lines.push_back(line);
+    }
+  }
+  if (lines.empty() || lines[0] != "kernelcost-enum v1") parse_fail("missing 'kernelcost-enum v1' header");
+  auto kw_rest = [](const std::string& l, std::string& rest) {
+    const size_t sp = l.find(' ');
+    rest = sp == std::string::npos ? "" : trim(l.substr(sp + 1));
+    return l.substr(0, sp);
+  };
+  EnumSymbolic E;
+  Builder b;
+  // pass 1: parameters, then every domain-variable name as a further variable
+  std::string rest;
+  for (const auto& l : lines) {
+    const std::string kw = kw_rest(l, rest);
+    if (kw == "param") {
+      if (rest.empty() || std::find(b.s.params.begin(), b.s.params.end(), rest) != b.s.params.end())
+        parse_fail("bad or duplicate param '" + rest + "'");
+      b.s.params.push_back(rest);
+    }
+  }
+  E.n_params = static_cast<int>(b.s.params.size());
+  for (const auto& l : lines) {
+    const std::string kw = kw_rest(l, rest);
+    if (kw != "var") continue;
+    const std::string name = rest.substr(0, rest.find(' '));
+    if (std::find(b.s.params.begin(), b.s.params.end(), name) == b.s.params.end()) b.s.params.push_back(name);
+  }
+  std::map<std::string, int> array_ids;
+  EnumStmt* cur = nullptr;
+  bool ended = false;
+  for (size_t li = 1; li < lines.size(); ++li) {
+    const std::string& l = lines[li];
+    const std::string kw = kw_rest(l, rest);
+    if (ended) parse_fail("text after 'end'");
+    if (kw == "kernel") {
+      b.s.kernel = rest;
+    } else if (kw == "param") {
+    } else if (kw == "assume") {
+      b.constraint(rest);
+      E.assumes.push_back(static_cast<int>(b.s.cons.size()) - 1);
+    } else if (kw == "array") {
+      std::istringstream is(rest);
+      EnumArray a;
+      std::string space;
+      if (!(is >> a.name >> space >> a.bits >> a.nd >> a.fast) || (space != "global" && space != "local") ||
+          a.nd < 1 || a.fast < 0 || a.fast >= a.nd)
+        parse_fail("bad array line '" + l + "'");
+      a.global = space == "global";
+      array_ids[a.name] = static_cast<int>(E.arrays.size());
+      E.arrays.push_back(a);
+    } else if (kw == "group") {
+      E.groups.push_back(b.add_poly(b.lin(rest)));
+    } else if (kw == "stmt") {
+      if (cur) parse_fail("nested 'stmt'");
+      if (rest != "assign" && rest != "barrier") parse_fail("bad stmt kind '" + rest + "'");
+      E.stmts.emplace_back();
+      cur = &E.stmts.back();
+      cur->barrier = rest == "barrier";
+    } else if (kw == "endstmt") {
+      if (!cur) parse_fail("'endstmt' outside a statement");
+      cur = nullptr;
+    } else if (kw == "end") {
+      if (cur) parse_fail("'end' inside a statement");
+      ended = true;
+    } else {
+      if (!cur) parse_fail("unknown line '" + l + "'");
+      if (kw == "var") {
+        const size_t sp = rest.find(' ');
+        const auto parts = split_bar(sp == std::string::npos ? "" : rest.substr(sp + 1));
+        if (parts.size() != 2) parse_fail("bad var line '" + l + "'");
+        EnumVar v;
+        v.name = rest.substr(0, sp);
+        v.lo = b.add_poly(b.lin(parts[0]));
+        v.hi = b.add_poly(b.lin(parts[1]));
+        cur->vars.push_back(v);
+      } else if (kw == "guard") {
+        b.constraint(rest);
+        cur->guards.push_back(static_cast<int>(b.s.cons.size()) - 1);
+      } else if (kw == "access") {
+        const auto parts = split_bar(rest);
+        std::istringstream is(parts[0]);
+        std::string arr, dir, stride;
+        is >> arr >> dir;
+        std::getline(is, stride);
+        stride = trim(stride);
+        auto it = array_ids.find(arr);
+        if (it == array_ids.end() || (dir != "load" && dir != "store") || stride.empty())
+          parse_fail("bad access line '" + l + "'");
+        EnumAccess a;
+        a.array = it->second;
+        a.store = dir == "store";
+        if (E.arrays[a.array].global) a.stride = b.add_poly(b.count_expr(stride));
+        for (size_t k = 1; k < parts.size(); ++k) a.idx.push_back(b.add_poly(b.lin(parts[k])));
+        if (static_cast<int>(a.idx.size()) != E.arrays[a.array].nd) parse_fail("access rank mismatch in '" + l + "'");
+        cur->acc.push_back(std::move(a));
+      } else if (kw == "op") {
+        std::istringstream is(rest);
+        std::string key, cnt;
+        is >> key >> cnt;
+        const int idx = schema_index(key);
+        i128 v;
+        if (idx < 0 || !parse_int(cnt, v)) parse_fail("bad op line '" + l + "'");
+        cur->ops.emplace_back(idx, v);
+      } else {
+        parse_fail("unknown line '" + l + "'");
+      }
+    }
+  }
+  if (!ended) parse_fail("missing 'end'");
+  E.sym = std::move(b.s);
+  return E;
+}
+
+// ---------------------------------------------------------------------------
 // Congruence substitution
 //
 // A parameter with divisibility facts p % m_i == r_i (AssumeCtx::add_constraint
