@@ -543,6 +543,25 @@ def _extras(kc, torch, dev, args):
         "note": "one fused launch per step; 24 B bindings in, int32 + fp64 out per size"}
     del cols, best, best_t
 
+    # ---- config 4 from a grid descriptor: the same 1e9
+    # (variant, size) points, bindings generated in registers -- 8 B/point out
+    preds = torch.empty(total, dtype=torch.float64, device=dev)
+    grids = [kc.Grid.for_program(p, {"n": (UNIT, UNIT, side), "m": (UNIT, UNIT, side), "l": (UNIT, UNIT, side)})
+             for p in progs]
+    gstructs = [g.c_struct() for g in grids]
+
+    def c4g():
+        for p, g in zip(progs, gstructs):
+            kc.api.check(kc.api.lib().kcg_eval_predict_grid(p.handle, ctypes.byref(g), 0, total, w.alpha_array(),
+                                                            preds.data_ptr(), None, 0, stream))
+    sec = _timed(torch, c4g, reps=5)
+    out["config4_grid_descriptor"] = {
+        "points": total * len(progs), "ms": sec * 1e3, "points_per_s": total * len(progs) / sec,
+        "bytes_per_point": 8, "hbm_frac": 8 * total * len(progs) / sec / 1e9 / hbm,
+        "note": "kcg_eval_predict_grid per variant: lattice (n,m,l)=336*(u,v,w) decoded per thread "
+                "(odometer), exact evaluate + predict, fp64 predictions streamed out"}
+    del preds
+
     # ---- config 3: Gram over 1e8 x 40 fp64 materialised rows ---------------
     N, F = 100_000_000, 40
     g = torch.Generator(device=dev).manual_seed(4242)
@@ -602,7 +621,40 @@ def _extras(kc, torch, dev, args):
         "residual_pass_ms": sec_r * 1e3, "objective": float(obj.item()),
         "note": "matmul_tiled_g16x16 rows (n,m,l)=16*(u,v,w) u,v,w<=1000, T = noiseless_time on the GPU; "
                 "9 columns of rank 2 (all flop/memory counts are multiples of n*m*l): min-norm solve"}
+    del cols5, T
+
+    # ---- GPU enumeration oracle vs the reference's CPU
+    # enumerate_points on this host (single-threaded, as in the reference)
+    ep = kc.load_enum_program("fd_stencil_g16x16")
+    ne = 16384
+    ep.enumerate_points({"n": 1024})  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    counts, pts = ep.enumerate_points({"n": ne})
+    sec_e = time.perf_counter() - t0
+    ref = None
+    exe = ROOT / "oracle" / "_ref" / "kcref_bench"
+    if exe.exists():
+        try:
+            r = subprocess.run([str(exe), "enumerate", "fd_stencil_g16x16", "512"], capture_output=True,
+                               text=True, timeout=120)
+            ref = json.loads(r.stdout)
+        except Exception as e:  # noqa: BLE001
+            ref = {"error": str(e)[:200]}
+    out["enumerate_fd_stencil"] = {
+        "n": ne, "visited_points": pts, "seconds": sec_e, "points_per_s": pts / sec_e,
+        "equals_symbolic": counts == {kc.schema_keys()[k]: v for k, v in _sym_counts(kc, torch, dev, ne).items()},
+        "cpu_reference_n512": ref,
+        "note": "kcg_enumerate_points (statement walks + footprint bitmaps + host tally), wall clock incl. "
+                "host compile and sync; CPU: reference enumerate_points (shim bigint), 1 thread"}
     return out
+
+
+def _sym_counts(kc, torch, dev, n):
+    p = kc.load_program("fd_stencil_g16x16")
+    bb = kc.evaluate_properties(p, {"n": torch.tensor([n], dtype=torch.int64, device=dev)})
+    torch.cuda.synchronize()
+    return {k: bb.counts_int(j, 0) for j, k in enumerate(p.props) if bb.counts_int(j, 0)}
 
 
 if __name__ == "__main__":

@@ -142,6 +142,32 @@ int kcg_eval_predict(const kcg_program* prog, const int64_t* const* param_cols,
                      uint8_t* status_out, int64_t* counts_lo,
                      int64_t* counts_hi, int simulate, void* stream);
 
+/* ---- grid descriptors: bindings from a lattice --------
+ * Point i of the lattice binds parameter j (program declaration order) to
+ * start[j] + step[j] * d_j, where (d_0 .. d_{P-1}) are the mixed-radix
+ * digits of i over count[] with the LAST parameter varying fastest
+ * (i = ((d_0 * count[1] + d_1) * count[2] + d_2) ...). Every value must fit
+ * int64 (checked). A descriptor replaces P int64 columns in HBM / over PCIe. */
+typedef struct kcg_grid {
+  int32_t n_params;   /* <= 8 */
+  int32_t reserved;
+  int64_t start[8];
+  int64_t step[8];
+  uint64_t count[8];  /* >= 1 each */
+} kcg_grid;
+
+/* materialise points [first, first + n) as SoA int64 columns (DEVICE
+ * pointers, one per parameter) -- the binary side format's generator      */
+int kcg_grid_bindings(const kcg_grid* grid, uint64_t first, size_t n,
+                      int64_t* const* cols, void* stream);
+
+/* kcg_eval_predict over lattice points [first, first + n) without reading
+ * bindings: pred_out / status_out (nullable, DEVICE) as in kcg_eval_predict;
+ * grid->n_params must equal the program's parameter count.                */
+int kcg_eval_predict_grid(const kcg_program* prog, const kcg_grid* grid, uint64_t first,
+                          size_t n, const double* alpha, double* pred_out,
+                          uint8_t* status_out, int simulate, void* stream);
+
 /* ---- autotuning: evaluate + predict over variants, argmin --------------
  * progs: n_variants programs with identical parameter-name sets; param_cols
  * follow progs[0]'s parameter order. For each size i: best_idx[i] = lowest
@@ -263,6 +289,29 @@ int kcg_enum_program_num_params(const kcg_enum_program* prog);
 const char* kcg_enum_program_param_name(const kcg_enum_program* prog, int i);
 int kcg_enumerate_points(const kcg_enum_program* prog, const int64_t* binding, uint64_t cap,
                          int64_t* counts_lo, int64_t* counts_hi, uint64_t* points, void* stream);
+
+/* ---- columnar binary side format "kcg-columns v1" -----
+ * SoA columns (int64 bindings, float64 timings / predictions, uint8
+ * statuses) at 4096-byte aligned offsets behind a 64-byte header and a
+ * 64-byte-per-column table (layout in csrc/columns.cpp). The reference's
+ * CSV and weights JSON stay the interchange formats; this carries 1e9-row
+ * grids. kcg_columns_write takes HOST pointers; kcg_columns_open maps the
+ * file (kcg_columns_data: host pointer into the mapping) and
+ * kcg_columns_load copies rows [row0, row0 + n) of a column to DEVICE
+ * memory on `stream` (page-locked mapping or a pinned staging ring).      */
+enum kcg_column_dtype { KCG_COL_INT64 = 1, KCG_COL_FLOAT64 = 2, KCG_COL_UINT8 = 3, KCG_COL_INT32 = 4 };
+typedef struct kcg_columns kcg_columns;
+int kcg_columns_write(const char* path, int n_cols, const char* const* names, const int* dtypes,
+                      const void* const* host_cols, uint64_t n_rows);
+int kcg_columns_open(const char* path, kcg_columns** out);
+void kcg_columns_close(kcg_columns* cols);
+uint64_t kcg_columns_num_rows(const kcg_columns* cols);
+int kcg_columns_num_cols(const kcg_columns* cols);
+const char* kcg_columns_name(const kcg_columns* cols, int j);
+int kcg_columns_dtype(const kcg_columns* cols, int j);
+int kcg_columns_find(const kcg_columns* cols, const char* name);  /* -1 if absent */
+const void* kcg_columns_data(const kcg_columns* cols, int j);
+int kcg_columns_load(kcg_columns* cols, int j, uint64_t row0, size_t n, void* dev, void* stream);
 
 /* ---- diagnostics -------------------------------------------------------- */
 const char* kcg_status_str(int status);

@@ -11,6 +11,9 @@
 //       sizes enumerated in the GPU bench's order from `offset`
 //   kcref_bench suite <threads> <n_points>
 //       config 2: skinny (16u,128u,16u) and conv n=16u, u = 1..n/2
+//   kcref_bench enumerate <kernel_id> <n>
+//       enumerate_points (enumerate.cpp:371-456) at the binding n (every
+//       parameter = n), single-threaded like the reference; visited points/s
 // Prints one JSON object: points, seconds, points_per_s, threads, checksum.
 #include <atomic>
 #include <chrono>
@@ -20,6 +23,7 @@
 #include <thread>
 #include <vector>
 
+#include "kernelcost/enumerate.hpp"
 #include "kernelcost/model.hpp"
 #include "kernelcost/parser.hpp"
 #include "kernelcost/props.hpp"
@@ -43,6 +47,19 @@ int main(int argc, char** argv) {
     return 2;
   }
   const std::string mode = argv[1];
+  if (mode == "enumerate") {
+    const kc::SuiteLibrary lib = kc::build_suite();
+    const kc::KernelIR k = kc::parse_kernel(lib.find(argv[2])->text);
+    kc::Binding b;
+    for (const auto& p : k.params) b[p.name] = kc::Int(std::atol(argv[3]));
+    const auto t0 = std::chrono::steady_clock::now();
+    const kc::EnumTally t = kc::enumerate_points(k, b, kc::Int("1000000000000"));
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const double pts = t.points.convert_to<double>();
+    std::printf("{\"points\": %.0f, \"seconds\": %.6f, \"points_per_s\": %.6g, \"threads\": 1}\n", pts, sec,
+                pts / sec);
+    return 0;
+  }
   const int threads = std::max(1, std::atoi(argv[2]));
   const long n = std::atol(argv[3]);
   const long offset = argc > 4 ? std::atol(argv[4]) : 0;

@@ -7,7 +7,13 @@ of the least-squares fit. See DESIGN.md; the C ABI is include/kcg.h.
 """
 from .api import (  # noqa: F401
     BoundBatch,
+    Columns,
     EnumProgram,
+    read_columns,
+    write_columns,
+    Grid,
+    grid_bindings,
+    predict_grid,
     load_enum_program,
     KernelMeasurements,
     eval_from_csv,

@@ -87,6 +87,18 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_enum_program_param_name": (ctypes.c_char_p, [P, ctypes.c_int]),
         "kcg_enumerate_points": (ctypes.c_int, [P, I64P, ctypes.c_uint64, I64P, I64P,
                                                 ctypes.POINTER(ctypes.c_uint64), P]),
+        "kcg_grid_bindings": (ctypes.c_int, [P, ctypes.c_uint64, ctypes.c_size_t, P, P]),
+        "kcg_eval_predict_grid": (ctypes.c_int, [P, P, ctypes.c_uint64, ctypes.c_size_t, DP, P, P, ctypes.c_int, P]),
+        "kcg_columns_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, P, P, P, ctypes.c_uint64]),
+        "kcg_columns_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(P)]),
+        "kcg_columns_close": (None, [P]),
+        "kcg_columns_num_rows": (ctypes.c_uint64, [P]),
+        "kcg_columns_num_cols": (ctypes.c_int, [P]),
+        "kcg_columns_name": (ctypes.c_char_p, [P, ctypes.c_int]),
+        "kcg_columns_dtype": (ctypes.c_int, [P, ctypes.c_int]),
+        "kcg_columns_find": (ctypes.c_int, [P, ctypes.c_char_p]),
+        "kcg_columns_data": (P, [P, ctypes.c_int]),
+        "kcg_columns_load": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_uint64, ctypes.c_size_t, P, P]),
         "kcg_status_str": (ctypes.c_char_p, [ctypes.c_int]),
         "kcg_point_status_str": (ctypes.c_char_p, [ctypes.c_int]),
         "kcg_last_error": (ctypes.c_char_p, []),

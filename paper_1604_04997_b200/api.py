@@ -569,3 +569,148 @@ class EnumProgram:
 def load_enum_program(kernel_id: str) -> EnumProgram:
     """Enumeration program of one bundled suite kernel (programs/enum/<id>.kce)."""
     return EnumProgram.from_file(ENUM_DIR / f"{kernel_id}.kce")
+
+
+# ---- grid descriptors (SURVEY 8f row 4) --------------------------------------
+
+
+class _KcgGrid(ctypes.Structure):
+    _fields_ = [("n_params", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("start", ctypes.c_int64 * 8), ("step", ctypes.c_int64 * 8), ("count", ctypes.c_uint64 * 8)]
+
+
+@dataclass
+class Grid:
+    """Lattice of bindings (include/kcg.h kcg_grid): parameter j takes
+    start[j] + step[j] * d_j, d_j in [0, count[j]), the last parameter
+    varying fastest. ``axes`` maps parameter name -> (start, step, count)
+    and is ordered by the program's declaration order when built with
+    :meth:`for_program`."""
+    params: list
+    start: list
+    step: list
+    count: list
+
+    @classmethod
+    def for_program(cls, prog, axes: Mapping) -> "Grid":
+        ps = list(prog.params)
+        return cls(ps, [int(axes[p][0]) for p in ps], [int(axes[p][1]) for p in ps], [int(axes[p][2]) for p in ps])
+
+    @property
+    def size(self) -> int:
+        n = 1
+        for c in self.count:
+            n *= c
+        return n
+
+    def c_struct(self) -> _KcgGrid:
+        g = _KcgGrid()
+        g.n_params = len(self.params)
+        for j in range(len(self.params)):
+            g.start[j], g.step[j], g.count[j] = self.start[j], self.step[j], self.count[j]
+        return g
+
+
+def grid_bindings(grid: Grid, first: int = 0, n: int | None = None, device="cuda", stream=None) -> dict:
+    """Materialise lattice points [first, first + n) as SoA int64 columns."""
+    torch = _torch()
+    n = grid.size - first if n is None else n
+    cols = {p: torch.empty(n, dtype=torch.int64, device=device) for p in grid.params}
+    arr = (ctypes.c_void_p * max(1, len(cols)))(*[c.data_ptr() for c in cols.values()])
+    g = grid.c_struct()
+    check(lib().kcg_grid_bindings(ctypes.byref(g), first, n, arr, _stream(stream)))
+    return cols
+
+
+def predict_grid(w: ModelWeights, prog: Program, grid: Grid, first: int = 0, n: int | None = None,
+                 with_status: bool = False, simulate: bool = False, device="cuda", stream=None):
+    """``predict`` (or ``noiseless_time`` with simulate=True) over lattice
+    points [first, first + n) without materialising the bindings."""
+    torch = _torch()
+    if list(grid.params) != list(prog.params):
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, f"grid params {grid.params} != kernel params {prog.params}")
+    n = grid.size - first if n is None else n
+    pred = torch.empty(n, dtype=torch.float64, device=device)
+    st = torch.empty(n, dtype=torch.uint8, device=device) if with_status else None
+    g = grid.c_struct()
+    check(lib().kcg_eval_predict_grid(prog.handle, ctypes.byref(g), first, n, w.alpha_array(), pred.data_ptr(),
+                                      _ptr(st), 1 if simulate else 0, _stream(stream)))
+    return (pred, st) if with_status else pred
+
+
+# ---- kcg-columns v1 binary side format (SURVEY 8f row 4) -----------------------
+
+_COL_DTYPES = {"int64": 1, "float64": 2, "uint8": 3, "int32": 4}
+_COL_NAMES = {v: k for k, v in _COL_DTYPES.items()}
+
+
+def write_columns(path, columns: Mapping) -> None:
+    """Write SoA columns (numpy arrays or CPU/CUDA tensors of int64, float64,
+    uint8 or int32, equal lengths) as a kcg-columns v1 file."""
+    import numpy as np
+    arrs = []
+    for name, c in columns.items():
+        if hasattr(c, "detach"):
+            c = c.detach().cpu().numpy()
+        a = np.ascontiguousarray(c)
+        if a.dtype.name not in _COL_DTYPES:
+            raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, f"column '{name}': unsupported dtype {a.dtype}")
+        arrs.append((name, a))
+    n = len(arrs[0][1]) if arrs else 0
+    if any(len(a) != n for _, a in arrs):
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "ragged columns")
+    k = len(arrs)
+    names = (ctypes.c_char_p * max(1, k))(*[nm.encode() for nm, _ in arrs])
+    dts = (ctypes.c_int * max(1, k))(*[_COL_DTYPES[a.dtype.name] for _, a in arrs])
+    ptrs = (ctypes.c_void_p * max(1, k))(*[a.ctypes.data for _, a in arrs])
+    check(lib().kcg_columns_write(str(path).encode(), k, names, dts, ptrs, n))
+
+
+class Columns:
+    """A mapped kcg-columns v1 file: ``numpy(name)`` is a zero-copy view of
+    the mapping, ``to_device(name)`` copies (a slice of) a column into a new
+    CUDA tensor through kcg_columns_load."""
+
+    def __init__(self, path):
+        h = ctypes.c_void_p()
+        check(lib().kcg_columns_open(str(path).encode(), ctypes.byref(h)))
+        self._h = h
+        L = lib()
+        self.n_rows = int(L.kcg_columns_num_rows(h))
+        self.names = [L.kcg_columns_name(h, j).decode() for j in range(L.kcg_columns_num_cols(h))]
+        self.dtypes = {nm: _COL_NAMES[L.kcg_columns_dtype(h, j)] for j, nm in enumerate(self.names)}
+
+    def _index(self, name: str) -> int:
+        j = lib().kcg_columns_find(self._h, name.encode())
+        if j < 0:
+            raise KeyError(name)
+        return j
+
+    def numpy(self, name: str):
+        import numpy as np
+        j = self._index(name)
+        dt = np.dtype(self.dtypes[name])
+        ptr = lib().kcg_columns_data(self._h, j)
+        buf = (ctypes.c_char * (self.n_rows * dt.itemsize)).from_address(ptr)
+        return np.frombuffer(buf, dtype=dt)
+
+    def to_device(self, name: str, row0: int = 0, n: int | None = None, device="cuda", stream=None):
+        torch = _torch()
+        j = self._index(name)
+        n = self.n_rows - row0 if n is None else n
+        out = torch.empty(n, dtype=getattr(torch, self.dtypes[name]), device=device)
+        check(lib().kcg_columns_load(self._h, j, row0, n, out.data_ptr(), _stream(stream)))
+        return out
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _capi._lib is not None:
+            _capi._lib.kcg_columns_close(h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def read_columns(path) -> Columns:
+    return Columns(path)

@@ -37,6 +37,8 @@ struct kcg_program {
   void* jit_eval = nullptr;
   void* jit_eval_gen = nullptr;
   void* jit_eval_tma = nullptr;
+  void* jit_eval_grid = nullptr;
+  void* jit_eval_grid_gen = nullptr;
   void* jit_gram = nullptr;
   void* jit_resid = nullptr;
 };
@@ -852,6 +854,158 @@ int kcg_enumerate_points(const kcg_enum_program* p, const int64_t* binding, uint
       hi[i] = static_cast<int64_t>(c[i] >> 64);
     }
     g_launches += static_cast<uint64_t>(launches);
+    return KCG_OK;
+  });
+}
+
+}  // extern "C"
+
+// ---- grid descriptors ----------------------------------------------------------
+
+namespace {
+
+// validates the lattice and [first, first + n) against it
+void check_grid(const kcg_grid* g, uint64_t first, size_t n) {
+  if (!g || g->n_params < 0 || g->n_params > 8) throw KcgError(KCG_E_INVALID_ARGUMENT, "bad grid descriptor");
+  unsigned __int128 total = 1;
+  for (int j = 0; j < g->n_params; ++j) {
+    if (g->count[j] == 0) throw KcgError(KCG_E_INVALID_ARGUMENT, "grid count must be >= 1");
+    total *= g->count[j];
+    if (total > (static_cast<unsigned __int128>(1) << 64)) throw KcgError(KCG_E_INVALID_ARGUMENT, "grid has more than 2^64 points");
+    const i128 last = static_cast<i128>(g->start[j]) + static_cast<i128>(g->step[j]) * static_cast<i128>(g->count[j] - 1);
+    if (last > INT64_MAX || last < INT64_MIN) throw KcgError(KCG_E_INVALID_ARGUMENT, "grid values exceed int64");
+  }
+  if (static_cast<unsigned __int128>(first) + n > total)
+    throw KcgError(KCG_E_INVALID_ARGUMENT, "points beyond the end of the grid");
+}
+
+}  // namespace
+
+extern "C" {
+
+int kcg_grid_bindings(const kcg_grid* g, uint64_t first, size_t n, int64_t* const* cols, void* stream) {
+  return guarded([&] {
+    check_grid(g, first, n);
+    if (g->n_params > 0 && !cols) throw KcgError(KCG_E_INVALID_ARGUMENT, "null columns");
+    require_device();
+    if (n == 0 || g->n_params == 0) return KCG_OK;
+    kcg::launch_grid_fill(g->n_params, g->start, g->step, g->count, first, n, cols, stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_eval_predict_grid(const kcg_program* cp, const kcg_grid* g, uint64_t first, size_t n,
+                          const double* alpha, double* pred_out, uint8_t* status_out, int simulate,
+                          void* stream) {
+  kcg_program* p = const_cast<kcg_program*>(cp);
+  if (!p) return fail(KCG_E_INVALID_ARGUMENT, "null program");
+  if (pred_out && !alpha) return fail(KCG_E_INVALID_ARGUMENT, "alpha required for predictions");
+  return guarded([&] {
+    check_grid(g, first, n);
+    const int np = p->low.n_params;
+    if (g->n_params != np) throw KcgError(KCG_E_INVALID_ARGUMENT, "grid parameter count != program's");
+    require_device();
+    if (n == 0) return KCG_OK;
+    const int F = static_cast<int>(p->low.keys.size());
+    if (!p->jit_eval_grid) {
+      const std::string nm = kname("kcg_eval_", p);
+      p->jit_eval_grid = kcg::jit_kernel(kcg_program_jit_source(p), nm + "_grid");
+      p->jit_eval_grid_gen = kcg::jit_kernel(kcg_program_jit_source(p), nm + "_grid_gen");
+    }
+    const unsigned grid = grid_for((n + 3) / 4);
+    ArgBuf ab;
+    for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(nullptr);  // KcgArgs.p (unused)
+    ab.push<void*>(pred_out);
+    ab.push<void*>(status_out);
+    ab.push<void*>(nullptr);  // clo
+    ab.push<void*>(nullptr);  // chi
+    ab.push<int64_t>(static_cast<int64_t>(n));
+    ab.push<int32_t>(simulate);
+    ab.push<int32_t>(0);  // vec
+    const bool vout = (reinterpret_cast<uintptr_t>(pred_out) % 16 == 0) &&
+                      (reinterpret_cast<uintptr_t>(status_out) % 4 == 0);
+    ab.push<int32_t>(vout ? 1 : 0);
+    std::vector<double> al(std::max(F, 1), 0.0);
+    compact_alpha(p, alpha, al.data());
+    for (double v : al) ab.push<double>(v);
+    ab.finish();  // end of the embedded KcgArgs
+    const int NP = std::max(np, 1);
+    for (int j = 0; j < NP; ++j) ab.push<int64_t>(j < np ? g->start[j] : 0);
+    for (int j = 0; j < NP; ++j) ab.push<int64_t>(j < np ? g->step[j] : 0);
+    for (int j = 0; j < NP; ++j) ab.push<uint64_t>(j < np ? g->count[j] : 1);
+    // digits of the per-step advance 4 * gridDim * blockDim (mod the lattice size)
+    uint64_t adv = 4ull * grid * 256ull, dig[8] = {0};
+    for (int j = np - 1; j >= 0; --j) {
+      dig[j] = adv % g->count[j];
+      adv /= g->count[j];
+    }
+    for (int j = 0; j < NP; ++j) ab.push<uint64_t>(j < np ? dig[j] : 0);
+    ab.push<uint64_t>(first);
+    ab.finish();
+    bool finite = true;
+    for (double v : al) finite = finite && std::isfinite(v);
+    kcg::launch_jit(finite ? p->jit_eval_grid : p->jit_eval_grid_gen, ab.b.data(), ab.b.size(), grid, 256,
+                    stream);
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+}  // extern "C"
+
+// ---- kcg-columns v1 ----------------------------------------------------------
+
+extern "C" {
+
+int kcg_columns_write(const char* path, int n_cols, const char* const* names, const int* dtypes,
+                      const void* const* host_cols, uint64_t n_rows) {
+  return guarded([&] {
+    kcg::columns_write(path, n_cols, names, dtypes, host_cols, n_rows);
+    return KCG_OK;
+  });
+}
+
+int kcg_columns_open(const char* path, kcg_columns** out) {
+  if (!out) return fail(KCG_E_INVALID_ARGUMENT, "null out");
+  *out = nullptr;
+  return guarded([&] {
+    *out = kcg::columns_open(path);
+    return KCG_OK;
+  });
+}
+
+void kcg_columns_close(kcg_columns* c) { delete c; }
+
+uint64_t kcg_columns_num_rows(const kcg_columns* c) { return c ? c->n_rows : 0; }
+
+int kcg_columns_num_cols(const kcg_columns* c) { return c ? static_cast<int>(c->cols.size()) : -1; }
+
+const char* kcg_columns_name(const kcg_columns* c, int j) {
+  return c && j >= 0 && j < static_cast<int>(c->cols.size()) ? c->cols[j].name.c_str() : nullptr;
+}
+
+int kcg_columns_dtype(const kcg_columns* c, int j) {
+  return c && j >= 0 && j < static_cast<int>(c->cols.size()) ? c->cols[j].dtype : -1;
+}
+
+int kcg_columns_find(const kcg_columns* c, const char* name) {
+  if (!c || !name) return -1;
+  for (size_t j = 0; j < c->cols.size(); ++j)
+    if (c->cols[j].name == name) return static_cast<int>(j);
+  return -1;
+}
+
+const void* kcg_columns_data(const kcg_columns* c, int j) {
+  return c && j >= 0 && j < static_cast<int>(c->cols.size())
+             ? static_cast<const char*>(c->map) + c->cols[j].offset
+             : nullptr;
+}
+
+int kcg_columns_load(kcg_columns* c, int j, uint64_t row0, size_t n, void* dev, void* stream) {
+  return guarded([&] {
+    require_device();
+    kcg::columns_load(c, j, row0, n, dev, stream);
     return KCG_OK;
   });
 }

@@ -432,11 +432,12 @@ void emit_eval_point(std::ostringstream& os, const Lowered& L) {
   const int F = static_cast<int>(L.keys.size());
   const int FA = F > 0 ? F : 1;
   os << "struct KcgRes { double s; int st; };\n";
-  // out-of-line wide path: reloads its parameters, writes counts
-  os << "__device__ __noinline__ KcgRes kcg_point_slow(const KcgArgs& a, kcg_i64 i) {\n"
-        "  kcg_i64 p["
-     << (L.n_params ? L.n_params : 1) << "];\n";
-  for (int j = 0; j < L.n_params; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
+  // out-of-line wide path: parameters by value (the grid kernels form them
+  // from a descriptor), writes counts; kcg_point_slow reloads them
+  os << "__device__ __noinline__ KcgRes kcg_point_slow_v(const KcgArgs& a, kcg_i64 i";
+  for (int j = 0; j < L.n_params; ++j) os << ", kcg_i64 v" << j;
+  os << ") {\n  kcg_i64 p[" << (L.n_params ? L.n_params : 1) << "];\n";
+  for (int j = 0; j < L.n_params; ++j) os << "  p[" << j << "] = v" << j << ";\n";
   os << "  KcgRes r; r.s = kcg_nan();\n"
         "  const int cls = kcg_class_0(p);\n"
         "  if (cls == 0) { r.st = KCG_PT_ASSUMPTION_VIOLATED; return r; }\n";
@@ -459,6 +460,10 @@ void emit_eval_point(std::ostringstream& os, const Lowered& L) {
        << "    if (a.chi) a.chi[(kcg_i64)" << j << " * a.n + i] = kcg_hi64(c[" << j
        << "]); else if (!kcg_fits_i64(c[" << j << "])) r.st = KCG_PT_COUNT_WIDE;\n";
   os << "  }\n  return r;\n}\n";
+  os << "__device__ __forceinline__ KcgRes kcg_point_slow(const KcgArgs& a, kcg_i64 i) {\n"
+        "  return kcg_point_slow_v(a, i";
+  for (int j = 0; j < L.n_params; ++j) os << ", a.p[" << j << "][i]";
+  os << ");\n}\n";
   // fast path only; returns -1 when the point needs kcg_point_slow
   os << "template <int GEN>\n__device__ __forceinline__ int kcg_point_fast(const kcg_i64* p, const KcgArgs& a, kcg_i64 i, double& out) {\n"
         "  if (kcg_class_0(p) != 1) return -1;\n"
@@ -479,6 +484,74 @@ void emit_eval_point(std::ostringstream& os, const Lowered& L) {
     os << "  s = GEN ? kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim) : "
        << "__dadd_rn(s, __dmul_rn(a.alpha[" << j << "], c[" << j << "]));\n";
   os << "  out = s;\n  return st;\n}\n";
+}
+
+// Grid-descriptor kernel: bindings are never read from HBM. Point i of the
+// lattice has parameter j = start_j + step_j * d_j with (d_0..d_{P-1}) the
+// mixed-radix digits of first + i (last parameter fastest). Each thread
+// handles 4 consecutive points per step: the digits are decoded once and
+// then advanced by odometer increments (+1 inside the quad, + the digits of
+// 4 * gridDim * blockDim between steps), so no division runs per point.
+int min_blocks();
+
+void emit_grid_kernel(std::ostringstream& os, int n_cols, const std::string& name, int gen) {
+  const int NP = n_cols > 0 ? n_cols : 1;
+  if (!gen) {  // shared by the two variants: emitted once
+    os << "struct KcgGridArgs { KcgArgs a; kcg_i64 start[" << NP << "]; kcg_i64 step[" << NP
+       << "]; kcg_u64 count[" << NP << "]; kcg_u64 sdig[" << NP << "]; kcg_u64 first; };\n";
+    os << "__device__ __forceinline__ void kcg_odo_add(kcg_u64* d, const kcg_u64* add, const kcg_u64* cnt) {\n"
+          "  kcg_u64 c = 0;\n  #pragma unroll\n  for (int j = "
+       << n_cols - 1 << "; j >= 0; --j) {\n"
+          "    kcg_u64 t = d[j] + add[j] + c;\n    c = t >= cnt[j];\n    d[j] = c ? t - cnt[j] : t;\n  }\n}\n";
+    os << "__device__ __forceinline__ void kcg_odo_inc(kcg_u64* d, const kcg_u64* cnt) {\n"
+          "  #pragma unroll\n  for (int j = "
+       << n_cols - 1 << "; j >= 0; --j) {\n    if (++d[j] < cnt[j]) return;\n    d[j] = 0;\n  }\n}\n";
+  }
+  os << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks() << ") " << name
+     << "(const __grid_constant__ KcgGridArgs g) {\n"
+        "  const KcgArgs& a = g.a;\n"
+        "  const kcg_i64 tid = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x;\n"
+        "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
+        "  const kcg_i64 nq = (a.n + 3) >> 2;\n"
+        "  if (tid >= nq) return;\n"
+        "  kcg_u64 d["
+     << NP << "];\n  { kcg_u64 r = g.first + 4 * (kcg_u64)tid;\n    #pragma unroll\n    for (int j = " << n_cols - 1
+     << "; j >= 0; --j) { d[j] = r % g.count[j]; r /= g.count[j]; } }\n"
+        "  for (kcg_i64 v = tid; v < nq; v += stride) {\n"
+        "    kcg_u64 e["
+     << NP << "];\n    #pragma unroll\n    for (int j = 0; j < " << n_cols << "; ++j) e[j] = d[j];\n"
+        "    double s[4]; int st[4];\n"
+        "    #pragma unroll\n"
+        "    for (int u = 0; u < 4; ++u) {\n"
+        "      kcg_i64 p["
+     << NP << "];\n      #pragma unroll\n      for (int j = 0; j < " << n_cols
+     << "; ++j) p[j] = g.start[j] + g.step[j] * (kcg_i64)e[j];\n"
+        "      s[u] = kcg_nan();\n"
+        "      st[u] = kcg_point_fast<"
+     << gen << ">(p, a, 4 * v + u, s[u]);\n"
+        "      if (st[u] < 0 && 4 * v + u < a.n) { const KcgRes r = kcg_point_slow_v(a, 4 * v + u";
+  for (int j = 0; j < n_cols; ++j) os << ", p[" << j << "]";
+  os << "); s[u] = r.s; st[u] = r.st; }\n"
+        "      if (st[u] != KCG_PT_OK && st[u] != KCG_PT_COUNT_WIDE) s[u] = kcg_nan();\n"
+        "      if (u < 3) kcg_odo_inc(e, g.count);\n"
+        "    }\n"
+        "    if (a.vout && 4 * v + 3 < a.n) {\n"
+        "      if (a.pred) {\n"
+        "        __stcs(reinterpret_cast<double2*>(a.pred) + 2 * v, make_double2(s[0], s[1]));\n"
+        "        __stcs(reinterpret_cast<double2*>(a.pred) + 2 * v + 1, make_double2(s[2], s[3]));\n"
+        "      }\n"
+        "      if (a.status) reinterpret_cast<unsigned*>(a.status)[v] =\n"
+        "          (unsigned)st[0] | ((unsigned)st[1] << 8) | ((unsigned)st[2] << 16) | ((unsigned)st[3] << 24);\n"
+        "    } else {\n"
+        "      #pragma unroll\n"
+        "      for (int u = 0; u < 4; ++u)\n"
+        "        if (4 * v + u < a.n) {\n"
+        "          if (a.pred) a.pred[4 * v + u] = s[u];\n"
+        "          if (a.status) a.status[4 * v + u] = (unsigned char)st[u];\n"
+        "        }\n"
+        "    }\n"
+        "    kcg_odo_add(d, g.sdig, g.count);\n"
+        "  }\n}\n";
 }
 
 int min_blocks() {
@@ -771,6 +844,8 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     emit_eval_kernel(os, n_cols, name, 0);
     emit_eval_kernel(os, n_cols, name + "_gen", 1);
     emit_tma_kernel(os, n_cols, name + "_tma");
+    emit_grid_kernel(os, n_cols, name + "_grid", 0);
+    emit_grid_kernel(os, n_cols, name + "_grid_gen", 1);
     return os.str();
   }
 

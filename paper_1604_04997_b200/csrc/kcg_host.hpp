@@ -148,6 +148,28 @@ struct EnumSymbolic {
 
 EnumSymbolic parse_enum_text(const std::string& text);
 
+/// kcg-columns v1 side format (columns.cpp)
+}  // namespace kcg
+struct kcg_columns {  // a mapped file (include/kcg.h)
+  int fd = -1;
+  void* map = nullptr;
+  size_t map_len = 0;
+  bool registered = false;  // mapping page-locked for DMA
+  uint64_t n_rows = 0;
+  struct Col {
+    std::string name;
+    int dtype;
+    uint64_t offset, nbytes;
+  };
+  std::vector<Col> cols;
+  ~kcg_columns();
+};
+namespace kcg {
+void columns_write(const char* path, int n_cols, const char* const* names, const int* dtypes,
+                   const void* const* data, uint64_t n_rows);
+kcg_columns* columns_open(const char* path);
+void columns_load(kcg_columns* h, int j, uint64_t row0, size_t n, void* dev, void* stream);
+
 /// enumerate_points at one binding (enumerate.cpp): counts149 gets the bound
 /// property vector, points_out the visited points. Synchronous on `stream`
 /// (a cudaStream_t). Throws KcgError (E_ASSUMPTION_VIOLATED, E_CAP_EXCEEDED,

@@ -64,6 +64,10 @@ void launch_enum_walk(const KeStmt* dev_stmt, unsigned long long box_total, cuda
 void launch_enum_bits(const unsigned long long* bm, unsigned long long words, unsigned long long* out,
                       cudaStream_t stream);
 
+/// grid descriptor -> SoA int64 bindings
+void launch_grid_fill(int np, const int64_t* start, const int64_t* step, const uint64_t* count, uint64_t first,
+                      size_t n, int64_t* const* cols, void* stream);
+
 int num_sms();
 
 }  // namespace kcg

@@ -678,3 +678,46 @@ void launch_residual_grad(const double* X, size_t n, int F, size_t ld, const dou
 }
 
 }  // namespace kcg
+
+// ---- grid descriptor -> SoA bindings (kcg_grid_bindings) -------------------
+namespace {
+struct GridArgsDev {
+  int np;
+  long long start[8], step[8];
+  unsigned long long count[8];
+  unsigned long long first;
+  long long n;
+  long long* cols[8];
+};
+
+__global__ void __launch_bounds__(256) kcg_grid_fill(const __grid_constant__ GridArgsDev g) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += stride) {
+    unsigned long long r = g.first + (unsigned long long)i;
+    for (int j = g.np - 1; j >= 0; --j) {
+      const unsigned long long d = r % g.count[j];
+      r /= g.count[j];
+      __stcs(g.cols[j] + i, g.start[j] + g.step[j] * (long long)d);
+    }
+  }
+}
+}  // namespace
+
+namespace kcg {
+void launch_grid_fill(int np, const int64_t* start, const int64_t* step, const uint64_t* count, uint64_t first,
+                      size_t n, int64_t* const* cols, void* stream) {
+  GridArgsDev g{};
+  g.np = np;
+  for (int j = 0; j < np; ++j) {
+    g.start[j] = start[j];
+    g.step[j] = step[j];
+    g.count[j] = count[j];
+    g.cols[j] = reinterpret_cast<long long*>(cols[j]);
+  }
+  g.first = first;
+  g.n = static_cast<long long>(n);
+  const size_t need = (n + 255) / 256, cap = static_cast<size_t>(num_sms()) * 8;
+  kcg_grid_fill<<<static_cast<unsigned>(need < cap ? need : cap), 256, 0, static_cast<cudaStream_t>(stream)>>>(g);
+  check(cudaGetLastError(), "kcg_grid_fill launch");
+}
+}  // namespace kcg
