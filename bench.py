@@ -289,12 +289,30 @@ def main():
                 "kind": "reference",
                 "sample": f"{r['points'] // 6} sizes x 6 variants, evaluate_properties+predict "
                           "per point (reference code + shim bigint), std::thread fan-out"}
+        if "fit" in line:
+            line["fit"]["cpu_reference"] = cpu_reference_fit(200_000, 40)
     if rank == 0 and args.extras:
         line["extras"] = _extras(kc, torch, dev, args)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line))
+
+
+def cpu_reference_fit(rows, cols):
+    """The reference's own build_design_matrix + fit_weights (model.cpp:11-93,
+    shim COD) on a config-3-shaped synthetic sample, 1 host thread."""
+    exe = ROOT / "oracle" / "_ref" / "kcref_bench"
+    if not exe.exists():
+        return None
+    try:
+        r = subprocess.run([str(exe), "fit", str(rows), str(cols)], capture_output=True, text=True, timeout=300)
+        d = json.loads(r.stdout)
+        d["unit"] = "rows/s"
+        d["sample"] = f"{rows} synthetic rows x {cols} keys (test_model.cpp pattern), build_design_matrix + fit_weights"
+        return d
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)[:200]}
 
 
 def _simdev_alpha(kc):

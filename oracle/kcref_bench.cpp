@@ -11,11 +11,18 @@
 //       sizes enumerated in the GPU bench's order from `offset`
 //   kcref_bench suite <threads> <n_points>
 //       config 2: skinny (16u,128u,16u) and conv n=16u, u = 1..n/2
+//   kcref_bench fit <n_rows> <n_cols>
+//       config 3 shape through the reference API: test_model.cpp-style
+//       synthetic FitCases (counts U{1..10000}, seed 4242, T = sum alpha c
+//       over the 16 simdev-v1 weights + log-uniform extras), then
+//       build_design_matrix + fit_weights (model.cpp:11-93); rows/s
 //   kcref_bench enumerate <kernel_id> <n>
 //       enumerate_points (enumerate.cpp:371-456) at the binding n (every
 //       parameter = n), single-threaded like the reference; visited points/s
 // Prints one JSON object: points, seconds, points_per_s, threads, checksum.
 #include <atomic>
+#include <cmath>
+#include <random>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -47,6 +54,43 @@ int main(int argc, char** argv) {
     return 2;
   }
   const std::string mode = argv[1];
+  if (mode == "fit") {
+    const long rows = std::atol(argv[2]);
+    const int F = std::atoi(argv[3]);
+    const kc::SimDevice dev = kc::SimDevice::reference();
+    std::vector<std::pair<std::string, double>> w;
+    const auto& keys = kc::schema_keys();
+    for (size_t i = 0; i < keys.size() && static_cast<int>(w.size()) < F; ++i)
+      if (dev.alpha[i] != 0) w.emplace_back(keys[i], dev.alpha[i]);
+    std::mt19937_64 rng(4242);
+    for (size_t i = 0; i < keys.size() && static_cast<int>(w.size()) < F; ++i)
+      if (dev.alpha[i] == 0)
+        w.emplace_back(keys[i], std::exp(std::log(1e-13) + (std::log(1e-9) - std::log(1e-13)) *
+                                                               std::uniform_real_distribution<double>(0, 1)(rng)));
+    std::vector<kc::FitCase> cases;
+    cases.reserve(rows);
+    for (long r = 0; r < rows; ++r) {
+      kc::PropertyVector pv;
+      double t = 0;
+      for (const auto& [key, alpha] : w) {
+        const long c = static_cast<long>(1 + rng() % 10000);
+        pv.at(key) = kc::CountExpr::from_int(kc::Int(c));
+        t += alpha * static_cast<double>(c);
+      }
+      cases.push_back({std::move(pv), t});
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const kc::DesignMatrix d = kc::build_design_matrix(cases);
+    const auto t1 = std::chrono::steady_clock::now();
+    auto [fw, rep] = kc::fit_weights(d, dev.name);
+    const auto t2 = std::chrono::steady_clock::now();
+    const double sb = std::chrono::duration<double>(t1 - t0).count();
+    const double sf = std::chrono::duration<double>(t2 - t1).count();
+    std::printf("{\"rows\": %ld, \"cols\": %d, \"build_s\": %.6f, \"fit_s\": %.6f, \"rows_per_s\": %.6g, "
+                "\"objective\": %.6g, \"threads\": 1}\n",
+                rows, F, sb, sf, rows / (sb + sf), rep.objective);
+    return 0;
+  }
   if (mode == "enumerate") {
     const kc::SuiteLibrary lib = kc::build_suite();
     const kc::KernelIR k = kc::parse_kernel(lib.find(argv[2])->text);

@@ -507,7 +507,9 @@ void emit_grid_kernel(std::ostringstream& os, int n_cols, const std::string& nam
           "  #pragma unroll\n  for (int j = "
        << n_cols - 1 << "; j >= 0; --j) {\n    if (++d[j] < cnt[j]) return;\n    d[j] = 0;\n  }\n}\n";
   }
-  os << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks() << ") " << name
+  // 2 CTAs/SM: the 4-point odometer state plus the exact evaluation need
+  // ~100 registers; the 64-register cap of the streaming kernels spills
+  os << "extern \"C\" __global__ void __launch_bounds__(256, 2) " << name
      << "(const __grid_constant__ KcgGridArgs g) {\n"
         "  const KcgArgs& a = g.a;\n"
         "  const kcg_i64 tid = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x;\n"

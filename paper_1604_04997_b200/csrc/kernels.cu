@@ -337,9 +337,11 @@ __global__ void __launch_bounds__(256, 2)
   double* red_s1 = red + FP * FP;
   double* red_mx = red_s1 + FP;
   __shared__ __align__(8) unsigned long long full[8];
+  __shared__ unsigned reads[8];  // warps done with stage s (the last one refills it)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, tig = lane & 3;
   for (int k = tid; k < FP * FP + 2 * FP; k += blockDim.x) red[k] = 0.0;
+  if (tid < 8) reads[tid] = 0;
   const unsigned fb = (unsigned)__cvta_generic_to_shared(full);
   const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);
   if (tid == 0) {
@@ -369,6 +371,18 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
   for (int b = 0; b < NB; ++b) s1[b] = mx[b] = 0.0;
 
+  auto kstep_regs = [&](const double* v) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      s1[b] += v[b];
+      mx[b] = fmax(mx[b], fabs(v[b]));
+    }
+    int t = 0;
+#pragma unroll
+    for (int I = 0; I < NB; ++I)
+#pragma unroll
+      for (int J = I; J < NB; ++J, ++t) dmma_8x8x4(acc[t][0], acc[t][1], v[I], v[J]);
+  };
   auto kstep = [&](const double* rowp, bool valid) {
     double v[NB];
 #pragma unroll
@@ -397,14 +411,31 @@ __global__ void __launch_bounds__(256, 2)
                    : "r"(fb + 8 * s), "r"(parity)
                    : "memory");
     const double* st = buf + s * stage_d;
-    // 8 warps x 2 k-steps x 4 rows = 64 rows
+    // 8 warps x 2 k-steps x 4 rows = 64 rows; fragments are loaded to
+    // registers first, then the stage is released: the last warp to finish
+    // reading it issues the refill, so warps drift freely between tiles
+    double v[NB];
 #pragma unroll
-    for (int ks = 0; ks < 2; ++ks) kstep(st + (warp * 8 + ks * 4 + tig) * F, true);
-    __syncthreads();
-    if (tid == 0) {
-      const kcg_i64 nt = blockIdx.x + (k + stages) * gridDim.x;
-      if (nt < ntiles) issue(s, nt);
+    for (int b = 0; b < NB; ++b) {
+      const int col = 8 * b + gid;
+      v[b] = col < F ? st[(warp * 8 + tig) * F + col] : 0.0;
     }
+    kstep_regs(v);
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      const int col = 8 * b + gid;
+      v[b] = col < F ? st[(warp * 8 + 4 + tig) * F + col] : 0.0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {
+        reads[s] = 0;
+        const kcg_i64 nt = blockIdx.x + (k + stages) * gridDim.x;
+        if (nt < ntiles) issue(s, nt);
+      }
+    }
+    kstep_regs(v);
   }
   // tail rows straight from global (block 0 only)
   if (blockIdx.x == 0)
@@ -615,7 +646,7 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
   if (n == 0) return;
   if (F < 1 || F > kGramMaxF) throw std::invalid_argument("gram: n_cols must be in [1, 64]");
   static const bool no_dmma = std::getenv("KCG_NO_DMMA") != nullptr;
-  if (!no_dmma && ld == (size_t)F && F <= 48 && F % 2 == 0 &&
+  if (!no_dmma && ld == (size_t)F && F <= 48 &&
       reinterpret_cast<uintptr_t>(X) % 16 == 0) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     switch ((F + 7) / 8) {

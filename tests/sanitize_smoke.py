@@ -36,5 +36,17 @@ kc.argmin(progs, w, {p: (u[j] * 336).contiguous() for j, p in enumerate(progs[0]
 for F in (3, 40, 64):
     X = torch.rand((20000 + F, F), dtype=torch.float64, device="cuda")
     kc.fit_weights(X, refine=1)
+# per-key (direct) fused Gram path too
+prog.set_gram_basis(False)
+kc.gram_fused(prog, cols, T)
+prog.set_gram_basis(True)
+# grid descriptors: fused evaluate + predict and the binding generator
+grid = kc.Grid.for_program(prog, {"n": (8, 8, 61), "m": (16, 16, 59), "l": (16, 48, 47)})
+kc.predict_grid(w, prog, grid, 17, grid.size - 20, with_status=True)
+kc.grid_bindings(grid, 5, 1000)
+# GPU enumeration oracle: box-flattened and triangular domains
+kc.load_enum_program("fd_stencil_g16x16").enumerate_points({"n": 256})
+kc.load_enum_program("x_triangle").enumerate_points({"n": 300})
+kc.load_enum_program("x_guarded").enumerate_points({"n": 200, "m": 150})
 torch.cuda.synchronize()
 print("sanitize smoke ok")

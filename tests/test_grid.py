@@ -161,5 +161,6 @@ def test_columns_file_to_device_predict_and_back(tmp_path, suite_alpha):
     out = tmp_path / "pred.kcgcol"
     kc.write_columns(out, {"pred": pred, "status": st})
     r = kc.read_columns(out)
-    assert torch.equal(torch.from_numpy(r.numpy("pred").copy()), pred.cpu())
+    # bitwise (NaN payloads included)
+    assert torch.equal(torch.from_numpy(r.numpy("pred").copy()).view(torch.int64), pred.cpu().view(torch.int64))
     assert torch.equal(torch.from_numpy(r.numpy("status").copy()), st.cpu())
