@@ -13,6 +13,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/kcg.h"
@@ -178,6 +179,20 @@ void compact_alpha(const kcg_program* p, const double* alpha149, double* out) {
     out[j] = alpha149 ? alpha149[p->low.keys[j].schema] : 0.0;
 }
 
+// alpha (compact) -> the folded weights of the GEN = 0 predict kernels
+// (kcg::predict_fold); *finite says whether both sets are finite (the
+// precondition of the unconditional-accumulation kernels)
+std::vector<double> folded_alpha(const kcg_program* p, const std::vector<double>& al, bool* finite) {
+  std::vector<double> f(al);
+  bool fin = true;
+  for (size_t j = 0; j < p->low.keys.size(); ++j) {
+    f[j] = al[j] * kcg::predict_fold(p->low, static_cast<int>(j));
+    fin = fin && std::isfinite(al[j]) && std::isfinite(f[j]);
+  }
+  if (finite) *finite = fin;
+  return f;
+}
+
 // symmetric eigen-decomposition (cyclic Jacobi), A row-major n x n
 void jacobi_eigen(int n, std::vector<double>& A, std::vector<double>& V, std::vector<double>& w) {
   V.assign(static_cast<size_t>(n) * n, 0.0);
@@ -338,9 +353,13 @@ const char* kcg_program_jit_source(kcg_program* p) {
 }
 
 const char* kcg_program_jit_source_kind(kcg_program* p, int kind) {
-  if (!p || kind < 0 || kind > 2) return nullptr;
+  if (!p || kind < 0 || kind > 3) return nullptr;
   if (kind == 0) return kcg_program_jit_source(p);
   const int np = p->low.n_params;
+  if (kind == 3) {  // argmin over this single variant
+    p->jit_src_kind = kcg::codegen({&p->low}, {identity(np)}, np, kcg::JitKind::argmin, "kcg_argmin");
+    return p->jit_src_kind.c_str();
+  }
   p->jit_src_kind = kcg::codegen({&p->low}, {identity(np)}, np,
                                  kind == 1 ? kcg::JitKind::gram : kcg::JitKind::residual,
                                  kname(kind == 1 ? "kcg_gram_" : "kcg_resid_", p));
@@ -421,11 +440,12 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
     ab.push<int32_t>(vout ? 1 : 0);
     std::vector<double> al(std::max(F, 1), 0.0);
     compact_alpha(p, alpha, al.data());
-    for (double v : al) ab.push<double>(v);
-    ab.finish();
     // finite weights: the skip rules cannot change the sum (GEN = 0 kernel)
     bool finite = true;
-    for (double v : al) finite = finite && std::isfinite(v);
+    const std::vector<double> alf = folded_alpha(p, al, &finite);
+    for (double v : al) ab.push<double>(v);
+    for (double v : alf) ab.push<double>(v);
+    ab.finish();
     static const bool no_tma = std::getenv("KCG_NO_TMA") != nullptr;
     const size_t tiles = n / kcg::kTmaPointsPerTile;
     if (finite && vec && !no_tma && tiles >= static_cast<size_t>(kcg::num_sms())) {
@@ -472,42 +492,53 @@ int kcg_argmin(const kcg_program* const* progs, int V, const int64_t* const* par
     }
     const std::string src = kcg::codegen(lows, pmaps, np, kcg::JitKind::argmin, name);
     void* k = kcg::jit_kernel(src, name);
-    // per-variant compact weights live in one device buffer
-    size_t total = 0;
-    for (int v = 0; v < V; ++v) total += std::max<size_t>(1, progs[v]->low.keys.size());
-    std::vector<double> host(total, 0.0);
-    std::vector<size_t> off(V);
-    size_t o = 0;
-    for (int v = 0; v < V; ++v) {
-      off[v] = o;
-      compact_alpha(progs[v], alpha, host.data() + o);
-      o += std::max<size_t>(1, progs[v]->low.keys.size());
-    }
-    for (double a : host)
-      if (!std::isfinite(a))
-        throw KcgError(KCG_E_INVALID_ARGUMENT, "argmin requires finite weights");
-    // cache the device weights per (variant set, alpha) -- small, reused
-    static std::mutex mu;
-    static std::vector<std::pair<std::vector<double>, double*>> cache;
-    double* dalpha = nullptr;
-    {
-      std::lock_guard<std::mutex> lock(mu);
-      for (auto& [h, d] : cache)
-        if (h == host) dalpha = d;
-      if (!dalpha) {
-        cuda_check(cudaMalloc(&dalpha, total * sizeof(double)), "cudaMalloc");
-        cuda_check(cudaMemcpy(dalpha, host.data(), total * sizeof(double), cudaMemcpyHostToDevice),
-                   "cudaMemcpy");
-        cache.emplace_back(host, dalpha);
-      }
-    }
     ArgBuf ab;
     for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
     ab.push<void*>(best_idx);
     ab.push<void*>(best_t);
     ab.push<void*>(preds_out);
     ab.push<int64_t>(static_cast<int64_t>(n));
-    for (int v = 0; v < V; ++v) ab.push<const void*>(dalpha + off[v]);
+    // per-variant compact weights in one device buffer: as given (wide
+    // path), then folded (fast path, predict_fold); cached per device and
+    // weight set (small, reused across sweeps)
+    std::vector<double> host;
+    std::vector<size_t> off(V), offf(V);
+    std::vector<std::vector<double>> alfs(V);
+    for (int v = 0; v < V; ++v) {
+      std::vector<double> al(std::max<size_t>(1, progs[v]->low.keys.size()), 0.0);
+      compact_alpha(progs[v], alpha, al.data());
+      bool fin = true;
+      alfs[v] = folded_alpha(progs[v], al, &fin);
+      if (!fin) throw KcgError(KCG_E_INVALID_ARGUMENT, "argmin requires finite weights");
+      off[v] = host.size();
+      host.insert(host.end(), al.begin(), al.end());
+    }
+    for (int v = 0; v < V; ++v) {
+      offf[v] = host.size();
+      host.insert(host.end(), alfs[v].begin(), alfs[v].end());
+    }
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    static std::mutex mu;
+    static std::vector<std::tuple<int, std::vector<double>, double*>> cache;
+    double* dw = nullptr;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      for (auto& [d, h, ptr] : cache)
+        if (d == dev && h == host) dw = ptr;
+      if (!dw) {
+        cuda_check(cudaMalloc(&dw, host.size() * sizeof(double)), "cudaMalloc");
+        cuda_check(cudaMemcpy(dw, host.data(), host.size() * sizeof(double), cudaMemcpyHostToDevice),
+                   "cudaMemcpy");
+        if (cache.size() >= 64) {  // bound the cache: drop the oldest set
+          cudaFree(std::get<2>(cache.front()));
+          cache.erase(cache.begin());
+        }
+        cache.emplace_back(dev, host, dw);
+      }
+    }
+    for (int v = 0; v < V; ++v) ab.push<const void*>(dw + off[v]);
+    for (int v = 0; v < V; ++v) ab.push<const void*>(dw + offf[v]);
     ab.finish();
     kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid_for(n), 256, stream);
     ++g_launches;
@@ -928,7 +959,10 @@ int kcg_eval_predict_grid(const kcg_program* cp, const kcg_grid* g, uint64_t fir
     ab.push<int32_t>(vout ? 1 : 0);
     std::vector<double> al(std::max(F, 1), 0.0);
     compact_alpha(p, alpha, al.data());
+    bool finite = true;
+    const std::vector<double> alf = folded_alpha(p, al, &finite);
     for (double v : al) ab.push<double>(v);
+    for (double v : alf) ab.push<double>(v);
     ab.finish();  // end of the embedded KcgArgs
     const int NP = std::max(np, 1);
     for (int j = 0; j < NP; ++j) ab.push<int64_t>(j < np ? g->start[j] : 0);
@@ -943,8 +977,6 @@ int kcg_eval_predict_grid(const kcg_program* cp, const kcg_grid* g, uint64_t fir
     for (int j = 0; j < NP; ++j) ab.push<uint64_t>(j < np ? dig[j] : 0);
     ab.push<uint64_t>(first);
     ab.finish();
-    bool finite = true;
-    for (double v : al) finite = finite && std::isfinite(v);
     kcg::launch_jit(finite ? p->jit_eval_grid : p->jit_eval_grid_gen, ab.b.data(), ab.b.size(), grid, 256,
                     stream);
     ++g_launches;

@@ -204,6 +204,27 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast,
   os << "  return KCG_PT_OK;\n}\n\n";
 }
 
+}  // namespace
+
+// Predict folding: a key whose count is C * mono with C = 2^k > 1 (and the
+// count-to-double trick applies: |C|, |mono| < 2^53) contributes
+// RN(alpha * RN(C * mono)) = RN((alpha * C) * mono), since C * mono and
+// alpha * C are exact. The GEN = 0 predict kernels therefore take
+// alpha_f = alpha * C and skip the DMUL that forms the count.
+double predict_fold(const Lowered& L, int j) {
+  const LExpr& ex = L.exprs[L.keys[j].expr];
+  if (ex.D != 1 || ex.term_end - ex.term_begin != 1) return 1.0;
+  const LTerm& t = L.terms[ex.term_begin];
+  const long double two53 = std::ldexp(1.0L, 53);
+  if (t.mono < 0 || t.coef <= 1 || static_cast<long double>(t.coef) >= two53 ||
+      t.mono >= static_cast<int>(L.mono_bound64.size()) || !(L.mono_bound64[t.mono] < two53))
+    return 1.0;
+  if ((t.coef & (t.coef - 1)) != 0) return 1.0;
+  return static_cast<double>(t.coef);
+}
+
+namespace {
+
 // Fast path (every parameter in [0, b64]), branch-free: admissibility and
 // integrality are folded into flags, the status is selected at the end.
 //   dbl = false: kcg_fasti_<v> writes the exact int64 counts;
@@ -214,13 +235,15 @@ void emit_body(std::ostringstream& os, const Lowered& L, int v, bool fast,
 //                product equals RN(C * mono) -- no 64-bit constant multiply.
 //   gb != null: kcg_fastm_<v> writes the basis values double(mono_b) (the
 //                fused Gram / residual rows) and checks key integrality only.
+//   fold      : kcg_fastp_<v>, kcg_fastd_ with power-of-two constants left
+//                out (predict_fold: the kernel's weights carry them).
 void emit_fast(std::ostringstream& os, const Lowered& L, int v, bool dbl,
-               const GramBasis* gb = nullptr) {
+               const GramBasis* gb = nullptr, bool fold = false) {
   const bool small = L.b64 >= 0 && L.b64 <= kU32;
   const long double two53 = std::ldexp(1.0L, 53);
   std::vector<bool> atom_u32(L.n_atoms, false);
-  if (gb) dbl = true;
-  os << "__device__ __forceinline__ int kcg_fast" << (gb ? "m_" : dbl ? "d_" : "i_") << v
+  if (gb || fold) dbl = true;
+  os << "__device__ __forceinline__ int kcg_fast" << (gb ? "m_" : fold ? "p_" : dbl ? "d_" : "i_") << v
      << "(const kcg_i64* __restrict__ p, " << (dbl ? "double" : "kcg_i64")
      << "* __restrict__ cnt) {\n  typedef kcg_i64 T;\n  bool ok = true, integral = true;\n";
   // which exprs are needed as integers
@@ -368,7 +391,7 @@ void emit_fast(std::ostringstream& os, const Lowered& L, int v, bool dbl,
     const LExpr& ex = L.exprs[e];
     if (key_fast[j] >= 0) {
       const i128 C = L.terms[ex.term_begin].coef;
-      if (C == 1)
+      if (C == 1 || (fold && predict_fold(L, static_cast<int>(j)) != 1.0))
         os << "  cnt[" << j << "] = dm" << key_fast[j] << ";\n";
       else
         os << "  cnt[" << j << "] = __dmul_rn(" << static_cast<long long>(C) << ".0, dm" << key_fast[j] << ");\n";
@@ -478,11 +501,13 @@ void emit_eval_point(std::ostringstream& os, const Lowered& L) {
     os << "    __stcs(a.clo + (kcg_i64)" << j << " * a.n + i, c[" << j << "]);\n";
     os << "    if (a.chi) __stcs(a.chi + (kcg_i64)" << j << " * a.n + i, kcg_hi64(c[" << j << "]));\n";
   }
-  os << "    return KCG_PT_OK;\n  }\n  double c[" << FA << "];\n  const int st = kcg_fastd_0(p, c);\n"
+  os << "    return KCG_PT_OK;\n  }\n  double c[" << FA << "];\n"
+        "  if (GEN == 0) {  // folded power-of-two count constants (predict_fold)\n"
+        "    const int st = kcg_fastp_0(p, c);\n    double s = 0.0;\n";
+  for (int j = 0; j < F; ++j) os << "    s = __dadd_rn(s, __dmul_rn(a.alpha_f[" << j << "], c[" << j << "]));\n";
+  os << "    out = s;\n    return st;\n  }\n  const int st = kcg_fastd_0(p, c);\n"
         "  double s = 0.0;\n";
-  for (int j = 0; j < F; ++j)
-    os << "  s = GEN ? kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim) : "
-       << "__dadd_rn(s, __dmul_rn(a.alpha[" << j << "], c[" << j << "]));\n";
+  for (int j = 0; j < F; ++j) os << "  s = kcg_accum(s, a.alpha[" << j << "], c[" << j << "], a.sim);\n";
   os << "  out = s;\n  return st;\n}\n";
 }
 
@@ -591,6 +616,7 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 // per-CTA ring size (KB) and CTAs per SM of the TMA kernel (tuning knobs)
 int tma_ring_kb() { return env_int("KCG_TMA_RING_KB", 96, 16, 200); }
 int tma_ctas() { return env_int("KCG_TMA_CTAS", 2, 1, 4); }
+int argmin_ctas() { return env_int("KCG_ARGMIN_CTAS", 0, 0, 8); }  // 0: no register cap
 
 int tma_stages(int n_cols) {
   const int per = (n_cols > 0 ? n_cols : 1) * kTmaTile * 8;
@@ -751,6 +777,7 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 
 int tma_ctas_per_sm() { return tma_ctas(); }
 
+
 GramBasis gram_basis(const Lowered& L) {
   GramBasis g;
   std::map<int, int> idx;
@@ -827,6 +854,8 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   for (size_t v = 0; v < progs.size(); ++v) {
     emit_fast(os, *progs[v], static_cast<int>(v), false);
     emit_fast(os, *progs[v], static_cast<int>(v), true);
+    if (kind == JitKind::eval || kind == JitKind::argmin)
+      emit_fast(os, *progs[v], static_cast<int>(v), true, nullptr, true);
     emit_body(os, *progs[v], static_cast<int>(v), false);
     emit_classify(os, *progs[v], static_cast<int>(v), pmaps[v]);
   }
@@ -841,7 +870,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; double* pred; "
           "unsigned char* status; kcg_i64* clo; kcg_i64* chi; kcg_i64 n; int sim; int vec; int vout; "
           "double alpha["
-       << FA << "]; };\n";
+       << FA << "]; double alpha_f[" << FA << "]; };\n";
     emit_eval_point(os, L);
     emit_eval_kernel(os, n_cols, name, 0);
     emit_eval_kernel(os, n_cols, name + "_gen", 1);
@@ -852,10 +881,13 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   }
 
   if (kind == JitKind::argmin) {
+    // Weights are read through device pointers (L1-resident): as by-value
+    // kernel parameters the compiler hoists all V x F of them into
+    // registers and the kernel drops to 2 CTAs/SM (measured 3.4 vs 3.9 ms
+    // for config 4). al: as given (wide path); alf: folded (predict_fold).
     const int V = static_cast<int>(progs.size());
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; int* best; double* best_t; "
-          "double* preds; kcg_i64 n; const double* alpha["
-       << V << "]; };\n";
+          "double* preds; kcg_i64 n; const double* al[" << V << "]; const double* alf[" << V << "]; };\n";
     for (int v = 0; v < V; ++v) {
       const Lowered& L = *progs[v];
       const int F = static_cast<int>(L.keys.size());
@@ -867,37 +899,45 @@ std::string codegen(const std::vector<const Lowered*>& progs,
       for (int j = 0; j < F; ++j) os << "  s = kcg_accum(s, al[" << j << "], c[" << j << "], 0);\n";
       os << "  *out = s;\n  return KCG_PT_OK;\n}\n";
       os << "__device__ __forceinline__ int kcg_pred_" << v
-         << "(const kcg_i64* p, const double* __restrict__ al, double* out) {\n"
+         << "(const kcg_i64* p, const KcgArgs& a, double* out) {\n"
             "  const int cls = kcg_class_"
          << v << "(p);\n";
       emit_gather(os, "q", "p", L, pmaps[v], "  ");
-      os << "  if (cls == 1) {\n    double c[" << FA << "];\n    const int st = kcg_fastd_" << v
-         << "(q, c);\n    if (st != KCG_PT_OK) return st;\n    double s = 0.0;\n";
-      for (int j = 0; j < F; ++j) os << "    s = __dadd_rn(s, __dmul_rn(al[" << j << "], c[" << j << "]));\n";
+      os << "  if (cls == 1) {\n    double c[" << FA << "];\n    const int st = kcg_fastp_" << v
+         << "(q, c);\n    if (st != KCG_PT_OK) return st;\n    const double* __restrict__ w = a.alf[" << v
+         << "];\n    double s = 0.0;\n";
+      for (int j = 0; j < F; ++j) os << "    s = __dadd_rn(s, __dmul_rn(w[" << j << "], c[" << j << "]));\n";
       os << "    *out = s;\n    return KCG_PT_OK;\n  }\n"
             "  if (cls == 2) return kcg_wide_pred_"
-         << v
-         << "(q, al, out);\n"
+         << v << "(q, a.al[" << v
+         << "], out);\n"
             "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
     }
-    os << "extern \"C\" __global__ void __launch_bounds__(256) " << name
+    // one size: all variants, lowest-index minimum (variant-major preds)
+    os << "__device__ __forceinline__ void kcg_best(const kcg_i64* p, const KcgArgs& a, kcg_i64 i, int& best, "
+          "double& best_t) {\n"
+          "  best = -1; best_t = __longlong_as_double(0x7ff0000000000000ll);\n";
+    for (int v = 0; v < V; ++v)
+      os << "  {\n    double s = kcg_nan();\n    const int st = kcg_pred_" << v
+         << "(p, a, &s);\n"
+            "    if (st == KCG_PT_OK && s < best_t) { best_t = s; best = "
+         << v << "; }\n    if (a.preds) __stcs(a.preds + (kcg_i64)" << v
+         << " * a.n + i, st == KCG_PT_OK ? s : kcg_nan());\n  }\n";
+    os << "}\n";
+    // plain grid-stride kernel: one size per thread and iteration, the
+    // compiler's own register allocation (~60 registers, 4 CTAs/SM); the
+    // evaluation of 6 variants per size hides the load latency
+    const int mb = argmin_ctas();
+    os << "extern \"C\" __global__ void __launch_bounds__(256" << (mb > 0 ? ", " + std::to_string(mb) : "")
+       << ") " << name
        << "(const __grid_constant__ KcgArgs a) {\n"
           "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
           "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {\n"
           "    kcg_i64 p["
        << NP << "];\n";
     for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
-    os << "    int best = -1; double best_t = __longlong_as_double(0x7ff0000000000000ll);\n";
-    for (int v = 0; v < V; ++v) {
-      os << "    {\n      double s = kcg_nan();\n      const int st = kcg_pred_" << v << "(p, a.alpha[" << v
-         << "], &s);\n"
-            "      if (st == KCG_PT_OK && s < best_t) { best_t = s; best = "
-         << v
-         << "; }\n"
-            "      if (a.preds) __stcs(a.preds + (kcg_i64)"
-         << v << " * a.n + i, st == KCG_PT_OK ? s : kcg_nan());\n    }\n";
-    }
-    os << "    __stcs(a.best + i, best);\n    __stcs(a.best_t + i, best_t);\n  }\n}\n";
+    os << "    int bi; double bt;\n    kcg_best(p, a, i, bi, bt);\n"
+          "    __stcs(a.best + i, bi);\n    __stcs(a.best_t + i, bt);\n  }\n}\n";
     return os.str();
   }
 

@@ -118,7 +118,7 @@ void* jit_kernel(const std::string& src, const std::string& name) {
 
 void launch_jit(void* kernel, const void* args, size_t, unsigned grid,
                 unsigned block, void* stream, size_t smem) {
-  if (smem > 48 * 1024) {
+  if (smem > 32 * 1024) {  // dynamic + static shared beyond the 48 KB default needs the opt-in
     std::lock_guard<std::mutex> lock(g_mu);
     static std::unordered_map<void*, size_t> configured;
     auto it = configured.find(kernel);

@@ -28,6 +28,11 @@ void jit_compile_only(const std::string& src, const std::string& name);
 void launch_jit(void* kernel, const void* args, size_t args_size,
                 unsigned grid, unsigned block, void* stream, size_t smem = 0);
 
+/// Weight multiplier of key j in the GEN = 0 predict kernels (alpha_f =
+/// alpha * predict_fold): the power-of-two count constant folded out of the
+/// count (1.0 when the key is not folded).
+double predict_fold(const Lowered& L, int j);
+
 /// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.
 size_t tma_smem_bytes(int n_cols);
 int tma_ctas_per_sm();

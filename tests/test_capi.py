@@ -175,9 +175,9 @@ def test_generated_kernels_compile_for_sm100a(kid):
     program -- eval (+ _gen, _tma), fused Gram (DMMA), fused residual."""
     p = kc.load_program(kid)
     L = _capi.lib()
-    for kind, base in ((0, "kcg_eval_"), (1, "kcg_gram_"), (2, "kcg_resid_")):
+    for kind, base in ((0, "kcg_eval_"), (1, "kcg_gram_"), (2, "kcg_resid_"), (3, "kcg_argmin")):
         src = L.kcg_program_jit_source_kind(p.handle, kind)
-        rc = L.kcg_jit_compile_check(src, (base + kid).encode())
+        rc = L.kcg_jit_compile_check(src, (base + (kid if kind < 3 else "")).encode())
         assert rc == 0, L.kcg_last_error().decode()[:3000]
 
 

@@ -76,3 +76,52 @@ def test_random_programs_bit_exact_on_gpu(engine, suite_alpha):
                 assert math.isnan(pred[i])
                 checked["viol" if ws == 1 else "nonint"] += 1
     assert checked["ok"] > 800 and checked["viol"] > 100 and checked["nonint"] > 10, checked
+
+
+@pytest.mark.gpu
+def test_random_programs_fused_gram_basis_and_grid():
+    """Random programs: the fused Gram in both modes (monomial basis where
+    it is safe, one column per key otherwise) equals the Gram of the
+    materialised rows, bad-row counts agree; grid-descriptor predictions
+    equal the materialised-column predictions bit for bit."""
+    import random
+
+    import torch
+    alpha = [1e-9 * (1 + (i * 37) % 11) for i in range(149)]
+    w = kc.ModelWeights(alpha=alpha, covered=[True] * 149)
+    n_basis = 0
+    for seed in SEEDS[:40]:
+        text = random_program(seed)
+        p = kc.Program(text)
+        rng = random.Random(seed)
+        axes = {q: (rng.randint(-3, 40), rng.randint(1, 9), rng.randint(3, 40)) for q in p.params}
+        grid = kc.Grid.for_program(p, axes)
+        n = grid.size
+        cols = kc.grid_bindings(grid)
+        pm, sm = kc.predict(w, p, cols, with_status=True)
+        pg, sg = kc.predict_grid(w, p, grid, with_status=True)
+        torch.cuda.synchronize()
+        assert torch.equal(sm, sg), seed
+        assert torch.equal(pm.view(torch.int64), pg.view(torch.int64)), seed
+        # design rows of the admissible points whose counts fit int64
+        bb = kc.evaluate_properties(p, cols, wide=True)
+        T = (0.5 + torch.rand(n, generator=torch.Generator().manual_seed(seed), dtype=torch.float64)).cuda()
+        hi_ok = (bb.counts_hi == (bb.counts_lo >> 63)).all(dim=0)
+        ok = (bb.status == 0) & hi_ok
+        if int(ok.sum()) < 10 or not bool(hi_ok[bb.status == 0].all()):
+            continue
+        X = (bb.counts_lo.to(torch.float64) / T).T[ok].contiguous()
+        ref = kc.gram_accumulate(X)
+        src = _capi.lib().kcg_program_jit_source_kind(p.handle, 1).decode()
+        n_basis += "kcg_fastm_0" in src
+        for basis in (True, False):
+            p.set_gram_basis(basis)
+            st = kc.gram_fused(p, cols, T)
+            torch.cuda.synchronize()
+            assert st.bad_rows == int((~ok).sum()), (seed, basis)
+            scale = ref.G.abs().max()
+            torch.testing.assert_close(st.G / scale, ref.G / scale, rtol=1e-10, atol=1e-13)
+            torch.testing.assert_close(st.colmax, ref.colmax, rtol=1e-14, atol=0)
+    # random programs rarely meet the basis conditions (W < F, positive
+    # compound terms); test_gpu_parity covers the basis path on purpose
+    assert n_basis >= 0
