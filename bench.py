@@ -405,8 +405,20 @@ def _e2e(kc, progs, w, args, torch, dev, world, rank):
     sec = (time.perf_counter() - t0) / reps
     h2d = 3 * 8 * n
     d2h = 8 * n * len(progs)
+    # the bound: a plain pinned D2H copy of the same size class on this box
+    del dcols, dpred
+    probe = torch.empty(1 << 27, dtype=torch.float64, device=dev)
+    hp = torch.empty(1 << 27, dtype=torch.float64).pin_memory()
+    hp.copy_(probe)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    for _ in range(3):
+        hp.copy_(probe, non_blocking=True)
+    torch.cuda.synchronize()
+    d2h_bw = 3 * 8 * (1 << 27) / (time.perf_counter() - t1)
     return {"value": n * len(progs) / sec, "unit": "points/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3,
+            "pcie_d2h_GBps_measured": d2h_bw / 1e9, "d2h_frac_of_measured": d2h / sec / d2h_bw,
             "note": "pinned host SoA bindings -> kcg_eval_predict (6 variants) -> pinned host predictions; "
                     "2 streams, 8M-size chunks; wall clock incl. all copies"}
 
