@@ -365,7 +365,8 @@ def _e2e(kc, progs, w, args, torch, dev, world, rank):
     import ctypes
     total = args.side ** 3
     n = total // world
-    chunk = 1 << 23
+    chunk = 1 << 22
+    nstreams = 3
     host_cols = {}
     idx = torch.arange(0, n, dtype=torch.int64)
     s2 = args.side * args.side
@@ -374,16 +375,16 @@ def _e2e(kc, progs, w, args, torch, dev, world, rank):
     host_cols["l"] = ((idx % args.side + 1) * UNIT).pin_memory()
     del idx
     host_pred = torch.empty((len(progs), n), dtype=torch.float64).pin_memory()
-    streams = [torch.cuda.Stream(dev) for _ in range(2)]
-    dcols = [{k: torch.empty(chunk, dtype=torch.int64, device=dev) for k in "nml"} for _ in range(2)]
-    dpred = [torch.empty((len(progs), chunk), dtype=torch.float64, device=dev) for _ in range(2)]
+    streams = [torch.cuda.Stream(dev) for _ in range(nstreams)]
+    dcols = [{k: torch.empty(chunk, dtype=torch.int64, device=dev) for k in "nml"} for _ in range(nstreams)]
+    dpred = [torch.empty((len(progs), chunk), dtype=torch.float64, device=dev) for _ in range(nstreams)]
     alpha = w.alpha_array()
     arrs = [{id(p): (ctypes.c_void_p * 3)(*[dcols[b][q].data_ptr() for q in p.params]) for p in progs}
-            for b in range(2)]
+            for b in range(nstreams)]
 
     def one():
         for c0 in range(0, n, chunk):
-            b = (c0 // chunk) % 2
+            b = (c0 // chunk) % nstreams
             s = streams[b]
             m = min(chunk, n - c0)
             with torch.cuda.stream(s):
@@ -420,7 +421,7 @@ def _e2e(kc, progs, w, args, torch, dev, world, rank):
             "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3,
             "pcie_d2h_GBps_measured": d2h_bw / 1e9, "d2h_frac_of_measured": d2h / sec / d2h_bw,
             "note": "pinned host SoA bindings -> kcg_eval_predict (6 variants) -> pinned host predictions; "
-                    "2 streams, 8M-size chunks; wall clock incl. all copies"}
+                    f"{nstreams} streams, {chunk >> 20}M-size chunks; wall clock incl. all copies"}
 
 
 def _sharded_fit(kc, torch, dev, world, rank, rows):
@@ -521,6 +522,44 @@ def _extras(kc, torch, dev, args):
     w = kc.ModelWeights(device="simdev-v1", alpha=sim_alpha, covered=[a != 0 for a in sim_alpha])
     stream = torch.cuda.current_stream(dev).cuda_stream
 
+    # ---- config 1: the reference's own campaign CSV (390 measurement cases,
+    # simdev-v1, sigma 0) -> fit -> predict the 16 test cases (suite.cpp
+    # test sizes, incl. fd_stencil n=512 and nbody n=2048) on the GPU; the
+    # reference CLI path (campaign + bound extraction + fit + eval) beside it
+    golden = ROOT / "tests" / "golden"
+    tests = json.loads((golden / "fit_suite.json").read_text())["test_predictions"]
+    tprogs = {t["kernel"]: kc.load_program(t["kernel"]) for t in tests}
+
+    def c1():
+        wf, rep = kc.fit_from_csv(golden / "meas_sigma0.csv", device="simdev-v1")
+        outp = []
+        for t in tests:
+            p = tprogs[t["kernel"]]
+            outp.append(kc.predict(wf, p, {q: torch.tensor([int(t["binding"][q])], dtype=torch.int64, device=dev)
+                                           for q in p.params}))
+        torch.cuda.synchronize()
+        return wf, rep, outp
+    c1()
+    t0 = time.perf_counter()
+    wf, rep, outp = c1()
+    sec1 = time.perf_counter() - t0
+    rel = max(abs(float(o.item()) - float.fromhex(t["predicted_s"][1])) / abs(float.fromhex(t["predicted_s"][1]))
+              for o, t in zip(outp, tests))
+    ref1 = None
+    exe = ROOT / "oracle" / "_ref" / "kcref_bench"
+    if exe.exists():
+        try:
+            ref1 = json.loads(subprocess.run([str(exe), "config1"], capture_output=True, text=True,
+                                             timeout=300).stdout)
+        except Exception as e:  # noqa: BLE001
+            ref1 = {"error": str(e)[:200]}
+    out["config1_suite_fit_eval"] = {
+        "cases": rep["n_cases"], "test_cases": len(tests), "gpu_ms": sec1 * 1e3,
+        "max_rel_diff_test_predictions_vs_reference": rel, "cpu_reference": ref1,
+        "note": "GPU: kcg_measurements_read_csv + per-kernel fused Gram + solve + residual + 16 predictions "
+                "(wall clock, ~70 launches); CPU: the reference's run_campaign + extract_properties (bound, "
+                "cap 2e7) + fit_weights + predict, 1 thread"}
+
     # ---- config 2: 1e6 points over the 4 test kernels (250k each) ----------
     U = 250_000
     u = torch.arange(1, U + 1, dtype=torch.int64, device=dev)
@@ -539,9 +578,19 @@ def _extras(kc, torch, dev, args):
             kc.api.check(kc.api.lib().kcg_eval_predict(p.handle, arr, U, w.alpha_array(), out.data_ptr(),
                                                        None, None, None, 0, stream))
     sec = _timed(torch, c2, reps=20)
+    # the same 4 launches replayed from a CUDA graph (the C ABI launches are
+    # capturable once the kernels are specialised): launch overhead removed
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2):
+        c2_stream = torch.cuda.current_stream(dev).cuda_stream
+        for p, _, arr, o in launches:
+            kc.api.check(kc.api.lib().kcg_eval_predict(p.handle, arr, U, w.alpha_array(), o.data_ptr(),
+                                                       None, None, None, 0, c2_stream))
+    sec_g = _timed(torch, g2.replay, reps=50)
     b64, _ = launches[0][0].safe_bounds()
     out["config2_suite_1e6"] = {
         "points": 4 * U, "ms": sec * 1e3, "points_per_s": 4 * U / sec, "launches": 4,
+        "graph_ms": sec_g * 1e3, "graph_points_per_s": 4 * U / sec_g,
         "note": "skinny (16u,128u,16u), conv 16u, fd_stencil 16u, nbody 256u, u=1..250000; skinny counts "
                 f"reach 5.8e20 (int128 path for n > {b64}); fd_stencil / nbody use the derived programs "
                 "(SURVEY 8f row 1); latency-bound (4 launches)"}

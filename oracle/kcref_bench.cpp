@@ -16,11 +16,18 @@
 //       synthetic FitCases (counts U{1..10000}, seed 4242, T = sum alpha c
 //       over the 16 simdev-v1 weights + log-uniform extras), then
 //       build_design_matrix + fit_weights (model.cpp:11-93); rows/s
+//   kcref_bench config1
+//       config 1 through the reference API, as the CLI runs it: the
+//       simulate campaign over the 390 measurement cases (run_campaign,
+//       sigma 0), fit (bound extract_properties per record,
+//       build_design_matrix, fit_weights), eval of the 16 test cases
+//       (extract + predict); seconds per phase, 1 thread
 //   kcref_bench enumerate <kernel_id> <n>
 //       enumerate_points (enumerate.cpp:371-456) at the binding n (every
 //       parameter = n), single-threaded like the reference; visited points/s
 // Prints one JSON object: points, seconds, points_per_s, threads, checksum.
 #include <atomic>
+#include <map>
 #include <cmath>
 #include <random>
 #include <chrono>
@@ -30,6 +37,7 @@
 #include <thread>
 #include <vector>
 
+#include "kernelcost/campaign.hpp"
 #include "kernelcost/enumerate.hpp"
 #include "kernelcost/model.hpp"
 #include "kernelcost/parser.hpp"
@@ -49,11 +57,43 @@ struct Kern {
 }  // namespace
 
 int main(int argc, char** argv) {
-  if (argc < 4) {
-    std::fprintf(stderr, "usage: kcref_bench autotune|suite <threads> <n> [offset]\n");
+  if (argc < 4 && !(argc == 2 && std::string(argv[1]) == "config1")) {
+    std::fprintf(stderr, "usage: kcref_bench autotune|suite <threads> <n> [offset] | config1 | fit <rows> <cols> | enumerate <id> <n>\n");
     return 2;
   }
   const std::string mode = argv[1];
+  if (mode == "config1") {
+    using clk = std::chrono::steady_clock;
+    const kc::SuiteLibrary lib = kc::build_suite();
+    const kc::SimDevice dev = kc::SimDevice::reference();
+    const kc::Int cap(20000000);
+    const auto t0 = clk::now();
+    const kc::CampaignResult cr = kc::run_campaign(dev, lib, lib.measurement_cases(), cap);
+    const auto t1 = clk::now();
+    std::map<std::string, kc::KernelIR> irs;
+    auto ir = [&](const std::string& id) -> const kc::KernelIR& {
+      auto it = irs.find(id);
+      if (it == irs.end()) it = irs.emplace(id, kc::parse_kernel(lib.find(id)->text)).first;
+      return it->second;
+    };
+    std::vector<kc::FitCase> cases;
+    for (const auto& r : cr.records) cases.push_back({kc::extract_properties(ir(r.kernel), r.binding, cap), r.time_s});
+    const kc::DesignMatrix d = kc::build_design_matrix(cases);
+    auto [w, rep] = kc::fit_weights(d, dev.name);
+    const auto t2 = clk::now();
+    double acc = 0;
+    int n_eval = 0;
+    for (const auto& c : lib.test_cases()) {
+      acc += kc::predict(w, kc::extract_properties(ir(c.kernel_id), c.binding, cap)).seconds;
+      ++n_eval;
+    }
+    const auto t3 = clk::now();
+    auto s = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+    std::printf("{\"cases\": %zu, \"test_cases\": %d, \"simulate_s\": %.6f, \"fit_s\": %.6f, \"eval_s\": %.6f, "
+                "\"total_s\": %.6f, \"objective\": %.6g, \"checksum\": %.17g, \"threads\": 1}\n",
+                cr.records.size(), n_eval, s(t0, t1), s(t1, t2), s(t2, t3), s(t0, t3), rep.objective, acc);
+    return 0;
+  }
   if (mode == "fit") {
     const long rows = std::atol(argv[2]);
     const int F = std::atoi(argv[3]);
