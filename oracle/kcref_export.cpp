@@ -21,6 +21,7 @@
 #include <fstream>
 #include <iostream>
 #include <random>
+#include <sstream>
 #include <tuple>
 
 #include "json.hpp"
@@ -78,7 +79,61 @@ const kc::Int kCap(20000000);
 
 }  // namespace
 
+// kcref_export --enum-kernels <kernels.txt> <out.json>: enum_text and the
+// reference's enumerate_points at small bindings for every kernel text of
+// the file (separated by "----" lines; tests/gen/gen_enum_kernels.py)
+int enum_kernels(const std::string& in, const std::string& out) {
+  std::ifstream f(in);
+  std::stringstream ss;
+  ss << f.rdbuf();
+  const std::string all = ss.str();
+  std::vector<std::string> texts;
+  size_t b = 0;
+  while (b < all.size()) {
+    size_t e = all.find("\n----\n", b);
+    texts.push_back(all.substr(b, e == std::string::npos ? std::string::npos : e - b + 1));
+    if (e == std::string::npos) break;
+    b = e + 6;
+  }
+  json ks = json::array();
+  int n_ok = 0;
+  for (const auto& text : texts) {
+    json ke;
+    try {
+      const kc::KernelIR k = kc::parse_kernel(text);
+      ke["id"] = k.name;
+      ke["enum_text"] = kcref::enum_text(k);
+      json cases = json::array();
+      const bool two = k.params.size() == 2;
+      for (long n : {0L, 1L, 2L, 3L, 5L, 8L, 13L, 20L})
+        for (long m : two ? std::vector<long>{1L, 4L, 9L} : std::vector<long>{0L}) {
+          kc::Binding bd{{"n", kc::Int(n)}};
+          if (two) bd["m"] = kc::Int(m);
+          json e{{"binding", binding_json(bd)}};
+          try {
+            const kc::EnumTally t = kc::enumerate_points(k, bd, kCap);
+            e["status"] = "ok";
+            e["counts"] = pv_json(t.props);
+            e["points"] = t.points.str();
+          } catch (const kc::Error& err) {
+            e["status"] = kc::errc_name(err.code());
+          }
+          cases.push_back(e);
+        }
+      ke["cases"] = cases;
+      ++n_ok;
+    } catch (const std::exception& err) {
+      ke["error"] = err.what();
+    }
+    ks.push_back(ke);
+  }
+  write(out, json{{"kernels", ks}});
+  std::cerr << "enum kernels: " << n_ok << "/" << texts.size() << " parsed\n";
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc == 4 && std::string(argv[1]) == "--enum-kernels") return enum_kernels(argv[2], argv[3]);
   if (argc < 3) {
     std::cerr << "usage: kcref_export <programs_dir> <golden_dir>\n";
     return 2;

@@ -114,3 +114,39 @@ def test_enumerate_equals_symbolic_beyond_cpu_cap(kid, b):
     counts, points = kc.load_enum_program(kid).enumerate_points(b)
     assert points > 0
     assert counts == _symbolic_counts(kid, b)
+
+
+def _random_kernels():
+    return [k for k in load_golden("enum_random.json")["kernels"] if "cases" in k]
+
+
+def test_random_kernel_enum_texts_parse():
+    ks = _random_kernels()
+    assert len(ks) == 120
+    for k in ks:
+        kc.EnumProgram(k["enum_text"])
+
+
+@pytest.mark.gpu
+def test_enumerate_random_kernels_match_reference():
+    """120 random kernels (tests/gen/gen_enum_kernels.py: parametric and
+    triangular loop nests, relational / divisibility / lane guards, 1-3D
+    arrays in both layouts, strided and offset indices, local arrays,
+    barriers) x up to 24 bindings: counts, visited points and errors equal
+    the reference's enumerate_points (tests/golden/enum_random.json)."""
+    n_ok = 0
+    for k in _random_kernels():
+        p = kc.EnumProgram(k["enum_text"])
+        for c in k["cases"]:
+            b = {q: int(v) for q, v in c["binding"].items()}
+            if c["status"] != "ok":
+                with pytest.raises(kc.KcgError) as e:
+                    p.enumerate_points(b)
+                assert e.value.name == c["status"], (k["id"], b)
+                continue
+            counts, points = p.enumerate_points(b)
+            want = {key: int(v) for key, v in c["counts"].items()}
+            assert counts == want, (k["id"], b, counts, want)
+            assert points == int(c["points"]), (k["id"], b, points, c["points"])
+            n_ok += 1
+    assert n_ok > 1500
