@@ -353,9 +353,13 @@ const char* kcg_program_jit_source(kcg_program* p) {
 }
 
 const char* kcg_program_jit_source_kind(kcg_program* p, int kind) {
-  if (!p || kind < 0 || kind > 3) return nullptr;
+  if (!p || kind < 0 || kind > 4) return nullptr;
   if (kind == 0) return kcg_program_jit_source(p);
   const int np = p->low.n_params;
+  if (kind == 4) {  // the evaluator as host C++ (kcg_host_eval), e.g. for a CPU baseline
+    p->jit_src_kind = kcg::codegen({&p->low}, {identity(np)}, np, kcg::JitKind::host_eval, "kcg_host_eval");
+    return p->jit_src_kind.c_str();
+  }
   if (kind == 3) {  // argmin over this single variant
     p->jit_src_kind = kcg::codegen({&p->low}, {identity(np)}, np, kcg::JitKind::argmin, "kcg_argmin");
     return p->jit_src_kind.c_str();

@@ -850,18 +850,54 @@ std::string codegen(const std::vector<const Lowered*>& progs,
                     const std::vector<std::vector<int>>& pmaps, int n_cols, JitKind kind,
                     const std::string& name) {
   std::ostringstream os;
+  if (kind == JitKind::host_eval)  // the same evaluator compiled for the host CPU (g++ -ffp-contract=off)
+    os << "// host build of the lowered program (baseline / cross-check)\n"
+          "#include <cmath>\n#include <cstring>\nusing std::scalbn;\n"
+          "#define __device__\n#define __forceinline__ inline __attribute__((always_inline))\n"
+          "#define __noinline__ __attribute__((noinline))\n"
+          "static inline double __dmul_rn(double a, double b) { return a * b; }\n"
+          "static inline double __dadd_rn(double a, double b) { return a + b; }\n"
+          "static inline double __ll2double_rn(long long x) { return (double)x; }\n"
+          "static inline double __ull2double_rn(unsigned long long x) { return (double)x; }\n"
+          "static inline int __clzll(long long x) { return x ? __builtin_clzll((unsigned long long)x) : 64; }\n"
+          "static inline double __longlong_as_double(long long x) { double d; std::memcpy(&d, &x, 8); return d; }\n"
+          "template <class T> static inline void __stcs(T* p, T v) { *p = v; }\n"
+          "template <class T> static inline T __ldcs(const T* p) { return *p; }\n";
   os << "// generated by kcg codegen\n" << kDeviceHelpers << "\n";
   for (size_t v = 0; v < progs.size(); ++v) {
     emit_fast(os, *progs[v], static_cast<int>(v), false);
     emit_fast(os, *progs[v], static_cast<int>(v), true);
-    if (kind == JitKind::eval || kind == JitKind::argmin)
+    if (kind == JitKind::eval || kind == JitKind::argmin || kind == JitKind::host_eval)
       emit_fast(os, *progs[v], static_cast<int>(v), true, nullptr, true);
     emit_body(os, *progs[v], static_cast<int>(v), false);
     emit_classify(os, *progs[v], static_cast<int>(v), pmaps[v]);
   }
-  if (kind == JitKind::eval && progs[0]->admit)
+  if ((kind == JitKind::eval || kind == JitKind::host_eval) && progs[0]->admit)
     emit_body(os, *progs[0]->admit, 0, false, "kcg_admit_");
   const int NP = n_cols > 0 ? n_cols : 1;
+
+  if (kind == JitKind::host_eval) {
+    const Lowered& L = *progs[0];
+    const int FA = std::max<int>(1, static_cast<int>(L.keys.size()));
+    os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; double* pred; "
+          "unsigned char* status; kcg_i64* clo; kcg_i64* chi; kcg_i64 n; int sim; int vec; int vout; "
+          "double alpha["
+       << FA << "]; double alpha_f[" << FA << "]; };\n";
+    emit_eval_point(os, L);
+    // points [begin, end): kcg_eval_predict semantics (general weights path)
+    os << "extern \"C\" void " << name
+       << "(const KcgArgs* ap, long long begin, long long end) {\n"
+          "  const KcgArgs& a = *ap;\n"
+          "  for (long long i = begin; i < end; ++i) {\n"
+          "    kcg_i64 p["
+       << NP << "];\n";
+    for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = a.p[" << j << "][i];\n";
+    os << "    double s = kcg_nan();\n    int st = kcg_point_fast<1>(p, a, i, s);\n"
+          "    if (st < 0) { const KcgRes r = kcg_point_slow(a, i); s = r.s; st = r.st; }\n"
+          "    if (st != KCG_PT_OK && st != KCG_PT_COUNT_WIDE) s = kcg_nan();\n"
+          "    if (a.pred) a.pred[i] = s;\n    if (a.status) a.status[i] = (unsigned char)st;\n  }\n}\n";
+    return os.str();
+  }
 
   if (kind == JitKind::eval) {
     const Lowered& L = *progs[0];

@@ -8,7 +8,7 @@
 
 namespace kcg {
 
-enum class JitKind { eval, argmin, gram, residual };
+enum class JitKind { eval, argmin, gram, residual, host_eval };
 
 /// CUDA source for one specialised kernel named `name`. pmaps[v][j] is the
 /// column (in the launch's parameter-column order) holding parameter j of

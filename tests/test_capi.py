@@ -227,3 +227,36 @@ def test_measurement_csv_errors(tmp_path):
     with pytest.raises(kc.KcgError) as e:
         kc.read_measurements(tmp_path / "missing.csv")
     assert e.value.code == _capi.E_IO
+
+
+def test_host_build_of_generated_evaluator_matches_goldens():
+    """The generated evaluator compiled for the host (source kind 4, g++
+    -ffp-contract=off) reproduces the reference's golden grid samples bit for
+    bit -- counts beyond 2^64 included: a CPU-side check of the code
+    generator. (Baseline/cross-check tooling only; the package never falls
+    back to it.)"""
+    import collections
+
+    import numpy as np
+
+    from paper_1604_04997_b200.hostbuild import HostEvaluator
+    d = load_golden("grid_samples.json")["samples"]
+    fit = load_golden("fit_suite.json")
+    alpha = [0.0] * 149
+    for k, v in fit["alpha"].items():
+        alpha[ko.SCHEMA_INDEX[k]] = hexf(v[1])
+    by = collections.defaultdict(list)
+    for s in d:
+        by[s["kernel"]].append(s)
+    checked = 0
+    for kid, ss in by.items():
+        p = kc.load_program(kid)
+        pred, st = HostEvaluator(p).predict(alpha, {q: np.array([int(s["binding"][q]) for s in ss], dtype=np.int64)
+                                                    for q in p.params}, threads=2)
+        for i, s in enumerate(ss):
+            if s["status"] == "ok":
+                assert st[i] == 0 and pred[i] == hexf(s["predicted_s"][1]), (kid, s["binding"])
+                checked += 1
+            else:
+                assert st[i] != 0, (kid, s["binding"])
+    assert checked > 1000
