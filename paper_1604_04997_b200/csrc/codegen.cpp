@@ -601,6 +601,8 @@ int env_int(const char* name, int dflt, int lo, int hi);
 
 // ring depth of the fused (bindings + T) kernels: 64 KB when two CTAs also
 // hold 35 KB of DMMA row buffers each, 96 KB otherwise (3 stages for P = 3)
+int fused_ctas() { return env_int("KCG_FUSED_CTAS", 2, 1, 4); }
+
 int fused_stages(int n_cols, bool dmma) {
   const int per = (n_cols + 1) * 1024 * 8;
   const int s = (env_int("KCG_FUSED_RING_KB", dmma ? 64 : 96, 16, 200) * 1024) / per;
@@ -776,6 +778,7 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 }  // namespace
 
 int tma_ctas_per_sm() { return tma_ctas(); }
+int fused_ctas_per_sm() { return fused_ctas(); }
 
 
 GramBasis gram_basis(const Lowered& L) {
@@ -1295,7 +1298,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     os << "        }\n      }\n";
   };
 
-  os << "extern \"C\" __global__ void __launch_bounds__(256, 2) " << name
+  os << "extern \"C\" __global__ void __launch_bounds__(256, " << fused_ctas() << ") " << name
      << "(const __grid_constant__ KcgArgs a) {\n"
         "  constexpr int TP = "
      << kTmaTile << ", S = " << S << ", NC = " << NC
