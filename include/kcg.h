@@ -116,10 +116,10 @@ int kcg_program_set_gram_basis(kcg_program* prog, int enable);
 const char* kcg_program_jit_source(kcg_program* prog);
 /* source of the other specialised kernels: kind 0 eval, 1 fused Gram,
  * 2 fused residual, 3 argmin over this one variant, 4 the same exact
- * evaluator as host C++ (`extern "C" void kcg_host_eval(const KcgArgs*,
- * long long begin, long long end)`, compile with g++ -ffp-contract=off; the
- * optimised-CPU baseline of bench.py) -- owned by the program, valid until
- * the next call                                                           */
+ * evaluator as host C++ (entry point kcg_host_eval, arguments: the eval
+ * kernel's argument struct and a point range [begin, end); compile with
+ * g++ -ffp-contract=off; the optimised-CPU baseline of bench.py) -- owned
+ * by the program, valid until the next call                               */
 const char* kcg_program_jit_source_kind(kcg_program* prog, int kind);
 /* NVRTC-compiles `src` for sm_100a without loading it (no GPU needed);
  * KCG_OK or KCG_E_JIT with the compiler log in kcg_last_error()          */

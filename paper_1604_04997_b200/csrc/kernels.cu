@@ -185,66 +185,75 @@ __global__ void __launch_bounds__(128)
 // materialised Gram
 
 constexpr int kGramRows = 32;
-constexpr int kGramThreads = 256;
-constexpr int kGramMaxF = 64;
+constexpr int kGramMaxF = 160;  // the 149-key schema fits (5 x 32 residual lanes, <= 820 tiles)
 
 struct GramGeom {
   int FP, nb, ntiles, slice_threads, S;
 };
 
-__host__ __device__ inline GramGeom gram_geom(int F) {
+// one 4x4 tile of the upper triangle per thread; S row-slices of the tile
+// set when the triangle is small (256 threads, F <= 64), one slice of up to
+// 1,024 threads for wide designs (F <= 176)
+__host__ __device__ inline GramGeom gram_geom(int F, int threads) {
   GramGeom g;
   g.FP = (F + 3) & ~3;
   g.nb = g.FP / 4;
   g.ntiles = g.nb * (g.nb + 1) / 2;
   g.slice_threads = ((g.ntiles + 31) / 32) * 32;
-  g.S = kGramThreads / g.slice_threads;
+  g.S = threads / g.slice_threads;
   if (g.S < 1) g.S = 1;
   return g;
 }
 
-__global__ void __launch_bounds__(kGramThreads)
+// CUDA-core Gram for strided / unaligned X and for wide designs (F > 48):
+// the upper triangle in 4x4 register tiles, rows staged through shared
+// memory; column sums and maxima by the first FP threads from the staged rows
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT)
     kcg_gram_x(const double* __restrict__ X, kcg_i64 n, int F, kcg_i64 ld,
                kcg_i64 rows_per_cta, double* __restrict__ G,
                double* __restrict__ xt1, double* __restrict__ cmax) {
   extern __shared__ double sm[];
-  const GramGeom g = gram_geom(F);
+  const GramGeom g = gram_geom(F, blockDim.x);
   double* tile = sm;                           // [kGramRows][FP]
-  double* red = sm + kGramRows * g.FP;         // [ntiles][16] + [FP] + [FP]
-  double* red_s1 = red + g.ntiles * 16;
-  double* red_mx = red_s1 + g.FP;
+  double* red = sm + kGramRows * g.FP;         // [ntiles][16]
 
   const int tid = threadIdx.x;
   const int slice = tid / g.slice_threads;
   const int t = tid % g.slice_threads;
   const bool active = slice < g.S && t < g.ntiles;
-  // tile t -> (bi, bj), bi <= bj, row-major over the upper triangle
   int bi = 0, bj = 0;
   {
-    int rem = t;
+    int rem = active ? t : 0;
     while (bi < g.nb && rem >= g.nb - bi) {
       rem -= g.nb - bi;
       ++bi;
     }
     bj = bi + rem;
   }
-  for (int k = tid; k < g.ntiles * 16 + 2 * g.FP; k += blockDim.x) red[k] = 0.0;
+  for (int k = tid; k < g.ntiles * 16; k += blockDim.x) red[k] = 0.0;
 
   double acc[4][4] = {};
-  double s1[4] = {}, mx[4] = {};
+  double cs = 0.0, cm = 0.0;  // column tid (< F): sum and max |x|
   const kcg_i64 r0 = (kcg_i64)blockIdx.x * rows_per_cta;
   kcg_i64 r1 = r0 + rows_per_cta;
   if (r1 > n) r1 = n;
-  const int warp = tid >> 5, lane = tid & 31;
+  const int warp = tid >> 5, lane = tid & 31, nwarps = blockDim.x >> 5;
   for (kcg_i64 base = r0; base < r1; base += kGramRows) {
     const int rows = (int)((r1 - base) < kGramRows ? (r1 - base) : kGramRows);
     __syncthreads();
-    for (int r = warp; r < kGramRows; r += kGramThreads / 32) {
+    for (int r = warp; r < kGramRows; r += nwarps) {
       const double* src = X + (base + r) * ld;
       for (int c = lane; c < g.FP; c += 32)
         tile[r * g.FP + c] = (r < rows && c < F) ? __ldcs(src + c) : 0.0;
     }
     __syncthreads();
+    if (tid < F)
+      for (int r = 0; r < rows; ++r) {
+        const double v = tile[r * g.FP + tid];
+        cs += v;
+        cm = fmax(cm, fabs(v));
+      }
     if (active) {
       for (int r = slice; r < rows; r += g.S) {
         const double* row = tile + r * g.FP;
@@ -258,29 +267,18 @@ __global__ void __launch_bounds__(kGramThreads)
         for (int x = 0; x < 4; ++x)
 #pragma unroll
           for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
-        if (bi == bj) {
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            s1[x] += av[x];
-            mx[x] = fmax(mx[x], fabs(av[x]));
-          }
-        }
       }
     }
   }
   __syncthreads();
-  if (active) {
+  if (active)
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
       for (int y = 0; y < 4; ++y) atomicAdd(red + t * 16 + x * 4 + y, acc[x][y]);
-    if (bi == bj)
-#pragma unroll
-      for (int x = 0; x < 4; ++x) {
-        atomicAdd(red_s1 + 4 * bi + x, s1[x]);
-        atomicMax(reinterpret_cast<unsigned long long*>(red_mx + 4 * bi + x),
-                  (unsigned long long)__double_as_longlong(mx[x]));
-      }
+  if (tid < F) {
+    atomicAdd(xt1 + tid, cs);
+    atomicMax(reinterpret_cast<unsigned long long*>(cmax + tid), (unsigned long long)__double_as_longlong(cm));
   }
   __syncthreads();
   if (slice == 0 && t < g.ntiles) {
@@ -293,14 +291,6 @@ __global__ void __launch_bounds__(kGramThreads)
         const double v = red[t * 16 + x * 4 + y];
         atomicAdd(G + r * F + c, v);
         if (bi != bj) atomicAdd(G + c * F + r, v);
-      }
-    if (bi == bj)
-      for (int x = 0; x < 4; ++x) {
-        const int c = 4 * bi + x;
-        if (c >= F) continue;
-        atomicAdd(xt1 + c, red_s1[c]);
-        atomicMax(reinterpret_cast<unsigned long long*>(cmax + c),
-                  (unsigned long long)__double_as_longlong(red_mx[c]));
       }
   }
 }
@@ -509,38 +499,61 @@ void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, 
   check(cudaGetLastError(), "kcg_gram_dmma launch");
 }
 
-// warp per row: lanes own columns lane and lane+32
-template <bool GRAD>
+// warp per row: lane owns columns lane + 32 c, c < NC (F <= 32 NC)
+template <bool GRAD, int NC>
 __global__ void __launch_bounds__(256)
     kcg_resid_x(const double* __restrict__ X, kcg_i64 n, int F, kcg_i64 ld,
                 const double* __restrict__ alpha, double* __restrict__ out) {
   const int lane = threadIdx.x & 31;
   const kcg_i64 warp = ((kcg_i64)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const kcg_i64 nwarps = ((kcg_i64)gridDim.x * blockDim.x) >> 5;
-  const double a0 = lane < F ? alpha[lane] : 0.0;
-  const double a1 = lane + 32 < F ? alpha[lane + 32] : 0.0;
-  double acc = 0.0, g0 = 0.0, g1 = 0.0;
+  double a[NC], g[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    a[c] = lane + 32 * c < F ? alpha[lane + 32 * c] : 0.0;
+    g[c] = 0.0;
+  }
+  double acc = 0.0;
   for (kcg_i64 r = warp; r < n; r += nwarps) {
     const double* row = X + r * ld;
-    const double x0 = lane < F ? __ldcs(row + lane) : 0.0;
-    const double x1 = lane + 32 < F ? __ldcs(row + lane + 32) : 0.0;
-    double d = fma(x1, a1, x0 * a0);
+    double x[NC];
+    double d = 0.0;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      x[c] = lane + 32 * c < F ? __ldcs(row + lane + 32 * c) : 0.0;
+      d = fma(x[c], a[c], d);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
     const double res = 1.0 - d;
     if (GRAD) {
-      g0 = fma(x0, res, g0);
-      g1 = fma(x1, res, g1);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) g[c] = fma(x[c], res, g[c]);
     } else {
       acc = fma(res, res, acc);
     }
   }
   if (GRAD) {
-    if (lane < F) atomicAdd(out + lane, g0);
-    if (lane + 32 < F) atomicAdd(out + lane + 32, g1);
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (lane + 32 * c < F) atomicAdd(out + lane + 32 * c, g[c]);
   } else if (lane == 0) {
     atomicAdd(out, acc);
   }
+}
+
+template <bool GRAD>
+void launch_resid_nc(const double* X, size_t n, int F, size_t ld, const double* alpha, double* out,
+                     cudaStream_t st) {
+  const unsigned grid = num_sms() * 8;
+  switch ((F + 31) / 32) {
+    case 1: kcg_resid_x<GRAD, 1><<<grid, 256, 0, st>>>(X, (kcg_i64)n, F, (kcg_i64)ld, alpha, out); break;
+    case 2: kcg_resid_x<GRAD, 2><<<grid, 256, 0, st>>>(X, (kcg_i64)n, F, (kcg_i64)ld, alpha, out); break;
+    case 3: kcg_resid_x<GRAD, 3><<<grid, 256, 0, st>>>(X, (kcg_i64)n, F, (kcg_i64)ld, alpha, out); break;
+    case 4: kcg_resid_x<GRAD, 4><<<grid, 256, 0, st>>>(X, (kcg_i64)n, F, (kcg_i64)ld, alpha, out); break;
+    default: kcg_resid_x<GRAD, 5><<<grid, 256, 0, st>>>(X, (kcg_i64)n, F, (kcg_i64)ld, alpha, out); break;
+  }
+  check(cudaGetLastError(), "kcg_resid_x launch");
 }
 
 // ---------------------------------------------------------------------------
@@ -644,7 +657,7 @@ void launch_interp_eval(const KcgDevProg* dprog, const KcgDevProg* dadmit, const
 void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double* xt1,
                  double* colmax, void* stream) {
   if (n == 0) return;
-  if (F < 1 || F > kGramMaxF) throw std::invalid_argument("gram: n_cols must be in [1, 64]");
+  if (F < 1 || F > kGramMaxF) throw std::invalid_argument("gram: n_cols must be in [1, 160]");
   static const bool no_dmma = std::getenv("KCG_NO_DMMA") != nullptr;
   if (!no_dmma && ld == (size_t)F && F <= 48 &&
       reinterpret_cast<uintptr_t>(X) % 16 == 0) {
@@ -658,21 +671,35 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
       default: return launch_gram_dmma<6>(X, n, F, G, xt1, colmax, st);
     }
   }
-  const GramGeom g = gram_geom(F);
-  const size_t smem = (size_t)(kGramRows * g.FP + g.ntiles * 16 + 2 * g.FP) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    check(cudaFuncSetAttribute(kcg_gram_x, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
-          "cudaFuncSetAttribute");
-    attr = true;
+  const bool wide = F > 64;
+  const GramGeom g0 = gram_geom(F, 256);
+  const int threads = wide ? g0.slice_threads : 256;  // wide: one thread per tile, <= 1024
+  const GramGeom g = gram_geom(F, threads);
+  const size_t smem = (size_t)(kGramRows * g.FP + g.ntiles * 16) * sizeof(double);
+  {
+    static std::mutex mu;
+    static int attr[64][2] = {};
+    int dev = 0;
+    check(cudaGetDevice(&dev), "cudaGetDevice");
+    std::lock_guard<std::mutex> lk(mu);
+    if (!attr[dev & 63][wide]) {
+      check(wide ? cudaFuncSetAttribute(kcg_gram_x<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024)
+                 : cudaFuncSetAttribute(kcg_gram_x<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024),
+            "cudaFuncSetAttribute");
+      attr[dev & 63][wide] = 1;
+    }
   }
   const kcg_i64 chunks = ((kcg_i64)n + kGramRows - 1) / kGramRows;
-  kcg_i64 ctas = (kcg_i64)num_sms() * 4;
+  kcg_i64 ctas = (kcg_i64)num_sms() * (wide ? 1 : 4);
   if (ctas > chunks) ctas = chunks;
   const kcg_i64 chunks_per_cta = (chunks + ctas - 1) / ctas;
   ctas = (chunks + chunks_per_cta - 1) / chunks_per_cta;
-  kcg_gram_x<<<(unsigned)ctas, kGramThreads, smem, static_cast<cudaStream_t>(stream)>>>(
-      X, (kcg_i64)n, F, (kcg_i64)ld, chunks_per_cta * kGramRows, G, xt1, colmax);
+  if (wide)
+    kcg_gram_x<1024><<<(unsigned)ctas, threads, smem, static_cast<cudaStream_t>(stream)>>>(
+        X, (kcg_i64)n, F, (kcg_i64)ld, chunks_per_cta * kGramRows, G, xt1, colmax);
+  else
+    kcg_gram_x<256><<<(unsigned)ctas, threads, smem, static_cast<cudaStream_t>(stream)>>>(
+        X, (kcg_i64)n, F, (kcg_i64)ld, chunks_per_cta * kGramRows, G, xt1, colmax);
   check(cudaGetLastError(), "kcg_gram_x launch");
 }
 
@@ -693,19 +720,15 @@ void launch_geomean(const double* pred, const double* actual, size_t n, double* 
 void launch_residual(const double* X, size_t n, int F, size_t ld, const double* alpha,
                      double* obj, void* stream) {
   if (n == 0) return;
-  if (F < 1 || F > 64) throw std::invalid_argument("residual: n_cols must be in [1, 64]");
-  kcg_resid_x<false><<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      X, (kcg_i64)n, F, (kcg_i64)ld, alpha, obj);
-  check(cudaGetLastError(), "kcg_resid_x launch");
+  if (F < 1 || F > kGramMaxF) throw std::invalid_argument("residual: n_cols must be in [1, 160]");
+  launch_resid_nc<false>(X, n, F, ld, alpha, obj, static_cast<cudaStream_t>(stream));
 }
 
 void launch_residual_grad(const double* X, size_t n, int F, size_t ld, const double* alpha,
                           double* g, void* stream) {
   if (n == 0) return;
-  if (F < 1 || F > 64) throw std::invalid_argument("residual grad: n_cols must be in [1, 64]");
-  kcg_resid_x<true><<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      X, (kcg_i64)n, F, (kcg_i64)ld, alpha, g);
-  check(cudaGetLastError(), "kcg_resid_grad_x launch");
+  if (F < 1 || F > kGramMaxF) throw std::invalid_argument("residual grad: n_cols must be in [1, 160]");
+  launch_resid_nc<true>(X, n, F, ld, alpha, g, static_cast<cudaStream_t>(stream));
 }
 
 }  // namespace kcg

@@ -200,7 +200,8 @@ def test_argmin_over_matmul_variants(suite_alpha):
 
 def test_gram_accumulate_matches_numpy():
     rng = np.random.default_rng(0)
-    for F, N in ((1, 5001), (3, 5003), (9, 300_009), (18, 5018), (40, 5040), (47, 200_047), (64, 5064)):
+    for F, N in ((1, 5001), (3, 5003), (9, 300_009), (18, 5018), (40, 5040), (47, 200_047), (64, 5064),
+                 (100, 20_100), (149, 30_149)):
         X = rng.uniform(0.5, 2.0, size=(N, F)) * 10.0 ** rng.integers(-3, 3, size=F)
         X[rng.random((N, F)) < 0.1] = 0.0
         Xd = torch.tensor(X, device="cuda")
@@ -502,3 +503,20 @@ def test_fused_gram_basis_matches_direct_and_materialised(kid):
             assert torch.equal(st.colmax, ref.colmax)
         assert obj == pytest.approx(want_obj, rel=1e-9)
     prog.set_gram_basis(True)
+
+
+def test_fit_weights_full_schema_width():
+    """A materialised design as wide as the schema (149 columns: the CUDA-core
+    Gram with one 4x4 tile per thread, the 5-column-per-lane residual and
+    gradient kernels) recovers the generating weights like the reference's
+    noiseless fits (test_model.cpp:43-61: rel 1e-6)."""
+    g = torch.Generator(device="cpu").manual_seed(149)
+    F, N = 149, 60_000
+    C = torch.randint(1, 10001, (N, F), generator=g).to(torch.float64)
+    alpha = torch.exp(torch.empty(F, dtype=torch.float64).uniform_(math.log(1e-13), math.log(1e-9), generator=g))
+    T = C @ alpha
+    X = (C / T[:, None]).cuda()
+    fit = kc.fit_weights(X, refine=2)
+    got = torch.tensor(fit.alpha, dtype=torch.float64)
+    assert float(((got - alpha).abs() / alpha).max()) < 1e-6
+    assert fit.objective < 1e-18
