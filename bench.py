@@ -399,8 +399,8 @@ def _e2e(kc, progs, w, args, torch, dev, world, rank):
     two streams so H2D / kernels / D2H overlap)."""
     import ctypes
     total = args.side ** 3
-    chunk = 1 << 22
-    nstreams = 3
+    chunk = int(os.environ.get("KCG_E2E_CHUNK", 1 << 22))
+    nstreams = int(os.environ.get("KCG_E2E_STREAMS", 3))
     r0 = total * rank // world
     n = total * (rank + 1) // world - r0
     host_cols = {}

@@ -11,6 +11,9 @@
 //   kcg::fit_weights()           <- build_design_matrix + fit_weights
 //                                   (model.hpp:43-49), Gram on the GPU
 //   kcg::read_weights_json()     <- read_weights_json (jsonio.hpp:29)
+//   kcg::EnumProgram             <- enumerate_points (enumerate.hpp:23-24) on the GPU
+//   kcg::Grid, predict_grid()    <- bulk grids from a lattice descriptor
+//   kcg::Columns, write_columns  <- the kcg-columns v1 binary side format
 // Errors are thrown as kcg::Error carrying the kcg_status code (1..11 ==
 // kernelcost::Errc + 1). All device pointers are caller-owned.
 #pragma once
@@ -162,6 +165,91 @@ inline FitResult fit_weights(const double* X, size_t n, int F, int refine = 1, c
   }
   cudaFree(G);
   return r;
+}
+
+/// GPU enumeration oracle over a "kernelcost-enum v1" text (enum_text).
+class EnumProgram {
+ public:
+  explicit EnumProgram(const std::string& text) { check(kcg_enum_program_create(text.data(), text.size(), &h_)); }
+  EnumProgram(const EnumProgram&) = delete;
+  EnumProgram& operator=(const EnumProgram&) = delete;
+  ~EnumProgram() { kcg_enum_program_destroy(h_); }
+  std::vector<std::string> params() const {
+    std::vector<std::string> v;
+    for (int i = 0; i < kcg_enum_program_num_params(h_); ++i) v.emplace_back(kcg_enum_program_param_name(h_, i));
+    return v;
+  }
+  struct Tally {
+    std::vector<__int128> counts = std::vector<__int128>(149, 0);  // schema order
+    uint64_t points = 0;
+  };
+  /// enumerate_points at one binding (parameter declaration order)
+  Tally enumerate_points(const std::vector<int64_t>& binding, uint64_t cap = 0, cudaStream_t s = nullptr) const {
+    std::vector<int64_t> lo(149), hi(149);
+    Tally t;
+    check(kcg_enumerate_points(h_, binding.data(), cap, lo.data(), hi.data(), &t.points, s));
+    for (int i = 0; i < 149; ++i)
+      t.counts[i] = static_cast<__int128>((static_cast<unsigned __int128>(static_cast<uint64_t>(hi[i])) << 64) |
+                                          static_cast<uint64_t>(lo[i]));
+    return t;
+  }
+
+ private:
+  kcg_enum_program* h_ = nullptr;
+};
+
+/// lattice of bindings: parameter j = start[j] + step[j] * d_j, last fastest
+struct Grid {
+  std::vector<int64_t> start, step;
+  std::vector<uint64_t> count;
+  kcg_grid c() const {
+    kcg_grid g{};
+    g.n_params = static_cast<int32_t>(start.size());
+    for (size_t j = 0; j < start.size() && j < 8; ++j) {
+      g.start[j] = start[j];
+      g.step[j] = step[j];
+      g.count[j] = count[j];
+    }
+    return g;
+  }
+};
+
+inline void predict_grid(const ModelWeights& w, const Program& p, const Grid& grid, uint64_t first, size_t n,
+                         double* seconds, uint8_t* status = nullptr, cudaStream_t s = nullptr) {
+  const kcg_grid g = grid.c();
+  check(kcg_eval_predict_grid(p.handle(), &g, first, n, w.alpha.data(), seconds, status, 0, s));
+}
+
+inline void grid_bindings(const Grid& grid, uint64_t first, size_t n, int64_t* const* cols, cudaStream_t s = nullptr) {
+  const kcg_grid g = grid.c();
+  check(kcg_grid_bindings(&g, first, n, cols, s));
+}
+
+/// a mapped kcg-columns v1 file
+class Columns {
+ public:
+  explicit Columns(const std::string& path) { check(kcg_columns_open(path.c_str(), &h_)); }
+  Columns(const Columns&) = delete;
+  Columns& operator=(const Columns&) = delete;
+  ~Columns() { kcg_columns_close(h_); }
+  uint64_t rows() const { return kcg_columns_num_rows(h_); }
+  int find(const std::string& name) const { return kcg_columns_find(h_, name.c_str()); }
+  const void* data(int j) const { return kcg_columns_data(h_, j); }
+  void load(int j, uint64_t row0, size_t n, void* dev, cudaStream_t s = nullptr) {
+    check(kcg_columns_load(h_, j, row0, n, dev, s));
+  }
+
+ private:
+  kcg_columns* h_ = nullptr;
+};
+
+inline void write_columns(const std::string& path, const std::vector<std::string>& names,
+                          const std::vector<int>& dtypes, const std::vector<const void*>& host_cols,
+                          uint64_t n_rows) {
+  std::vector<const char*> nm;
+  for (const auto& s : names) nm.push_back(s.c_str());
+  check(kcg_columns_write(path.c_str(), static_cast<int>(names.size()), nm.data(), dtypes.data(),
+                          host_cols.data(), n_rows));
 }
 
 }  // namespace kcg

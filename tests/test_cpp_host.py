@@ -71,3 +71,28 @@ def test_cpp_host_fit_matches_reference(tmp_path):
     for a, b in zip(alpha, ref):
         assert abs(a - b) <= 1e-6 * abs(b)
     assert obj <= 1e-18
+
+
+@pytest.mark.gpu
+def test_cpp_host_grid_and_columns(tmp_path):
+    """kcg::predict_grid == kcg::grid_bindings -> kcg-columns file ->
+    kcg::Columns::load -> kcg::predict, bitwise, from C++."""
+    r = subprocess.run([str(DRIVER), "grid", str(PROGRAMS / "matmul_tiled_g16x16.kcp"),
+                        str(GOLDEN / "weights_suite.json"), str(tmp_path)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "grid ok" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_host_enumerate_matches_golden():
+    """kcg::EnumProgram from C++ reproduces a reference enumerate_points tally."""
+    c = next(c for c in load_golden("enum_points.json")["cases"]
+             if c["kernel"] == "fd_stencil_g16x16" and c["status"] == "ok")
+    n = int(c["binding"]["n"])
+    r = subprocess.run([str(DRIVER), "enum", str(PROGRAMS / "enum" / "fd_stencil_g16x16.kce"), str(n)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = r.stdout.split("\n")
+    assert lines[0] == f"points {c['points']}"
+    got = dict(l.split(" ") for l in lines[1:] if l)
+    assert got == c["counts"]
