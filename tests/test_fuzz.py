@@ -11,7 +11,10 @@ from fuzz_programs import random_bindings, random_program
 import paper_1604_04997_b200 as kc
 from paper_1604_04997_b200 import _capi
 
-SEEDS = list(range(60))
+import os
+
+# KCG_FUZZ_SEEDS=N widens the GPU fuzz (default 60 programs x 150 bindings)
+SEEDS = list(range(int(os.environ.get("KCG_FUZZ_SEEDS", "60"))))
 
 
 def test_random_programs_parse_and_lower_like_the_oracle():
@@ -76,6 +79,7 @@ def test_random_programs_bit_exact_on_gpu(engine, suite_alpha):
                 assert math.isnan(pred[i])
                 checked["viol" if ws == 1 else "nonint"] += 1
     assert checked["ok"] > 800 and checked["viol"] > 100 and checked["nonint"] > 10, checked
+    print(f"fuzz {engine}: {len(SEEDS)} programs, {checked}")
 
 
 @pytest.mark.gpu
