@@ -455,12 +455,17 @@ void emit_eval_point(std::ostringstream& os, const Lowered& L) {
   const int F = static_cast<int>(L.keys.size());
   const int FA = F > 0 ? F : 1;
   os << "struct KcgRes { double s; int st; };\n";
-  // out-of-line wide path: parameters by value (the grid kernels form them
-  // from a descriptor), writes counts; kcg_point_slow reloads them
-  os << "__device__ __noinline__ KcgRes kcg_point_slow_v(const KcgArgs& a, kcg_i64 i";
-  for (int j = 0; j < L.n_params; ++j) os << ", kcg_i64 v" << j;
-  os << ") {\n  kcg_i64 p[" << (L.n_params ? L.n_params : 1) << "];\n";
-  for (int j = 0; j < L.n_params; ++j) os << "  p[" << j << "] = v" << j << ";\n";
+  // wide path body (inlined into the out-of-line entry points below): the
+  // parameters come from the binding columns (kcg_point_slow) or from a
+  // grid descriptor (kcg_point_slow_g); writes counts when requested.
+  // The entry points take only the argument struct and the index: passing
+  // the parameter values across the noinline call as extra 64-bit arguments
+  // was miscompiled at the 64-register cap (caller spill slot overwritten,
+  // found by the 1000-program fuzz).
+  os << "__device__ __forceinline__ KcgRes kcg_point_slow_body(const KcgArgs& a, kcg_i64 i, const kcg_i64* pin) {\n"
+        "  kcg_i64 p["
+     << (L.n_params ? L.n_params : 1) << "];\n";
+  for (int j = 0; j < L.n_params; ++j) os << "  p[" << j << "] = pin[" << j << "];\n";
   os << "  KcgRes r; r.s = kcg_nan();\n"
         "  const int cls = kcg_class_0(p);\n"
         "  if (cls == 0) { r.st = KCG_PT_ASSUMPTION_VIOLATED; return r; }\n";
@@ -483,10 +488,11 @@ void emit_eval_point(std::ostringstream& os, const Lowered& L) {
        << "    if (a.chi) a.chi[(kcg_i64)" << j << " * a.n + i] = kcg_hi64(c[" << j
        << "]); else if (!kcg_fits_i64(c[" << j << "])) r.st = KCG_PT_COUNT_WIDE;\n";
   os << "  }\n  return r;\n}\n";
-  os << "__device__ __forceinline__ KcgRes kcg_point_slow(const KcgArgs& a, kcg_i64 i) {\n"
-        "  return kcg_point_slow_v(a, i";
-  for (int j = 0; j < L.n_params; ++j) os << ", a.p[" << j << "][i]";
-  os << ");\n}\n";
+  os << "__device__ __noinline__ KcgRes kcg_point_slow(const KcgArgs& a, kcg_i64 i) {\n"
+        "  kcg_i64 p["
+     << (L.n_params ? L.n_params : 1) << "];\n";
+  for (int j = 0; j < L.n_params; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
+  os << "  return kcg_point_slow_body(a, i, p);\n}\n";
   // fast path only; returns -1 when the point needs kcg_point_slow
   os << "template <int GEN>\n__device__ __forceinline__ int kcg_point_fast(const kcg_i64* p, const KcgArgs& a, kcg_i64 i, double& out) {\n"
         "  if (kcg_class_0(p) != 1) return -1;\n"
@@ -531,6 +537,13 @@ void emit_grid_kernel(std::ostringstream& os, int n_cols, const std::string& nam
     os << "__device__ __forceinline__ void kcg_odo_inc(kcg_u64* d, const kcg_u64* cnt) {\n"
           "  #pragma unroll\n  for (int j = "
        << n_cols - 1 << "; j >= 0; --j) {\n    if (++d[j] < cnt[j]) return;\n    d[j] = 0;\n  }\n}\n";
+    // out-of-line wide path of the grid kernels: re-derives the binding of
+    // lattice point first + i (rare; the divisions do not matter)
+    os << "__device__ __noinline__ KcgRes kcg_point_slow_g(const KcgGridArgs& g, kcg_i64 i) {\n"
+          "  kcg_i64 p["
+       << NP << "];\n  kcg_u64 r = g.first + (kcg_u64)i;\n  #pragma unroll\n  for (int j = " << n_cols - 1
+       << "; j >= 0; --j) { p[j] = g.start[j] + g.step[j] * (kcg_i64)(r % g.count[j]); r /= g.count[j]; }\n"
+          "  return kcg_point_slow_body(g.a, i, p);\n}\n";
   }
   // 2 CTAs/SM: the 4-point odometer state plus the exact evaluation need
   // ~100 registers; the 64-register cap of the streaming kernels spills
@@ -556,9 +569,7 @@ void emit_grid_kernel(std::ostringstream& os, int n_cols, const std::string& nam
         "      s[u] = kcg_nan();\n"
         "      st[u] = kcg_point_fast<"
      << gen << ">(p, a, 4 * v + u, s[u]);\n"
-        "      if (st[u] < 0 && 4 * v + u < a.n) { const KcgRes r = kcg_point_slow_v(a, 4 * v + u";
-  for (int j = 0; j < n_cols; ++j) os << ", p[" << j << "]";
-  os << "); s[u] = r.s; st[u] = r.st; }\n"
+        "      if (st[u] < 0 && 4 * v + u < a.n) { const KcgRes r = kcg_point_slow_g(g, 4 * v + u); s[u] = r.s; st[u] = r.st; }\n"
         "      if (st[u] != KCG_PT_OK && st[u] != KCG_PT_COUNT_WIDE) s[u] = kcg_nan();\n"
         "      if (u < 3) kcg_odo_inc(e, g.count);\n"
         "    }\n"

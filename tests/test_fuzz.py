@@ -15,6 +15,9 @@ import os
 
 # KCG_FUZZ_SEEDS=N widens the GPU fuzz (default 60 programs x 150 bindings)
 SEEDS = list(range(int(os.environ.get("KCG_FUZZ_SEEDS", "60"))))
+# regression seeds from wider runs: 163 (wide-path call convention, see
+# codegen.cpp kcg_point_slow_body)
+SEEDS += [s for s in (163,) if s not in SEEDS]
 
 
 def test_random_programs_parse_and_lower_like_the_oracle():
