@@ -666,7 +666,20 @@ def _extras(kc, torch, dev, args):
         "bytes_per_size": 36, "hbm_frac": 36 * total / sec / 1e9 / hbm,
         "best_variant_histogram": torch.bincount(best.to(torch.int64) + 1, minlength=len(progs) + 1).tolist(),
         "note": "one fused launch per step; 24 B bindings in, int32 + fp64 out per size"}
-    del cols, best, best_t
+    # the same launch also writing every variant's prediction (variant-major):
+    # all 1e9 predictions with the bindings read once (24 + 48 B per size
+    # instead of 6 x 32 B for six separate launches)
+    preds_all = torch.empty((len(progs), total), dtype=torch.float64, device=dev)
+
+    def c4p():
+        kc.api.check(kc.api.lib().kcg_argmin(handles, len(progs), carr, total, w.alpha_array(),
+                                             best.data_ptr(), best_t.data_ptr(), preds_all.data_ptr(), stream))
+    sec = _timed(torch, c4p, reps=5)
+    out["config4_fused_all_predictions"] = {
+        "points": total * len(progs), "ms": sec * 1e3, "points_per_s": total * len(progs) / sec,
+        "bytes_per_size": 24 + 12 + 8 * len(progs), "hbm_frac": (36 + 8 * len(progs)) * total / sec / 1e9 / hbm,
+        "note": "kcg_argmin with preds_out: every (variant, size) prediction plus the argmin in one launch"}
+    del preds_all, cols, best, best_t
 
     # ---- config 4 from a grid descriptor: the same 1e9
     # (variant, size) points, bindings generated in registers -- 8 B/point out

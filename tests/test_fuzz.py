@@ -45,7 +45,7 @@ def test_random_programs_bit_exact_on_gpu(engine, suite_alpha):
     import torch
     alpha = [a if a != 0 else 1e-12 * (1 + i % 7) for i, a in enumerate(suite_alpha)]
     w = kc.ModelWeights(alpha=alpha, covered=[True] * 149)
-    checked = {"ok": 0, "viol": 0, "nonint": 0, "over": 0}
+    checked = {"ok": 0, "viol": 0, "nonint": 0, "over": 0, "interp_tables": 0}
     for seed in SEEDS:
         text = random_program(seed)
         p, o = kc.Program(text), ko.Program(text)
@@ -53,7 +53,14 @@ def test_random_programs_bit_exact_on_gpu(engine, suite_alpha):
         _, b128 = p.safe_bounds()
         bs = random_bindings(seed, p.params, 150)
         cols = {q: torch.tensor([b[q] for b in bs], dtype=torch.int64, device="cuda") for q in p.params}
-        bb = kc.evaluate_properties(p, cols, wide=True)
+        try:
+            bb = kc.evaluate_properties(p, cols, wide=True)
+        except kc.KcgError as e:
+            # the table interpreter has static limits (kcg_devprog.h) and says
+            # so loudly; the JIT engine covers every program
+            assert engine == "interp" and e.code == _capi.E_UNSUPPORTED, (seed, e)
+            checked["interp_tables"] += 1
+            continue
         pred, st = kc.predict(w, p, cols, with_status=True)
         torch.cuda.synchronize()
         lo, hi = bb.counts_lo.cpu().tolist(), bb.counts_hi.cpu().tolist()
