@@ -315,6 +315,8 @@ const char* kcg_columns_name(const kcg_columns* cols, int j);
 int kcg_columns_dtype(const kcg_columns* cols, int j);
 int kcg_columns_find(const kcg_columns* cols, const char* name);  /* -1 if absent */
 const void* kcg_columns_data(const kcg_columns* cols, int j);
+/* asynchronous on `stream`; kcg_columns_close waits for the copies still
+ * reading the mapping (loads on several streams: synchronise them first)  */
 int kcg_columns_load(kcg_columns* cols, int j, uint64_t row0, size_t n, void* dev, void* stream);
 
 /* ---- diagnostics -------------------------------------------------------- */

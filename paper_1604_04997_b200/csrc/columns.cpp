@@ -32,6 +32,10 @@
 #include "kcg_host.hpp"
 
 kcg_columns::~kcg_columns() {
+  if (pending) {  // DMA out of the mapping must finish before it goes away
+    cudaEventSynchronize(static_cast<cudaEvent_t>(pending));
+    cudaEventDestroy(static_cast<cudaEvent_t>(pending));
+  }
   if (registered) cudaHostUnregister(map);
   if (map && map != MAP_FAILED) munmap(map, map_len);
   if (fd >= 0) close(fd);
@@ -160,6 +164,14 @@ void columns_load(kcg_columns* h, int j, uint64_t row0, size_t n, void* dev, voi
   if (h->registered) {
     if (cudaMemcpyAsync(dev, src, bytes, cudaMemcpyHostToDevice, stream) != cudaSuccess)
       throw KcgError(KCG_E_CUDA, "kcg_columns_load copy failed");
+    if (!h->pending) {
+      cudaEvent_t ev;
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess)
+        throw KcgError(KCG_E_CUDA, "cudaEventCreate failed");
+      h->pending = ev;
+    }
+    // close waits for the last copy (stream-ordered loads complete in order)
+    cudaEventRecord(static_cast<cudaEvent_t>(h->pending), stream);
     return;
   }
   // pinned staging ring: memcpy chunk k+1 while chunk k is in flight

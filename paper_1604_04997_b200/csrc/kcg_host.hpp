@@ -162,6 +162,7 @@ struct kcg_columns {  // a mapped file (include/kcg.h)
     uint64_t offset, nbytes;
   };
   std::vector<Col> cols;
+  void* pending = nullptr;  // cudaEvent_t of the last async copy out of the mapping
   ~kcg_columns();
 };
 namespace kcg {
