@@ -150,3 +150,36 @@ def test_enumerate_random_kernels_match_reference():
             assert points == int(c["points"]), (k["id"], b, points, c["points"])
             n_ok += 1
     assert n_ok > 1500
+
+
+def _scaled_cases():
+    """Every suite kernel at its largest golden binding scaled by an integer
+    k (divisibility is preserved) so that the walk visits ~1e7-3e8 points:
+    far past the reference's 2e7 cap for most kernels."""
+    best = {}
+    for c in _cases():
+        if c["status"] == "ok" and (c["kernel"] not in best or int(c["points"]) > int(best[c["kernel"]]["points"])):
+            best[c["kernel"]] = c
+    out = []
+    for kid, c in sorted(best.items()):
+        if not (PROGRAMS / f"{kid}.kcp").exists():  # x_* test kernels have no symbolic program
+            continue
+        b = {p: int(v) for p, v in c["binding"].items()}
+        pts = max(1, int(c["points"]))
+        k = 1
+        while k < 64 and pts * (k + 1) ** (len(b) + 1) <= 1.5e8:
+            k += 1
+        if k >= 2:
+            out.append((kid, {p: v * k for p, v in b.items()}))
+    return out
+
+
+@pytest.mark.gpu
+def test_enumerate_equals_symbolic_on_every_suite_kernel_scaled():
+    """GPU brute force == the symbolic programs on every bundled suite kernel
+    at scaled bindings (counts bit-exact)."""
+    cases = _scaled_cases()
+    assert len(cases) >= 50
+    for kid, b in cases:
+        counts, points = kc.load_enum_program(kid).enumerate_points(b)
+        assert counts == _symbolic_counts(kid, b), (kid, b)
