@@ -314,7 +314,9 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
-template <int NB>
+// R: rows per tile (64 * m): narrow designs take taller tiles so every
+// stage is still a multi-KB bulk copy
+template <int NB, int R>
 __global__ void __launch_bounds__(256, 2)
     kcg_gram_dmma(const double* __restrict__ X, kcg_i64 n, int F, int stages,
                   double* __restrict__ G, double* __restrict__ xt1, double* __restrict__ cmax) {
@@ -322,7 +324,8 @@ __global__ void __launch_bounds__(256, 2)
   constexpr int FP = NB * 8;
   extern __shared__ __align__(128) unsigned char kcg_smem[];
   double* buf = reinterpret_cast<double*>(kcg_smem);
-  const int stage_d = kDmmaRows * F;
+  constexpr int RW = R / 8;  // rows per warp per tile
+  const int stage_d = R * F;
   double* red = buf + stages * stage_d;  // [FP][FP] + s1[FP] + mx[FP]
   double* red_s1 = red + FP * FP;
   double* red_mx = red_s1 + FP;
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(256, 2)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const kcg_i64 ntiles = n / kDmmaRows;
+  const kcg_i64 ntiles = n / R;
   const unsigned bytes = (unsigned)(stage_d * 8);
   auto issue = [&](int s, kcg_i64 tile) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -357,15 +360,25 @@ __global__ void __launch_bounds__(256, 2)
   double acc[NT][2];
 #pragma unroll
   for (int t = 0; t < NT; ++t) acc[t][0] = acc[t][1] = 0.0;
-  double s1[NB], mx[NB];
+  // column maxima on the integer pipe: |x| compared as its bit pattern
+  // (monotone for non-negative doubles), keeping the FP64/DMMA pipe -- which
+  // ncu shows shared by DSETP and DMMA -- for the tensor work
+  double s1[NB];
+  unsigned long long mx[NB];
 #pragma unroll
-  for (int b = 0; b < NB; ++b) s1[b] = mx[b] = 0.0;
+  for (int b = 0; b < NB; ++b) {
+    s1[b] = 0.0;
+    mx[b] = 0ull;
+  }
 
   auto kstep_regs = [&](const double* v) {
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       s1[b] += v[b];
-      mx[b] = fmax(mx[b], fabs(v[b]));
+      {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(v[b]) & 0x7fffffffffffffffull;
+        mx[b] = bits > mx[b] ? bits : mx[b];
+      }
     }
     int t = 0;
 #pragma unroll
@@ -380,7 +393,10 @@ __global__ void __launch_bounds__(256, 2)
       const int col = 8 * b + gid;
       v[b] = (valid && col < F) ? rowp[col] : 0.0;
       s1[b] += v[b];
-      mx[b] = fmax(mx[b], fabs(v[b]));
+      {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(v[b]) & 0x7fffffffffffffffull;
+        mx[b] = bits > mx[b] ? bits : mx[b];
+      }
     }
     int t = 0;
 #pragma unroll
@@ -401,20 +417,23 @@ __global__ void __launch_bounds__(256, 2)
                    : "r"(fb + 8 * s), "r"(parity)
                    : "memory");
     const double* st = buf + s * stage_d;
-    // 8 warps x 2 k-steps x 4 rows = 64 rows; fragments are loaded to
-    // registers first, then the stage is released: the last warp to finish
-    // reading it issues the refill, so warps drift freely between tiles
+    // 8 warps x RW/4 k-steps x 4 rows = R rows; the last k-step's fragments
+    // are loaded to registers, then the stage is released: the last warp to
+    // finish reading it issues the refill, so warps drift freely
     double v[NB];
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      const int col = 8 * b + gid;
-      v[b] = col < F ? st[(warp * 8 + tig) * F + col] : 0.0;
+    for (int ks = 0; ks < RW / 4 - 1; ++ks) {
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int col = 8 * b + gid;
+        v[b] = col < F ? st[(warp * RW + 4 * ks + tig) * F + col] : 0.0;
+      }
+      kstep_regs(v);
     }
-    kstep_regs(v);
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
       const int col = 8 * b + gid;
-      v[b] = col < F ? st[(warp * 8 + 4 + tig) * F + col] : 0.0;
+      v[b] = col < F ? st[(warp * RW + RW - 4 + tig) * F + col] : 0.0;
     }
     __syncwarp();
     if (lane == 0) {
@@ -429,22 +448,25 @@ __global__ void __launch_bounds__(256, 2)
   }
   // tail rows straight from global (block 0 only)
   if (blockIdx.x == 0)
-    for (kcg_i64 r0 = ntiles * kDmmaRows + warp * 4; r0 < n; r0 += 32) {
+    for (kcg_i64 r0 = ntiles * R + warp * 4; r0 < n; r0 += 32) {
       const kcg_i64 r = r0 + tig;
       kstep(X + (r < n ? r : 0) * F, r < n);
     }
   // reduce warps through shared memory, then one atomic per entry
 #pragma unroll
   for (int b = 0; b < NB; ++b) {
-    double a = s1[b], m = mx[b];
+    double a = s1[b];
+    unsigned long long m = mx[b];
     a += __shfl_xor_sync(0xffffffffu, a, 1);
     a += __shfl_xor_sync(0xffffffffu, a, 2);
-    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 1));
-    m = fmax(m, __shfl_xor_sync(0xffffffffu, m, 2));
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+      m = y > m ? y : m;
+    }
     if (tig == 0) {
       atomicAdd(red_s1 + 8 * b + gid, a);
-      atomicMax(reinterpret_cast<unsigned long long*>(red_mx + 8 * b + gid),
-                (unsigned long long)__double_as_longlong(m));
+      atomicMax(reinterpret_cast<unsigned long long*>(red_mx + 8 * b + gid), m);
     }
   }
   {
@@ -475,8 +497,12 @@ __global__ void __launch_bounds__(256, 2)
 template <int NB>
 void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, double* colmax,
                       cudaStream_t stream) {
-  const int stages = F <= 40 ? 4 : 3;
-  const size_t smem = (size_t)(stages * kDmmaRows * F + NB * 8 * NB * 8 + 2 * NB * 8) * sizeof(double);
+  constexpr int R = NB <= 2 ? 256 : (NB == 3 ? 128 : 64);
+  // ring: up to 4 stages within ~100 KB so that two CTAs share an SM
+  int stages = (int)((100 * 1024) / ((size_t)R * F * 8));
+  stages = stages < 2 ? 2 : (stages > 4 ? 4 : stages);
+  if (NB >= 5) stages = F <= 40 ? 4 : 3;
+  const size_t smem = (size_t)(stages * R * F + NB * 8 * NB * 8 + 2 * NB * 8) * sizeof(double);
   // the opt-in size grows with F within one NB (per device, process-wide)
   static std::mutex mu;
   static size_t attr_smem[64] = {};
@@ -486,16 +512,16 @@ void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, 
     std::lock_guard<std::mutex> lk(mu);
     size_t& cur = attr_smem[dev & 63];
     if (smem + 4096 > cur) {
-      check(cudaFuncSetAttribute(kcg_gram_dmma<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      check(cudaFuncSetAttribute(kcg_gram_dmma<NB, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem + 4096),
             "cudaFuncSetAttribute");
       cur = smem + 4096;
     }
   }
-  const kcg_i64 tiles = (kcg_i64)n / kDmmaRows;
+  const kcg_i64 tiles = (kcg_i64)n / R;
   kcg_i64 grid = (kcg_i64)num_sms() * 2;
   if (grid > tiles) grid = tiles > 0 ? tiles : 1;
-  kcg_gram_dmma<NB><<<(unsigned)grid, 256, smem, stream>>>(X, (kcg_i64)n, F, stages, G, xt1, colmax);
+  kcg_gram_dmma<NB, R><<<(unsigned)grid, 256, smem, stream>>>(X, (kcg_i64)n, F, stages, G, xt1, colmax);
   check(cudaGetLastError(), "kcg_gram_dmma launch");
 }
 
