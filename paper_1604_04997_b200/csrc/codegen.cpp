@@ -1215,13 +1215,15 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   } else if (regsm) {
     const int NG = W * (W + 1) / 2;
     cons_decl << red_decl
-              << "  double g[" << (NG ? NG : 1) << "], s1[" << WA << "], mx[" << WA << "];\n"
+              << "  double g[" << (NG ? NG : 1) << "], s1[" << WA << "];\n"
+              << "  unsigned long long mx[" << WA << "];  // |x| bit patterns: max on the integer pipe\n"
               << "  #pragma unroll\n  for (int k = 0; k < " << NG << "; ++k) g[k] = 0.0;\n"
-              << "  #pragma unroll\n  for (int k = 0; k < " << W << "; ++k) { s1[k] = 0.0; mx[k] = 0.0; }\n"
+              << "  #pragma unroll\n  for (int k = 0; k < " << W << "; ++k) { s1[k] = 0.0; mx[k] = 0ull; }\n"
               << mxc_decl << "  unsigned long long bad = 0;\n";
     int k = 0;
     for (int r = 0; r < W; ++r) {
-      cons_row << "      s1[" << r << "] += x[" << r << "]; mx[" << r << "] = fmax(mx[" << r << "], fabs(x[" << r << "]));\n";
+      cons_row << "      s1[" << r << "] += x[" << r << "]; { const unsigned long long b = (unsigned long long)__double_as_longlong(x["
+               << r << "]) & 0x7fffffffffffffffull; mx[" << r << "] = b > mx[" << r << "] ? b : mx[" << r << "]; }\n";
       for (int c = r; c < W; ++c, ++k)
         cons_row << "      g[" << k << "] = fma(x[" << r << "], x[" << c << "], g[" << k << "]);\n";
     }
@@ -1229,7 +1231,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     cons_end << "  #pragma unroll\n  for (int o = 16; o > 0; o >>= 1) {\n"
              << "    #pragma unroll\n    for (int k = 0; k < " << NG << "; ++k) g[k] += __shfl_down_sync(0xffffffffu, g[k], o);\n"
              << "    #pragma unroll\n    for (int k = 0; k < " << W
-             << "; ++k) { s1[k] += __shfl_down_sync(0xffffffffu, s1[k], o); mx[k] = fmax(mx[k], __shfl_down_sync(0xffffffffu, mx[k], o)); }\n";
+             << "; ++k) { s1[k] += __shfl_down_sync(0xffffffffu, s1[k], o); const unsigned long long y = __shfl_down_sync(0xffffffffu, mx[k], o); mx[k] = y > mx[k] ? y : mx[k]; }\n";
     if (NCMP)
       cons_end << "    #pragma unroll\n    for (int k = 0; k < " << NCMP
                << "; ++k) mxc[k] = fmax(mxc[k], __shfl_down_sync(0xffffffffu, mxc[k], o));\n";
@@ -1239,7 +1241,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     for (int r = 0; r < W; ++r) {
       cons_end << "    atomicAdd(red + " << S1OFF + r << ", s1[" << r << "]);\n"
                << "    atomicMax((unsigned long long*)(red + " << MXOFF + r
-               << "), (unsigned long long)__double_as_longlong(mx[" << r << "]));\n";
+               << "), mx[" << r << "]);\n";
       for (int c = r; c < W; ++c, ++k) cons_end << "    atomicAdd(red + " << (r * W + c) << ", g[" << k << "]);\n";
     }
     for (int q = 0; q < NCMP; ++q)
