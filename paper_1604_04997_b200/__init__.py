@@ -12,6 +12,8 @@ from .api import (  # noqa: F401
     read_columns,
     write_columns,
     Grid,
+    Prediction,
+    predict_detail,
     grid_bindings,
     predict_grid,
     load_enum_program,

@@ -714,3 +714,48 @@ class Columns:
 
 def read_columns(path) -> Columns:
     return Columns(path)
+
+
+# ---- Prediction detail (model.cpp:95-117) -------------------------------------
+
+
+@dataclass
+class Prediction:
+    """``kernelcost::Prediction``: seconds, the per-key (key, part)
+    breakdown in schema order and the uncovered keys that contributed."""
+    seconds: float
+    breakdown: list
+    warnings: list
+
+
+def predict_detail(w: ModelWeights, prog: Program, bindings, indices=None, stream=None) -> list:
+    """``predict`` with its breakdown and warnings for selected points
+    (model.cpp:95-117): the exact counts come from the GPU
+    (evaluate_properties), the per-key parts are formed on the host in
+    schema order exactly as the reference does (double(count) round to
+    nearest even, part = alpha * count, seconds += part). Inadmissible
+    points give None (the reference raises E_ASSUMPTION_VIOLATED)."""
+    w.alpha_array()  # schema check (model.cpp:96-100)
+    bb = evaluate_properties(prog, bindings, wide=True, stream=stream)
+    torch = _torch()
+    torch.cuda.synchronize()
+    st = bb.status.cpu().tolist()
+    n = len(st)
+    keys = schema_keys()
+    out = []
+    for i in (range(n) if indices is None else indices):
+        if st[i] != _capi.PT_OK:
+            out.append(None)
+            continue
+        seconds, br, warn = 0.0, [], []
+        for j, k in enumerate(prog.props):
+            c = bb.counts_int(j, i)
+            if c == 0:
+                continue
+            part = w.alpha[k] * float(c)
+            seconds += part
+            br.append((keys[k], part))
+            if not w.covered[k]:
+                warn.append(keys[k])
+        out.append(Prediction(seconds, br, warn))
+    return out

@@ -520,3 +520,32 @@ def test_fit_weights_full_schema_width():
     got = torch.tensor(fit.alpha, dtype=torch.float64)
     assert float(((got - alpha).abs() / alpha).max()) < 1e-6
     assert fit.objective < 1e-18
+
+
+def test_predict_detail_matches_reference_predictions():
+    """Prediction{seconds, breakdown, warnings} (model.cpp:95-117) for the 16
+    test cases with the reference-fitted weights: seconds bitwise, the same
+    (empty) warnings as the reference, breakdown parts summing in schema
+    order; with keys marked uncovered the warnings list exactly those keys
+    that carry a nonzero count."""
+    fit = load_golden("fit_suite.json")
+    w = kc.ModelWeights(device="ref", alpha=[0.0] * 149, covered=[False] * 149)
+    for k, v in fit["alpha"].items():
+        w.alpha[ko.SCHEMA_INDEX[k]] = hexf(v[1])
+    for k in fit["covered"]:
+        w.covered[ko.SCHEMA_INDEX[k]] = True
+    for t in fit["test_predictions"]:
+        prog = kc.load_program(t["kernel"])
+        b = {p: int(v) for p, v in t["binding"].items()}
+        (pd,) = kc.predict_detail(w, prog, _cols(prog, [b]))
+        assert pd.seconds == hexf(t["predicted_s"][1]), t["kernel"]
+        assert pd.warnings == t["warnings"]
+        s = 0.0
+        for _, part in pd.breakdown:
+            s += part
+        assert s == pd.seconds
+    prog = kc.load_program("matmul_tiled_g16x16")
+    w2 = kc.ModelWeights(device="x", alpha=list(w.alpha), covered=[False] * 149)
+    (pd,) = kc.predict_detail(w2, prog, _cols(prog, [{"n": 64, "m": 32, "l": 48}, {"n": 65, "m": 32, "l": 48}]), [0])
+    assert pd.warnings == [ko.SCHEMA[k] for k in prog.props]
+    assert kc.predict_detail(w2, prog, _cols(prog, [{"n": 65, "m": 32, "l": 48}]))[0] is None
