@@ -11,6 +11,7 @@
 //   kcg::fit_weights()           <- build_design_matrix + fit_weights
 //                                   (model.hpp:43-49), Gram on the GPU
 //   kcg::read_weights_json()     <- read_weights_json (jsonio.hpp:29)
+//   kcg::prediction()            <- predict's Prediction{seconds, breakdown, warnings}
 //   kcg::EnumProgram             <- enumerate_points (enumerate.hpp:23-24) on the GPU
 //   kcg::Grid, predict_grid()    <- bulk grids from a lattice descriptor
 //   kcg::Columns, write_columns  <- the kcg-columns v1 binary side format
@@ -250,6 +251,33 @@ inline void write_columns(const std::string& path, const std::vector<std::string
   for (const auto& s : names) nm.push_back(s.c_str());
   check(kcg_columns_write(path.c_str(), static_cast<int>(names.size()), nm.data(), dtypes.data(),
                           host_cols.data(), n_rows));
+}
+
+/// predict's full result for one point (model.cpp:95-117) from its exact
+/// counts (kcg::evaluate_properties output copied to the host: the F lo/hi
+/// words of the point, program property order = schema order)
+struct Prediction {
+  double seconds = 0.0;
+  std::vector<std::pair<std::string, double>> breakdown;
+  std::vector<std::string> warnings;
+};
+
+inline Prediction prediction(const ModelWeights& w, const Program& p, const int64_t* lo, const int64_t* hi) {
+  if (w.alpha.size() != static_cast<size_t>(kcg_schema_size()))
+    throw Error(KCG_E_SCHEMA_MISMATCH, "weight vector does not match schema v1");
+  Prediction out;
+  const std::vector<int> props = p.props();
+  for (size_t j = 0; j < props.size(); ++j) {
+    const __int128 c = static_cast<__int128>((static_cast<unsigned __int128>(static_cast<uint64_t>(hi[j])) << 64) |
+                                             static_cast<uint64_t>(lo[j]));
+    if (c == 0) continue;
+    const double count = static_cast<double>(c);  // round to nearest even
+    const double part = w.alpha[props[j]] * count;
+    out.seconds += part;
+    out.breakdown.emplace_back(kcg_schema_key(props[j]), part);
+    if (!w.covered[props[j]]) out.warnings.emplace_back(kcg_schema_key(props[j]));
+  }
+  return out;
 }
 
 }  // namespace kcg
