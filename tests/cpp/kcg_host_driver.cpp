@@ -63,6 +63,22 @@ int eval(int argc, char** argv) {
   kcg::cuda_check(cudaMemcpy(st.data(), dst, n, cudaMemcpyDeviceToHost));
   kcg::cuda_check(cudaMemcpy(lo.data(), dlo, sizeof(int64_t) * F * n, cudaMemcpyDeviceToHost));
   kcg::cuda_check(cudaMemcpy(hi.data(), dhi, sizeof(int64_t) * F * n, cudaMemcpyDeviceToHost));
+  // the host-side Prediction of every admissible point == the GPU prediction
+  int64_t mismatch = 0;
+  std::vector<int64_t> plo(F), phi(F);
+  for (int64_t i = 0; i < n; ++i) {
+    if (st[i] != 0) continue;
+    for (int j = 0; j < F; ++j) {
+      plo[j] = lo[j * n + i];
+      phi[j] = hi[j * n + i];
+    }
+    const kcg::Prediction pd = kcg::prediction(w, prog, plo.data(), phi.data());
+    if (std::memcmp(&pd.seconds, &pred[i], 8) != 0) ++mismatch;
+  }
+  if (mismatch) {
+    std::cout << "prediction mismatch: " << mismatch << "\n";
+    return 1;
+  }
   std::ofstream out(argv[5], std::ios::binary);
   out.write(reinterpret_cast<const char*>(pred.data()), sizeof(double) * n);
   out.write(reinterpret_cast<const char*>(st.data()), n);
