@@ -556,6 +556,24 @@ int kcg_gram_accumulate(const double* X, size_t n, int F, size_t ld, double* G, 
     return fail(KCG_E_INVALID_ARGUMENT, "bad gram arguments");
   return guarded([&] {
     require_device();
+    static const bool no_wide = std::getenv("KCG_NO_WIDE_DMMA") != nullptr;  // A/B knob
+    if (!no_wide && F > 48 && F <= 160 && ld == static_cast<size_t>(F) && reinterpret_cast<uintptr_t>(X) % 16 == 0 &&
+        n >= 32) {
+      // wide design on the tensor cores: one NVRTC specialisation per width
+      const std::string name = "kcg_gram_wide_" + std::to_string(F);
+      void* k = kcg::jit_kernel(kcg::gram_wide_source(F, name), name);
+      struct {
+        const double* X;
+        int64_t n;
+        double *G, *xt1, *cmax;
+      } args{X, static_cast<int64_t>(n), G, xt1, colmax};
+      const size_t tiles = n / 32;
+      const unsigned grid = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(tiles, kcg::num_sms())));
+      void* argv[] = {&args.X, &args.n, &args.G, &args.xt1, &args.cmax};
+      kcg::launch_jit_argv(k, argv, grid, 512, stream, kcg::gram_wide_smem(F));
+      ++g_launches;
+      return KCG_OK;
+    }
     kcg::launch_gram(X, n, F, ld, G, xt1, colmax, stream);
     ++g_launches;
     return KCG_OK;

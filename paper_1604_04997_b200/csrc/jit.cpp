@@ -141,4 +141,24 @@ void launch_jit(void* kernel, const void* args, size_t, unsigned grid,
     throw KcgError(KCG_E_CUDA, std::string("JIT kernel launch: ") + cudaGetErrorString(e));
 }
 
+void launch_jit_argv(void* kernel, void** argv, unsigned grid, unsigned block, void* stream, size_t smem) {
+  if (smem > 32 * 1024) {
+    std::lock_guard<std::mutex> lock(g_mu);
+    static std::unordered_map<void*, size_t> configured;
+    auto it = configured.find(kernel);
+    if (it == configured.end() || it->second < smem) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      const cudaError_t e = cudaKernelSetAttributeForDevice(
+          reinterpret_cast<cudaKernel_t>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
+          static_cast<int>(smem), dev);
+      if (e != cudaSuccess)
+        throw KcgError(KCG_E_CUDA, std::string("cudaKernelSetAttributeForDevice: ") + cudaGetErrorString(e));
+      configured[kernel] = smem;
+    }
+  }
+  const cudaError_t e = cudaLaunchKernel(kernel, dim3(grid), dim3(block), argv, smem, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) throw KcgError(KCG_E_CUDA, std::string("JIT kernel launch: ") + cudaGetErrorString(e));
+}
+
 }  // namespace kcg

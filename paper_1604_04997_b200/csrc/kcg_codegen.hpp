@@ -24,6 +24,10 @@ void* jit_kernel(const std::string& src, const std::string& name);
 /// NVRTC compile only (no module load, no GPU needed); throws KcgError.
 void jit_compile_only(const std::string& src, const std::string& name);
 
+/// Launches a JIT kernel with a regular parameter list (argv as for
+/// cudaLaunchKernel).
+void launch_jit_argv(void* kernel, void** argv, unsigned grid, unsigned block, void* stream, size_t smem = 0);
+
 /// Launches a JIT kernel with a single by-value argument struct.
 void launch_jit(void* kernel, const void* args, size_t args_size,
                 unsigned grid, unsigned block, void* stream, size_t smem = 0);
@@ -32,6 +36,12 @@ void launch_jit(void* kernel, const void* args, size_t args_size,
 /// alpha * predict_fold): the power-of-two count constant folded out of the
 /// count (1.0 when the key is not folded).
 double predict_fold(const Lowered& L, int j);
+
+/// Materialised Gram for wide designs (49 <= F <= 160) on DMMA, one
+/// NVRTC-specialised kernel per width (gram_wide.cpp): its source, its ring
+/// size (dynamic shared memory) and launch shape (512 threads, 1 CTA/SM).
+std::string gram_wide_source(int F, const std::string& name);
+size_t gram_wide_smem(int F);
 
 /// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.
 size_t tma_smem_bytes(int n_cols);
