@@ -568,9 +568,10 @@ int kcg_gram_accumulate(const double* X, size_t n, int F, size_t ld, double* G, 
         double *G, *xt1, *cmax;
       } args{X, static_cast<int64_t>(n), G, xt1, colmax};
       const size_t tiles = n / 32;
-      const unsigned grid = static_cast<unsigned>(std::max<size_t>(1, std::min<size_t>(tiles, kcg::num_sms())));
+      const unsigned grid = static_cast<unsigned>(
+          std::max<size_t>(1, std::min<size_t>(tiles, static_cast<size_t>(kcg::num_sms()) * kcg::gram_wide_ctas(F))));
       void* argv[] = {&args.X, &args.n, &args.G, &args.xt1, &args.cmax};
-      kcg::launch_jit_argv(k, argv, grid, 512, stream, kcg::gram_wide_smem(F));
+      kcg::launch_jit_argv(k, argv, grid, 32 * kcg::gram_wide_warps(F), stream, kcg::gram_wide_smem(F));
       ++g_launches;
       return KCG_OK;
     }

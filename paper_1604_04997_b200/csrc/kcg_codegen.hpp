@@ -42,6 +42,8 @@ double predict_fold(const Lowered& L, int j);
 /// size (dynamic shared memory) and launch shape (512 threads, 1 CTA/SM).
 std::string gram_wide_source(int F, const std::string& name);
 size_t gram_wide_smem(int F);
+int gram_wide_warps(int F);
+int gram_wide_ctas(int F);
 
 /// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.
 size_t tma_smem_bytes(int n_cols);
