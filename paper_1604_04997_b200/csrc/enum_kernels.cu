@@ -15,8 +15,10 @@
 //     are all zero.
 //   * Every leaf marks the cells of the statement's global accesses in the
 //     array's bitmaps (distinct cells, the projection on the non-fastest
-//     axes, and the fastest-axis coordinates); a bit is read before the
-//     atomic so repeated cells cost a load, not an L2 atomic.
+//     axes, and the fastest-axis coordinates); lanes hitting the same word
+//     combine their bits (__match_any_sync / __reduce_or_sync) and the word
+//     is read before the atomic, so repeated cells cost a load, not an L2
+//     atomic.
 // Leaves and visited points are reduced per warp into out[0..1].
 #include <cuda_runtime.h>
 
@@ -63,10 +65,15 @@ __device__ __forceinline__ bool ke_guard(const KeGuard& g, const i64* x, int nv)
   }
 }
 
-__device__ __forceinline__ void ke_set(u64* bm, u64 bit) {
-  u64* w = bm + (bit >> 6);
-  const u64 m = 1ull << (bit & 63);
-  if ((__ldcg(w) & m) == 0) atomicOr(w, m);
+// set a bit; lanes of a warp that hit the same 32-bit word combine their
+// bits first (one load and at most one atomic per distinct word)
+__device__ __forceinline__ void ke_set(u64* bm64, u64 bit) {
+  unsigned* w = reinterpret_cast<unsigned*>(bm64) + (bit >> 5);  // little endian: same bit numbering
+  const unsigned m = 1u << (bit & 31);
+  const unsigned act = __activemask();
+  const unsigned grp = __match_any_sync(act, reinterpret_cast<unsigned long long>(w));
+  const unsigned bits = __reduce_or_sync(grp, m);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(grp) - 1) && (__ldcg(w) & bits) != bits) atomicOr(w, bits);
 }
 
 __device__ __forceinline__ void ke_mark(const KeStmt& S, const i64* x) {
