@@ -35,3 +35,24 @@ def allreduce_gram(stats, group=None):
     stats.n_rows = int(flat[F * F + F].item())
     stats.bad_rows = int(flat[F * F + F + 1].item())
     return stats
+
+
+def gather_shards(local, total: int, dst: int = 0, group=None):
+    """Concatenate the per-rank output slices (rank order, shard_bounds
+    blocks of a length-`total` result along dim 0) on rank `dst`; other
+    ranks get None. Works with NCCL (CUDA tensors) and gloo (CPU)."""
+    import torch
+    import torch.distributed as dist
+
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return local
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    width = (total + world - 1) // world  # the largest shard
+    pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    pad[:local.shape[0]] = local
+    parts = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+    dist.gather(pad, parts, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([parts[r][:shard_bounds(total, r, world)[1] - shard_bounds(total, r, world)[0]]
+                      for r in range(world)])

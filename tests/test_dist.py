@@ -12,7 +12,7 @@ import torch.multiprocessing as mp
 
 from conftest import hexf, load_golden
 from paper_1604_04997_b200.api import GramStats
-from paper_1604_04997_b200.dist import allreduce_gram, shard_bounds
+from paper_1604_04997_b200.dist import allreduce_gram, gather_shards, shard_bounds
 
 
 def test_shard_bounds_cover_exactly():
@@ -62,3 +62,23 @@ def test_gloo_world2_gram_allreduce_equals_single_process():
         assert (c == cm).all() and n == X.shape[0]
     # both ranks hold bit-identical statistics -> identical redundant solves
     assert (out[0][0] == out[1][0]).all() and (out[0][1] == out[1][1]).all()
+
+
+def _gather_worker(rank, world, port, total, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a, b = shard_bounds(total, rank, world)
+    local = torch.arange(a, b, dtype=torch.float64) * 0.5  # this rank's predictions
+    g = gather_shards(local, total)
+    out[rank] = None if g is None else g.numpy().copy()
+    dist.destroy_process_group()
+
+
+def test_gloo_world3_gather_shards_reassembles_the_grid():
+    """Ragged shards (10 sizes over 3 ranks) gather back in grid order on rank 0."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gather_worker, args=(3, _free_port(), 10, out), nprocs=3, join=True)
+    np.testing.assert_array_equal(out[0], np.arange(10) * 0.5)
+    assert out[1] is None and out[2] is None
