@@ -549,3 +549,24 @@ def test_predict_detail_matches_reference_predictions():
     (pd,) = kc.predict_detail(w2, prog, _cols(prog, [{"n": 64, "m": 32, "l": 48}, {"n": 65, "m": 32, "l": 48}]), [0])
     assert pd.warnings == [ko.SCHEMA[k] for k in prog.props]
     assert kc.predict_detail(w2, prog, _cols(prog, [{"n": 65, "m": 32, "l": 48}]))[0] is None
+
+
+def test_gram_accumulate_random_shapes():
+    """Every Gram path (DMMA row-split for F <= 48, per-width DMMA for
+    49..160, CUDA-core for strided / unaligned X) against torch fp64 on random
+    widths, row counts (tails included) and layouts."""
+    rng = np.random.default_rng(123)
+    widths = [1, 2, 5, 8, 13, 31, 48, 49, 57, 64, 65, 80, 81, 111, 131, 149, 160]
+    for F in widths:
+        N = int(rng.integers(1, 5000)) + (70_000 if F in (57, 131) else 0)
+        ld = F + (3 if F % 3 == 0 else 0)  # some strided layouts
+        base = torch.tensor(rng.uniform(0.5, 2.0, size=(N, ld)) * 10.0 ** rng.integers(-2, 3, size=ld),
+                            device="cuda")
+        X = base[:, :F]
+        st = kc.GramStats.zeros(F, X.device)
+        _capi.check(_capi.lib().kcg_gram_accumulate(X.data_ptr(), N, F, ld, st.G.data_ptr(), st.xt1.data_ptr(),
+                                                    st.colmax.data_ptr(), torch.cuda.current_stream().cuda_stream))
+        ref = X.T @ X
+        torch.testing.assert_close(st.G, ref, rtol=1e-12, atol=0, msg=f"F={F} N={N} ld={ld}")
+        torch.testing.assert_close(st.xt1, X.sum(0), rtol=1e-12, atol=0)
+        assert torch.equal(st.colmax, X.abs().max(0).values), F
