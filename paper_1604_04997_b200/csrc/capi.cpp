@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <limits>
 #include <memory>
 #include <mutex>
@@ -581,6 +582,52 @@ int kcg_gram_accumulate(const double* X, size_t n, int F, size_t ld, double* G, 
   });
 }
 
+namespace {
+
+// Fused Gram / residual for programs whose design rows stay wider than 48
+// columns even over the monomial basis: a register-resident row of that
+// width would spill (and takes NVRTC minutes to compile), so rows are
+// formed in HBM chunk by chunk -- exact counts (eval kernel), then
+// x = RN(count) / T (kcg_form_rows) -- and reduced by the materialised-X
+// kernels (per-width DMMA Gram, residual). Same statistics as the fused path.
+constexpr size_t kWideChunk = 1 << 18;
+
+bool fused_too_wide(const kcg_program* p) {
+  return kcg::gram_basis(p->low).width(static_cast<int>(p->low.keys.size())) > 48;
+}
+
+void chunked_rows(const kcg_program* p, const int64_t* const* param_cols, const double* T, size_t n,
+                  unsigned long long* bad_rows, void* stream, const std::function<void(const double*, size_t)>& reduce) {
+  const int np = p->low.n_params;
+  const int F = static_cast<int>(p->low.keys.size());
+  const size_t chunk = std::min(n, kWideChunk);
+  const cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* buf = nullptr;
+  const size_t bytes = chunk * (8 * F * 3 + 1) + 64;
+  cuda_check(cudaMallocAsync(&buf, bytes, st), "cudaMallocAsync");
+  int64_t* lo = static_cast<int64_t*>(buf);
+  int64_t* hi = lo + chunk * F;
+  double* X = reinterpret_cast<double*>(hi + chunk * F);
+  uint8_t* status = reinterpret_cast<uint8_t*>(X + chunk * F);
+  try {
+    std::vector<const int64_t*> cols(std::max(np, 1), nullptr);
+    for (size_t c0 = 0; c0 < n; c0 += chunk) {
+      const size_t m = std::min(chunk, n - c0);
+      for (int j = 0; j < np; ++j) cols[j] = param_cols[j] + c0;
+      const int rc = kcg_eval_predict(p, cols.data(), m, nullptr, nullptr, status, lo, hi, 0, stream);
+      if (rc != KCG_OK) throw KcgError(rc, kcg_last_error());
+      kcg::launch_form_rows(lo, hi, status, T + c0, m, F, X, bad_rows, stream);
+      reduce(X, m);
+    }
+  } catch (...) {
+    cudaFreeAsync(buf, st);
+    throw;
+  }
+  cuda_check(cudaFreeAsync(buf, st), "cudaFreeAsync");
+}
+
+}  // namespace
+
 int kcg_gram_fused(const kcg_program* cp, const int64_t* const* param_cols, const double* T,
                    size_t n, double* G, double* xt1, double* colmax,
                    unsigned long long* bad_rows, void* stream) {
@@ -590,6 +637,14 @@ int kcg_gram_fused(const kcg_program* cp, const int64_t* const* param_cols, cons
     require_device();
     if (n == 0) return KCG_OK;
     const int np = p->low.n_params;
+    if (fused_too_wide(p)) {
+      const int F = static_cast<int>(p->low.keys.size());
+      chunked_rows(p, param_cols, T, n, bad_rows, stream, [&](const double* X, size_t m) {
+        const int rc = kcg_gram_accumulate(X, m, F, F, G, xt1, colmax, stream);
+        if (rc != KCG_OK) throw KcgError(rc, kcg_last_error());
+      });
+      return KCG_OK;
+    }
     if (!p->jit_gram) {
       const std::string name = kname("kcg_gram_", p);
       p->jit_gram = kcg::jit_kernel(
@@ -648,6 +703,21 @@ int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, 
     if (n == 0) return KCG_OK;
     const int np = p->low.n_params;
     const int F = static_cast<int>(p->low.keys.size());
+    if (fused_too_wide(p)) {
+      std::vector<double> al(std::max(F, 1), 0.0);
+      compact_alpha(p, alpha, al.data());
+      double* da = nullptr;
+      cuda_check(cudaMallocAsync(&da, sizeof(double) * al.size(), static_cast<cudaStream_t>(stream)), "cudaMallocAsync");
+      cuda_check(cudaMemcpyAsync(da, al.data(), sizeof(double) * al.size(), cudaMemcpyHostToDevice,
+                                 static_cast<cudaStream_t>(stream)), "cudaMemcpyAsync");
+      chunked_rows(p, param_cols, T, n, nullptr, stream, [&](const double* X, size_t m) {
+        const int rc = kcg_residual_accumulate(X, m, F, F, da, obj, stream);
+        if (rc != KCG_OK) throw KcgError(rc, kcg_last_error());
+      });
+      cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "residual");  // al outlives the copy
+      cudaFreeAsync(da, static_cast<cudaStream_t>(stream));
+      return KCG_OK;
+    }
     if (!p->jit_resid) {
       const std::string name = kname("kcg_resid_", p);
       p->jit_resid = kcg::jit_kernel(

@@ -64,6 +64,11 @@ void launch_enum_walk(const KeStmt* dev_stmt, unsigned long long box_total, cuda
 void launch_enum_bits(const unsigned long long* bm, unsigned long long words, unsigned long long* out,
                       cudaStream_t stream);
 
+/// design rows x = RN(count) / T (row-major n x F; zero rows, counted in
+/// *bad, for inadmissible points or T <= 0) from prop-major exact counts
+void launch_form_rows(const int64_t* lo, const int64_t* hi, const uint8_t* status, const double* T, size_t n,
+                      int F, double* X, unsigned long long* bad, void* stream);
+
 /// grid descriptor -> SoA int64 bindings
 void launch_grid_fill(int np, const int64_t* start, const int64_t* step, const uint64_t* count, uint64_t first,
                       size_t n, int64_t* const* cols, void* stream);

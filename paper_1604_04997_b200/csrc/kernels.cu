@@ -801,3 +801,42 @@ void launch_grid_fill(int np, const int64_t* start, const int64_t* step, const u
   check(cudaGetLastError(), "kcg_grid_fill launch");
 }
 }  // namespace kcg
+
+// ---- design rows from exact counts (wide fused Gram / residual) -----------
+namespace {
+__global__ void __launch_bounds__(256)
+    kcg_form_rows(const long long* __restrict__ lo, const long long* __restrict__ hi,
+                  const unsigned char* __restrict__ st, const double* __restrict__ T, long long n, int F,
+                  double* __restrict__ X, unsigned long long* bad) {
+  unsigned long long nb = 0;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double t = T[i];
+    const bool ok = st[i] == KCG_PT_OK && t > 0.0;
+    nb += !ok;
+    for (int j = 0; j < F; ++j) {
+      double x = 0.0;
+      if (ok) {
+        const kcg_i128 c = (kcg_i128)(((kcg_u128)(kcg_u64)hi[(long long)j * n + i] << 64) |
+                                      (kcg_u128)(kcg_u64)lo[(long long)j * n + i]);
+        if (c != 0) x = __ddiv_rn(kcg_to_double(c), t);  // model.cpp:29
+      }
+      X[i * F + j] = x;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) nb += __shfl_down_sync(0xffffffffu, nb, o);
+  if ((threadIdx.x & 31) == 0 && nb && bad) atomicAdd(bad, nb);
+}
+}  // namespace
+
+namespace kcg {
+void launch_form_rows(const int64_t* lo, const int64_t* hi, const uint8_t* status, const double* T, size_t n,
+                      int F, double* X, unsigned long long* bad, void* stream) {
+  if (n == 0) return;
+  const size_t need = (n + 255) / 256, cap = static_cast<size_t>(num_sms()) * 8;
+  kcg_form_rows<<<static_cast<unsigned>(need < cap ? need : cap), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const long long*>(lo), reinterpret_cast<const long long*>(hi), status, T,
+      static_cast<long long>(n), F, X, bad);
+  check(cudaGetLastError(), "kcg_form_rows launch");
+}
+}  // namespace kcg

@@ -570,3 +570,43 @@ def test_gram_accumulate_random_shapes():
         torch.testing.assert_close(st.G, ref, rtol=1e-12, atol=0, msg=f"F={F} N={N} ld={ld}")
         torch.testing.assert_close(st.xt1, X.sum(0), rtol=1e-12, atol=0)
         assert torch.equal(st.colmax, X.abs().max(0).values), F
+
+
+def _wide_program(nkeys=60):
+    keys = kc.schema_keys()
+    lines = ["kernelcost-program v1", f"kernel wide{nkeys}", "param n", "param m", "assume n >= 1", "assume m >= 1"]
+    k = 0
+    for a in range(1, 9):
+        for b in range(0, 8):
+            if k < nkeys:
+                lines.append(f"prop {keys[k]} (* (^ n {a}) (^ m {b}))" if b else f"prop {keys[k]} (^ n {a})")
+                k += 1
+    return kc.Program("\n".join(lines + ["end"]) + "\n")
+
+
+def test_fused_gram_wide_rows_take_the_chunked_path():
+    """60 keys over 60 distinct monomials (no narrower basis): the fused Gram
+    and residual form rows in HBM chunk by chunk (exact counts -> RN(count)/T
+    -> the per-width DMMA Gram) and equal the materialised statistics; bad
+    rows are counted."""
+    prog = _wide_program()
+    g = torch.Generator(device="cpu").manual_seed(60)
+    n = (1 << 18) + 1234  # two chunks
+    cols = {p: torch.randint(1, 21, (n,), generator=g).cuda() for p in prog.params}
+    cols["n"][::97] = -1  # inadmissible
+    T = (0.5 + torch.rand(n, generator=g, dtype=torch.float64)).cuda()
+    st = kc.gram_fused(prog, cols, T)
+    bb = kc.evaluate_properties(prog, cols)
+    ok = bb.status == 0
+    X = (bb.counts_lo.to(torch.float64) / T).T[ok].contiguous()
+    ref = kc.gram_accumulate(X)
+    alpha = [1e-12 * (1 + (i % 5)) for i in range(149)]
+    a = torch.tensor([alpha[k] for k in prog.props], dtype=torch.float64, device="cuda")
+    want = float(((1.0 - X @ a) ** 2).sum())
+    got = kc.residual_fused(prog, cols, T, alpha)
+    torch.cuda.synchronize()
+    assert st.bad_rows == int((~ok).sum())
+    torch.testing.assert_close(st.G, ref.G, rtol=1e-12, atol=0)
+    torch.testing.assert_close(st.xt1, ref.xt1, rtol=1e-12, atol=0)
+    assert torch.equal(st.colmax, ref.colmax)
+    assert got == pytest.approx(want, rel=1e-12)
