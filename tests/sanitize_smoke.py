@@ -44,6 +44,13 @@ prog.set_gram_basis(True)
 grid = kc.Grid.for_program(prog, {"n": (8, 8, 61), "m": (16, 16, 59), "l": (16, 48, 47)})
 kc.predict_grid(w, prog, grid, 17, grid.size - 20, with_status=True)
 kc.grid_bindings(grid, 5, 1000)
+# fused rows wider than 48 columns: the chunked path (counts -> rows -> wide DMMA Gram)
+keys = kc.schema_keys()
+wl = ["kernelcost-program v1", "kernel wide52", "param n", "param m", "assume n >= 1", "assume m >= 1"]
+wl += [f"prop {keys[k]} (* (^ n {1 + k // 8}) (^ m {k % 8}))" for k in range(52)] + ["end"]
+wp = kc.Program("\n".join(wl) + "\n")
+wc = {q: torch.randint(1, 9, (5000,), device="cuda") for q in wp.params}
+kc.gram_fused(wp, wc, torch.rand(5000, dtype=torch.float64, device="cuda") + 0.5)
 # GPU enumeration oracle: box-flattened and triangular domains
 kc.load_enum_program("fd_stencil_g16x16").enumerate_points({"n": 256})
 kc.load_enum_program("x_triangle").enumerate_points({"n": 300})
