@@ -533,7 +533,9 @@ def _sharded_fit(kc, torch, dev, world, rank, rows):
             # two streaming passes over the rows (Gram, then residual at the
             # solved weights), 8*P + 8 = 32 B per row each
             "bytes_per_row": 64,
-            "hbm_frac": 64.0 * rows / sec / 1e9 / peaks()[0]}
+            "hbm_frac": 64.0 * rows / sec / 1e9 / peaks()[0],
+            "peak_note": "the peak is MEASURED_PEAKS' copy rate (read + write); these passes only read, "
+                         "and read streams run above it"}
 
 
 def _timed(torch, fn, reps=5, warm=2):

@@ -663,7 +663,7 @@ int kcg_gram_fused(const kcg_program* cp, const int64_t* const* param_cols, cons
     ab.push<int32_t>(vec ? 1 : 0);
     ab.finish();
     // persistent TMA-streamed kernel (2 CTAs/SM for the DMMA variant)
-    kcg::launch_jit(p->jit_gram, ab.b.data(), ab.b.size(), kcg::num_sms() * kcg::fused_ctas_per_sm(), 256, stream,
+    kcg::launch_jit(p->jit_gram, ab.b.data(), ab.b.size(), kcg::num_sms() * kcg::fused_ctas_per_sm(p->low, true), 256, stream,
                     kcg::fused_smem_bytes(np, p->low, true));
     ++g_launches;
     return KCG_OK;
@@ -744,7 +744,7 @@ int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, 
     }
     for (double v : al) ab.push<double>(v);
     ab.finish();
-    kcg::launch_jit(p->jit_resid, ab.b.data(), ab.b.size(), kcg::num_sms() * kcg::fused_ctas_per_sm(), 256, stream,
+    kcg::launch_jit(p->jit_resid, ab.b.data(), ab.b.size(), kcg::num_sms() * kcg::fused_ctas_per_sm(p->low, false), 256, stream,
                     kcg::fused_smem_bytes(np, p->low, false));
     ++g_launches;
     return KCG_OK;

@@ -612,11 +612,16 @@ int env_int(const char* name, int dflt, int lo, int hi);
 
 // ring depth of the fused (bindings + T) kernels: 64 KB when two CTAs also
 // hold 35 KB of DMMA row buffers each, 96 KB otherwise (3 stages for P = 3)
-int fused_ctas() { return env_int("KCG_FUSED_CTAS", 2, 1, 4); }
+// Register-path fused kernels (residual, basis Gram) evaluate one row at a
+// time straight from the stage (~80 registers) and run 3 CTAs per SM with a
+// 64 KB ring each (measured: Gram 5.35 -> 6.12 TB/s, residual 6.25 -> 7.0
+// TB/s); the DMMA Gram keeps 2 CTAs (its row buffers need the shared memory).
+int fused_ctas(bool dmma) { return env_int("KCG_FUSED_CTAS", dmma ? 2 : 3, 1, 4); }
+bool fused_rowwise(bool dmma) { return env_int("KCG_FUSED_ROWWISE", dmma ? 0 : 1, 0, 1) == 1; }
 
 int fused_stages(int n_cols, bool dmma) {
   const int per = (n_cols + 1) * 1024 * 8;
-  const int s = (env_int("KCG_FUSED_RING_KB", dmma ? 64 : 96, 16, 200) * 1024) / per;
+  const int s = (env_int("KCG_FUSED_RING_KB", 64, 16, 200) * 1024) / per;
   return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
 
@@ -789,7 +794,6 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 }  // namespace
 
 int tma_ctas_per_sm() { return tma_ctas(); }
-int fused_ctas_per_sm() { return fused_ctas(); }
 
 
 GramBasis gram_basis(const Lowered& L) {
@@ -854,6 +858,10 @@ size_t fused_smem_bytes(int n_cols, const Lowered& L, bool gram) {
   else
     b += static_cast<size_t>(256) * WA * 8;      // slow-path rows
   return b;
+}
+
+int fused_ctas_per_sm(const Lowered& L, bool gram) {
+  return fused_ctas(gram && gram_dmma(gram_basis(L).width(static_cast<int>(L.keys.size()))));
 }
 
 size_t tma_smem_bytes(int n_cols) {
@@ -1311,7 +1319,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     os << "        }\n      }\n";
   };
 
-  os << "extern \"C\" __global__ void __launch_bounds__(256, " << fused_ctas() << ") " << name
+  os << "extern \"C\" __global__ void __launch_bounds__(256, " << fused_ctas(dmma) << ") " << name
      << "(const __grid_constant__ KcgArgs a) {\n"
         "  constexpr int TP = "
      << kTmaTile << ", S = " << S << ", NC = " << NC
@@ -1356,32 +1364,48 @@ std::string codegen(const std::vector<const Lowered*>& progs,
         "      while (!done)\n"
         "        asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\"\n"
         "                     : \"=r\"(done) : \"r\"(fb + 8 * s), \"r\"(parity) : \"memory\"); }\n"
-        "    kcg_i64 q[4]["
-     << NP << "]; double tq[4];\n"
-              "    #pragma unroll\n"
-              "    for (int j = 0; j < NC; ++j) {\n"
-              "      const longlong2* src = reinterpret_cast<const longlong2*>(buf + (s * NC + j) * TP) + 2 * threadIdx.x;\n"
-              "      const longlong2 x0 = src[0], x1 = src[1];\n"
-              "      if (j < NC - 1) { q[0][j] = x0.x; q[1][j] = x0.y; q[2][j] = x1.x; q[3][j] = x1.y; }\n"
-              "      else { tq[0] = __longlong_as_double(x0.x); tq[1] = __longlong_as_double(x0.y);\n"
-              "             tq[2] = __longlong_as_double(x1.x); tq[3] = __longlong_as_double(x1.y); }\n"
-              "    }\n"
-              "    // last warp to finish reading stage s refills it (no CTA-wide barrier:\n"
-              "    // warps drift apart freely between tiles)\n"
-              "    __syncwarp();\n"
-              "    if ((threadIdx.x & 31) == 0) {\n"
-              "      __threadfence_block();\n"
-              "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
-              "        reads[s] = 0;\n"
-              "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
-              "        if (nt < ntiles) issue(s, nt);\n"
-              "      }\n"
-              "    }\n"
-              "    const kcg_i64 base = tile * TP + 4 * threadIdx.x;\n"
-              "    #pragma unroll\n"
-              "    for (int u = 0; u < 4; ++u) {\n";
-  emit_make_row("q[u]", "tq[u]", "base + u", "true");
-  os << cons_row.str() << "    }\n  }\n";
+        "";
+  const std::string release =
+      "    // last warp to finish reading stage s refills it (no CTA-wide barrier:\n"
+      "    // warps drift apart freely between tiles)\n"
+      "    __syncwarp();\n"
+      "    if ((threadIdx.x & 31) == 0) {\n"
+      "      __threadfence_block();\n"
+      "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
+      "        reads[s] = 0;\n"
+      "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+      "        if (nt < ntiles) issue(s, nt);\n"
+      "      }\n"
+      "    }\n";
+  if (fused_rowwise(dmma)) {
+    // one row at a time straight from the stage (fewer live registers), the
+    // stage released after the thread's 4 rows
+    os << "    const kcg_i64 base = tile * TP + 4 * threadIdx.x;\n"
+          "    #pragma unroll 1\n"
+          "    for (int u = 0; u < 4; ++u) {\n"
+          "      kcg_i64 qu["
+       << NP << "];\n      #pragma unroll\n      for (int j = 0; j < NC - 1; ++j) qu[j] = buf[(s * NC + j) * TP + 4 * threadIdx.x + u];\n"
+                "      const double tu = __longlong_as_double(buf[(s * NC + NC - 1) * TP + 4 * threadIdx.x + u]);\n";
+    emit_make_row("qu", "tu", "base + u", "true");
+    os << cons_row.str() << "    }\n" << release << "  }\n";
+  } else {
+    os << "    kcg_i64 q[4]["
+       << NP << "]; double tq[4];\n"
+                "    #pragma unroll\n"
+                "    for (int j = 0; j < NC; ++j) {\n"
+                "      const longlong2* src = reinterpret_cast<const longlong2*>(buf + (s * NC + j) * TP) + 2 * threadIdx.x;\n"
+                "      const longlong2 x0 = src[0], x1 = src[1];\n"
+                "      if (j < NC - 1) { q[0][j] = x0.x; q[1][j] = x0.y; q[2][j] = x1.x; q[3][j] = x1.y; }\n"
+                "      else { tq[0] = __longlong_as_double(x0.x); tq[1] = __longlong_as_double(x0.y);\n"
+                "             tq[2] = __longlong_as_double(x1.x); tq[3] = __longlong_as_double(x1.y); }\n"
+                "    }\n"
+             << release
+             << "    const kcg_i64 base = tile * TP + 4 * threadIdx.x;\n"
+                "    #pragma unroll\n"
+                "    for (int u = 0; u < 4; ++u) {\n";
+    emit_make_row("q[u]", "tq[u]", "base + u", "true");
+    os << cons_row.str() << "    }\n  }\n";
+  }
   // tail (and the whole range when not aligned): warp-uniform trip counts
   os << "  {\n"
         "    const kcg_i64 t0 = ntiles * TP;\n"
