@@ -267,6 +267,8 @@ def main():
                    "parallelism": f"dp{world} (contiguous size shards)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
+                     "peak_note": "MEASURED_PEAKS hbm_gbs is a copy (50% writes); this kernel's traffic is "
+                                  "75% reads (24 B in, 8 B out per point), which HBM serves faster",
                      "traffic_source": "profiles/r01_launches_eval.csv (ncu, per launch)",
                      "kernel": "kcg_eval_<variant> (NVRTC sm_100a)",
                      "algorithmic_bytes_per_launch": bytes_per_launch,

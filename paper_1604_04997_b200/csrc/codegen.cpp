@@ -547,6 +547,33 @@ void emit_grid_kernel(std::ostringstream& os, int n_cols, const std::string& nam
   }
   // 2 CTAs/SM: the 4-point odometer state plus the exact evaluation need
   // ~100 registers; the 64-register cap of the streaming kernels spills
+  if (grid_rowwise()) {
+    // one point per thread and step (coalesced scalar stores), digits
+    // advanced by those of gridDim * blockDim: few registers, 3 CTAs/SM
+    os << "extern \"C\" __global__ void __launch_bounds__(256, 3) " << name
+       << "(const __grid_constant__ KcgGridArgs g) {\n"
+          "  const KcgArgs& a = g.a;\n"
+          "  const kcg_i64 tid = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x;\n"
+          "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
+          "  if (tid >= a.n) return;\n"
+          "  kcg_u64 d["
+       << NP << "];\n  { kcg_u64 r = g.first + (kcg_u64)tid;\n    #pragma unroll\n    for (int j = " << n_cols - 1
+       << "; j >= 0; --j) { d[j] = r % g.count[j]; r /= g.count[j]; } }\n"
+          "  for (kcg_i64 i = tid; i < a.n; i += stride) {\n"
+          "    kcg_i64 p["
+       << NP << "];\n    #pragma unroll\n    for (int j = 0; j < " << n_cols
+       << "; ++j) p[j] = g.start[j] + g.step[j] * (kcg_i64)d[j];\n"
+          "    double s = kcg_nan();\n"
+          "    int st = kcg_point_fast<"
+       << gen << ">(p, a, i, s);\n"
+          "    if (st < 0) { const KcgRes r = kcg_point_slow_g(g, i); s = r.s; st = r.st; }\n"
+          "    if (st != KCG_PT_OK && st != KCG_PT_COUNT_WIDE) s = kcg_nan();\n"
+          "    if (a.pred) __stcs(a.pred + i, s);\n"
+          "    if (a.status) a.status[i] = (unsigned char)st;\n"
+          "    kcg_odo_add(d, g.sdig, g.count);\n"
+          "  }\n}\n";
+    return;
+  }
   os << "extern \"C\" __global__ void __launch_bounds__(256, 2) " << name
      << "(const __grid_constant__ KcgGridArgs g) {\n"
         "  const KcgArgs& a = g.a;\n"
@@ -632,8 +659,12 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 }
 
 // per-CTA ring size (KB) and CTAs per SM of the TMA kernel (tuning knobs)
-int tma_ring_kb() { return env_int("KCG_TMA_RING_KB", 96, 16, 200); }
-int tma_ctas() { return env_int("KCG_TMA_CTAS", 2, 1, 4); }
+// one point at a time from the stage: ~80 registers, 3 CTAs/SM with a 64 KB
+// ring each (measured on the headline step: 1.92e11 -> 2.13e11 points/s);
+// KCG_TMA_ROWWISE=0 restores the 4-points-in-registers consumer (2 CTAs/SM)
+bool tma_rowwise() { return env_int("KCG_TMA_ROWWISE", 1, 0, 1) == 1; }
+int tma_ring_kb() { return env_int("KCG_TMA_RING_KB", tma_rowwise() ? 64 : 96, 16, 200); }
+int tma_ctas() { return env_int("KCG_TMA_CTAS", tma_rowwise() ? 3 : 2, 1, 4); }
 int argmin_ctas() { return env_int("KCG_ARGMIN_CTAS", 0, 0, 8); }  // 0: no register cap
 
 int tma_stages(int n_cols) {
@@ -653,6 +684,8 @@ void emit_tma_kernel(std::ostringstream& os, int n_cols, const std::string& name
         "  extern __shared__ __align__(128) unsigned char kcg_smem[];\n"
         "  kcg_i64* buf = reinterpret_cast<kcg_i64*>(kcg_smem);\n"
         "  __shared__ __align__(8) unsigned long long full[S];\n"
+        "  __shared__ unsigned reads[S];  // row-wise variant: warps done with stage s\n"
+        "  if (threadIdx.x < S) reads[threadIdx.x] = 0;\n"
         "  const kcg_i64 ntiles = a.n / TP;\n"
         "  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);\n"
         "  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);\n"
@@ -685,6 +718,35 @@ void emit_tma_kernel(std::ostringstream& os, int n_cols, const std::string& name
         "        asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\"\n"
         "                     : \"=r\"(done) : \"r\"(fb + 8 * s), \"r\"(parity) : \"memory\");\n"
         "    }\n"
+        << (tma_rowwise()
+                ? std::string(
+                      "    // one point at a time straight from the stage (points tid + 256 u:\n"
+                      "    // conflict-free loads, coalesced stores), ~80 registers -> 3 CTAs/SM\n"
+                      "    const kcg_i64 rb = tile * TP;\n"
+                      "    #pragma unroll 1\n"
+                      "    for (int u = 0; u < 4; ++u) {\n"
+                      "      const int o = u * 256 + threadIdx.x;\n"
+                      "      kcg_i64 q[NP];\n"
+                      "      #pragma unroll\n"
+                      "      for (int j = 0; j < NP; ++j) q[j] = buf[(s * NP + j) * TP + o];\n"
+                      "      double r = kcg_nan();\n"
+                      "      int st = kcg_point_fast<0>(q, a, rb + o, r);\n"
+                      "      if (st < 0) { const KcgRes x = kcg_point_slow(a, rb + o); r = x.s; st = x.st; }\n"
+                      "      if (st != KCG_PT_OK && st != KCG_PT_COUNT_WIDE) r = kcg_nan();\n"
+                      "      if (a.pred) __stcs(a.pred + rb + o, r);\n"
+                      "      if (a.status) a.status[rb + o] = (unsigned char)st;\n"
+                      "    }\n"
+                      "    __syncwarp();\n"
+                      "    if ((threadIdx.x & 31) == 0) {\n"
+                      "      __threadfence_block();\n"
+                      "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
+                      "        reads[s] = 0;\n"
+                      "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+                      "        if (nt < ntiles) issue(s, nt);\n"
+                      "      }\n"
+                      "    }\n"
+                      "    continue;\n")
+                : std::string()) <<
         "    kcg_i64 q[4][NP];\n"
         "    #pragma unroll\n"
         "    for (int j = 0; j < NP; ++j) {\n"
@@ -793,6 +855,7 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 
 }  // namespace
 
+bool grid_rowwise() { return env_int("KCG_GRID_ROWWISE", 0, 0, 1) == 1; }
 int tma_ctas_per_sm() { return tma_ctas(); }
 
 
