@@ -1037,8 +1037,7 @@ int kcg_eval_predict_grid(const kcg_program* cp, const kcg_grid* g, uint64_t fir
       p->jit_eval_grid = kcg::jit_kernel(kcg_program_jit_source(p), nm + "_grid");
       p->jit_eval_grid_gen = kcg::jit_kernel(kcg_program_jit_source(p), nm + "_grid_gen");
     }
-    const bool rowwise = kcg::grid_rowwise();
-    const unsigned grid = rowwise ? grid_for(n, 256, 3) : grid_for((n + 3) / 4);
+    const unsigned grid = grid_for((n + 3) / 4);
     ArgBuf ab;
     for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(nullptr);  // KcgArgs.p (unused)
     ab.push<void*>(pred_out);
@@ -1063,7 +1062,7 @@ int kcg_eval_predict_grid(const kcg_program* cp, const kcg_grid* g, uint64_t fir
     for (int j = 0; j < NP; ++j) ab.push<int64_t>(j < np ? g->step[j] : 0);
     for (int j = 0; j < NP; ++j) ab.push<uint64_t>(j < np ? g->count[j] : 1);
     // digits of the per-step advance 4 * gridDim * blockDim (mod the lattice size)
-    uint64_t adv = (rowwise ? 1ull : 4ull) * grid * 256ull, dig[8] = {0};
+    uint64_t adv = 4ull * grid * 256ull, dig[8] = {0};
     for (int j = np - 1; j >= 0; --j) {
       dig[j] = adv % g->count[j];
       adv /= g->count[j];

@@ -547,33 +547,6 @@ void emit_grid_kernel(std::ostringstream& os, int n_cols, const std::string& nam
   }
   // 2 CTAs/SM: the 4-point odometer state plus the exact evaluation need
   // ~100 registers; the 64-register cap of the streaming kernels spills
-  if (grid_rowwise()) {
-    // one point per thread and step (coalesced scalar stores), digits
-    // advanced by those of gridDim * blockDim: few registers, 3 CTAs/SM
-    os << "extern \"C\" __global__ void __launch_bounds__(256, 3) " << name
-       << "(const __grid_constant__ KcgGridArgs g) {\n"
-          "  const KcgArgs& a = g.a;\n"
-          "  const kcg_i64 tid = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x;\n"
-          "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
-          "  if (tid >= a.n) return;\n"
-          "  kcg_u64 d["
-       << NP << "];\n  { kcg_u64 r = g.first + (kcg_u64)tid;\n    #pragma unroll\n    for (int j = " << n_cols - 1
-       << "; j >= 0; --j) { d[j] = r % g.count[j]; r /= g.count[j]; } }\n"
-          "  for (kcg_i64 i = tid; i < a.n; i += stride) {\n"
-          "    kcg_i64 p["
-       << NP << "];\n    #pragma unroll\n    for (int j = 0; j < " << n_cols
-       << "; ++j) p[j] = g.start[j] + g.step[j] * (kcg_i64)d[j];\n"
-          "    double s = kcg_nan();\n"
-          "    int st = kcg_point_fast<"
-       << gen << ">(p, a, i, s);\n"
-          "    if (st < 0) { const KcgRes r = kcg_point_slow_g(g, i); s = r.s; st = r.st; }\n"
-          "    if (st != KCG_PT_OK && st != KCG_PT_COUNT_WIDE) s = kcg_nan();\n"
-          "    if (a.pred) __stcs(a.pred + i, s);\n"
-          "    if (a.status) a.status[i] = (unsigned char)st;\n"
-          "    kcg_odo_add(d, g.sdig, g.count);\n"
-          "  }\n}\n";
-    return;
-  }
   os << "extern \"C\" __global__ void __launch_bounds__(256, 2) " << name
      << "(const __grid_constant__ KcgGridArgs g) {\n"
         "  const KcgArgs& a = g.a;\n"
@@ -855,7 +828,6 @@ void emit_eval_kernel(std::ostringstream& os, int n_cols, const std::string& nam
 
 }  // namespace
 
-bool grid_rowwise() { return env_int("KCG_GRID_ROWWISE", 0, 0, 1) == 1; }
 int tma_ctas_per_sm() { return tma_ctas(); }
 
 

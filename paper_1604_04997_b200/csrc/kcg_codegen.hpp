@@ -48,7 +48,6 @@ int gram_wide_ctas(int F);
 /// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.
 size_t tma_smem_bytes(int n_cols);
 int tma_ctas_per_sm();
-bool grid_rowwise();  // grid kernels: one point per thread-step (KCG_GRID_ROWWISE)
 int fused_ctas_per_sm(const Lowered& L, bool gram);  // fused Gram / residual kernels (KCG_FUSED_CTAS)
 /// Monomial basis of a program's property columns for the fused design-row
 /// reductions. Every key is count_j = sum_t coef_t * mono_t / D_j, so a
