@@ -254,6 +254,7 @@ def main():
     avg_launch = statistics.mean(kern_ms) / 1e3
     bytes_per_launch = 32.0 * n  # 8*P + 8 with P = 3
     achieved = bytes_per_launch / avg_launch / 1e9
+    mix = _same_mix_stream(torch, dev, n, stream)
 
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
@@ -269,6 +270,10 @@ def main():
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
                      "peak_note": "MEASURED_PEAKS hbm_gbs is a copy (50% writes); this kernel's traffic is "
                                   "75% reads (24 B in, 8 B out per point), which HBM serves faster",
+                     "same_mix_stream_gbs": mix,
+                     "frac_of_same_mix": achieved / mix,
+                     "same_mix_note": "torch.addcmul over three f64 columns of the same length into a fourth "
+                                      "(24 B in, 8 B out per element: this kernel's traffic mix), CUDA events",
                      "traffic_source": "profiles/r01_launches_eval.csv (ncu, per launch)",
                      "kernel": "kcg_eval_<variant> (NVRTC sm_100a)",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
@@ -375,6 +380,26 @@ def _colarr(p, cols):
     if key not in _COLS_CACHE:
         _COLS_CACHE[key] = (ctypes.c_void_p * len(p.params))(*[cols[q].data_ptr() for q in p.params])
     return _COLS_CACHE[key]
+
+
+def _same_mix_stream(torch, dev, n, stream, reps=10):
+    """GB/s of a plain streaming kernel with the headline kernel's traffic
+    mix (3 x 8 B read, 8 B written per element), timed like it: the
+    bandwidth this read:write ratio gets from HBM on this box."""
+    a, b, c = (torch.rand(n, dtype=torch.float64, device=dev) for _ in range(3))
+    d = torch.empty_like(a)
+    for _ in range(3):
+        torch.addcmul(a, b, c, out=d)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda.synchronize()
+    for e0, e1 in ev:
+        e0.record(stream)
+        torch.addcmul(a, b, c, out=d)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.median(e0.elapsed_time(e1) for e0, e1 in ev)
+    del a, b, c, d
+    return 32.0 * n / (ms / 1e3) / 1e9
 
 
 def _spot_check(kc, progs, cols, preds, alpha, r0, side):
