@@ -618,6 +618,11 @@ int env_int(const char* name, int dflt, int lo, int hi);
 // TB/s); the DMMA Gram keeps 2 CTAs (its row buffers need the shared memory).
 int fused_ctas(bool dmma) { return env_int("KCG_FUSED_CTAS", dmma ? 2 : 3, 1, 4); }
 bool fused_rowwise(bool dmma) { return env_int("KCG_FUSED_ROWWISE", dmma ? 0 : 1, 0, 1) == 1; }
+// row order and unroll of the row-wise consumer: the Gram is fastest with
+// rows tid + 256 u fully unrolled (6.17 -> 6.45 TB/s), the residual with
+// rows 4 tid + u rolled (7.01 vs 6.82 TB/s) -- profiles/ab_fused.sh
+int fused_unroll(bool gram) { return env_int("KCG_FUSED_UNROLL", gram ? 4 : 1, 1, 4); }
+bool fused_strided(bool gram) { return env_int("KCG_FUSED_STRIDED", gram ? 1 : 0, 0, 1) == 1; }
 
 int fused_stages(int n_cols, bool dmma) {
   const int per = (n_cols + 1) * 1024 * 8;
@@ -638,7 +643,9 @@ int env_int(const char* name, int dflt, int lo, int hi) {
 bool tma_rowwise() { return env_int("KCG_TMA_ROWWISE", 1, 0, 1) == 1; }
 int tma_ring_kb() { return env_int("KCG_TMA_RING_KB", tma_rowwise() ? 64 : 96, 16, 200); }
 int tma_ctas() { return env_int("KCG_TMA_CTAS", tma_rowwise() ? 3 : 2, 1, 4); }
+int tma_unroll() { return env_int("KCG_TMA_UNROLL", 4, 1, 4); }  // 1 -> 4: 2.10e11 -> 2.18e11 points/s
 int argmin_ctas() { return env_int("KCG_ARGMIN_CTAS", 0, 0, 8); }  // 0: no register cap
+bool argmin_prefetch() { return env_int("KCG_ARGMIN_PREFETCH", 1, 0, 1) == 1; }
 
 int tma_stages(int n_cols) {
   const int per = (n_cols > 0 ? n_cols : 1) * kTmaTile * 8;
@@ -696,7 +703,7 @@ void emit_tma_kernel(std::ostringstream& os, int n_cols, const std::string& name
                       "    // one point at a time straight from the stage (points tid + 256 u:\n"
                       "    // conflict-free loads, coalesced stores), ~80 registers -> 3 CTAs/SM\n"
                       "    const kcg_i64 rb = tile * TP;\n"
-                      "    #pragma unroll 1\n"
+                      "    #pragma unroll " + std::to_string(tma_unroll()) + "\n"
                       "    for (int u = 0; u < 4; ++u) {\n"
                       "      const int o = u * 256 + threadIdx.x;\n"
                       "      kcg_i64 q[NP];\n"
@@ -1024,11 +1031,26 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     os << "extern \"C\" __global__ void __launch_bounds__(256" << (mb > 0 ? ", " + std::to_string(mb) : "")
        << ") " << name
        << "(const __grid_constant__ KcgArgs a) {\n"
-          "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n"
-          "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {\n"
-          "    kcg_i64 p["
-       << NP << "];\n";
-    for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
+          "  const kcg_i64 stride = (kcg_i64)gridDim.x * blockDim.x;\n";
+    if (argmin_prefetch()) {
+      // the next size's bindings are loaded before this size is evaluated:
+      // the load latency hides behind the V evaluations (ncu: the first use
+      // of the bindings was the kernel's dominant stall)
+      os << "  kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x;\n"
+            "  kcg_i64 pn["
+         << NP << "];\n  if (i < a.n) {\n";
+      for (int j = 0; j < n_cols; ++j) os << "    pn[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
+      os << "  }\n  for (; i < a.n; i += stride) {\n    kcg_i64 p[" << NP << "];\n";
+      for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = pn[" << j << "];\n";
+      os << "    if (i + stride < a.n) {\n";
+      for (int j = 0; j < n_cols; ++j) os << "      pn[" << j << "] = __ldcs(a.p[" << j << "] + i + stride);\n";
+      os << "    }\n";
+    } else {
+      os << "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += stride) {\n"
+            "    kcg_i64 p["
+         << NP << "];\n";
+      for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
+    }
     os << "    int bi; double bt;\n    kcg_best(p, a, i, bi, bt);\n"
           "    __stcs(a.best + i, bi);\n    __stcs(a.best_t + i, bt);\n  }\n}\n";
     return os.str();
@@ -1415,13 +1437,18 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   if (fused_rowwise(dmma)) {
     // one row at a time straight from the stage (fewer live registers), the
     // stage released after the thread's 4 rows
-    os << "    const kcg_i64 base = tile * TP + 4 * threadIdx.x;\n"
-          "    #pragma unroll 1\n"
+    // rows tid + 256 u (conflict-free stage loads) or 4 tid + u
+    const bool strided = fused_strided(gram);
+    const std::string off = strided ? "u * 256 + threadIdx.x" : "4 * threadIdx.x + u";
+    os << "    const kcg_i64 base = tile * TP;\n"
+          "    #pragma unroll "
+       << fused_unroll(gram) << "\n"
           "    for (int u = 0; u < 4; ++u) {\n"
+          "      const int o = " << off << ";\n"
           "      kcg_i64 qu["
-       << NP << "];\n      #pragma unroll\n      for (int j = 0; j < NC - 1; ++j) qu[j] = buf[(s * NC + j) * TP + 4 * threadIdx.x + u];\n"
-                "      const double tu = __longlong_as_double(buf[(s * NC + NC - 1) * TP + 4 * threadIdx.x + u]);\n";
-    emit_make_row("qu", "tu", "base + u", "true");
+       << NP << "];\n      #pragma unroll\n      for (int j = 0; j < NC - 1; ++j) qu[j] = buf[(s * NC + j) * TP + o];\n"
+                "      const double tu = __longlong_as_double(buf[(s * NC + NC - 1) * TP + o]);\n";
+    emit_make_row("qu", "tu", "base + o", "true");
     os << cons_row.str() << "    }\n" << release << "  }\n";
   } else {
     os << "    kcg_i64 q[4]["
