@@ -454,7 +454,7 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
     static const bool no_tma = std::getenv("KCG_NO_TMA") != nullptr;
     const size_t tiles = n / kcg::kTmaPointsPerTile;
     if (finite && vec && !no_tma && tiles >= static_cast<size_t>(kcg::num_sms())) {
-      // TMA-staged persistent kernel: 2 CTAs per SM
+      // TMA-staged persistent kernel: tma_ctas_per_sm() CTAs per SM
       const unsigned grid = static_cast<unsigned>(
           std::min<size_t>(tiles, static_cast<size_t>(kcg::num_sms()) * kcg::tma_ctas_per_sm()));
       kcg::launch_jit(p->jit_eval_tma, ab.b.data(), ab.b.size(), grid, 256, stream,

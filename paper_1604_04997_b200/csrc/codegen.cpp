@@ -647,8 +647,12 @@ int tma_unroll() { return env_int("KCG_TMA_UNROLL", 4, 1, 4); }  // 1 -> 4: 2.10
 int argmin_ctas() { return env_int("KCG_ARGMIN_CTAS", 0, 0, 8); }  // 0: no register cap
 bool argmin_prefetch() { return env_int("KCG_ARGMIN_PREFETCH", 1, 0, 1) == 1; }
 
+// points per TMA stage of the eval kernel (row-wise consumers: a multiple
+// of the 256-thread CTA)
+int tma_tile() { return tma_rowwise() ? 256 * env_int("KCG_TMA_TILE_Q", 4, 1, 8) : kTmaTile; }
+
 int tma_stages(int n_cols) {
-  const int per = (n_cols > 0 ? n_cols : 1) * kTmaTile * 8;
+  const int per = (n_cols > 0 ? n_cols : 1) * tma_tile() * 8;
   int s = (tma_ring_kb() * 1024) / per;
   return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
@@ -659,7 +663,7 @@ void emit_tma_kernel(std::ostringstream& os, int n_cols, const std::string& name
   os << "extern \"C\" __global__ void __launch_bounds__(256, " << tma_ctas() << ") " << name
      << "(const __grid_constant__ KcgArgs a) {\n"
         "  constexpr int TP = "
-     << kTmaTile << ", S = " << S << ", NP = " << NP
+     << tma_tile() << ", S = " << S << ", NP = " << NP
      << ";\n"
         "  extern __shared__ __align__(128) unsigned char kcg_smem[];\n"
         "  kcg_i64* buf = reinterpret_cast<kcg_i64*>(kcg_smem);\n"
@@ -704,7 +708,7 @@ void emit_tma_kernel(std::ostringstream& os, int n_cols, const std::string& name
                       "    // conflict-free loads, coalesced stores), ~80 registers -> 3 CTAs/SM\n"
                       "    const kcg_i64 rb = tile * TP;\n"
                       "    #pragma unroll " + std::to_string(tma_unroll()) + "\n"
-                      "    for (int u = 0; u < 4; ++u) {\n"
+                      "    for (int u = 0; u < TP / 256; ++u) {\n"
                       "      const int o = u * 256 + threadIdx.x;\n"
                       "      kcg_i64 q[NP];\n"
                       "      #pragma unroll\n"
@@ -907,7 +911,7 @@ int fused_ctas_per_sm(const Lowered& L, bool gram) {
 }
 
 size_t tma_smem_bytes(int n_cols) {
-  return static_cast<size_t>(tma_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * kTmaTile * 8;
+  return static_cast<size_t>(tma_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * tma_tile() * 8;
 }
 
 std::string codegen(const std::vector<const Lowered*>& progs,
