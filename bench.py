@@ -255,6 +255,7 @@ def main():
     bytes_per_launch = 32.0 * n  # 8*P + 8 with P = 3
     achieved = bytes_per_launch / avg_launch / 1e9
     mix = _same_mix_stream(torch, dev, n, stream)
+    pipes = _pipe_peaks(kc)
 
     line = {
         "metric": METRIC, "value": value, "unit": "points/s", "n_gpus": world,
@@ -278,6 +279,10 @@ def main():
                      "kernel": "kcg_eval_<variant> (NVRTC sm_100a)",
                      "algorithmic_bytes_per_launch": bytes_per_launch,
                      "avg_launch_ms": avg_launch * 1e3},
+        "instruction_roofline": _instr_roofline(_ncu_lane_instr("r01_eval_tma_ncu_full.txt"),
+                                                avg_launch and n / avg_launch, pipes,
+                                                "profiles/r01_eval_tma_ncu_full.txt (ncu, same kernel)"),
+        "pipe_peaks_lane_ops_per_s": pipes,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "spot_checked_points": checked,
@@ -380,6 +385,35 @@ def _colarr(p, cols):
     if key not in _COLS_CACHE:
         _COLS_CACHE[key] = (ctypes.c_void_p * len(p.params))(*[cols[q].data_ptr() for q in p.params])
     return _COLS_CACHE[key]
+
+
+def _pipe_peaks(kc):
+    """Measured lane-op rates of the pipes the exact evaluation runs on
+    (csrc/peaks.cu via kcg_measure_pipe_peak): the instruction roofline's
+    denominators (MEASURED_PEAKS has no INT32 / FP64 figures)."""
+    return {k: kc.measure_pipe_peak(k) for k in ("imad", "lop3", "dfma", "issue")}
+
+
+def _ncu_lane_instr(name):
+    """Lane instructions per point of a kernel, from its committed ncu
+    capture (profiles/<name>: SASS instructions executed / points)."""
+    try:
+        for ln in (ROOT / "profiles" / name).read_text().splitlines():
+            if ln.strip().startswith("lane instructions per point:"):
+                return float(ln.split(":")[1])
+    except OSError:
+        pass
+    return None
+
+
+def _instr_roofline(lane_instr, points_per_s, peaks, source):
+    if lane_instr is None:
+        return None
+    achieved = lane_instr * points_per_s
+    return {"bound": "issue", "lane_instr_per_point": lane_instr, "achieved_lane_ops_per_s": achieved,
+            "peak_lane_ops_per_s": peaks["issue"], "frac": achieved / peaks["issue"],
+            "peak_note": "measured: IMAD and LOP3 alternating at full occupancy (kcg_measure_pipe_peak kind 3)",
+            "lane_instr_source": source}
 
 
 def _same_mix_stream(torch, dev, n, stream, reps=10):
@@ -694,6 +728,8 @@ def _extras(kc, torch, dev, args):
         "points_per_s": total * len(progs) / sec, "sizes_per_s": total / sec,
         "bytes_per_size": 36, "hbm_frac": 36 * total / sec / 1e9 / hbm,
         "best_variant_histogram": torch.bincount(best.to(torch.int64) + 1, minlength=len(progs) + 1).tolist(),
+        "instruction_roofline": _instr_roofline(_ncu_lane_instr("r01_argmin_ncu.txt"), total * len(progs) / sec,
+                                                _pipe_peaks(kc), "profiles/r01_argmin_ncu.txt (ncu, same kernel)"),
         "note": "one fused launch per step; 24 B bindings in, int32 + fp64 out per size"}
     # the same launch also writing every variant's prediction (variant-major):
     # all 1e9 predictions with the bindings read once (24 + 48 B per size

@@ -325,6 +325,12 @@ const char* kcg_point_status_str(int point_status);
 const char* kcg_last_error(void);
 /* number of kernels this library launched since load (all entry points)  */
 uint64_t kcg_launch_count(void);
+/* measured pipe throughput of the current device, lane operations per
+ * second (the instruction roofline's denominators): kind 0 IMAD, 1 LOP3,
+ * 2 DFMA, 3 IMAD + LOP3 alternating (the issue rate of an integer mix).
+ * `iters` x 128 steps of 8 chains per thread, full occupancy; synchronous,
+ * on the default stream. Its launches are not counted by kcg_launch_count. */
+int kcg_measure_pipe_peak(int kind, uint64_t iters, double* lane_ops_per_s);
 
 #ifdef __cplusplus
 }

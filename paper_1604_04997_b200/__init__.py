@@ -32,6 +32,7 @@ from .api import (  # noqa: F401
     gram_accumulate,
     gram_fused,
     launch_count,
+    measure_pipe_peak,
     load_program,
     noiseless_time,
     predict,

@@ -103,6 +103,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_point_status_str": (ctypes.c_char_p, [ctypes.c_int]),
         "kcg_last_error": (ctypes.c_char_p, []),
         "kcg_launch_count": (ctypes.c_uint64, []),
+        "kcg_measure_pipe_peak": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

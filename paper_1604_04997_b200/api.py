@@ -411,6 +411,19 @@ def launch_count() -> int:
     return int(lib().kcg_launch_count())
 
 
+PIPE_KINDS = {"imad": 0, "lop3": 1, "dfma": 2, "issue": 3}
+
+
+def measure_pipe_peak(kind: str, iters: int = 4096) -> float:
+    """Measured lane operations per second of one pipe of the current device
+    (csrc/peaks.cu): "imad", "lop3", "dfma", or "issue" (IMAD and LOP3
+    alternating, i.e. the scheduler's issue rate for an integer mix)."""
+    import ctypes
+    out = ctypes.c_double()
+    check(lib().kcg_measure_pipe_peak(PIPE_KINDS[kind], iters, ctypes.byref(out)))
+    return out.value
+
+
 # ---------------------------------------------------------------------------
 # measurement CSVs -> GPU fit / eval (the CLI's `fit` and `eval`,
 # kernelcost.cpp:236-272 and 366-400)

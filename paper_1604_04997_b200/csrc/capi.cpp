@@ -936,6 +936,16 @@ const char* kcg_last_error(void) { return g_last_error.c_str(); }
 
 uint64_t kcg_launch_count(void) { return g_launches.load(); }
 
+int kcg_measure_pipe_peak(int kind, uint64_t iters, double* lane_ops_per_s) {
+  if (kind < 0 || kind > 3 || iters == 0 || !lane_ops_per_s)
+    return fail(KCG_E_INVALID_ARGUMENT, "bad pipe-peak arguments");
+  return guarded([&] {
+    require_device();
+    *lane_ops_per_s = kcg::measure_pipe_peak(kind, iters);
+    return KCG_OK;
+  });
+}
+
 }  // extern "C"
 
 // ---- GPU enumeration oracle --------------------------------------------------

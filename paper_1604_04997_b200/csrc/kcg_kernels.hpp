@@ -74,5 +74,8 @@ void launch_grid_fill(int np, const int64_t* start, const int64_t* step, const u
                       size_t n, int64_t* const* cols, void* stream);
 
 int num_sms();
+// lane operations per second of one pipe (peaks.cu: 0 IMAD, 1 LOP3, 2 DFMA,
+// 3 IMAD+LOP3 issue mix); synchronous on the current device
+double measure_pipe_peak(int kind, unsigned long long iters);
 
 }  // namespace kcg

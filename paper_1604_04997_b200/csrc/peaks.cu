@@ -1,0 +1,114 @@
+// Pipe-throughput probes: the measured denominators of the instruction
+// roofline that SURVEY §8(d) asks for (config 4 is bound by the instruction
+// pipes; MEASURED_PEAKS.json holds only HBM and bf16 tensor figures).
+//
+// Every thread runs 8 independent dependency chains of one PTX instruction
+// (inline asm volatile, so ptxas keeps exactly one SASS instruction per step):
+//   kind 0  mad.lo.u32          -> IMAD  (integer multiply-add)
+//   kind 1  lop3.b32            -> LOP3  (integer ALU pipe)
+//   kind 2  fma.rn.f64          -> DFMA  (FP64 pipe)
+//   kind 3  IMAD and LOP3 alternating: two pipes fed at once, i.e. the
+//           warp-scheduler issue rate for the integer mix the eval / argmin
+//           kernels execute
+// at full occupancy (8 CTAs x 256 threads per SM). The result is lane
+// operations per second; the loop's own 3 instructions per 128 steps are not
+// counted, so the figure is a slight underestimate of the pipe peak.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kcg_kernels.hpp"
+
+namespace {
+
+constexpr int kChains = 8;
+constexpr int kUnroll = 16;
+
+template <int KIND>
+__global__ void __launch_bounds__(256) kcg_peak_probe(unsigned long long iters, unsigned seed,
+                                                      unsigned long long* sink) {
+  if constexpr (KIND == 2) {
+    double a[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) a[c] = 1.0 + 1e-9 * (threadIdx.x + c + seed);
+    const double b = 0.999999, d = 1e-12;
+    for (unsigned long long i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(a[c]) : "d"(b), "d"(d));
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += a[c];
+    if (s == 12345.0) sink[0] = 1;
+  } else {
+    unsigned a[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) a[c] = threadIdx.x * 2654435761u + c + seed;
+    const unsigned b = seed | 1u, d = 0x9e3779b9u;
+    for (unsigned long long i = 0; i < iters; ++i) {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u)
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) {
+          if (KIND == 0 || (KIND == 3 && (c & 1) == 0))
+            asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[c]) : "r"(b), "r"(d));
+          else
+            asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(a[c]) : "r"(b), "r"(d));
+        }
+    }
+    unsigned s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s ^= a[c];
+    if (s == 0x12345678u) sink[0] = s;
+  }
+}
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+namespace kcg {
+
+double measure_pipe_peak(int kind, unsigned long long iters) {
+  const unsigned grid = static_cast<unsigned>(num_sms()) * 8;
+  unsigned long long* sink = nullptr;
+  check(cudaMalloc(&sink, sizeof(unsigned long long)), "cudaMalloc");
+  cudaEvent_t e0, e1;
+  check(cudaEventCreate(&e0), "cudaEventCreate");
+  check(cudaEventCreate(&e1), "cudaEventCreate");
+  auto launch = [&](unsigned long long it) {
+    switch (kind) {
+      case 0: kcg_peak_probe<0><<<grid, 256>>>(it, 7u, sink); break;
+      case 1: kcg_peak_probe<1><<<grid, 256>>>(it, 7u, sink); break;
+      case 2: kcg_peak_probe<2><<<grid, 256>>>(it, 7u, sink); break;
+      default: kcg_peak_probe<3><<<grid, 256>>>(it, 7u, sink); break;
+    }
+    check(cudaGetLastError(), "kcg_peak_probe launch");
+  };
+  launch(iters / 8 + 1);  // warm-up (clocks up, module loaded)
+  std::vector<float> ms;
+  for (int r = 0; r < 3; ++r) {
+    check(cudaEventRecord(e0), "cudaEventRecord");
+    launch(iters);
+    check(cudaEventRecord(e1), "cudaEventRecord");
+    check(cudaEventSynchronize(e1), "cudaEventSynchronize");
+    float t = 0;
+    check(cudaEventElapsedTime(&t, e0, e1), "cudaEventElapsedTime");
+    ms.push_back(t);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  std::sort(ms.begin(), ms.end());
+  const double ops = static_cast<double>(grid) * 256.0 * static_cast<double>(iters) * kUnroll * kChains;
+  return ops / (ms[1] / 1e3);
+}
+
+}  // namespace kcg

@@ -95,6 +95,31 @@ def test_launches_fail_loudly_without_gpu():
     assert b"no CUDA device" in _capi.lib().kcg_last_error()
 
 
+def test_pipe_peak_probe_arguments_and_no_gpu():
+    out = ctypes.c_double()
+    assert _capi.lib().kcg_measure_pipe_peak(4, 16, ctypes.byref(out)) == _capi.E_INVALID_ARGUMENT
+    assert _capi.lib().kcg_measure_pipe_peak(0, 0, ctypes.byref(out)) == _capi.E_INVALID_ARGUMENT
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    assert _capi.lib().kcg_measure_pipe_peak(0, 16, ctypes.byref(out)) == _capi.E_CUDA
+
+
+@pytest.mark.gpu
+def test_pipe_peaks_are_plausible():
+    """The instruction-roofline denominators (csrc/peaks.cu) on this device:
+    every pipe below the issue bound (4 warp-instructions per clock per SM),
+    the IMAD + LOP3 mix above either pipe alone."""
+    import torch
+    p = torch.cuda.get_device_properties(0)
+    clock = 2.1e9  # above the B200's 1965 MHz boost
+    issue_bound = p.multi_processor_count * 4 * 32 * clock
+    r = {k: kc.measure_pipe_peak(k) for k in ("imad", "lop3", "dfma", "issue")}
+    for k, v in r.items():
+        assert 1e12 < v < issue_bound, (k, v)
+    assert r["issue"] > 1.2 * max(r["imad"], r["lop3"]), r
+
+
 def test_weights_json_round_trip_is_byte_identical(tmp_path):
     src = GOLDEN / "weights_suite.json"
     w = kc.read_weights_json(src)
