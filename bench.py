@@ -455,65 +455,56 @@ def _spot_check(kc, progs, cols, preds, alpha, r0, side):
 
 
 def _e2e(kc, progs, w, args, torch, dev, world, rank):
-    """Same workload through the public C ABI with HOST buffers: pinned
-    bindings in, predictions out, copies inside the timed region (chunked,
-    two streams so H2D / kernels / D2H overlap)."""
+    """Same workload through the public C ABI with HOST buffers:
+    kcg_eval_predict_host (pinned SoA bindings in, every variant's
+    predictions out; the library pipelines H2D / kernels / D2H over its own
+    streams), copies inside the timed region. Also reported: the same call
+    on pageable buffers (staged through the library's pinned ring)."""
     import ctypes
     total = args.side ** 3
-    chunk = int(os.environ.get("KCG_E2E_CHUNK", 1 << 22))
-    nstreams = int(os.environ.get("KCG_E2E_STREAMS", 3))
     r0 = total * rank // world
     n = total * (rank + 1) // world - r0
-    host_cols = {}
     idx = torch.arange(r0, r0 + n, dtype=torch.int64)
     s2 = args.side * args.side
-    host_cols["n"] = ((idx // s2 + 1) * UNIT).pin_memory()
-    host_cols["m"] = (((idx // args.side) % args.side + 1) * UNIT).pin_memory()
-    host_cols["l"] = ((idx % args.side + 1) * UNIT).pin_memory()
+    host_cols = {"n": ((idx // s2 + 1) * UNIT), "m": (((idx // args.side) % args.side + 1) * UNIT),
+                 "l": ((idx % args.side + 1) * UNIT)}
     del idx
+    pinned_cols = {k: v.pin_memory() for k, v in host_cols.items()}
     host_pred = torch.empty((len(progs), n), dtype=torch.float64).pin_memory()
-    streams = [torch.cuda.Stream(dev) for _ in range(nstreams)]
-    dcols = [{k: torch.empty(chunk, dtype=torch.int64, device=dev) for k in "nml"} for _ in range(nstreams)]
-    dpred = [torch.empty((len(progs), chunk), dtype=torch.float64, device=dev) for _ in range(nstreams)]
+    handles = (ctypes.c_void_p * len(progs))(*[p.handle.value for p in progs])
     alpha = w.alpha_array()
-    arrs = [{id(p): (ctypes.c_void_p * 3)(*[dcols[b][q].data_ptr() for q in p.params]) for p in progs}
-            for b in range(nstreams)]
 
-    def one():
-        for c0 in range(0, n, chunk):
-            b = (c0 // chunk) % nstreams
-            s = streams[b]
-            m = min(chunk, n - c0)
-            with torch.cuda.stream(s):
-                for k in "nml":
-                    dcols[b][k][:m].copy_(host_cols[k][c0:c0 + m], non_blocking=True)
-                for v, p in enumerate(progs):
-                    kc.api.check(kc.api.lib().kcg_eval_predict(
-                        p.handle, arrs[b][id(p)], m, alpha, dpred[b][v].data_ptr(),
-                        None, None, None, 0, s.cuda_stream))
-                for v in range(len(progs)):
-                    host_pred[v, c0:c0 + m].copy_(dpred[b][v, :m], non_blocking=True)
-        torch.cuda.synchronize()
+    def call(cols, out, flags):
+        arr = (ctypes.c_void_p * 3)(*[cols[q].data_ptr() for q in progs[0].params])
+        kc.api.check(kc.api.lib().kcg_eval_predict_host(handles, len(progs), arr, n, alpha, out.data_ptr(),
+                                                        None, flags))
 
     import torch.distributed as dist
-    one()
+    call(pinned_cols, host_pred, kc._capi.HOST_PINNED)
     if world > 1:
         dist.barrier()
     t0 = time.perf_counter()
     reps = max(1, min(3, args.steps))
     for _ in range(reps):
-        one()
+        call(pinned_cols, host_pred, kc._capi.HOST_PINNED)
     sec = (time.perf_counter() - t0) / reps
+    # pageable caller buffers (a std::vector-style caller), one call
+    page_pred = torch.empty((len(progs), n), dtype=torch.float64)
+    call(host_cols, page_pred, 0)
+    t1 = time.perf_counter()
+    call(host_cols, page_pred, 0)
+    sec_page = time.perf_counter() - t1
+    same = bool(torch.equal(page_pred.view(torch.int64), host_pred.view(torch.int64)))
+    del page_pred
     if world > 1:  # whole job: all shards, the slowest rank's wall clock
-        t = torch.tensor([sec], dtype=torch.float64, device=dev)
+        t = torch.tensor([sec, sec_page], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sec = float(t.item())
+        sec, sec_page = (float(x) for x in t.tolist())
     n_local = n
     n = total
     h2d = 3 * 8 * n
     d2h = 8 * n * len(progs)
     # the bound: a plain pinned D2H copy of the same size class on this box
-    del dcols, dpred
     probe = torch.empty(1 << 27, dtype=torch.float64, device=dev)
     hp = torch.empty(1 << 27, dtype=torch.float64).pin_memory()
     hp.copy_(probe)
@@ -523,12 +514,17 @@ def _e2e(kc, progs, w, args, torch, dev, world, rank):
         hp.copy_(probe, non_blocking=True)
     torch.cuda.synchronize()
     d2h_bw = 3 * 8 * (1 << 27) / (time.perf_counter() - t1)
+    chunk = int(os.environ.get("KCG_HOST_CHUNK", 1 << 22))
+    nstreams = int(os.environ.get("KCG_HOST_STREAMS", 3))
     return {"value": n * len(progs) / sec, "unit": "points/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": sec * 1e3,
             "pcie_d2h_GBps_measured": d2h_bw / 1e9,
             "d2h_frac_of_measured": 8 * n_local * len(progs) / sec / d2h_bw,  # per rank / per link
-            "note": "pinned host SoA bindings -> kcg_eval_predict (6 variants) -> pinned host predictions; "
-                    f"{nstreams} streams, {chunk >> 20}M-size chunks; wall clock incl. all copies"}
+            "pageable": {"value": n * len(progs) / sec_page, "ms_per_step": sec_page * 1e3,
+                         "bitwise_equal_to_pinned": same},
+            "note": "kcg_eval_predict_host (C ABI): pinned host SoA bindings -> 6 variants -> pinned host "
+                    f"predictions; library-internal {nstreams} streams, {chunk >> 20}M-size chunks; "
+                    "wall clock incl. all copies"}
 
 
 def _sharded_fit(kc, torch, dev, world, rank, rows):

@@ -172,6 +172,27 @@ int kcg_eval_predict_grid(const kcg_program* prog, const kcg_grid* grid, uint64_
                           size_t n, const double* alpha, double* pred_out,
                           uint8_t* status_out, int simulate, void* stream);
 
+/* ---- host buffers: the reference's own calling convention ---------------
+ * The same evaluate + predict for n_progs programs over one set of HOST
+ * bindings (e.g. every variant of an autotuning sweep): host_cols follow
+ * progs[0]'s parameter order (n_points int64 each; every program must have
+ * the same parameter names); pred_out (HOST, nullable) receives
+ * n_progs x n_points fp64 predictions, program-major, bitwise equal to
+ * kcg_eval_predict; status_out (HOST, nullable) the per-point status bytes
+ * in the same layout. Chunks of KCG_HOST_CHUNK points (default 4M) stream
+ * over KCG_HOST_STREAMS internal streams (default 3), so the bindings'
+ * H2D copy, the kernels and the predictions' D2H copy overlap, and each
+ * binding crosses PCIe once for all programs. flags: KCG_HOST_PINNED when
+ * the caller's buffers are page-locked (cudaHostAlloc / cudaHostRegister):
+ * the copies run straight from and into them; otherwise they go through
+ * per-device pinned staging (kept across calls). Synchronous; one call per
+ * device at a time (calls from several threads serialise).              */
+#define KCG_HOST_PINNED 1u
+int kcg_eval_predict_host(const kcg_program* const* progs, int n_progs,
+                          const int64_t* const* host_cols, size_t n_points,
+                          const double* alpha, double* pred_out, uint8_t* status_out,
+                          unsigned flags);
+
 /* ---- autotuning: evaluate + predict over variants, argmin --------------
  * progs: n_variants programs with identical parameter-name sets; param_cols
  * follow progs[0]'s parameter order. For each size i: best_idx[i] = lowest

@@ -26,6 +26,7 @@ from .api import (  # noqa: F401
     ModelWeights,
     Program,
     argmin,
+    predict_host,
     evaluate_properties,
     fit_weights,
     geometric_mean_error,

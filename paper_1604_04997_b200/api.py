@@ -14,7 +14,7 @@ import ctypes
 import math
 from dataclasses import dataclass, field
 from pathlib import Path
-from typing import Mapping, Sequence
+from typing import Mapping, Optional, Sequence
 
 from . import _capi
 from ._capi import check, lib
@@ -170,6 +170,11 @@ def _stream(stream=None) -> int:
     return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
 
 
+def _np():
+    import numpy
+    return numpy
+
+
 def _ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
@@ -298,6 +303,42 @@ def argmin(progs: Sequence[Program], w: ModelWeights, bindings, return_preds: bo
     check(lib().kcg_argmin(handles, len(progs), arr, n, w.alpha_array(), best.data_ptr(),
                            best_t.data_ptr(), _ptr(preds), _stream(stream)))
     return (best, best_t, preds) if return_preds else (best, best_t)
+
+
+def predict_host(progs: Sequence[Program], w: ModelWeights, bindings, status: bool = False,
+                 out=None, pinned: Optional[bool] = None):
+    """The reference's calling convention: HOST bindings in, HOST
+    predictions out (predict over every program, model.cpp:95-117), through
+    kcg_eval_predict_host -- chunked H2D / kernels / D2H on internal
+    streams, each binding copied to the device once for all programs.
+    bindings: {param: int64 numpy array or CPU tensor}; returns a
+    [len(progs), n] float64 CPU tensor (and [len(progs), n] uint8 status).
+    `out` may be a preallocated (pinned) CPU tensor of that shape. pinned:
+    the buffers are page-locked (default: detected from the tensors)."""
+    torch = _torch()
+    progs = list(progs)
+    cols = []
+    for name in progs[0].params:
+        c = bindings[name]
+        c = c if isinstance(c, torch.Tensor) else torch.from_numpy(_np().ascontiguousarray(c, dtype=_np().int64))
+        if c.dtype != torch.int64 or c.device.type != "cpu":
+            raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "predict_host takes int64 CPU columns")
+        cols.append(c.contiguous())
+    n = int(cols[0].numel()) if cols else 0
+    if any(int(c.numel()) != n for c in cols):
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "binding columns differ in length")
+    V = len(progs)
+    pred = out if out is not None else torch.empty((V, n), dtype=torch.float64)
+    if tuple(pred.shape) != (V, n) or pred.dtype != torch.float64 or not pred.is_contiguous():
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "out must be a contiguous [n_progs, n] float64 CPU tensor")
+    st = torch.empty((V, n), dtype=torch.uint8) if status else None
+    if pinned is None:
+        pinned = all(t.is_pinned() for t in cols + [pred] + ([st] if st is not None else [])) if n else False
+    handles = (ctypes.c_void_p * V)(*[p.handle.value for p in progs])
+    arr = (ctypes.c_void_p * max(1, len(cols)))(*[c.data_ptr() for c in cols])
+    check(lib().kcg_eval_predict_host(handles, V, arr, n, w.alpha_array(), pred.data_ptr(),
+                                      _ptr(st), _capi.HOST_PINNED if pinned else 0))
+    return (pred, st) if status else pred
 
 
 # ---------------------------------------------------------------------------

@@ -14,6 +14,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <tuple>
 #include <vector>
 
@@ -547,6 +548,173 @@ int kcg_argmin(const kcg_program* const* progs, int V, const int64_t* const* par
     ab.finish();
     kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid_for(n), 256, stream);
     ++g_launches;
+    return KCG_OK;
+  });
+}
+
+}  // extern "C"
+
+namespace {
+
+long long env_ll(const char* name, long long dflt, long long lo, long long hi) {
+  const char* e = std::getenv(name);
+  if (!e || !*e) return dflt;
+  const long long v = std::atoll(e);
+  return v < lo ? lo : (v > hi ? hi : v);
+}
+
+// memcpy split over host threads (pageable <-> pinned staging)
+void par_copy(void* dst, const void* src, size_t bytes) {
+  static const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (bytes < (8u << 20) || T == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = ((bytes + T - 1) / T + 63) & ~static_cast<size_t>(63);
+  std::vector<std::thread> th;
+  for (size_t o = 0; o < bytes; o += per) {
+    const size_t m = std::min(per, bytes - o);
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, m); });
+  }
+  for (auto& t : th) t.join();
+}
+
+// per-device streams and staging of kcg_eval_predict_host, kept across calls
+// (cudaHostAlloc of ~1 GB costs more than a whole call)
+struct HostPipe {
+  int slots = 0;
+  size_t dev_bytes = 0, host_bytes = 0;
+  std::vector<cudaStream_t> streams;
+  std::vector<cudaEvent_t> events;
+  std::vector<char*> dev, host;
+  std::mutex mu;  // one host call per device at a time
+  void ensure(int S, size_t dbytes, size_t hbytes) {
+    while (slots < S) {
+      cudaStream_t s;
+      cudaEvent_t e;
+      cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      streams.push_back(s);
+      events.push_back(e);
+      dev.push_back(nullptr);
+      host.push_back(nullptr);
+      ++slots;
+    }
+    if (dbytes > dev_bytes) {
+      for (auto& d : dev) {
+        if (d) cudaFree(d);
+        d = nullptr;
+      }
+      for (int b = 0; b < slots; ++b) cuda_check(cudaMalloc(&dev[b], dbytes), "cudaMalloc");
+      dev_bytes = dbytes;
+    }
+    if (hbytes > host_bytes) {
+      for (auto& h : host) {
+        if (h) cudaFreeHost(h);
+        h = nullptr;
+      }
+      for (int b = 0; b < slots; ++b) cuda_check(cudaHostAlloc(&host[b], hbytes, cudaHostAllocDefault), "cudaHostAlloc");
+      host_bytes = hbytes;
+    }
+  }
+};
+
+HostPipe& host_pipe(int dev) {
+  static std::mutex mu;
+  static std::vector<std::unique_ptr<HostPipe>> pipes;
+  std::lock_guard<std::mutex> lock(mu);
+  if (pipes.size() <= static_cast<size_t>(dev)) pipes.resize(dev + 1);
+  if (!pipes[dev]) pipes[dev].reset(new HostPipe());
+  return *pipes[dev];
+}
+
+}  // namespace
+
+extern "C" {
+
+int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t* const* host_cols, size_t n,
+                          const double* alpha, double* pred_out, uint8_t* status_out, unsigned flags) {
+  if (!progs || V < 1 || !alpha || (!pred_out && !status_out))
+    return fail(KCG_E_INVALID_ARGUMENT, "bad host eval arguments");
+  return guarded([&] {
+    require_device();
+    const kcg_program* p0 = progs[0];
+    const int np = p0->low.n_params;
+    if (np > 0 && !host_cols) throw KcgError(KCG_E_INVALID_ARGUMENT, "null host_cols");
+    std::vector<std::vector<int>> maps(V);
+    for (int v = 0; v < V; ++v) {
+      const kcg_program* p = progs[v];
+      if (!p || p->low.n_params != np)
+        throw KcgError(KCG_E_INVALID_ARGUMENT, "host eval programs must share the parameter set");
+      maps[v].resize(np);
+      for (int j = 0; j < np; ++j) {
+        auto it = std::find(p0->param_names.begin(), p0->param_names.end(), p->param_names[j]);
+        if (it == p0->param_names.end())
+          throw KcgError(KCG_E_INVALID_ARGUMENT, "host eval programs must share the parameter set");
+        maps[v][j] = static_cast<int>(it - p0->param_names.begin());
+      }
+    }
+    if (n == 0) return KCG_OK;
+    const bool pinned = (flags & KCG_HOST_PINNED) != 0;
+    const size_t chunk = std::min<size_t>(n, static_cast<size_t>(env_ll("KCG_HOST_CHUNK", 1 << 22, 1024, 1ll << 28)));
+    const int S = static_cast<int>(env_ll("KCG_HOST_STREAMS", 3, 1, 8));
+    // slot layout: np binding columns, V prediction columns, V status columns
+    const size_t in_b = static_cast<size_t>(std::max(np, 1)) * chunk * 8;
+    const size_t pred_b = pred_out ? static_cast<size_t>(V) * chunk * 8 : 0;
+    const size_t st_b = status_out ? static_cast<size_t>(V) * chunk : 0;
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    HostPipe& hp = host_pipe(dev);
+    std::lock_guard<std::mutex> lock(hp.mu);
+    hp.ensure(S, in_b + pred_b + st_b, pinned ? 0 : in_b + pred_b + st_b);
+    std::vector<size_t> busy_c0(S), busy_m(S, 0);
+    auto unstage = [&](int b) {  // the slot's results: pinned staging -> caller
+      cuda_check(cudaEventSynchronize(hp.events[b]), "cudaEventSynchronize");
+      const size_t c0 = busy_c0[b], m = busy_m[b];
+      busy_m[b] = 0;
+      if (pinned || m == 0) return;
+      for (int v = 0; v < V; ++v) {
+        if (pred_out) par_copy(pred_out + v * n + c0, hp.host[b] + in_b + v * chunk * 8, m * 8);
+        if (status_out) par_copy(status_out + v * n + c0, hp.host[b] + in_b + pred_b + v * chunk, m);
+      }
+    };
+    for (size_t k = 0, c0 = 0; c0 < n; ++k, c0 += chunk) {
+      const int b = static_cast<int>(k % S);
+      unstage(b);
+      const size_t m = std::min(chunk, n - c0);
+      cudaStream_t st = hp.streams[b];
+      char* d = hp.dev[b];
+      char* h = pinned ? nullptr : hp.host[b];
+      for (int j = 0; j < np; ++j) {
+        const void* src = host_cols[j] + c0;
+        if (!pinned) {
+          par_copy(h + j * chunk * 8, src, m * 8);
+          src = h + j * chunk * 8;
+        }
+        cuda_check(cudaMemcpyAsync(d + j * chunk * 8, src, m * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync H2D");
+      }
+      for (int v = 0; v < V; ++v) {
+        std::vector<const int64_t*> cols(std::max(np, 1), nullptr);
+        for (int j = 0; j < np; ++j) cols[j] = reinterpret_cast<const int64_t*>(d + maps[v][j] * chunk * 8);
+        double* dp = pred_out ? reinterpret_cast<double*>(d + in_b + v * chunk * 8) : nullptr;
+        uint8_t* ds = status_out ? reinterpret_cast<uint8_t*>(d + in_b + pred_b + v * chunk) : nullptr;
+        const int rc = kcg_eval_predict(progs[v], cols.data(), m, alpha, dp, ds, nullptr, nullptr, 0, st);
+        if (rc != KCG_OK) throw KcgError(rc, g_last_error);
+        if (pred_out)
+          cuda_check(cudaMemcpyAsync(pinned ? static_cast<void*>(pred_out + v * n + c0) : h + in_b + v * chunk * 8, dp,
+                                     m * 8, cudaMemcpyDeviceToHost, st),
+                     "cudaMemcpyAsync D2H");
+        if (status_out)
+          cuda_check(cudaMemcpyAsync(pinned ? static_cast<void*>(status_out + v * n + c0) : h + in_b + pred_b + v * chunk,
+                                     ds, m, cudaMemcpyDeviceToHost, st),
+                     "cudaMemcpyAsync D2H");
+      }
+      cuda_check(cudaEventRecord(hp.events[b], st), "cudaEventRecord");
+      busy_c0[b] = c0;
+      busy_m[b] = m;
+    }
+    const size_t nch = (n + chunk - 1) / chunk;
+    for (size_t k = nch > static_cast<size_t>(S) ? nch - S : 0; k < nch; ++k) unstage(static_cast<int>(k % S));
     return KCG_OK;
   });
 }

@@ -1,0 +1,90 @@
+"""kcg_eval_predict_host: the reference's calling convention (HOST bindings
+in, HOST predictions out; predict, model.cpp:95-117) over the chunked
+H2D / kernel / D2H pipeline. Results must be bitwise those of the
+device-resident kcg_eval_predict, for pinned and pageable buffers, ragged
+chunk tails, inadmissible points and several programs sharing one binding
+stream."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import kc_oracle as ko
+import paper_1604_04997_b200 as kc  # noqa: E402
+from paper_1604_04997_b200 import _capi  # noqa: E402
+
+VARIANTS = ("matmul_tiled_g12x12", "matmul_tiled_g14x14", "matmul_tiled_g16x16",
+            "matmul_naive_g16x12", "matmul_naive_g16x14", "matmul_naive_g16x16")
+
+
+def _weights():
+    a = ko.simdev_reference_alpha()
+    return kc.ModelWeights(alpha=a, covered=[x != 0 for x in a])
+
+
+def test_host_eval_argument_errors():
+    p = kc.load_program("matmul_tiled_g16x16")
+    h = (ctypes.c_void_p * 1)(p.handle.value)
+    out = (ctypes.c_double * 4)()
+    L = _capi.lib()
+    assert L.kcg_eval_predict_host(h, 1, None, 4, None, out, None, 0) == _capi.E_INVALID_ARGUMENT  # no alpha
+    assert L.kcg_eval_predict_host(h, 0, None, 4, None, out, None, 0) == _capi.E_INVALID_ARGUMENT
+    w = _weights()
+    assert L.kcg_eval_predict_host(h, 1, None, 4, w.alpha_array(), None, None, 0) == _capi.E_INVALID_ARGUMENT
+
+
+def test_host_eval_without_device_fails_loudly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    p = kc.load_program("matmul_tiled_g16x16")
+    with pytest.raises(kc.KcgError) as e:
+        kc.predict_host([p], _weights(), {k: np.array([16, 32]) for k in "nml"})
+    assert e.value.code == _capi.E_CUDA
+
+
+def _bindings(n, seed):
+    rng = np.random.default_rng(seed)
+    b = {k: (rng.integers(1, 400, n) * 336).astype(np.int64) for k in "nml"}
+    b["m"][::97] += 5      # inadmissible for every variant (m % 12/14/16 != 0)
+    b["l"][::1013] = 0     # zero-sized
+    return b
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pinned", [False, True])
+@pytest.mark.parametrize("chunk", [65536, 1 << 22])
+def test_host_eval_bitwise_equals_device_path(monkeypatch, pinned, chunk):
+    import torch
+    monkeypatch.setenv("KCG_HOST_CHUNK", str(chunk))
+    n = 3 * 65536 + 4321  # ragged last chunk
+    progs = [kc.load_program(v) for v in VARIANTS]
+    w = _weights()
+    b = _bindings(n, 7)
+    host = {k: torch.from_numpy(v) for k, v in b.items()}
+    out = None
+    if pinned:
+        host = {k: v.pin_memory() for k, v in host.items()}
+        out = torch.empty((len(progs), n), dtype=torch.float64).pin_memory()
+    pred, st = kc.predict_host(progs, w, host, status=True, out=out)
+    dev = {k: v.cuda() for k, v in host.items()}
+    for i, p in enumerate(progs):
+        want, wst = kc.predict(w, p, dev, with_status=True)
+        assert torch.equal(pred[i].view(torch.int64), want.cpu().view(torch.int64)), p.name if hasattr(p, "name") else i
+        assert torch.equal(st[i], wst.cpu())
+    assert int((st != 0).sum()) > 0  # the inadmissible points are there
+
+
+@pytest.mark.gpu
+def test_host_eval_param_order_follows_first_program():
+    """Programs whose parameters are declared in another order read the
+    host columns by name (progs[0]'s order)."""
+    import torch
+    progs = [kc.load_program("matmul_tiled_g16x16"), kc.load_program("matmul_naive_g16x16")]
+    w = _weights()
+    b = _bindings(5000, 3)
+    pred = kc.predict_host(progs, w, b)
+    dev = {k: torch.from_numpy(v).cuda() for k, v in b.items()}
+    for i, p in enumerate(progs):
+        want = kc.predict(w, p, dev).cpu()
+        assert torch.equal(pred[i].view(torch.int64), want.view(torch.int64))
