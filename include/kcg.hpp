@@ -7,6 +7,7 @@
 //   kcg::evaluate_properties()   <- evaluate_properties (props.hpp:49-50)
 //   kcg::predict()               <- predict (model.hpp:61)
 //   kcg::noiseless_time()        <- noiseless_time (simdevice.hpp:33)
+//   kcg::predict_host()          <- the same over host vectors (chunked H2D / D2H inside)
 //   kcg::argmin()                <- the autotuning sweep over kernel variants
 //   kcg::fit_weights()           <- build_design_matrix + fit_weights
 //                                   (model.hpp:43-49), Gram on the GPU
@@ -103,6 +104,22 @@ inline void predict(const ModelWeights& w, const Program& p, const int64_t* cons
   if (w.alpha.size() != static_cast<size_t>(kcg_schema_size()))
     throw Error(KCG_E_SCHEMA_MISMATCH, "weight vector does not match schema v1");
   check(kcg_eval_predict(p.handle(), cols, n, w.alpha.data(), seconds, status, nullptr, nullptr, 0, s));
+}
+
+/// Host-buffer predict over several programs sharing one set of bindings
+/// (host_cols in programs[0]'s parameter order): returns programs x n
+/// seconds, program-major. flags: KCG_HOST_PINNED for page-locked buffers.
+inline std::vector<double> predict_host(const ModelWeights& w, const std::vector<const Program*>& programs,
+                                        const int64_t* const* host_cols, size_t n,
+                                        uint8_t* status = nullptr, unsigned flags = 0) {
+  if (w.alpha.size() != static_cast<size_t>(kcg_schema_size()))
+    throw Error(KCG_E_SCHEMA_MISMATCH, "weight vector does not match schema v1");
+  std::vector<const kcg_program*> h;
+  for (const Program* p : programs) h.push_back(p->handle());
+  std::vector<double> out(programs.size() * n);
+  check(kcg_eval_predict_host(h.data(), static_cast<int>(h.size()), host_cols, n, w.alpha.data(), out.data(),
+                              status, flags));
+  return out;
 }
 
 /// Batched noiseless_time (simulate order: skip zero weights).

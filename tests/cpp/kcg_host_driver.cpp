@@ -79,6 +79,15 @@ int eval(int argc, char** argv) {
     std::cout << "prediction mismatch: " << mismatch << "\n";
     return 1;
   }
+  // the host-buffer entry point (pageable vectors) == the device path
+  std::vector<const int64_t*> hcols;
+  for (int64_t j = 0; j < P; ++j) hcols.push_back(hdr + 2 + j * n);
+  std::vector<uint8_t> hst(n);
+  const std::vector<double> hpred = kcg::predict_host(w, {&prog}, hcols.data(), n, hst.data());
+  if (std::memcmp(hpred.data(), pred.data(), sizeof(double) * n) != 0 || hst != st) {
+    std::cout << "predict_host differs from the device path\n";
+    return 1;
+  }
   std::ofstream out(argv[5], std::ios::binary);
   out.write(reinterpret_cast<const char*>(pred.data()), sizeof(double) * n);
   out.write(reinterpret_cast<const char*>(st.data()), n);
