@@ -116,23 +116,32 @@ void* jit_kernel(const std::string& src, const std::string& name) {
   return reinterpret_cast<void*>(k);
 }
 
+namespace {
+
+// dynamic + static shared memory beyond the 48 KB default needs the opt-in,
+// per kernel and per device
+void ensure_smem(void* kernel, size_t smem) {
+  if (smem <= 32 * 1024) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_mu);
+  static std::unordered_map<std::string, size_t> configured;
+  char key[48];
+  std::snprintf(key, sizeof key, "%p:%d", kernel, dev);
+  auto it = configured.find(key);
+  if (it != configured.end() && it->second >= smem) return;
+  const cudaError_t e = cudaKernelSetAttributeForDevice(
+      reinterpret_cast<cudaKernel_t>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem), dev);
+  if (e != cudaSuccess)
+    throw KcgError(KCG_E_CUDA, std::string("cudaKernelSetAttributeForDevice: ") + cudaGetErrorString(e));
+  configured[key] = smem;
+}
+
+}  // namespace
+
 void launch_jit(void* kernel, const void* args, size_t, unsigned grid,
                 unsigned block, void* stream, size_t smem) {
-  if (smem > 32 * 1024) {  // dynamic + static shared beyond the 48 KB default needs the opt-in
-    std::lock_guard<std::mutex> lock(g_mu);
-    static std::unordered_map<void*, size_t> configured;
-    auto it = configured.find(kernel);
-    if (it == configured.end() || it->second < smem) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      const cudaError_t e = cudaKernelSetAttributeForDevice(
-          reinterpret_cast<cudaKernel_t>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-          static_cast<int>(smem), dev);
-      if (e != cudaSuccess)
-        throw KcgError(KCG_E_CUDA, std::string("cudaKernelSetAttributeForDevice: ") + cudaGetErrorString(e));
-      configured[kernel] = smem;
-    }
-  }
+  ensure_smem(kernel, smem);
   void* argv[] = {const_cast<void*>(args)};
   const cudaError_t e =
       cudaLaunchKernel(kernel, dim3(grid), dim3(block), argv, smem,
@@ -142,21 +151,7 @@ void launch_jit(void* kernel, const void* args, size_t, unsigned grid,
 }
 
 void launch_jit_argv(void* kernel, void** argv, unsigned grid, unsigned block, void* stream, size_t smem) {
-  if (smem > 32 * 1024) {
-    std::lock_guard<std::mutex> lock(g_mu);
-    static std::unordered_map<void*, size_t> configured;
-    auto it = configured.find(kernel);
-    if (it == configured.end() || it->second < smem) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      const cudaError_t e = cudaKernelSetAttributeForDevice(
-          reinterpret_cast<cudaKernel_t>(kernel), cudaFuncAttributeMaxDynamicSharedMemorySize,
-          static_cast<int>(smem), dev);
-      if (e != cudaSuccess)
-        throw KcgError(KCG_E_CUDA, std::string("cudaKernelSetAttributeForDevice: ") + cudaGetErrorString(e));
-      configured[kernel] = smem;
-    }
-  }
+  ensure_smem(kernel, smem);
   const cudaError_t e = cudaLaunchKernel(kernel, dim3(grid), dim3(block), argv, smem, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) throw KcgError(KCG_E_CUDA, std::string("JIT kernel launch: ") + cudaGetErrorString(e));
 }
