@@ -308,6 +308,16 @@ __global__ void __launch_bounds__(MAXT)
 
 constexpr int kDmmaRows = 64;
 
+// |x| as its bit pattern with the sign cleared on the integer pipe (a plain
+// `& 0x7fff...` is turned into DADD |x|, which occupies the FP64 pipe the
+// DMMAs run on)
+__device__ __forceinline__ unsigned long long abs_bits(double x) {
+  unsigned lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(x));
+  asm volatile("and.b32 %0, %0, 0x7fffffff;" : "+r"(hi));
+  return ((unsigned long long)hi << 32) | lo;
+}
+
 __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
@@ -376,7 +386,7 @@ __global__ void __launch_bounds__(256, 2)
     for (int b = 0; b < NB; ++b) {
       s1[b] += v[b];
       {
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(v[b]) & 0x7fffffffffffffffull;
+        const unsigned long long bits = abs_bits(v[b]);
         mx[b] = bits > mx[b] ? bits : mx[b];
       }
     }
@@ -394,7 +404,7 @@ __global__ void __launch_bounds__(256, 2)
       v[b] = (valid && col < F) ? rowp[col] : 0.0;
       s1[b] += v[b];
       {
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(v[b]) & 0x7fffffffffffffffull;
+        const unsigned long long bits = abs_bits(v[b]);
         mx[b] = bits > mx[b] ? bits : mx[b];
       }
     }
