@@ -1244,7 +1244,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
               << "  for (int e = lane; e < 32 * " << LDX << "; e += 32) xw[e] = 0.0;  // padding stays zero\n"
               << "  __syncwarp();\n";
     cons_row << "      #pragma unroll\n      for (int j = 0; j < " << W << "; ++j) { xw[lane * " << LDX
-             << " + j] = x[j]; { const unsigned long long b = (unsigned long long)__double_as_longlong(x[j]) & 0x7fffffffffffffffull; mxr[j] = b > mxr[j] ? b : mxr[j]; }"
+             << " + j] = x[j]; { const unsigned long long b = kcg_abs_bits(x[j]); mxr[j] = b > mxr[j] ? b : mxr[j]; }"
              << (ones ? "" : " s1r[j] += x[j];") << " }\n"
              << cmp_row.str();
     if (ones) cons_row << "      xw[lane * " << LDX << " + " << W << "] = ok ? 1.0 : 0.0;\n";
@@ -1291,8 +1291,8 @@ std::string codegen(const std::vector<const Lowered*>& progs,
               << mxc_decl << "  unsigned long long bad = 0;\n";
     int k = 0;
     for (int r = 0; r < W; ++r) {
-      cons_row << "      s1[" << r << "] += x[" << r << "]; { const unsigned long long b = (unsigned long long)__double_as_longlong(x["
-               << r << "]) & 0x7fffffffffffffffull; mx[" << r << "] = b > mx[" << r << "] ? b : mx[" << r << "]; }\n";
+      cons_row << "      s1[" << r << "] += x[" << r << "]; { const unsigned long long b = kcg_abs_bits(x["
+               << r << "]); mx[" << r << "] = b > mx[" << r << "] ? b : mx[" << r << "]; }\n";
       for (int c = r; c < W; ++c, ++k)
         cons_row << "      g[" << k << "] = fma(x[" << r << "], x[" << c << "], g[" << k << "]);\n";
     }

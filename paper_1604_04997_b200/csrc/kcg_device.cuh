@@ -100,5 +100,13 @@ __device__ __forceinline__ double kcg_accum(double s, double alpha, double count
 }
 
 __device__ __forceinline__ double kcg_nan() { return __longlong_as_double(0x7ff8000000000000ll); }
+__device__ __forceinline__ unsigned long long kcg_abs_bits(double x) {
+  // |x| as a bit pattern with the sign cleared on the integer pipe (a plain
+  // mask compiles to DADD |x| on the FP64 pipe, which the DMMAs share)
+  unsigned lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(x));
+  asm volatile("and.b32 %0, %0, 0x7fffffff;" : "+r"(hi));
+  return ((unsigned long long)hi << 32) | lo;
+}
 
 #endif  // KCG_DEVICE_HELPERS
