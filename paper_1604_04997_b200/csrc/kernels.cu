@@ -326,8 +326,8 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
 
 // R: rows per tile (64 * m): narrow designs take taller tiles so every
 // stage is still a multi-KB bulk copy
-template <int NB, int R>
-__global__ void __launch_bounds__(256, 2)
+template <int NB, int R, int CT>
+__global__ void __launch_bounds__(256, CT)
     kcg_gram_dmma(const double* __restrict__ X, kcg_i64 n, int F, int stages,
                   double* __restrict__ G, double* __restrict__ xt1, double* __restrict__ cmax) {
   constexpr int NT = NB * (NB + 1) / 2;
@@ -504,34 +504,43 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
-template <int NB>
+template <int NB, int CT>
 void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, double* colmax,
                       cudaStream_t stream) {
   constexpr int R = NB <= 2 ? 256 : (NB == 3 ? 128 : 64);
-  // ring: up to 4 stages within ~100 KB so that two CTAs share an SM
-  int stages = (int)((100 * 1024) / ((size_t)R * F * 8));
-  stages = stages < 2 ? 2 : (stages > 4 ? 4 : stages);
-  if (NB >= 5) stages = F <= 40 ? 4 : 3;
-  const size_t smem = (size_t)(stages * R * F + NB * 8 * NB * 8 + 2 * NB * 8) * sizeof(double);
+  const size_t red_b = (size_t)(NB * 8 * NB * 8 + 2 * NB * 8) * sizeof(double);
+  int stages;
+  if (CT == 1) {
+    // one CTA per SM (the 8 x 8 block triangle of NB >= 7 needs > 128
+    // registers per thread): a deep ring within ~200 KB
+    stages = (int)((200 * 1024 - red_b) / ((size_t)R * F * 8));
+    stages = stages < 2 ? 2 : (stages > 8 ? 8 : stages);
+  } else {
+    // ring: up to 4 stages within ~100 KB so that two CTAs share an SM
+    stages = (int)((100 * 1024) / ((size_t)R * F * 8));
+    stages = stages < 2 ? 2 : (stages > 4 ? 4 : stages);
+    if (NB >= 5) stages = F <= 40 ? 4 : 3;
+  }
+  const size_t smem = (size_t)stages * R * F * sizeof(double) + red_b;
   // the opt-in size grows with F within one NB (per device, process-wide)
   static std::mutex mu;
-  static size_t attr_smem[64] = {};
+  static size_t attr_smem[64] = {};  // per device, this <NB, CT> instantiation
   int dev = 0;
   check(cudaGetDevice(&dev), "cudaGetDevice");
   {
     std::lock_guard<std::mutex> lk(mu);
     size_t& cur = attr_smem[dev & 63];
     if (smem + 4096 > cur) {
-      check(cudaFuncSetAttribute(kcg_gram_dmma<NB, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      check(cudaFuncSetAttribute(kcg_gram_dmma<NB, R, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem + 4096),
             "cudaFuncSetAttribute");
       cur = smem + 4096;
     }
   }
   const kcg_i64 tiles = (kcg_i64)n / R;
-  kcg_i64 grid = (kcg_i64)num_sms() * 2;
+  kcg_i64 grid = (kcg_i64)num_sms() * CT;
   if (grid > tiles) grid = tiles > 0 ? tiles : 1;
-  kcg_gram_dmma<NB, R><<<(unsigned)grid, 256, smem, stream>>>(X, (kcg_i64)n, F, stages, G, xt1, colmax);
+  kcg_gram_dmma<NB, R, CT><<<(unsigned)grid, 256, smem, stream>>>(X, (kcg_i64)n, F, stages, G, xt1, colmax);
   check(cudaGetLastError(), "kcg_gram_dmma launch");
 }
 
@@ -695,16 +704,23 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
   if (n == 0) return;
   if (F < 1 || F > kGramMaxF) throw std::invalid_argument("gram: n_cols must be in [1, 160]");
   static const bool no_dmma = std::getenv("KCG_NO_DMMA") != nullptr;
-  if (!no_dmma && ld == (size_t)F && F <= 48 &&
+  if (!no_dmma && ld == (size_t)F && F <= 64 &&
       reinterpret_cast<uintptr_t>(X) % 16 == 0) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    switch ((F + 7) / 8) {
-      case 1: return launch_gram_dmma<1>(X, n, F, G, xt1, colmax, st);
-      case 2: return launch_gram_dmma<2>(X, n, F, G, xt1, colmax, st);
-      case 3: return launch_gram_dmma<3>(X, n, F, G, xt1, colmax, st);
-      case 4: return launch_gram_dmma<4>(X, n, F, G, xt1, colmax, st);
-      case 5: return launch_gram_dmma<5>(X, n, F, G, xt1, colmax, st);
-      default: return launch_gram_dmma<6>(X, n, F, G, xt1, colmax, st);
+    // one CTA per SM from NB = KCG_DMMA_ONE_CTA_NB (default 6): measured
+    // F = 48: 4.84 -> 4.35 ms; NB = 7, 8 need it (> 128 registers)
+    static const int one_from = std::getenv("KCG_DMMA_ONE_CTA_NB") ? std::atoi(std::getenv("KCG_DMMA_ONE_CTA_NB")) : 6;
+    const int nb = (F + 7) / 8;
+    const bool one = nb >= one_from;
+    switch (nb) {
+      case 1: return one ? launch_gram_dmma<1, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<1, 2>(X, n, F, G, xt1, colmax, st);
+      case 2: return one ? launch_gram_dmma<2, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<2, 2>(X, n, F, G, xt1, colmax, st);
+      case 3: return one ? launch_gram_dmma<3, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<3, 2>(X, n, F, G, xt1, colmax, st);
+      case 4: return one ? launch_gram_dmma<4, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<4, 2>(X, n, F, G, xt1, colmax, st);
+      case 5: return one ? launch_gram_dmma<5, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<5, 2>(X, n, F, G, xt1, colmax, st);
+      case 6: return one ? launch_gram_dmma<6, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<6, 2>(X, n, F, G, xt1, colmax, st);
+      case 7: return launch_gram_dmma<7, 1>(X, n, F, G, xt1, colmax, st);
+      default: return launch_gram_dmma<8, 1>(X, n, F, G, xt1, colmax, st);
     }
   }
   const bool wide = F > 64;
