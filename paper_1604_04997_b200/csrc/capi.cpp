@@ -726,9 +726,9 @@ int kcg_gram_accumulate(const double* X, size_t n, int F, size_t ld, double* G, 
   return guarded([&] {
     require_device();
     static const bool no_wide = std::getenv("KCG_NO_WIDE_DMMA") != nullptr;  // A/B knob
-    // F <= KCG_DMMA_MAXF (default 64): the row-split DMMA kernel (one CTA per
+    // F <= KCG_DMMA_MAXF (default 72): the row-split DMMA kernel (one CTA per
     // SM from F = 49); wider: one specialisation per width
-    static const long long row_split_max = env_ll("KCG_DMMA_MAXF", 64, 48, 64);
+    static const long long row_split_max = env_ll("KCG_DMMA_MAXF", 72, 48, 72);
     if (!no_wide && F > row_split_max && F <= 160 && ld == static_cast<size_t>(F) &&
         reinterpret_cast<uintptr_t>(X) % 16 == 0 && n >= 32) {
       // wide design on the tensor cores: one NVRTC specialisation per width

@@ -704,7 +704,7 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
   if (n == 0) return;
   if (F < 1 || F > kGramMaxF) throw std::invalid_argument("gram: n_cols must be in [1, 160]");
   static const bool no_dmma = std::getenv("KCG_NO_DMMA") != nullptr;
-  if (!no_dmma && ld == (size_t)F && F <= 64 &&
+  if (!no_dmma && ld == (size_t)F && F <= 72 &&
       reinterpret_cast<uintptr_t>(X) % 16 == 0) {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // one CTA per SM from NB = KCG_DMMA_ONE_CTA_NB (default 6): measured
@@ -720,7 +720,8 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
       case 5: return one ? launch_gram_dmma<5, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<5, 2>(X, n, F, G, xt1, colmax, st);
       case 6: return one ? launch_gram_dmma<6, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<6, 2>(X, n, F, G, xt1, colmax, st);
       case 7: return launch_gram_dmma<7, 1>(X, n, F, G, xt1, colmax, st);
-      default: return launch_gram_dmma<8, 1>(X, n, F, G, xt1, colmax, st);
+      case 8: return launch_gram_dmma<8, 1>(X, n, F, G, xt1, colmax, st);
+      default: return launch_gram_dmma<9, 1>(X, n, F, G, xt1, colmax, st);
     }
   }
   const bool wide = F > 64;
