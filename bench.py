@@ -785,7 +785,7 @@ def _extras(kc, torch, dev, args):
         "hbm_achieved_GBps": 8 * F * N / sec / 1e9, "hbm_frac": 8 * F * N / sec / 1e9 / hbm,
         "fp64_tflops": flops / sec / 1e12, "fp64_peak_tflops_measured_dgemm": fp64,
         "fp64_frac": flops / sec / 1e12 / fp64, "slice_rel_err_vs_torch": rel,
-        "kernel": "kcg_gram_x (AOT, 4x4 register tiles over the upper triangle)"}
+        "kernel": "kcg_gram_dmma<5,64,2> (AOT, DMMA m8n8k4 f64, TMA-staged rows)"}
     del X, Xs, st, st2, ref
 
     # ---- config 5 (single GPU): fused evaluate -> row -> Gram, 1e9 rows ----
