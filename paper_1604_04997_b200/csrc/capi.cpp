@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
@@ -563,20 +564,100 @@ long long env_ll(const char* name, long long dflt, long long lo, long long hi) {
   return v < lo ? lo : (v > hi ? hi : v);
 }
 
-// memcpy split over host threads (pageable <-> pinned staging)
-void par_copy(void* dst, const void* src, size_t bytes) {
-  static const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-  if (bytes < (8u << 20) || T == 1) {
-    std::memcpy(dst, src, bytes);
-    return;
+// Host copies between pageable caller buffers and the pinned staging: a
+// persistent pool of threads that split every batch of segments into 2 MB
+// parts (spawning threads per copy cost more than the copies themselves)
+struct CopySeg {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+
+class CopyPool {
+ public:
+  CopyPool() {
+    const unsigned T = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    for (unsigned t = 1; t < T; ++t) workers_.emplace_back([this] { work(); });
   }
-  const size_t per = ((bytes + T - 1) / T + 63) & ~static_cast<size_t>(63);
-  std::vector<std::thread> th;
-  for (size_t o = 0; o < bytes; o += per) {
-    const size_t m = std::min(per, bytes - o);
-    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, m); });
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
   }
-  for (auto& t : th) t.join();
+  // copies every segment; returns when all are done
+  void run(const std::vector<CopySeg>& segs) {
+    size_t total = 0;
+    for (const CopySeg& g : segs) total += g.bytes;
+    if (workers_.empty() || total < (8u << 20)) {
+      for (const CopySeg& g : segs) std::memcpy(g.dst, g.src, g.bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> one_batch(run_mu_);  // callers on several devices share the pool
+    std::unique_lock<std::mutex> lk(mu_);
+    // a worker that woke late for the previous batch may still be scanning it
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    parts_.clear();
+    for (const CopySeg& g : segs)
+      for (size_t o = 0; o < g.bytes; o += kPart)
+        parts_.push_back({static_cast<char*>(g.dst) + o, static_cast<const char*>(g.src) + o,
+                          std::min(kPart, g.bytes - o)});
+    next_.store(0);
+    finished_ = 0;
+    ++gen_;
+    lk.unlock();
+    cv_.notify_all();
+    drain();
+    lk.lock();
+    done_cv_.wait(lk, [&] { return finished_ == parts_.size() && active_ == 0; });
+  }
+
+ private:
+  static constexpr size_t kPart = 2u << 20;
+  void drain() {
+    size_t mine = 0;
+    for (;;) {
+      const size_t p = next_.fetch_add(1);
+      if (p >= parts_.size()) break;
+      std::memcpy(parts_[p].dst, parts_[p].src, parts_[p].bytes);
+      ++mine;
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    finished_ += mine;
+    if (finished_ == parts_.size()) done_cv_.notify_all();
+  }
+  void work() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+        ++active_;
+      }
+      drain();
+      std::lock_guard<std::mutex> lk(mu_);
+      --active_;
+      done_cv_.notify_all();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex run_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  std::vector<CopySeg> parts_;
+  std::atomic<size_t> next_{0};
+  size_t finished_ = 0;
+  unsigned active_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+CopyPool& copy_pool() {
+  static CopyPool pool;
+  return pool;
 }
 
 // per-device streams and staging of kcg_eval_predict_host, kept across calls
@@ -673,10 +754,12 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
       const size_t c0 = busy_c0[b], m = busy_m[b];
       busy_m[b] = 0;
       if (pinned || m == 0) return;
+      std::vector<CopySeg> segs;
       for (int v = 0; v < V; ++v) {
-        if (pred_out) par_copy(pred_out + v * n + c0, hp.host[b] + in_b + v * chunk * 8, m * 8);
-        if (status_out) par_copy(status_out + v * n + c0, hp.host[b] + in_b + pred_b + v * chunk, m);
+        if (pred_out) segs.push_back({pred_out + v * n + c0, hp.host[b] + in_b + v * chunk * 8, m * 8});
+        if (status_out) segs.push_back({status_out + v * n + c0, hp.host[b] + in_b + pred_b + v * chunk, m});
       }
+      copy_pool().run(segs);
     };
     for (size_t k = 0, c0 = 0; c0 < n; ++k, c0 += chunk) {
       const int b = static_cast<int>(k % S);
@@ -685,12 +768,13 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
       cudaStream_t st = hp.streams[b];
       char* d = hp.dev[b];
       char* h = pinned ? nullptr : hp.host[b];
+      if (!pinned) {
+        std::vector<CopySeg> segs;
+        for (int j = 0; j < np; ++j) segs.push_back({h + j * chunk * 8, host_cols[j] + c0, m * 8});
+        copy_pool().run(segs);
+      }
       for (int j = 0; j < np; ++j) {
-        const void* src = host_cols[j] + c0;
-        if (!pinned) {
-          par_copy(h + j * chunk * 8, src, m * 8);
-          src = h + j * chunk * 8;
-        }
+        const void* src = pinned ? static_cast<const void*>(host_cols[j] + c0) : h + j * chunk * 8;
         cuda_check(cudaMemcpyAsync(d + j * chunk * 8, src, m * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync H2D");
       }
       for (int v = 0; v < V; ++v) {
