@@ -815,6 +815,24 @@ int kcg_gram_accumulate(const double* X, size_t n, int F, size_t ld, double* G, 
     static const long long row_split_max = env_ll("KCG_DMMA_MAXF", 72, 48, 72);
     if (!no_wide && F > row_split_max && F <= 160 && ld == static_cast<size_t>(F) &&
         reinterpret_cast<uintptr_t>(X) % 16 == 0 && n >= 32) {
+      static const bool grouped = env_ll("KCG_WIDE_GROUPED", 1, 0, 1) == 1;
+      if (grouped) {
+        // block-run groups x row-split warps (one CTA per SM), rows shared via L2
+        const std::string name = "kcg_gram_group_" + std::to_string(F);
+        void* k = kcg::jit_kernel(kcg::gram_group_source(F, name), name);
+        struct {
+          const double* X;
+          int64_t n;
+          double *G, *xt1, *cmax;
+        } args{X, static_cast<int64_t>(n), G, xt1, colmax};
+        const int NGr = kcg::gram_group_count(F);
+        const size_t tiles = std::max<size_t>(1, n / 64);
+        const size_t per = std::max<size_t>(1, std::min<size_t>(tiles, static_cast<size_t>(kcg::num_sms()) / NGr));
+        void* argv[] = {&args.X, &args.n, &args.G, &args.xt1, &args.cmax};
+        kcg::launch_jit_argv(k, argv, static_cast<unsigned>(per * NGr), 256, stream, kcg::gram_group_smem(F));
+        ++g_launches;
+        return KCG_OK;
+      }
       // wide design on the tensor cores: one NVRTC specialisation per width
       const std::string name = "kcg_gram_wide_" + std::to_string(F);
       void* k = kcg::jit_kernel(kcg::gram_wide_source(F, name), name);

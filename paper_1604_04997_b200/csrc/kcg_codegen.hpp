@@ -41,6 +41,10 @@ double predict_fold(const Lowered& L, int j);
 /// NVRTC-specialised kernel per width (gram_wide.cpp): its source, its ring
 /// size (dynamic shared memory) and launch shape (512 threads, 1 CTA/SM).
 std::string gram_wide_source(int F, const std::string& name);
+// grouped row-split DMMA Gram (gram_wide.cpp): G groups of block runs, 8 warps split rows
+int gram_group_count(int F);
+size_t gram_group_smem(int F);
+std::string gram_group_source(int F, const std::string& name);
 size_t gram_wide_smem(int F);
 int gram_wide_warps(int F);
 int gram_wide_ctas(int F);

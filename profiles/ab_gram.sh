@@ -1,5 +1,7 @@
-# A/B: row-split DMMA (one CTA/SM) vs the per-width kernel for 65 <= F <= 72 (KCG_DMMA_MAXF)
-for e in "KCG_DMMA_MAXF=64" "KCG_DMMA_MAXF=72"; do
-  echo "$e $(env $e python profiles/time_gram.py 50000000 66,72)"
+# A/B: grouped row-split DMMA Gram (KCG_WIDE_GROUPED=1) vs the per-warp-run kernel for F > 72
+for e in "KCG_WIDE_GROUPED=0" "KCG_WIDE_GROUPED=1"; do
+  echo "$e $(env $e python profiles/time_gram.py 20000000 80,96,111,149,160)"
 done
-KCG_DMMA_MAXF=72 python -m pytest tests/test_gpu_parity.py -m gpu -q -k "gram" 2>&1 | tail -1
+python -m pytest tests/test_gpu_parity.py -m gpu -q -k "gram" 2>&1 | tail -1
+timeout 300 compute-sanitizer --tool memcheck --print-limit 10 python tests/sanitize_gram.py 2>&1 | tail -1
+timeout 300 compute-sanitizer --tool racecheck --print-limit 10 python tests/sanitize_gram.py 2>&1 | tail -1
