@@ -504,10 +504,9 @@ __global__ void __launch_bounds__(256, CT)
   }
 }
 
-template <int NB, int CT>
+template <int NB, int CT, int R = (NB <= 2 ? 256 : (NB == 3 ? 128 : 64))>
 void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, double* colmax,
                       cudaStream_t stream) {
-  constexpr int R = NB <= 2 ? 256 : (NB == 3 ? 128 : 64);
   const size_t red_b = (size_t)(NB * 8 * NB * 8 + 2 * NB * 8) * sizeof(double);
   int stages;
   if (CT == 1) {
@@ -519,7 +518,7 @@ void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, 
     // ring: up to 4 stages within ~100 KB so that two CTAs share an SM
     stages = (int)((100 * 1024) / ((size_t)R * F * 8));
     stages = stages < 2 ? 2 : (stages > 4 ? 4 : stages);
-    if (NB >= 5) stages = F <= 40 ? 4 : 3;
+    if (NB >= 5 && R == 64) stages = F <= 40 ? 4 : 3;
   }
   const size_t smem = (size_t)stages * R * F * sizeof(double) + red_b;
   // the opt-in size grows with F within one NB (per device, process-wide)
@@ -712,12 +711,19 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
     static const int one_from = std::getenv("KCG_DMMA_ONE_CTA_NB") ? std::atoi(std::getenv("KCG_DMMA_ONE_CTA_NB")) : 6;
     const int nb = (F + 7) / 8;
     const bool one = nb >= one_from;
+    // 128-row tiles for NB = 4, 5 at two CTAs/SM (F = 40: 6.49 -> 6.17 ms);
+    // KCG_DMMA_TALL=0 restores 64
+    static const bool tall = !(std::getenv("KCG_DMMA_TALL") && std::atoi(std::getenv("KCG_DMMA_TALL")) == 0);
     switch (nb) {
       case 1: return one ? launch_gram_dmma<1, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<1, 2>(X, n, F, G, xt1, colmax, st);
       case 2: return one ? launch_gram_dmma<2, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<2, 2>(X, n, F, G, xt1, colmax, st);
       case 3: return one ? launch_gram_dmma<3, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<3, 2>(X, n, F, G, xt1, colmax, st);
-      case 4: return one ? launch_gram_dmma<4, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<4, 2>(X, n, F, G, xt1, colmax, st);
-      case 5: return one ? launch_gram_dmma<5, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<5, 2>(X, n, F, G, xt1, colmax, st);
+      case 4:
+        if (tall && !one) return launch_gram_dmma<4, 2, 128>(X, n, F, G, xt1, colmax, st);
+        return one ? launch_gram_dmma<4, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<4, 2>(X, n, F, G, xt1, colmax, st);
+      case 5:
+        if (tall && !one) return launch_gram_dmma<5, 2, 128>(X, n, F, G, xt1, colmax, st);
+        return one ? launch_gram_dmma<5, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<5, 2>(X, n, F, G, xt1, colmax, st);
       case 6: return one ? launch_gram_dmma<6, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<6, 2>(X, n, F, G, xt1, colmax, st);
       case 7: return launch_gram_dmma<7, 1>(X, n, F, G, xt1, colmax, st);
       case 8: return launch_gram_dmma<8, 1>(X, n, F, G, xt1, colmax, st);
