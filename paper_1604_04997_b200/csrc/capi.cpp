@@ -761,44 +761,51 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
       }
       copy_pool().run(segs);
     };
-    for (size_t k = 0, c0 = 0; c0 < n; ++k, c0 += chunk) {
-      const int b = static_cast<int>(k % S);
-      unstage(b);
-      const size_t m = std::min(chunk, n - c0);
-      cudaStream_t st = hp.streams[b];
-      char* d = hp.dev[b];
-      char* h = pinned ? nullptr : hp.host[b];
-      if (!pinned) {
-        std::vector<CopySeg> segs;
-        for (int j = 0; j < np; ++j) segs.push_back({h + j * chunk * 8, host_cols[j] + c0, m * 8});
-        copy_pool().run(segs);
+    // on any failure, let the in-flight copies finish before the staging can
+    // be reused or freed by a later call
+    try {
+      for (size_t k = 0, c0 = 0; c0 < n; ++k, c0 += chunk) {
+        const int b = static_cast<int>(k % S);
+        unstage(b);
+        const size_t m = std::min(chunk, n - c0);
+        cudaStream_t st = hp.streams[b];
+        char* d = hp.dev[b];
+        char* h = pinned ? nullptr : hp.host[b];
+        if (!pinned) {
+          std::vector<CopySeg> segs;
+          for (int j = 0; j < np; ++j) segs.push_back({h + j * chunk * 8, host_cols[j] + c0, m * 8});
+          copy_pool().run(segs);
+        }
+        for (int j = 0; j < np; ++j) {
+          const void* src = pinned ? static_cast<const void*>(host_cols[j] + c0) : h + j * chunk * 8;
+          cuda_check(cudaMemcpyAsync(d + j * chunk * 8, src, m * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync H2D");
+        }
+        for (int v = 0; v < V; ++v) {
+          std::vector<const int64_t*> cols(std::max(np, 1), nullptr);
+          for (int j = 0; j < np; ++j) cols[j] = reinterpret_cast<const int64_t*>(d + maps[v][j] * chunk * 8);
+          double* dp = pred_out ? reinterpret_cast<double*>(d + in_b + v * chunk * 8) : nullptr;
+          uint8_t* ds = status_out ? reinterpret_cast<uint8_t*>(d + in_b + pred_b + v * chunk) : nullptr;
+          const int rc = kcg_eval_predict(progs[v], cols.data(), m, alpha, dp, ds, nullptr, nullptr, 0, st);
+          if (rc != KCG_OK) throw KcgError(rc, g_last_error);
+          if (pred_out)
+            cuda_check(cudaMemcpyAsync(pinned ? static_cast<void*>(pred_out + v * n + c0) : h + in_b + v * chunk * 8, dp,
+                                       m * 8, cudaMemcpyDeviceToHost, st),
+                       "cudaMemcpyAsync D2H");
+          if (status_out)
+            cuda_check(cudaMemcpyAsync(pinned ? static_cast<void*>(status_out + v * n + c0) : h + in_b + pred_b + v * chunk,
+                                       ds, m, cudaMemcpyDeviceToHost, st),
+                       "cudaMemcpyAsync D2H");
+        }
+        cuda_check(cudaEventRecord(hp.events[b], st), "cudaEventRecord");
+        busy_c0[b] = c0;
+        busy_m[b] = m;
       }
-      for (int j = 0; j < np; ++j) {
-        const void* src = pinned ? static_cast<const void*>(host_cols[j] + c0) : h + j * chunk * 8;
-        cuda_check(cudaMemcpyAsync(d + j * chunk * 8, src, m * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync H2D");
-      }
-      for (int v = 0; v < V; ++v) {
-        std::vector<const int64_t*> cols(std::max(np, 1), nullptr);
-        for (int j = 0; j < np; ++j) cols[j] = reinterpret_cast<const int64_t*>(d + maps[v][j] * chunk * 8);
-        double* dp = pred_out ? reinterpret_cast<double*>(d + in_b + v * chunk * 8) : nullptr;
-        uint8_t* ds = status_out ? reinterpret_cast<uint8_t*>(d + in_b + pred_b + v * chunk) : nullptr;
-        const int rc = kcg_eval_predict(progs[v], cols.data(), m, alpha, dp, ds, nullptr, nullptr, 0, st);
-        if (rc != KCG_OK) throw KcgError(rc, g_last_error);
-        if (pred_out)
-          cuda_check(cudaMemcpyAsync(pinned ? static_cast<void*>(pred_out + v * n + c0) : h + in_b + v * chunk * 8, dp,
-                                     m * 8, cudaMemcpyDeviceToHost, st),
-                     "cudaMemcpyAsync D2H");
-        if (status_out)
-          cuda_check(cudaMemcpyAsync(pinned ? static_cast<void*>(status_out + v * n + c0) : h + in_b + pred_b + v * chunk,
-                                     ds, m, cudaMemcpyDeviceToHost, st),
-                     "cudaMemcpyAsync D2H");
-      }
-      cuda_check(cudaEventRecord(hp.events[b], st), "cudaEventRecord");
-      busy_c0[b] = c0;
-      busy_m[b] = m;
+      const size_t nch = (n + chunk - 1) / chunk;
+      for (size_t k = nch > static_cast<size_t>(S) ? nch - S : 0; k < nch; ++k) unstage(static_cast<int>(k % S));
+    } catch (...) {
+      for (int b = 0; b < S; ++b) cudaStreamSynchronize(hp.streams[b]);
+      throw;
     }
-    const size_t nch = (n + chunk - 1) / chunk;
-    for (size_t k = nch > static_cast<size_t>(S) ? nch - S : 0; k < nch; ++k) unstage(static_cast<int>(k % S));
     return KCG_OK;
   });
 }
