@@ -739,6 +739,8 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
     const bool pinned = (flags & KCG_HOST_PINNED) != 0;
     const size_t chunk = std::min<size_t>(n, static_cast<size_t>(env_ll("KCG_HOST_CHUNK", 1 << 22, 1024, 1ll << 28)));
     const int S = static_cast<int>(env_ll("KCG_HOST_STREAMS", 3, 1, 8));
+    // pinned callers: one 2D D2H copy per chunk for all programs (KCG_HOST_2D=0: one per program)
+    const bool copy2d = env_ll("KCG_HOST_2D", 1, 0, 1) == 1;
     // slot layout: np binding columns, V prediction columns, V status columns
     const size_t in_b = static_cast<size_t>(std::max(np, 1)) * chunk * 8;
     const size_t pred_b = pred_out ? static_cast<size_t>(V) * chunk * 8 : 0;
@@ -787,7 +789,7 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
           uint8_t* ds = status_out ? reinterpret_cast<uint8_t*>(d + in_b + pred_b + v * chunk) : nullptr;
           const int rc = kcg_eval_predict(progs[v], cols.data(), m, alpha, dp, ds, nullptr, nullptr, 0, st);
           if (rc != KCG_OK) throw KcgError(rc, g_last_error);
-          if (pred_out)
+          if (pred_out && !(pinned && copy2d))
             cuda_check(cudaMemcpyAsync(pinned ? static_cast<void*>(pred_out + v * n + c0) : h + in_b + v * chunk * 8, dp,
                                        m * 8, cudaMemcpyDeviceToHost, st),
                        "cudaMemcpyAsync D2H");
@@ -796,6 +798,9 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
                                        ds, m, cudaMemcpyDeviceToHost, st),
                        "cudaMemcpyAsync D2H");
         }
+        if (pred_out && pinned && copy2d)  // all programs' predictions of the chunk in one copy
+          cuda_check(cudaMemcpy2DAsync(pred_out + c0, n * 8, d + in_b, chunk * 8, m * 8, V, cudaMemcpyDeviceToHost, st),
+                     "cudaMemcpy2DAsync D2H");
         cuda_check(cudaEventRecord(hp.events[b], st), "cudaEventRecord");
         busy_c0[b] = c0;
         busy_m[b] = m;
