@@ -88,3 +88,23 @@ def test_host_eval_param_order_follows_first_program():
     for i, p in enumerate(progs):
         want = kc.predict(w, p, dev).cpu()
         assert torch.equal(pred[i].view(torch.int64), want.view(torch.int64))
+
+
+@pytest.mark.gpu
+def test_host_eval_int128_and_single_param_programs(monkeypatch):
+    """Skinny matmul past the int64-safe box (int128 counts, > 2^53
+    conversions) and a one-parameter program through the host pipeline,
+    several chunks each: bitwise the device path."""
+    import torch
+    monkeypatch.setenv("KCG_HOST_CHUNK", "4096")
+    w = _weights()
+    u = np.arange(1, 20001, dtype=np.int64) * 97
+    cases = [(kc.load_program("matmul_skinny_g16x16"), {"n": 16 * u, "m": 128 * u, "l": 16 * u}),
+             (kc.load_program("conv_g16x16"), {"n": 16 * u})]
+    for prog, b in cases:
+        pred, st = kc.predict_host([prog], w, b, status=True)
+        dev = {k: torch.from_numpy(v).cuda() for k, v in b.items()}
+        want, wst = kc.predict(w, prog, dev, with_status=True)
+        assert torch.equal(pred[0].view(torch.int64), want.cpu().view(torch.int64))
+        assert torch.equal(st[0], wst.cpu())
+        assert int((wst == 0).sum()) > 0
