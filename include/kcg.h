@@ -173,6 +173,9 @@ int kcg_eval_predict_grid(const kcg_program* prog, const kcg_grid* grid, uint64_
                           uint8_t* status_out, int simulate, void* stream);
 
 /* ---- host buffers: the reference's own calling convention ---------------
+ * Replaces the reference's per-point host loop `evaluate_properties` +
+ * `predict` (props.hpp:49-50, model.hpp:61; the loop of bench.cpp:47-56 and
+ * of the CLI's predict/eval over variants, kernelcost.cpp:236-400).
  * The same evaluate + predict for n_progs programs over one set of HOST
  * bindings (e.g. every variant of an autotuning sweep): host_cols follow
  * progs[0]'s parameter order (n_points int64 each; every program must have
