@@ -24,6 +24,7 @@
  *   - Buffers are caller-owned. Unless stated otherwise, array arguments of
  *     the launch functions are DEVICE pointers and `stream` is a cudaStream_t
  *     (NULL = legacy default stream). Launch functions are asynchronous.
+ *     kcg_eval_predict_host is the exception: HOST buffers, synchronous.
  *   - Handles are thread-compatible (externally synchronised), not
  *     thread-safe.
  *   - There is no CPU fallback: launch functions return KCG_E_CUDA when no
