@@ -714,10 +714,14 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
     // 128-row tiles for NB = 4, 5 at two CTAs/SM (F = 40: 6.49 -> 6.17 ms);
     // KCG_DMMA_TALL=0 restores 64
     static const bool tall = !(std::getenv("KCG_DMMA_TALL") && std::atoi(std::getenv("KCG_DMMA_TALL")) == 0);
+    // 256-row tiles for NB = 3 too (F = 24: 2.81 -> 2.74 ms, 7.0 TB/s); KCG_DMMA_TALL3=0 restores 128
+    static const bool tall3 = !(std::getenv("KCG_DMMA_TALL3") && std::atoi(std::getenv("KCG_DMMA_TALL3")) == 0);
     switch (nb) {
       case 1: return one ? launch_gram_dmma<1, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<1, 2>(X, n, F, G, xt1, colmax, st);
       case 2: return one ? launch_gram_dmma<2, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<2, 2>(X, n, F, G, xt1, colmax, st);
-      case 3: return one ? launch_gram_dmma<3, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<3, 2>(X, n, F, G, xt1, colmax, st);
+      case 3:
+        if (tall3 && !one) return launch_gram_dmma<3, 2, 256>(X, n, F, G, xt1, colmax, st);
+        return one ? launch_gram_dmma<3, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<3, 2>(X, n, F, G, xt1, colmax, st);
       case 4:
         if (tall && !one) return launch_gram_dmma<4, 2, 128>(X, n, F, G, xt1, colmax, st);
         return one ? launch_gram_dmma<4, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<4, 2>(X, n, F, G, xt1, colmax, st);
