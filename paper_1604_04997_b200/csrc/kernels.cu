@@ -717,7 +717,11 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
     // 256-row tiles for NB = 3 too (F = 24: 2.81 -> 2.74 ms, 7.0 TB/s); KCG_DMMA_TALL3=0 restores 128
     static const bool tall3 = !(std::getenv("KCG_DMMA_TALL3") && std::atoi(std::getenv("KCG_DMMA_TALL3")) == 0);
     switch (nb) {
-      case 1: return one ? launch_gram_dmma<1, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<1, 2>(X, n, F, G, xt1, colmax, st);
+      case 1:
+        // very narrow rows: taller tiles keep every bulk copy >= 16 KB
+        if (!one && tall && F <= 2) return launch_gram_dmma<1, 2, 1024>(X, n, F, G, xt1, colmax, st);
+        if (!one && tall && F <= 4) return launch_gram_dmma<1, 2, 512>(X, n, F, G, xt1, colmax, st);
+        return one ? launch_gram_dmma<1, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<1, 2>(X, n, F, G, xt1, colmax, st);
       case 2: return one ? launch_gram_dmma<2, 1>(X, n, F, G, xt1, colmax, st) : launch_gram_dmma<2, 2>(X, n, F, G, xt1, colmax, st);
       case 3:
         if (tall3 && !one) return launch_gram_dmma<3, 2, 256>(X, n, F, G, xt1, colmax, st);
