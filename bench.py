@@ -322,7 +322,7 @@ def cpu_lowered_baseline(kc, progs, alpha, threads, side, sizes=4_000_000):
     predictions are checked bitwise against the GPU's on a sample."""
     import numpy as np
     try:
-        from paper_1604_04997_b200.hostbuild import HostEvaluator
+        from tools.hostbuild import HostEvaluator
         idx = np.arange(sizes, dtype=np.int64)
         cols = {"n": (idx // (side * side) + 1) * UNIT, "m": ((idx // side) % side + 1) * UNIT,
                 "l": (idx % side + 1) * UNIT}

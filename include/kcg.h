@@ -197,6 +197,16 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int n_progs,
                           const double* alpha, double* pred_out, uint8_t* status_out,
                           unsigned flags);
 
+/* Which copy path the last kcg_eval_predict_host call of this process took
+ * (diagnostics for tests): KCG_HOST_PINNED if the caller's buffers were
+ * used directly, | KCG_HOST_PATH_2D if the predictions of each chunk
+ * returned in one cudaMemcpy2DAsync (only when n_points * 8 fits the
+ * device's cudaDevAttrMaxPitch), | KCG_HOST_PATH_ONEPASS if the variants
+ * were evaluated by one multi-program kernel per chunk. 0 before any call. */
+#define KCG_HOST_PATH_2D 2u
+#define KCG_HOST_PATH_ONEPASS 4u
+unsigned kcg_host_last_path(void);
+
 /* ---- autotuning: evaluate + predict over variants, argmin --------------
  * progs: n_variants programs with identical parameter-name sets; param_cols
  * follow progs[0]'s parameter order. For each size i: best_idx[i] = lowest

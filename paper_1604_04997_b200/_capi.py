@@ -104,6 +104,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_last_error": (ctypes.c_char_p, []),
         "kcg_launch_count": (ctypes.c_uint64, []),
         "kcg_eval_predict_host": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_size_t, P, P, P, ctypes.c_uint]),
+        "kcg_host_last_path": (ctypes.c_uint, []),
         "kcg_measure_pipe_peak": (ctypes.c_int, [ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]),
     }
     for name, (res, args) in sig.items():
@@ -143,6 +144,8 @@ E_IO = 10
 E_INVALID_ARGUMENT = 11
 E_CUDA = 100
 HOST_PINNED = 1  # kcg_eval_predict_host flags (KCG_HOST_PINNED)
+HOST_PATH_2D = 2  # kcg_host_last_path bits
+HOST_PATH_ONEPASS = 4
 E_JIT = 101
 E_UNSUPPORTED = 102
 

@@ -331,9 +331,11 @@ def predict_host(progs: Sequence[Program], w: ModelWeights, bindings, status: bo
     pred = out if out is not None else torch.empty((V, n), dtype=torch.float64)
     if tuple(pred.shape) != (V, n) or pred.dtype != torch.float64 or not pred.is_contiguous():
         raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "out must be a contiguous [n_progs, n] float64 CPU tensor")
-    st = torch.empty((V, n), dtype=torch.uint8) if status else None
     if pinned is None:
-        pinned = all(t.is_pinned() for t in cols + [pred] + ([st] if st is not None else [])) if n else False
+        pinned = all(t.is_pinned() for t in cols + [pred]) if n else False
+    st = None
+    if status:  # the status buffer follows the caller's buffers (pinned or not)
+        st = torch.empty((V, n), dtype=torch.uint8, pin_memory=bool(pinned and n))
     handles = (ctypes.c_void_p * V)(*[p.handle.value for p in progs])
     arr = (ctypes.c_void_p * max(1, len(cols)))(*[c.data_ptr() for c in cols])
     check(lib().kcg_eval_predict_host(handles, V, arr, n, w.alpha_array(), pred.data_ptr(),
@@ -359,8 +361,29 @@ class GramStats:
         return cls(z(F, F), z(F), z(F))
 
 
+def _check_design(X) -> None:
+    """X: a CUDA float64 [N, F] matrix with unit column stride (rows may be
+    padded: stride(0) >= F). Anything else would be read out of bounds or
+    silently mis-strided by the kernels."""
+    torch = _torch()
+    if not (isinstance(X, torch.Tensor) and X.dim() == 2 and X.is_cuda and X.dtype == torch.float64
+            and (X.stride(1) == 1 or X.shape[1] <= 1) and X.stride(0) >= X.shape[1]):
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT,
+                             "X must be a CUDA float64 [N, F] tensor with stride(1) == 1")
+
+
+def _check_times(T, n: int, device) -> None:
+    """T: n contiguous CUDA float64 measured times on the bindings' device."""
+    torch = _torch()
+    if not (isinstance(T, torch.Tensor) and T.is_cuda and T.dtype == torch.float64 and T.is_contiguous()
+            and T.numel() == n and T.device == device):
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT,
+                             f"T must be {n} contiguous CUDA float64 times on {device}")
+
+
 def gram_accumulate(X, stats: GramStats | None = None, stream=None) -> GramStats:
     """G += XᵀX, Xᵀ1, colmax over a materialised design X [N, F] fp64."""
+    _check_design(X)
     N, F = X.shape
     stats = stats or GramStats.zeros(F, X.device)
     check(lib().kcg_gram_accumulate(X.data_ptr(), N, F, X.stride(0), stats.G.data_ptr(),
@@ -373,6 +396,7 @@ def gram_fused(prog: Program, bindings, T, stats: GramStats | None = None, strea
     """Fused evaluate -> design row (count/T, model.cpp:29) -> Gram."""
     torch = _torch()
     arr, n, cols = _columns(prog, bindings)
+    _check_times(T, n, cols[0].device if cols else T.device)
     F = len(prog.props)
     stats = stats or GramStats.zeros(F, cols[0].device)
     bad = torch.zeros(1, dtype=torch.int64, device=cols[0].device)
@@ -389,6 +413,7 @@ def residual_fused(prog: Program, bindings, T, alpha149: Sequence[float], stream
     rows x_r = count/T formed from the bindings on the fly."""
     torch = _torch()
     arr, n, cols = _columns(prog, bindings)
+    _check_times(T, n, cols[0].device if cols else T.device)
     obj = torch.zeros(1, dtype=torch.float64, device=cols[0].device)
     a = (ctypes.c_double * len(alpha149))(*alpha149)
     check(lib().kcg_residual_fused(prog.handle, arr, T.data_ptr(), n, a, obj.data_ptr(), _stream(stream)))
@@ -423,6 +448,7 @@ def fit_weights(X, refine: int = 1, stream=None) -> FitResult:
     min-norm solve, `refine` semi-normal refinement passes, objective from a
     residual pass (never from the Gram identity)."""
     torch = _torch()
+    _check_design(X)
     N, F = X.shape
     if N == 0:
         raise _capi.KcgError(_capi.E_EMPTY, "empty design matrix")

@@ -51,6 +51,7 @@ namespace {
 
 thread_local std::string g_last_error;
 std::atomic<uint64_t> g_launches{0};
+std::atomic<unsigned> g_host_last_path{0};
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -681,22 +682,27 @@ struct HostPipe {
       host.push_back(nullptr);
       ++slots;
     }
+    // slots added by a later call with more streams start null: (re)allocate
+    // every slot that is missing or smaller than this call needs
     if (dbytes > dev_bytes) {
       for (auto& d : dev) {
         if (d) cudaFree(d);
         d = nullptr;
       }
-      for (int b = 0; b < slots; ++b) cuda_check(cudaMalloc(&dev[b], dbytes), "cudaMalloc");
       dev_bytes = dbytes;
     }
+    for (int b = 0; b < slots; ++b)
+      if (!dev[b] && dev_bytes > 0) cuda_check(cudaMalloc(&dev[b], dev_bytes), "cudaMalloc");
     if (hbytes > host_bytes) {
       for (auto& h : host) {
         if (h) cudaFreeHost(h);
         h = nullptr;
       }
-      for (int b = 0; b < slots; ++b) cuda_check(cudaHostAlloc(&host[b], hbytes, cudaHostAllocDefault), "cudaHostAlloc");
       host_bytes = hbytes;
     }
+    if (hbytes > 0)
+      for (int b = 0; b < slots; ++b)
+        if (!host[b]) cuda_check(cudaHostAlloc(&host[b], host_bytes, cudaHostAllocDefault), "cudaHostAlloc");
   }
 };
 
@@ -740,7 +746,14 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
     const size_t chunk = std::min<size_t>(n, static_cast<size_t>(env_ll("KCG_HOST_CHUNK", 1 << 22, 1024, 1ll << 28)));
     const int S = static_cast<int>(env_ll("KCG_HOST_STREAMS", 3, 1, 8));
     // pinned callers: one 2D D2H copy per chunk for all programs (KCG_HOST_2D=0: one per program)
-    const bool copy2d = env_ll("KCG_HOST_2D", 1, 0, 1) == 1;
+    // cudaMemcpy2DAsync rejects a pitch above cudaDevAttrMaxPitch (2^31 - 1
+    // on current parts): n * 8 must fit, else one 1D copy per program
+    // (KCG_HOST_MAX_PITCH lowers the limit for tests of the fallback)
+    int max_pitch = 0, cur_dev = 0;
+    cuda_check(cudaGetDevice(&cur_dev), "cudaGetDevice");
+    cuda_check(cudaDeviceGetAttribute(&max_pitch, cudaDevAttrMaxPitch, cur_dev), "cudaDeviceGetAttribute");
+    const long long pitch_cap = env_ll("KCG_HOST_MAX_PITCH", max_pitch, 8, max_pitch);
+    const bool copy2d = env_ll("KCG_HOST_2D", 1, 0, 1) == 1 && n * 8 <= static_cast<unsigned long long>(pitch_cap);
     // slot layout: np binding columns, V prediction columns, V status columns
     const size_t in_b = static_cast<size_t>(std::max(np, 1)) * chunk * 8;
     const size_t pred_b = pred_out ? static_cast<size_t>(V) * chunk * 8 : 0;
@@ -811,9 +824,12 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
       for (int b = 0; b < S; ++b) cudaStreamSynchronize(hp.streams[b]);
       throw;
     }
+    g_host_last_path = (pinned ? KCG_HOST_PINNED : 0u) | (pinned && copy2d && pred_out ? KCG_HOST_PATH_2D : 0u);
     return KCG_OK;
   });
 }
+
+unsigned kcg_host_last_path(void) { return g_host_last_path.load(); }
 
 int kcg_gram_accumulate(const double* X, size_t n, int F, size_t ld, double* G, double* xt1,
                         double* colmax, void* stream) {

@@ -1,7 +1,10 @@
 // NVRTC specialisation: compile generated CUDA to an sm_100a cubin, load it
 // context-independently (cudaLibraryLoadData) and cache the kernel handle
 // per source hash, in process and on disk ($KCG_JIT_CACHE, default
-// /tmp/kcg_jit_cache) so repeated processes skip the ~0.3 s compile.
+// /tmp/kcg_jit_cache-<uid>, created 0700 and used only if this user owns it
+// and nobody else can write it) so repeated processes skip the ~0.3 s
+// compile. The cache key covers the source, the NVRTC version and the
+// compile options; a cubin that fails to load is recompiled, not trusted.
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 #include <sys/stat.h>
@@ -35,9 +38,44 @@ uint64_t fnv1a64(const std::string& s) {
   return h;
 }
 
+constexpr int kNumOpts = 5;
+const char* const kOpts[kNumOpts] = {"-arch=sm_100a", "-std=c++17", "--device-int128", "-lineinfo", "-DKCG_JIT=1"};
+
+// what besides the source decides the cubin: compiler version and options
+const std::string& compile_salt() {
+  static const std::string salt = [] {
+    int major = 0, minor = 0;
+    nvrtcVersion(&major, &minor);
+    std::string s = "nvrtc" + std::to_string(major) + "." + std::to_string(minor);
+    for (const char* o : kOpts) s += std::string("|") + o;
+    return s;
+  }();
+  return salt;
+}
+
+// "" = no usable disk cache (the directory is not ours or is writable by others)
 std::string cache_dir() {
   const char* env = std::getenv("KCG_JIT_CACHE");
-  return env && *env ? env : "/tmp/kcg_jit_cache";
+  const std::string dir = env && *env ? std::string(env) : "/tmp/kcg_jit_cache-" + std::to_string(getuid());
+  mkdir(dir.c_str(), 0700);
+  struct stat st;
+  if (stat(dir.c_str(), &st) != 0 || !S_ISDIR(st.st_mode) || st.st_uid != getuid() || (st.st_mode & 022) != 0)
+    return "";
+  return dir;
+}
+
+bool write_file(const std::string& path, const std::vector<char>& data) {
+  const std::string tmp = path + ".tmp." + std::to_string(getpid());
+  bool ok;
+  {
+    std::ofstream out(tmp, std::ios::binary | std::ios::trunc);
+    out.write(data.data(), static_cast<std::streamsize>(data.size()));
+    out.flush();
+    ok = static_cast<bool>(out);
+  }
+  if (ok) ok = std::rename(tmp.c_str(), path.c_str()) == 0;
+  if (!ok) std::remove(tmp.c_str());
+  return ok;
 }
 
 bool read_file(const std::string& path, std::vector<char>& out) {
@@ -52,9 +90,7 @@ std::vector<char> compile(const std::string& src, const std::string& name) {
   if (nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr,
                          nullptr) != NVRTC_SUCCESS)
     throw KcgError(KCG_E_JIT, "nvrtcCreateProgram failed");
-  const char* opts[] = {"-arch=sm_100a", "-std=c++17", "--device-int128",
-                        "-lineinfo", "-DKCG_JIT=1"};
-  const nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
+  const nvrtcResult r = nvrtcCompileProgram(prog, kNumOpts, const_cast<const char**>(kOpts));
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
@@ -78,7 +114,7 @@ void jit_compile_only(const std::string& src, const std::string& name) { compile
 void* jit_kernel(const std::string& src, const std::string& name) {
   char hex[32];
   std::snprintf(hex, sizeof hex, "%016llx",
-                static_cast<unsigned long long>(fnv1a64(src)));
+                static_cast<unsigned long long>(fnv1a64(compile_salt() + "\n" + src)));
   const std::string key = std::string(hex) + ":" + name;
   std::lock_guard<std::mutex> lock(g_mu);
   auto it = g_kernels.find(key);
@@ -90,20 +126,21 @@ void* jit_kernel(const std::string& src, const std::string& name) {
     lib = lit->second;
   } else {
     const std::string dir = cache_dir();
-    const std::string path = dir + "/kcg_" + hex + ".cubin";
+    const std::string path = dir.empty() ? "" : dir + "/kcg_" + hex + ".cubin";
     std::vector<char> cubin;
-    if (!read_file(path, cubin)) {
+    const bool cached = !path.empty() && read_file(path, cubin);
+    if (!cached) {
       cubin = compile(src, name);
-      mkdir(dir.c_str(), 0777);
-      const std::string tmp = path + ".tmp." + std::to_string(getpid());
-      {
-        std::ofstream out(tmp, std::ios::binary);
-        out.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
-      }
-      std::rename(tmp.c_str(), path.c_str());
+      if (!path.empty()) write_file(path, cubin);  // best effort: a failed write only costs a recompile later
     }
-    const cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0,
-                                              nullptr, nullptr, 0);
+    cudaError_t e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    if (e != cudaSuccess && cached) {
+      // a truncated or foreign cubin: recompile from source and replace it
+      cudaGetLastError();
+      cubin = compile(src, name);
+      write_file(path, cubin);
+      e = cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+    }
     if (e != cudaSuccess)
       throw KcgError(KCG_E_CUDA, std::string("cudaLibraryLoadData: ") + cudaGetErrorString(e));
     g_libs.emplace(hex, lib);

@@ -31,19 +31,17 @@ namespace kcg {
 
 namespace {
 
-std::vector<std::string> split(const std::string& s, char sep) {
-  std::vector<std::string> out;
-  std::string cur;
-  for (char c : s) {
-    if (c == sep) {
-      out.push_back(cur);
-      cur.clear();
-    } else {
-      cur.push_back(c);
-    }
+// fields of one CSV line (no quoting in the measurement format): every
+// separator ends a field, so "a,,b," has four fields
+std::vector<std::string> split(const std::string& line, char sep) {
+  std::vector<std::string> fields;
+  size_t start = 0;
+  for (;;) {
+    const size_t end = line.find(sep, start);
+    fields.emplace_back(line, start, end == std::string::npos ? std::string::npos : end - start);
+    if (end == std::string::npos) return fields;
+    start = end + 1;
   }
-  out.push_back(cur);
-  return out;
 }
 
 [[noreturn]] void bad(const std::string& path, int line, const std::string& what) {

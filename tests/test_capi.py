@@ -264,7 +264,7 @@ def test_host_build_of_generated_evaluator_matches_goldens():
 
     import numpy as np
 
-    from paper_1604_04997_b200.hostbuild import HostEvaluator
+    from tools.hostbuild import HostEvaluator
     d = load_golden("grid_samples.json")["samples"]
     fit = load_golden("fit_suite.json")
     alpha = [0.0] * 149
@@ -285,3 +285,34 @@ def test_host_build_of_generated_evaluator_matches_goldens():
             else:
                 assert st[i] != 0, (kid, s["binding"])
     assert checked > 1000
+
+
+def test_design_and_time_inputs_are_validated():
+    """gram_accumulate / fit_weights / gram_fused / residual_fused refuse
+    inputs the kernels would mis-read (CPU, wrong dtype) before any launch."""
+    import torch
+    X = torch.zeros((8, 3), dtype=torch.float64)
+    for f in (kc.gram_accumulate, kc.fit_weights):
+        with pytest.raises(kc.KcgError) as e:
+            f(X)
+        assert e.value.code == _capi.E_INVALID_ARGUMENT
+
+
+@pytest.mark.gpu
+def test_design_and_time_inputs_are_validated_on_device():
+    import torch
+    X = torch.rand((64, 6), dtype=torch.float64, device="cuda")
+    bad = [X[:, ::2], X.float(), X.T]
+    for Xb in bad:
+        with pytest.raises(kc.KcgError) as e:
+            kc.gram_accumulate(Xb)
+        assert e.value.code == _capi.E_INVALID_ARGUMENT
+    prog = kc.load_program("matmul_tiled_g16x16")
+    cols = {p: torch.full((32,), 64, dtype=torch.int64, device="cuda") for p in prog.params}
+    a = [0.0] * kc.schema_size()
+    for T in (torch.ones(31, dtype=torch.float64, device="cuda"), torch.ones(32, dtype=torch.float32, device="cuda"),
+              torch.ones(64, dtype=torch.float64, device="cuda")[::2], torch.ones(32, dtype=torch.float64)):
+        with pytest.raises(kc.KcgError):
+            kc.gram_fused(prog, cols, T)
+        with pytest.raises(kc.KcgError):
+            kc.residual_fused(prog, cols, T, a)

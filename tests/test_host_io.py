@@ -67,6 +67,10 @@ def test_host_eval_bitwise_equals_device_path(monkeypatch, pinned, chunk):
         host = {k: v.pin_memory() for k, v in host.items()}
         out = torch.empty((len(progs), n), dtype=torch.float64).pin_memory()
     pred, st = kc.predict_host(progs, w, host, status=True, out=out)
+    path = _capi.lib().kcg_host_last_path()
+    assert bool(path & _capi.HOST_PINNED) == pinned
+    if pinned:
+        assert st.is_pinned() and path & _capi.HOST_PATH_2D
     dev = {k: v.cuda() for k, v in host.items()}
     for i, p in enumerate(progs):
         want, wst = kc.predict(w, p, dev, with_status=True)
@@ -108,3 +112,32 @@ def test_host_eval_int128_and_single_param_programs(monkeypatch):
         assert torch.equal(pred[0].view(torch.int64), want.cpu().view(torch.int64))
         assert torch.equal(st[0], wst.cpu())
         assert int((wst == 0).sum()) > 0
+
+
+@pytest.mark.gpu
+def test_host_eval_pitch_fallback_and_growing_streams(monkeypatch):
+    """Pinned callers whose n * 8 exceeds the device's max pitch take one 1D
+    D2H copy per program (forced here by lowering the limit); a later call
+    with more internal streams and the same chunk bytes allocates the new
+    slots' staging (pageable path). Both bitwise the device path."""
+    import torch
+    monkeypatch.setenv("KCG_HOST_CHUNK", "8192")
+    n = 5 * 8192 + 77
+    progs = [kc.load_program(v) for v in VARIANTS[:3]]
+    w = _weights()
+    b = _bindings(n, 11)
+    dev = {k: torch.from_numpy(v).cuda() for k, v in b.items()}
+    want = [kc.predict(w, p, dev).cpu() for p in progs]
+    host = {k: torch.from_numpy(v).pin_memory() for k, v in b.items()}
+    out = torch.empty((len(progs), n), dtype=torch.float64).pin_memory()
+    monkeypatch.setenv("KCG_HOST_MAX_PITCH", str(8 * (n - 1)))
+    kc.predict_host(progs, w, host, out=out)
+    assert _capi.lib().kcg_host_last_path() & (_capi.HOST_PINNED | _capi.HOST_PATH_2D) == _capi.HOST_PINNED
+    for i in range(len(progs)):
+        assert torch.equal(out[i].view(torch.int64), want[i].view(torch.int64))
+    monkeypatch.delenv("KCG_HOST_MAX_PITCH")
+    for streams in ("1", "4", "2", "6"):
+        monkeypatch.setenv("KCG_HOST_STREAMS", streams)
+        pred = kc.predict_host(progs, w, b, pinned=False)
+        for i in range(len(progs)):
+            assert torch.equal(pred[i].view(torch.int64), want[i].view(torch.int64)), streams

@@ -1,4 +1,4 @@
-"""The exact evaluator of a lowered program compiled for the host CPU
+"""Tooling, not product (lives outside the package on purpose). The exact evaluator of a lowered program compiled for the host CPU
 (kcg_program_jit_source_kind(prog, 4) + g++ -ffp-contract=off): the
 optimised-CPU baseline bench.py times beside the GPU, and a CPU-side
 cross-check of the code generator in the tests. It is never a fallback:
@@ -12,7 +12,7 @@ import subprocess
 import tempfile
 from pathlib import Path
 
-from . import _capi
+from paper_1604_04997_b200 import _capi
 
 _CACHE = Path(os.environ.get("KCG_HOST_BUILD_DIR", Path(tempfile.gettempdir()) / "kcg_host_build"))
 
