@@ -6,17 +6,20 @@ Headline workload (config 4, materialised mode): the 6 matmul variants of
 the bundled suite (matmul_tiled_g{12,14,16}, matmul_naive_g16x{12,14,16})
 at every size (n,m,l) = 336*(u,v,w), u,v,w in [1,551] -- 551^3 =
 1.673e8 sizes x 6 variants = 1.004e9 (variant, size) points. A step is one
-exact evaluate_properties + predict of every point: per variant one launch
-reads the SoA int64 bindings (24 B/point) and writes one fp64 prediction
-(8 B/point). Inputs (4.0 GB) and outputs (8.0 GB) exceed L2, so no flush is
-needed. Sizes shard contiguously across ranks (strong scaling, no
-collective on the data path).
+exact evaluate_properties + predict of every point: ONE launch of the
+one-pass multi-program kernel (kcg_eval_predict_multi) reads each size's SoA
+int64 bindings once (24 B) and writes all six fp64 predictions (48 B).
+Inputs (4.0 GB) and outputs (8.0 GB) exceed L2, so no flush is needed.
+Sizes shard contiguously across ranks (strong scaling, no collective on the
+data path). The default line also carries the fused argmin (config 4),
+config 2 (1e6 points of the four test kernels) and the config-3 Gram.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import shutil
@@ -99,6 +102,9 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+CPU_SAMPLE_SIZES = 1_000_000  # sizes per CPU sample (x 6 variants): ~5 s on 16 threads
+
+
 def cpu_reference(threads: int, n_sizes: int, offset: int = 0):
     exe = ROOT / "oracle" / "_ref" / "kcref_bench"
     if not exe.exists():
@@ -108,27 +114,57 @@ def cpu_reference(threads: int, n_sizes: int, offset: int = 0):
     return json.loads(out)
 
 
+def host_info(threads: int) -> dict:
+    model = ""
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count(), "threads_used": threads,
+            "build": "oracle/_ref: the reference's own core sources compiled in place, g++ -std=c++20 -O3 "
+                     "-DNDEBUG -ffp-contract=off (CMake Release, the reference default), against the repo's "
+                     "shims: bigint (cpp_int/cpp_rational) instead of Boost.Multiprecision, COD instead of Eigen"}
+
+
+def cpu_reference_line(threads: int, offset: int = 0) -> dict | None:
+    """The one CPU routine behind both the in-line cpu_baseline and the
+    --impl reference arm: the reference's evaluate_properties + predict per
+    (variant, size) point (bench.cpp:47-56 pattern) over CPU_SAMPLE_SIZES
+    sizes of the headline lattice, std::thread fan-out over `threads`."""
+    r = cpu_reference(threads, CPU_SAMPLE_SIZES, offset)
+    if r is None:
+        return None
+    return {"value": r["points_per_s"], "unit": "points/s", "cores": threads, "kind": "reference",
+            "seconds": r["seconds"], "points": r["points"],
+            "sample": f"{r['points'] // len(VARIANTS)} sizes x {len(VARIANTS)} variants of the headline lattice "
+                      f"(from size {offset}), evaluate_properties+predict per point",
+            "host": host_info(threads)}
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference's own CPU path (oracle/_ref: reference
-    sources + shim bigint/COD), all host threads, bounded sample per step."""
+    sources + shim bigint/COD), all host threads, a fixed sample of
+    CPU_SAMPLE_SIZES sizes per step (warm-up steps: a tenth of it)."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    cal = cpu_reference(threads, max(threads * 50, 400))
-    if cal is None:
+    if cpu_reference(threads, 1000) is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/kcref_bench not built"}))
         return
-    rate_sizes = cal["points_per_s"] / len(VARIANTS)
-    n_sizes = int(max(threads * 20, min(rate_sizes * 10.0, 5e6)))  # ~10 s per step
     for w in range(args.warmup):
-        cpu_reference(threads, max(threads * 20, n_sizes // 10), offset=w * 7919)
-    times, pts = [], 0
+        cpu_reference(threads, CPU_SAMPLE_SIZES // 10, offset=w * 7919)
+    times, pts, last = [], 0, None
     for s in range(args.steps):
-        r = cpu_reference(threads, n_sizes, offset=(s * 1_000_003) % (SIDE ** 3 - n_sizes))
-        times.append(r["seconds"])
-        pts = r["points"]
+        last = cpu_reference_line(threads, offset=(s * 1_000_003) % (SIDE ** 3 - CPU_SAMPLE_SIZES))
+        times.append(last["seconds"])
+        pts = last["points"]
     sec = sum(times) / len(times)
     value = pts / sec
+    cb = dict(last)
+    cb["value"] = value
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "points/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -136,9 +172,7 @@ def run_reference_arm(args, rank, world):
         "vs_baseline": None, "dtype": "bigint", "data": "synthetic",
         "config": {"workload": "config4 autotune sample: 6 matmul variants x sizes 336*(u,v,w)",
                    "points_per_step": pts, "threads": threads},
-        "cpu_baseline": {"value": value, "unit": "points/s", "cores": threads, "kind": "reference",
-                         "sample": f"{pts // len(VARIANTS)} sizes x 6 variants per step via "
-                                   "evaluate_properties+predict (reference code + shim bigint)"},
+        "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -155,7 +189,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fit", action="store_true", help="skip the sharded fit (config 5)")
     ap.add_argument("--fit-rows", type=int, default=10**9, help="fit rows per rank")
-    ap.add_argument("--extras", action="store_true", help="also time configs 2/3/5 and argmin")
+    ap.add_argument("--extras", action="store_true", help="also time config 1, config 5 on one GPU, the grid "
+                    "descriptor path and the enumeration oracle")
+    ap.add_argument("--no-configs", action="store_true", help="skip argmin / config 2 / config 3 in the line")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -173,6 +209,9 @@ def main():
     # one process per GPU; KCG_DIST_BACKEND=gloo lets several ranks share
     # one device for a functional dry run of the multi-rank path
     backend = os.environ.get("KCG_DIST_BACKEND", "nccl")
+    if world > 1 and backend == "nccl":  # init lines (ring / NVLS / P2P) for the driver's rank check
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
@@ -196,28 +235,29 @@ def main():
     del idx
     cols = {k: v.contiguous() for k, v in cols.items()}
     # rows padded to a 16-byte multiple so every variant's output row is
-    # aligned for the vector stores (the kernels also accept unaligned rows)
+    # aligned (the kernels also accept unaligned rows)
     ld = (n + 1) // 2 * 2
-    preds = torch.empty((len(VARIANTS), ld), dtype=torch.float64, device=dev)[:, :n]
+    preds = torch.empty((len(VARIANTS), ld), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
+    handles = (ctypes.c_void_p * len(progs))(*[p.handle.value for p in progs])
+    carr = _colarr(progs[0], cols)
+    alpha_arr = w.alpha_array()
 
     def step(ev=None):
-        for v, p in enumerate(progs):
-            if ev is not None:
-                ev[v][0].record(stream)
-            kc.api.check(kc.api.lib().kcg_eval_predict(
-                p.handle, _colarr(p, cols), n, w.alpha_array(), preds[v].data_ptr(),
-                None, None, None, 0, stream.cuda_stream))
-            if ev is not None:
-                ev[v][1].record(stream)
+        # one launch: every variant's evaluate + predict, bindings read once
+        if ev is not None:
+            ev[0].record(stream)
+        kc.api.check(kc.api.lib().kcg_eval_predict_multi(handles, len(progs), carr, n, alpha_arr, preds.data_ptr(),
+                                                         ld, None, 0, stream.cuda_stream))
+        if ev is not None:
+            ev[1].record(stream)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
 
     launches0 = kc.launch_count()
-    evs = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in VARIANTS]
-           for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -233,7 +273,7 @@ def main():
         dist.barrier()
     launches = kc.launch_count() - launches0
     elapsed = start.elapsed_time(end) / 1e3
-    kern_ms = [e[0].elapsed_time(e[1]) for st in evs for e in st]
+    kern_ms = [e[0].elapsed_time(e[1]) for e in evs]
     if world > 1:
         t = torch.tensor([elapsed], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -242,19 +282,29 @@ def main():
     value = points / elapsed
 
     # sanity: a few points against the oracle (checker only)
-    checked = _spot_check(kc, progs, cols, preds, sim_alpha, r0, args.side) if rank == 0 else 0
+    checked = _spot_check(kc, progs, cols, preds[:, :n], sim_alpha, r0, args.side) if rank == 0 else 0
+
+    # the same step as six kcg_eval_predict launches (one per variant, the
+    # bindings re-read six times): context for the one-pass kernel
+    six = _timed(torch, lambda: [kc.api.check(kc.api.lib().kcg_eval_predict(
+        p.handle, _colarr(p, cols), n, alpha_arr, preds[v].data_ptr(), None, None, None, 0, stream.cuda_stream))
+        for v, p in enumerate(progs)], reps=3, warm=1)
+    step()
+    torch.cuda.synchronize()
 
     hbm, peak_kind = peaks()
+    V = len(VARIANTS)
     traffic = None
     try:  # ncu dram__bytes_read.sum + dram__bytes_write.sum per launch (profiles/)
-        traffic = json.loads((ROOT / "profiles" / "r01_traffic.json").read_text())["traffic_bytes_per_launch"]
-        traffic *= n / 167284151  # the capture is of the full-size launch
+        tr = json.loads((ROOT / "profiles" / "r02_traffic.json").read_text())
+        traffic = tr["traffic_bytes_per_launch"] * n / tr["sizes_per_launch"]
     except Exception:
         pass
     avg_launch = statistics.mean(kern_ms) / 1e3
-    bytes_per_launch = 32.0 * n  # 8*P + 8 with P = 3
+    bytes_per_size = 8 * 3 + 8 * V  # 8 P in (P = 3), 8 V out
+    bytes_per_launch = float(bytes_per_size) * n
     achieved = bytes_per_launch / avg_launch / 1e9
-    mix = _same_mix_stream(torch, dev, n, stream)
+    mix = kc.measure_stream(3, V, 1 << 27) / 1e9
     pipes = _pipe_peaks(kc)
 
     line = {
@@ -263,32 +313,42 @@ def main():
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int64", "data": "synthetic",
         "config": {"workload": "config4 materialised evaluate+predict: 6 matmul variants x "
-                               f"{total} sizes (n,m,l)=336*(u,v,w), u,v,w<= {args.side}",
-                   "points_per_step": total * len(VARIANTS), "bytes_per_point": 32,
+                               f"{total} sizes (n,m,l)=336*(u,v,w), u,v,w<= {args.side}, one multi-program "
+                               "launch per step",
+                   "points_per_step": total * V, "bytes_per_size": bytes_per_size,
+                   "bytes_per_point": bytes_per_size / V,
                    "l2": "inputs 4.0 GB + outputs 8.0 GB per step exceed the 126 MB L2 (no flush)",
                    "parallelism": f"dp{world} (contiguous size shards)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "peak_kind": peak_kind,
-                     "peak_note": "MEASURED_PEAKS hbm_gbs is a copy (50% writes); this kernel's traffic is "
-                                  "75% reads (24 B in, 8 B out per point), which HBM serves faster",
-                     "same_mix_stream_gbs": mix,
-                     "frac_of_same_mix": achieved / mix,
-                     "same_mix_note": "torch.addcmul over three f64 columns of the same length into a fourth "
-                                      "(24 B in, 8 B out per element: this kernel's traffic mix), CUDA events",
-                     "traffic_source": "profiles/r01_launches_eval.csv (ncu, per launch)",
-                     "kernel": "kcg_eval_<variant> (NVRTC sm_100a)",
-                     "algorithmic_bytes_per_launch": bytes_per_launch,
-                     "avg_launch_ms": avg_launch * 1e3},
-        "instruction_roofline": _instr_roofline(_ncu_lane_instr("r01_eval_tma_ncu_full.txt"),
-                                                avg_launch and n / avg_launch, pipes,
-                                                "profiles/r01_eval_tma_ncu_full.txt (ncu, same kernel)"),
+                     "algorithmic_bytes": "8 P + 8 V per size (P = 3 binding columns read once, V = 6 "
+                                          "predictions written) = 72 B per size, 12 B per (variant, size) point",
+                     "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch * 1e3,
+                     "same_mix_stream_gbs": mix, "frac_of_same_mix": achieved / mix,
+                     "same_mix_note": "kcg_measure_stream(3, 6): a plain kernel reading 3 int64 and writing 6 "
+                                      "fp64 columns (this kernel's 1:2 read:write mix), measured live",
+                     "traffic_source": "profiles/r02_traffic.json (ncu dram bytes of the same launch)",
+                     "kernel": "kcg_multi_v6_tma (NVRTC sm_100a)",
+                     "per_point_8P_plus_8_GBps": 32.0 * n * V / avg_launch / 1e9,
+                     "per_point_note": "SURVEY 8(d)'s per-point figure (8 P + 8 = 32 B per point, bindings "
+                                       "counted once per variant) over the same launch time: what six "
+                                       "per-variant launches would have to stream"},
+        "instruction_roofline": _instr_roofline(_ncu_lane_instr("r02_multi_ncu.txt"),
+                                                avg_launch and n * V / avg_launch, pipes,
+                                                "profiles/r02_multi_ncu.txt (ncu, same kernel)"),
         "pipe_peaks_lane_ops_per_s": pipes,
+        "six_launch_step_ms": six * 1e3,
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "spot_checked_points": checked,
     }
+    if rank == 0 and not args.no_configs:
+        del preds
+        line["configs"] = _configs(kc, torch, dev, args, cols, progs, w)
+    else:
+        del preds
     if not args.no_fit:
-        del preds, cols
+        del cols
         line["fit"] = _sharded_fit(kc, torch, dev, world, rank, args.fit_rows)
     if not args.no_e2e:  # every rank streams its own shard over its own PCIe link
         e2e = _e2e(kc, progs, w, args, torch, dev, world, rank)
@@ -296,13 +356,9 @@ def main():
             line["e2e"] = e2e
     if rank == 0 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        r = cpu_reference(threads, max(threads * 400, 4000))
-        if r:
-            line["cpu_baseline"] = {
-                "value": r["points_per_s"], "unit": "points/s", "cores": threads,
-                "kind": "reference",
-                "sample": f"{r['points'] // 6} sizes x 6 variants, evaluate_properties+predict "
-                          "per point (reference code + shim bigint), std::thread fan-out"}
+        cb = cpu_reference_line(threads)
+        if cb:
+            line["cpu_baseline"] = cb
         if "fit" in line:
             line["fit"]["cpu_reference"] = cpu_reference_fit(200_000, 40)
         line["cpu_optimized"] = cpu_lowered_baseline(kc, progs, sim_alpha, threads, args.side)
@@ -618,8 +674,117 @@ def _fp64_peak(torch, dev):
     return 2 * n ** 3 / sec / 1e12
 
 
+def _configs(kc, torch, dev, args, cols, progs, w):
+    """Configs the default line carries beside the headline:
+    the fused config-4 argmin over the same lattice, config 2 (1e6 points of
+    the four test kernels) and the config-3 Gram (1e8 x 40 fp64 rows)."""
+    out = {}
+    hbm, _ = peaks()
+    stream = torch.cuda.current_stream(dev).cuda_stream
+
+    # ---- config 2: 1e6 points over the 4 test kernels (250k each) ----------
+    U = 250_000
+    u = torch.arange(1, U + 1, dtype=torch.int64, device=dev)
+    specs = [("matmul_skinny_g16x16", {"n": 16 * u, "m": 128 * u, "l": 16 * u}),
+             ("conv_g16x16", {"n": 16 * u}),
+             ("fd_stencil_g16x16", {"n": 16 * u}),
+             ("nbody_g256", {"n": 256 * u})]
+    launches = []
+    for kid, cdict in specs:
+        p = kc.load_program(kid)
+        cdict = {k: v.contiguous() for k, v in cdict.items()}
+        launches.append((p, cdict, _colarr(p, cdict), torch.empty(U, dtype=torch.float64, device=dev)))
+
+    def c2():
+        for p, _, arr, out in launches:
+            kc.api.check(kc.api.lib().kcg_eval_predict(p.handle, arr, U, w.alpha_array(), out.data_ptr(),
+                                                       None, None, None, 0, stream))
+    sec = _timed(torch, c2, reps=20)
+    # the same 4 launches replayed from a CUDA graph (the C ABI launches are
+    # capturable once the kernels are specialised): launch overhead removed
+    g2 = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g2):
+        c2_stream = torch.cuda.current_stream(dev).cuda_stream
+        for p, _, arr, o in launches:
+            kc.api.check(kc.api.lib().kcg_eval_predict(p.handle, arr, U, w.alpha_array(), o.data_ptr(),
+                                                       None, None, None, 0, c2_stream))
+    sec_g = _timed(torch, g2.replay, reps=50)
+    b64, _ = launches[0][0].safe_bounds()
+    out["config2_suite_1e6"] = {
+        "points": 4 * U, "ms": sec * 1e3, "points_per_s": 4 * U / sec, "launches": 4,
+        "graph_ms": sec_g * 1e3, "graph_points_per_s": 4 * U / sec_g,
+        "note": "skinny (16u,128u,16u), conv 16u, fd_stencil 16u, nbody 256u, u=1..250000; skinny counts "
+                f"reach 5.8e20 (int128 path for n > {b64}); fd_stencil / nbody use the derived programs "
+                "(SURVEY 8f row 1); latency-bound (4 launches)"}
+    del launches, u
+
+    # ---- config 4 fused: evaluate + predict + argmin over the 6 variants ---
+    total = cols["n"].numel()
+    best = torch.empty(total, dtype=torch.int32, device=dev)
+    best_t = torch.empty(total, dtype=torch.float64, device=dev)
+    handles = (ctypes.c_void_p * len(progs))(*[p.handle.value for p in progs])
+    carr = _colarr(progs[0], cols)
+
+    def c4():
+        kc.api.check(kc.api.lib().kcg_argmin(handles, len(progs), carr, total, w.alpha_array(),
+                                             best.data_ptr(), best_t.data_ptr(), None, stream))
+    sec = _timed(torch, c4, reps=5)
+    out["config4_argmin_fused"] = {
+        "sizes": total, "points": total * len(progs), "ms": sec * 1e3,
+        "points_per_s": total * len(progs) / sec, "sizes_per_s": total / sec,
+        "bytes_per_size": 36, "hbm_frac": 36 * total / sec / 1e9 / hbm,
+        "best_variant_histogram": torch.bincount(best.to(torch.int64) + 1, minlength=len(progs) + 1).tolist(),
+        "instruction_roofline": _instr_roofline(_ncu_lane_instr("r01_argmin_ncu.txt"), total * len(progs) / sec,
+                                                _pipe_peaks(kc), "profiles/r01_argmin_ncu.txt (ncu, same kernel)"),
+        "note": "one fused launch per step; 24 B bindings in, int32 + fp64 out per size"}
+    # the same launch also writing every variant's prediction (variant-major):
+    # all 1e9 predictions with the bindings read once (24 + 48 B per size
+    # instead of 6 x 32 B for six separate launches)
+    preds_all = torch.empty((len(progs), total), dtype=torch.float64, device=dev)
+
+    def c4p():
+        kc.api.check(kc.api.lib().kcg_argmin(handles, len(progs), carr, total, w.alpha_array(),
+                                             best.data_ptr(), best_t.data_ptr(), preds_all.data_ptr(), stream))
+    sec = _timed(torch, c4p, reps=5)
+    out["config4_fused_all_predictions"] = {
+        "points": total * len(progs), "ms": sec * 1e3, "points_per_s": total * len(progs) / sec,
+        "bytes_per_size": 24 + 12 + 8 * len(progs), "hbm_frac": (36 + 8 * len(progs)) * total / sec / 1e9 / hbm,
+        "note": "kcg_argmin with preds_out: every (variant, size) prediction plus the argmin in one launch"}
+    del preds_all, best, best_t
+
+    # ---- config 3: Gram over 1e8 x 40 fp64 materialised rows ---------------
+    N, F = 100_000_000, 40
+    g = torch.Generator(device=dev).manual_seed(4242)
+    X = torch.rand((N, F), dtype=torch.float64, device=dev, generator=g)
+    X.mul_(9999.0).add_(1.0)
+    st = kc.GramStats.zeros(F, dev)
+
+    def c3():
+        st.G.zero_(); st.xt1.zero_(); st.colmax.zero_()
+        kc.api.check(kc.api.lib().kcg_gram_accumulate(X.data_ptr(), N, F, F, st.G.data_ptr(),
+                                                      st.xt1.data_ptr(), st.colmax.data_ptr(), stream))
+    sec = _timed(torch, c3, reps=5)
+    # parity at full size: Gram vs a float64 torch reference on a 1e6-row slice
+    Xs = X[:1_000_000]
+    st2 = kc.gram_accumulate(Xs)
+    ref = Xs.T @ Xs
+    rel = float(((st2.G - ref).abs().max() / ref.abs().max()).item())
+    fp64 = _fp64_peak(torch, dev)
+    flops = N * F * (F + 1) + 2 * N * F
+    out["config3_gram_1e8x40"] = {
+        "rows": N, "cols": F, "ms": sec * 1e3, "rows_per_s": N / sec,
+        "hbm_achieved_GBps": 8 * F * N / sec / 1e9, "hbm_frac": 8 * F * N / sec / 1e9 / hbm,
+        "fp64_tflops": flops / sec / 1e12, "fp64_peak_tflops_measured_dgemm": fp64,
+        "fp64_frac": flops / sec / 1e12 / fp64, "slice_rel_err_vs_torch": rel,
+        "kernel": "kcg_gram_dmma<5,64,2> (AOT, DMMA m8n8k4 f64, TMA-staged rows)"}
+    del X, Xs, st, st2, ref
+
+    return out
+
+
 def _extras(kc, torch, dev, args):
-    """Configs 2, 3, 5 (single GPU) and the fused config-4 argmin."""
+    """Config 1, config 5 on one GPU, the grid-descriptor path and the GPU
+    enumeration oracle (--extras)."""
     import ctypes
     out = {}
     hbm, _ = peaks()
@@ -665,83 +830,9 @@ def _extras(kc, torch, dev, args):
                 "(wall clock, ~70 launches); CPU: the reference's run_campaign + extract_properties (bound, "
                 "cap 2e7) + fit_weights + predict, 1 thread"}
 
-    # ---- config 2: 1e6 points over the 4 test kernels (250k each) ----------
-    U = 250_000
-    u = torch.arange(1, U + 1, dtype=torch.int64, device=dev)
-    specs = [("matmul_skinny_g16x16", {"n": 16 * u, "m": 128 * u, "l": 16 * u}),
-             ("conv_g16x16", {"n": 16 * u}),
-             ("fd_stencil_g16x16", {"n": 16 * u}),
-             ("nbody_g256", {"n": 256 * u})]
-    launches = []
-    for kid, cdict in specs:
-        p = kc.load_program(kid)
-        cdict = {k: v.contiguous() for k, v in cdict.items()}
-        launches.append((p, cdict, _colarr(p, cdict), torch.empty(U, dtype=torch.float64, device=dev)))
-
-    def c2():
-        for p, _, arr, out in launches:
-            kc.api.check(kc.api.lib().kcg_eval_predict(p.handle, arr, U, w.alpha_array(), out.data_ptr(),
-                                                       None, None, None, 0, stream))
-    sec = _timed(torch, c2, reps=20)
-    # the same 4 launches replayed from a CUDA graph (the C ABI launches are
-    # capturable once the kernels are specialised): launch overhead removed
-    g2 = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g2):
-        c2_stream = torch.cuda.current_stream(dev).cuda_stream
-        for p, _, arr, o in launches:
-            kc.api.check(kc.api.lib().kcg_eval_predict(p.handle, arr, U, w.alpha_array(), o.data_ptr(),
-                                                       None, None, None, 0, c2_stream))
-    sec_g = _timed(torch, g2.replay, reps=50)
-    b64, _ = launches[0][0].safe_bounds()
-    out["config2_suite_1e6"] = {
-        "points": 4 * U, "ms": sec * 1e3, "points_per_s": 4 * U / sec, "launches": 4,
-        "graph_ms": sec_g * 1e3, "graph_points_per_s": 4 * U / sec_g,
-        "note": "skinny (16u,128u,16u), conv 16u, fd_stencil 16u, nbody 256u, u=1..250000; skinny counts "
-                f"reach 5.8e20 (int128 path for n > {b64}); fd_stencil / nbody use the derived programs "
-                "(SURVEY 8f row 1); latency-bound (4 launches)"}
-    del launches, u
-
-    # ---- config 4 fused: evaluate + predict + argmin over the 6 variants ---
     side = args.side
     total = side ** 3
     progs = [kc.load_program(v) for v in VARIANTS]
-    idx = torch.arange(0, total, dtype=torch.int64, device=dev)
-    cols = {"n": ((idx // (side * side) + 1) * UNIT).contiguous(),
-            "m": (((idx // side) % side + 1) * UNIT).contiguous(),
-            "l": ((idx % side + 1) * UNIT).contiguous()}
-    del idx
-    best = torch.empty(total, dtype=torch.int32, device=dev)
-    best_t = torch.empty(total, dtype=torch.float64, device=dev)
-    handles = (ctypes.c_void_p * len(progs))(*[p.handle.value for p in progs])
-    carr = _colarr(progs[0], cols)
-
-    def c4():
-        kc.api.check(kc.api.lib().kcg_argmin(handles, len(progs), carr, total, w.alpha_array(),
-                                             best.data_ptr(), best_t.data_ptr(), None, stream))
-    sec = _timed(torch, c4, reps=5)
-    out["config4_argmin_fused"] = {
-        "sizes": total, "points": total * len(progs), "ms": sec * 1e3,
-        "points_per_s": total * len(progs) / sec, "sizes_per_s": total / sec,
-        "bytes_per_size": 36, "hbm_frac": 36 * total / sec / 1e9 / hbm,
-        "best_variant_histogram": torch.bincount(best.to(torch.int64) + 1, minlength=len(progs) + 1).tolist(),
-        "instruction_roofline": _instr_roofline(_ncu_lane_instr("r01_argmin_ncu.txt"), total * len(progs) / sec,
-                                                _pipe_peaks(kc), "profiles/r01_argmin_ncu.txt (ncu, same kernel)"),
-        "note": "one fused launch per step; 24 B bindings in, int32 + fp64 out per size"}
-    # the same launch also writing every variant's prediction (variant-major):
-    # all 1e9 predictions with the bindings read once (24 + 48 B per size
-    # instead of 6 x 32 B for six separate launches)
-    preds_all = torch.empty((len(progs), total), dtype=torch.float64, device=dev)
-
-    def c4p():
-        kc.api.check(kc.api.lib().kcg_argmin(handles, len(progs), carr, total, w.alpha_array(),
-                                             best.data_ptr(), best_t.data_ptr(), preds_all.data_ptr(), stream))
-    sec = _timed(torch, c4p, reps=5)
-    out["config4_fused_all_predictions"] = {
-        "points": total * len(progs), "ms": sec * 1e3, "points_per_s": total * len(progs) / sec,
-        "bytes_per_size": 24 + 12 + 8 * len(progs), "hbm_frac": (36 + 8 * len(progs)) * total / sec / 1e9 / hbm,
-        "note": "kcg_argmin with preds_out: every (variant, size) prediction plus the argmin in one launch"}
-    del preds_all, cols, best, best_t
-
     # ---- config 4 from a grid descriptor: the same 1e9
     # (variant, size) points, bindings generated in registers -- 8 B/point out
     preds = torch.empty(total, dtype=torch.float64, device=dev)
@@ -760,33 +851,6 @@ def _extras(kc, torch, dev, args):
         "note": "kcg_eval_predict_grid per variant: lattice (n,m,l)=336*(u,v,w) decoded per thread "
                 "(odometer), exact evaluate + predict, fp64 predictions streamed out"}
     del preds
-
-    # ---- config 3: Gram over 1e8 x 40 fp64 materialised rows ---------------
-    N, F = 100_000_000, 40
-    g = torch.Generator(device=dev).manual_seed(4242)
-    X = torch.rand((N, F), dtype=torch.float64, device=dev, generator=g)
-    X.mul_(9999.0).add_(1.0)
-    st = kc.GramStats.zeros(F, dev)
-
-    def c3():
-        st.G.zero_(); st.xt1.zero_(); st.colmax.zero_()
-        kc.api.check(kc.api.lib().kcg_gram_accumulate(X.data_ptr(), N, F, F, st.G.data_ptr(),
-                                                      st.xt1.data_ptr(), st.colmax.data_ptr(), stream))
-    sec = _timed(torch, c3, reps=5)
-    # parity at full size: Gram vs a float64 torch reference on a 1e6-row slice
-    Xs = X[:1_000_000]
-    st2 = kc.gram_accumulate(Xs)
-    ref = Xs.T @ Xs
-    rel = float(((st2.G - ref).abs().max() / ref.abs().max()).item())
-    fp64 = _fp64_peak(torch, dev)
-    flops = N * F * (F + 1) + 2 * N * F
-    out["config3_gram_1e8x40"] = {
-        "rows": N, "cols": F, "ms": sec * 1e3, "rows_per_s": N / sec,
-        "hbm_achieved_GBps": 8 * F * N / sec / 1e9, "hbm_frac": 8 * F * N / sec / 1e9 / hbm,
-        "fp64_tflops": flops / sec / 1e12, "fp64_peak_tflops_measured_dgemm": fp64,
-        "fp64_frac": flops / sec / 1e12 / fp64, "slice_rel_err_vs_torch": rel,
-        "kernel": "kcg_gram_dmma<5,64,2> (AOT, DMMA m8n8k4 f64, TMA-staged rows)"}
-    del X, Xs, st, st2, ref
 
     # ---- config 5 (single GPU): fused evaluate -> row -> Gram, 1e9 rows ----
     tiled = kc.load_program("matmul_tiled_g16x16")

@@ -173,6 +173,30 @@ int kcg_eval_predict_grid(const kcg_program* prog, const kcg_grid* grid, uint64_
                           size_t n, const double* alpha, double* pred_out,
                           uint8_t* status_out, int simulate, void* stream);
 
+/* ---- several programs over one binding stream ---------------------------
+ * Replaces the per-variant loop of `evaluate_properties` + `predict`
+ * (props.hpp:49-50, model.hpp:61) that an autotuning sweep runs over the
+ * same sizes for every kernel variant (bench.cpp:47-56 per variant; the
+ * CLI's predict over variants, kernelcost.cpp:236-400).
+ * One pass: each point's bindings are read once and all n_progs
+ * predictions written. param_cols follow progs[0]'s parameter order (every
+ * program must have the same parameter names). pred_out (DEVICE, nullable):
+ * program v's predictions at pred_out + v * ld_pred (ld_pred >= n_points);
+ * status_out (DEVICE, nullable): kcg_point_status bytes at
+ * status_out + v * ld_status. Bitwise equal to n_progs kcg_eval_predict
+ * calls (NaN where the status is not OK). Non-finite weights or
+ * interpreter-engine programs take one kcg_eval_predict per program.   */
+int kcg_eval_predict_multi(const kcg_program* const* progs, int n_progs,
+                           const int64_t* const* param_cols, size_t n_points,
+                           const double* alpha, double* pred_out, size_t ld_pred,
+                           uint8_t* status_out, size_t ld_status, void* stream);
+
+/* The generated CUDA source of kcg_eval_predict_multi's kernels for these
+ * programs (kernels kcg_multi_v<n_progs> and kcg_multi_v<n_progs>_tma;
+ * diagnostics / compile checks). Owned by the library, valid until the
+ * next call on this thread; NULL on error (see kcg_last_error).          */
+const char* kcg_multi_jit_source(const kcg_program* const* progs, int n_progs);
+
 /* ---- host buffers: the reference's own calling convention ---------------
  * Replaces the reference's per-point host loop `evaluate_properties` +
  * `predict` (props.hpp:49-50, model.hpp:61; the loop of bench.cpp:47-56 and
@@ -366,6 +390,12 @@ uint64_t kcg_launch_count(void);
  * `iters` x 128 steps of 8 chains per thread, full occupancy; synchronous,
  * on the default stream. Its launches are not counted by kcg_launch_count. */
 int kcg_measure_pipe_peak(int kind, uint64_t iters, double* lane_ops_per_s);
+/* measured HBM bandwidth (bytes/s, best of 5) of a stream that reads
+ * n_read int64 columns and writes n_write fp64 columns of n_points each:
+ * the same-mix roofline of a kernel with that traffic (supported mixes:
+ * 3/6, 3/1, 1/6, 1/1, 4/0). Allocates 8 (n_read + n_write) n_points bytes;
+ * synchronous, default stream; not counted by kcg_launch_count.          */
+int kcg_measure_stream(int n_read, int n_write, uint64_t n_points, double* bytes_per_s);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,8 @@ from .api import (  # noqa: F401
     Program,
     argmin,
     predict_host,
+    predict_multi,
+    multi_jit_source,
     evaluate_properties,
     fit_weights,
     geometric_mean_error,
@@ -34,6 +36,7 @@ from .api import (  # noqa: F401
     gram_fused,
     launch_count,
     measure_pipe_peak,
+    measure_stream,
     load_program,
     noiseless_time,
     predict,

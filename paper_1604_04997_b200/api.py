@@ -305,6 +305,40 @@ def argmin(progs: Sequence[Program], w: ModelWeights, bindings, return_preds: bo
     return (best, best_t, preds) if return_preds else (best, best_t)
 
 
+def predict_multi(progs: Sequence[Program], w: ModelWeights, bindings, status: bool = False, out=None,
+                  stream=None):
+    """``predict`` of every program over one set of device bindings in one
+    pass (kcg_eval_predict_multi): each size's bindings are read once.
+    bindings follow progs[0]'s parameters; returns a [len(progs), n] float64
+    CUDA tensor (and the [len(progs), n] uint8 status). `out` may be a
+    preallocated [len(progs), >= n] float64 CUDA tensor with unit column
+    stride (its row stride is the leading dimension)."""
+    torch = _torch()
+    progs = list(progs)
+    arr, n, cols = _columns(progs[0], bindings)
+    dev = cols[0].device if cols else torch.device("cuda")
+    V = len(progs)
+    pred = out if out is not None else torch.empty((V, n), dtype=torch.float64, device=dev)
+    if (pred.dim() != 2 or pred.shape[0] != V or pred.shape[1] < n or pred.dtype != torch.float64
+            or not pred.is_cuda or (pred.stride(1) != 1 and n > 1)):
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "out must be a [n_progs, >= n] float64 CUDA tensor")
+    st = torch.empty((V, n), dtype=torch.uint8, device=dev) if status else None
+    handles = (ctypes.c_void_p * V)(*[p.handle.value for p in progs])
+    check(lib().kcg_eval_predict_multi(handles, V, arr, n, w.alpha_array(), pred.data_ptr(), max(pred.stride(0), n),
+                                       _ptr(st), n, _stream(stream)))
+    return (pred, st) if status else pred
+
+
+def multi_jit_source(progs: Sequence[Program]) -> str:
+    """Generated CUDA of the one-pass multi-program kernels (diagnostics)."""
+    progs = list(progs)
+    handles = (ctypes.c_void_p * len(progs))(*[p.handle.value for p in progs])
+    src = lib().kcg_multi_jit_source(handles, len(progs))
+    if src is None:
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, lib().kcg_last_error().decode())
+    return src.decode()
+
+
 def predict_host(progs: Sequence[Program], w: ModelWeights, bindings, status: bool = False,
                  out=None, pinned: Optional[bool] = None):
     """The reference's calling convention: HOST bindings in, HOST
@@ -479,6 +513,14 @@ def launch_count() -> int:
 
 
 PIPE_KINDS = {"imad": 0, "lop3": 1, "dfma": 2, "issue": 3}
+
+
+def measure_stream(n_read: int, n_write: int, n_points: int = 1 << 27) -> float:
+    """HBM bytes/s of a stream reading n_read int64 and writing n_write fp64
+    columns (kcg_measure_stream): the same-mix bandwidth roofline."""
+    out = ctypes.c_double()
+    check(lib().kcg_measure_stream(n_read, n_write, n_points, ctypes.byref(out)))
+    return out.value
 
 
 def measure_pipe_peak(kind: str, iters: int = 4096) -> float:

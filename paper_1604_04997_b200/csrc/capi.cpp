@@ -89,6 +89,29 @@ void require_device() {
 }
 
 // byte-exact image of the generated `struct KcgArgs` (natural C alignment)
+// progs[v]'s parameter j lives in launch column pmaps[v][j] (progs[0]'s
+// declaration order); every program must have the same parameter names
+void variant_maps(const kcg_program* const* progs, int V, std::vector<const kcg::Lowered*>& lows,
+                  std::vector<std::vector<int>>& pmaps) {
+  const kcg_program* p0 = progs[0];
+  if (!p0) throw KcgError(KCG_E_INVALID_ARGUMENT, "null program");
+  const int np = p0->low.n_params;
+  for (int v = 0; v < V; ++v) {
+    const kcg_program* p = progs[v];
+    if (!p || p->low.n_params != np)
+      throw KcgError(KCG_E_INVALID_ARGUMENT, "the programs must share the parameter set");
+    std::vector<int> map(np);
+    for (int j = 0; j < np; ++j) {
+      auto it = std::find(p0->param_names.begin(), p0->param_names.end(), p->param_names[j]);
+      if (it == p0->param_names.end())
+        throw KcgError(KCG_E_INVALID_ARGUMENT, "the programs must share the parameter set");
+      map[j] = static_cast<int>(it - p0->param_names.begin());
+    }
+    lows.push_back(&p->low);
+    pmaps.push_back(map);
+  }
+}
+
 struct ArgBuf {
   std::vector<unsigned char> b;
   template <class T>
@@ -471,6 +494,102 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
   });
 }
 
+const char* kcg_multi_jit_source(const kcg_program* const* progs, int V) {
+  static thread_local std::string src;
+  if (!progs || V < 1) return nullptr;
+  try {
+    std::vector<const kcg::Lowered*> lows;
+    std::vector<std::vector<int>> pmaps;
+    variant_maps(progs, V, lows, pmaps);
+    src = kcg::codegen(lows, pmaps, progs[0]->low.n_params, kcg::JitKind::multi, "kcg_multi_v" + std::to_string(V));
+  } catch (const KcgError& e) {
+    fail(e.code, e.what());
+    return nullptr;
+  }
+  return src.c_str();
+}
+
+int kcg_eval_predict_multi(const kcg_program* const* progs, int V, const int64_t* const* param_cols, size_t n,
+                           const double* alpha, double* pred_out, size_t ld_pred, uint8_t* status_out,
+                           size_t ld_status, void* stream) {
+  if (!progs || V < 1 || !alpha || (!pred_out && !status_out))
+    return fail(KCG_E_INVALID_ARGUMENT, "bad multi eval arguments");
+  if ((pred_out && ld_pred < n) || (status_out && ld_status < n))
+    return fail(KCG_E_INVALID_ARGUMENT, "output leading dimension below n_points");
+  return guarded([&] {
+    require_device();
+    std::vector<const kcg::Lowered*> lows;
+    std::vector<std::vector<int>> pmaps;
+    variant_maps(progs, V, lows, pmaps);
+    const int np = progs[0]->low.n_params;
+    if (np > 0 && !param_cols) throw KcgError(KCG_E_INVALID_ARGUMENT, "null param_cols");
+    if (n == 0) return KCG_OK;
+    // non-finite weights (skip rules matter) or the interpreter engine: one
+    // kcg_eval_predict per program (same results, V binding reads)
+    bool finite = true, jit = true;
+    std::vector<std::vector<double>> als(V), alfs(V);
+    for (int v = 0; v < V; ++v) {
+      als[v].assign(std::max<size_t>(1, progs[v]->low.keys.size()), 0.0);
+      compact_alpha(progs[v], alpha, als[v].data());
+      bool fin = true;
+      alfs[v] = folded_alpha(progs[v], als[v], &fin);
+      finite = finite && fin;
+      jit = jit && progs[v]->engine == KCG_ENGINE_JIT;
+    }
+    // shared products (multi_plan): alpha (x) constant count; alpha * 2^k
+    const kcg::MultiPlan plan = kcg::multi_plan(lows, pmaps, np);
+    std::vector<double> shk, shw;
+    for (const auto& [schema, c] : plan.kprods) shk.push_back(alpha[schema] * static_cast<double>(static_cast<int64_t>(c)));
+    for (const auto& [schema, c, m] : plan.wprods) {
+      shw.push_back(alpha[schema] * static_cast<double>(c));
+      finite = finite && std::isfinite(shw.back());
+    }
+    if (!finite || !jit || !pred_out || std::getenv("KCG_NO_MULTI")) {
+      for (int v = 0; v < V; ++v) {
+        std::vector<const int64_t*> cols(std::max(np, 1), nullptr);
+        for (int j = 0; j < progs[v]->low.n_params; ++j) cols[j] = param_cols[pmaps[v][j]];
+        const int rc = kcg_eval_predict(progs[v], cols.data(), n, alpha, pred_out ? pred_out + v * ld_pred : nullptr,
+                                        status_out ? status_out + v * ld_status : nullptr, nullptr, nullptr, 0, stream);
+        if (rc != KCG_OK) throw KcgError(rc, g_last_error);
+      }
+      return KCG_OK;
+    }
+    const std::string name = "kcg_multi_v" + std::to_string(V);
+    const std::string src = kcg::codegen(lows, pmaps, np, kcg::JitKind::multi, name);
+    bool vec = true;
+    for (int j = 0; j < np; ++j) vec = vec && reinterpret_cast<uintptr_t>(param_cols[j]) % 16 == 0;
+    static const bool no_tma = std::getenv("KCG_NO_TMA") != nullptr;
+    const size_t tiles = n / static_cast<size_t>(kcg::multi_tile());
+    const bool tma = vec && !no_tma && np > 0 && tiles >= static_cast<size_t>(kcg::num_sms());
+    void* k = kcg::jit_kernel(src, name + (tma ? "_tma" : "") + (status_out ? "_st" : ""));
+    ArgBuf ab;
+    for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
+    ab.push<void*>(pred_out);
+    ab.push<void*>(status_out);
+    ab.push<int64_t>(static_cast<int64_t>(n));
+    ab.push<int64_t>(static_cast<int64_t>(ld_pred));
+    ab.push<int64_t>(static_cast<int64_t>(ld_status));
+    for (int v = 0; v < V; ++v)
+      for (double x : als[v]) ab.push<double>(x);
+    for (int v = 0; v < V; ++v)
+      for (double x : alfs[v]) ab.push<double>(x);
+    for (double x : shk) ab.push<double>(x);
+    if (shk.empty()) ab.push<double>(0.0);
+    for (double x : shw) ab.push<double>(x);
+    if (shw.empty()) ab.push<double>(0.0);
+    ab.finish();
+    if (tma) {
+      const unsigned grid = static_cast<unsigned>(
+          std::min<size_t>(tiles, static_cast<size_t>(kcg::num_sms()) * kcg::multi_ctas_per_sm()));
+      kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid, 256, stream, kcg::multi_smem_bytes(np));
+    } else {
+      kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid_for(n), 256, stream);
+    }
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
 int kcg_argmin(const kcg_program* const* progs, int V, const int64_t* const* param_cols,
                size_t n, const double* alpha, int32_t* best_idx, double* best_t,
                double* preds_out, void* stream) {
@@ -754,6 +873,8 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
     cuda_check(cudaDeviceGetAttribute(&max_pitch, cudaDevAttrMaxPitch, cur_dev), "cudaDeviceGetAttribute");
     const long long pitch_cap = env_ll("KCG_HOST_MAX_PITCH", max_pitch, 8, max_pitch);
     const bool copy2d = env_ll("KCG_HOST_2D", 1, 0, 1) == 1 && n * 8 <= static_cast<unsigned long long>(pitch_cap);
+    // several programs: one kcg_eval_predict_multi per chunk (KCG_HOST_ONEPASS=0: one launch per program)
+    const bool onepass = V > 1 && pred_out && env_ll("KCG_HOST_ONEPASS", 1, 0, 1) == 1;
     // slot layout: np binding columns, V prediction columns, V status columns
     const size_t in_b = static_cast<size_t>(std::max(np, 1)) * chunk * 8;
     const size_t pred_b = pred_out ? static_cast<size_t>(V) * chunk * 8 : 0;
@@ -795,13 +916,23 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
           const void* src = pinned ? static_cast<const void*>(host_cols[j] + c0) : h + j * chunk * 8;
           cuda_check(cudaMemcpyAsync(d + j * chunk * 8, src, m * 8, cudaMemcpyHostToDevice, st), "cudaMemcpyAsync H2D");
         }
-        for (int v = 0; v < V; ++v) {
+        if (onepass) {  // every program in one launch: the chunk's bindings read once
           std::vector<const int64_t*> cols(std::max(np, 1), nullptr);
-          for (int j = 0; j < np; ++j) cols[j] = reinterpret_cast<const int64_t*>(d + maps[v][j] * chunk * 8);
+          for (int j = 0; j < np; ++j) cols[j] = reinterpret_cast<const int64_t*>(d + j * chunk * 8);
+          const int rc = kcg_eval_predict_multi(
+              progs, V, cols.data(), m, alpha, pred_out ? reinterpret_cast<double*>(d + in_b) : nullptr, chunk,
+              status_out ? reinterpret_cast<uint8_t*>(d + in_b + pred_b) : nullptr, chunk, st);
+          if (rc != KCG_OK) throw KcgError(rc, g_last_error);
+        }
+        for (int v = 0; v < V; ++v) {
           double* dp = pred_out ? reinterpret_cast<double*>(d + in_b + v * chunk * 8) : nullptr;
           uint8_t* ds = status_out ? reinterpret_cast<uint8_t*>(d + in_b + pred_b + v * chunk) : nullptr;
-          const int rc = kcg_eval_predict(progs[v], cols.data(), m, alpha, dp, ds, nullptr, nullptr, 0, st);
-          if (rc != KCG_OK) throw KcgError(rc, g_last_error);
+          if (!onepass) {
+            std::vector<const int64_t*> cols(std::max(np, 1), nullptr);
+            for (int j = 0; j < np; ++j) cols[j] = reinterpret_cast<const int64_t*>(d + maps[v][j] * chunk * 8);
+            const int rc = kcg_eval_predict(progs[v], cols.data(), m, alpha, dp, ds, nullptr, nullptr, 0, st);
+            if (rc != KCG_OK) throw KcgError(rc, g_last_error);
+          }
           if (pred_out && !(pinned && copy2d))
             cuda_check(cudaMemcpyAsync(pinned ? static_cast<void*>(pred_out + v * n + c0) : h + in_b + v * chunk * 8, dp,
                                        m * 8, cudaMemcpyDeviceToHost, st),
@@ -824,7 +955,8 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
       for (int b = 0; b < S; ++b) cudaStreamSynchronize(hp.streams[b]);
       throw;
     }
-    g_host_last_path = (pinned ? KCG_HOST_PINNED : 0u) | (pinned && copy2d && pred_out ? KCG_HOST_PATH_2D : 0u);
+    g_host_last_path = (pinned ? KCG_HOST_PINNED : 0u) | (pinned && copy2d && pred_out ? KCG_HOST_PATH_2D : 0u) |
+                       (onepass ? KCG_HOST_PATH_ONEPASS : 0u);
     return KCG_OK;
   });
 }
@@ -1243,6 +1375,20 @@ int kcg_measure_pipe_peak(int kind, uint64_t iters, double* lane_ops_per_s) {
   return guarded([&] {
     require_device();
     *lane_ops_per_s = kcg::measure_pipe_peak(kind, iters);
+    return KCG_OK;
+  });
+}
+
+int kcg_measure_stream(int n_read, int n_write, uint64_t n_points, double* bytes_per_s) {
+  if (n_read < 0 || n_write < 0 || n_points < 2 || !bytes_per_s)
+    return fail(KCG_E_INVALID_ARGUMENT, "bad stream arguments");
+  return guarded([&] {
+    require_device();
+    try {
+      *bytes_per_s = kcg::measure_stream(n_read, n_write, n_points);
+    } catch (const std::runtime_error& e) {
+      throw KcgError(KCG_E_UNSUPPORTED, e.what());
+    }
     return KCG_OK;
   });
 }

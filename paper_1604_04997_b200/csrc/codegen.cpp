@@ -914,6 +914,317 @@ size_t tma_smem_bytes(int n_cols) {
   return static_cast<size_t>(tma_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * tma_tile() * 8;
 }
 
+// ---------------------------------------------------------------------------
+// One-pass multi-program evaluate + predict (kcg_eval_predict_multi).
+//
+// The autotuning sweep evaluates V variants over the same sizes. One
+// program per launch re-reads every size's bindings V times (config 4: 24 B
+// x 6 per size, 2.65x the unique bytes). This kernel streams each size's
+// bindings once through the TMA ring and writes all V predictions (and
+// status bytes): HBM traffic per size is 8 P + 8 V (+ V) bytes.
+//   * fast path: one range check against the smallest int64-safe bound of
+//     all variants, then each variant's branch-free kcg_fastp_<v> + its
+//     folded-weight inner product, straight-line; quotients and monomials
+//     that several variants share are CSE'd by the compiler;
+//   * anything else (negative / beyond an int64 bound / int128 counts):
+//     kcg_mslow, out of line, which reloads the size's bindings from the
+//     columns and writes every variant's outputs itself (no parameter values
+//     or local addresses cross the call, see kcg_point_slow);
+//   * weights: one flat table of compact weights per variant in the
+//     argument struct (constant bank): as given (wide path), folded (fast).
+// measured on the config-4 lattice (profiles/gpu_r02_multi*.sh): one CTA
+// per SM with a 72 KB ring (3 stages) 2.40-2.50 ms; 2 CTAs x 96 KB 2.74,
+// 3 CTAs x 64 KB 2.57-2.83, 1 CTA x 192 KB 2.89; loading the thread's
+// whole share of a stage up front (KCG_MULTI_PREFETCH=1) 2.60
+int multi_ctas() { return env_int("KCG_MULTI_CTAS", 1, 1, 4); }
+int multi_ring_kb() { return env_int("KCG_MULTI_RING_KB", 72, 16, 200); }
+int multi_tile() { return 256 * env_int("KCG_MULTI_TILE_Q", 4, 1, 8); }
+int multi_ctas_per_sm() { return multi_ctas(); }
+bool multi_share() { return env_int("KCG_MULTI_SHARE", 1, 0, 1) == 1; }
+bool multi_prefetch() { return env_int("KCG_MULTI_PREFETCH", 0, 0, 1) == 1; }
+int multi_stages(int n_cols) {
+  const int per = (n_cols > 0 ? n_cols : 1) * multi_tile() * 8;
+  const int s = (multi_ring_kb() * 1024) / per;
+  return s < 2 ? 2 : (s > 8 ? 8 : s);
+}
+size_t multi_smem_bytes(int n_cols) {
+  return static_cast<size_t>(multi_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * multi_tile() * 8;
+}
+
+// Which products the one-pass kernel forms once per point and shares:
+//   * form-1 keys (constant count C): alpha_key (x) RN(C) is a constant of
+//     the launch, computed on the host (shk[]): the kernel only adds it;
+//   * form-2 keys (count = 2^k * a parameter monomial): RN(count) =
+//     2^k * RN(mono) and alpha (x) RN(count) = (alpha * 2^k) (x) RN(mono)
+//     (alpha * 2^k is exact when finite), so every program whose key has
+//     the same (schema key, 2^k, monomial) uses one product sh[t] =
+//     shw[t] (x) RN(mono), the monomial an exact u64 product of the
+//     parameters (valid on the fast path: every parameter <= min_v b64_v,
+//     and bmin^deg < 2^64 is checked here).
+// Both are bitwise what the per-program kernel adds for that key.
+MultiPlan multi_plan(const std::vector<const Lowered*>& progs, const std::vector<std::vector<int>>& pmaps,
+                     int n_cols) {
+  MultiPlan P;
+  const int V = static_cast<int>(progs.size());
+  P.bmin = INT64_MAX;
+  P.all_small = true;
+  for (int v = 0; v < V; ++v) {
+    P.bmin = std::min<int64_t>(P.bmin, progs[v]->b64);
+    P.all_small = P.all_small && progs[v]->b64 >= 0 && progs[v]->b64 <= kU32;
+  }
+  P.use.resize(V);
+  const long double two62 = std::ldexp(1.0L, 62), two64 = std::ldexp(1.0L, 64);
+  for (int v = 0; v < V; ++v) {
+    const Lowered& L = *progs[v];
+    P.use[v].assign(L.keys.size(), {0, -1});
+    if (!multi_share()) continue;
+    for (size_t k = 0; k < L.keys.size(); ++k) {
+      const LKey& key = L.keys[k];
+      if (key.form == 1 && static_cast<long double>(key.coef < 0 ? -key.coef : key.coef) < two62) {
+        int t = -1;
+        for (size_t i = 0; i < P.kprods.size(); ++i)
+          if (P.kprods[i].first == key.schema && P.kprods[i].second == key.coef) t = static_cast<int>(i);
+        if (t < 0) {
+          t = static_cast<int>(P.kprods.size());
+          P.kprods.push_back({key.schema, key.coef});
+        }
+        P.use[v][k] = {1, t};
+      } else if (key.form == 2 && P.bmin >= 0 && n_cols > 0 &&
+                 static_cast<long double>(key.coef) < std::ldexp(1.0L, 1000)) {
+        std::vector<int> ex(n_cols, 0);
+        int deg = 0;
+        for (int j = 0; j < L.n_params; ++j) {
+          ex[pmaps[v][j]] += key.pexp[j];
+          deg += key.pexp[j];
+        }
+        if (std::pow(static_cast<long double>(std::max<int64_t>(P.bmin, 1)), deg) >= two64) continue;
+        int m = -1;
+        for (size_t i = 0; i < P.monos.size(); ++i)
+          if (P.monos[i] == ex) m = static_cast<int>(i);
+        if (m < 0) {
+          m = static_cast<int>(P.monos.size());
+          P.monos.push_back(ex);
+        }
+        int t = -1;
+        for (size_t i = 0; i < P.wprods.size(); ++i)
+          if (std::get<0>(P.wprods[i]) == key.schema && std::get<1>(P.wprods[i]) == key.coef &&
+              std::get<2>(P.wprods[i]) == m)
+            t = static_cast<int>(i);
+        if (t < 0) {
+          t = static_cast<int>(P.wprods.size());
+          P.wprods.emplace_back(key.schema, key.coef, m);
+        }
+        P.use[v][k] = {2, t};
+      }
+    }
+  }
+  return P;
+}
+
+void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs,
+                const std::vector<std::vector<int>>& pmaps, int n_cols, const std::string& name) {
+  const int V = static_cast<int>(progs.size());
+  const int NP = n_cols > 0 ? n_cols : 1;
+  const MultiPlan P = multi_plan(progs, pmaps, n_cols);
+  std::vector<int> off(V);
+  int tot = 0;
+  for (int v = 0; v < V; ++v) {
+    off[v] = tot;
+    tot += std::max<int>(1, static_cast<int>(progs[v]->keys.size()));
+  }
+  const int NK = std::max<int>(1, static_cast<int>(P.kprods.size()));
+  const int NW = std::max<int>(1, static_cast<int>(P.wprods.size()));
+  os << "struct KcgMArgs { const kcg_i64* p[" << NP << "]; double* pred; unsigned char* status; kcg_i64 n; "
+        "kcg_i64 ldp; kcg_i64 lds; double al[" << tot << "]; double alf[" << tot << "]; double shk[" << NK
+     << "]; double shw[" << NW << "]; };\n";
+  // combined fast-path range: every parameter in [0, min_v b64_v]
+  os << "__device__ __forceinline__ bool kcg_mfast(const kcg_i64* p) {\n";
+  if (P.bmin < 0 || n_cols == 0) {
+    os << "  return " << (P.bmin >= 0 ? "true" : "false") << ";\n}\n";
+  } else if (P.all_small) {
+    os << "  return ((";
+    for (int j = 0; j < n_cols; ++j) os << (j ? " | " : "") << "p[" << j << "]";
+    os << ") >> 32) == 0";
+    for (int j = 0; j < n_cols; ++j) os << " && (unsigned)p[" << j << "] <= " << P.bmin << "u";
+    os << ";\n}\n";
+  } else {
+    os << "  return ";
+    for (int j = 0; j < n_cols; ++j)
+      os << (j ? " && " : "") << "p[" << j << "] >= 0 && p[" << j << "] <= " << P.bmin << "ll";
+    os << ";\n}\n";
+  }
+  // variant v on the fast path: SH = 1 uses the shared products sh[] (only
+  // valid when kcg_mfast holds), SH = 0 the program's own products
+  for (int v = 0; v < V; ++v) {
+    const Lowered& L = *progs[v];
+    const int F = static_cast<int>(L.keys.size());
+    os << "template <int SH>\n__device__ __forceinline__ int kcg_mfastv_" << v
+       << "(const kcg_i64* p, const KcgMArgs& a, const double* sh, double& out) {\n";
+    emit_gather(os, "q", "p", L, pmaps[v], "  ");
+    os << "  double c[" << std::max(F, 1) << "];\n  const int st = kcg_fastp_" << v << "(q, c);\n  double s = 0.0;\n";
+    for (int j = 0; j < F; ++j) {
+      const auto [form, t] = P.use[v][j];
+      const std::string own = "__dmul_rn(a.alf[" + std::to_string(off[v] + j) + "], c[" + std::to_string(j) + "])";
+      if (form == 1)
+        os << "  s = __dadd_rn(s, a.shk[" << t << "]);\n";
+      else if (form == 2)
+        os << "  s = __dadd_rn(s, SH ? sh[" << t << "] : " << own << ");\n";
+      else
+        os << "  s = __dadd_rn(s, " << own << ");\n";
+    }
+    // one opaque select (a plain ?: is pushed into every admissibility
+    // check as a pair of FSELs on the result: 18 per variant)
+    os << "  asm(\"{ .reg .pred p; setp.eq.s32 p, %1, 0; selp.f64 %0, %2, 0d7FF8000000000000, p; }\"\n"
+          "      : \"=d\"(out) : \"r\"(st), \"d\"(s));\n  return st;\n}\n";
+  }
+  // out-of-line: every variant of size i, any parameter range
+  os << "__device__ __noinline__ void kcg_mslow(const KcgMArgs& a, kcg_i64 i) {\n  kcg_i64 p[" << NP << "];\n";
+  for (int j = 0; j < n_cols; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
+  for (int v = 0; v < V; ++v) {
+    const Lowered& L = *progs[v];
+    const int F = static_cast<int>(L.keys.size());
+    os << "  {\n    double s = kcg_nan();\n    int st;\n    const int cls = kcg_class_" << v << "(p);\n";
+    emit_gather(os, "q", "p", L, pmaps[v], "    ");
+    os << "    if (cls == 1) {\n      st = kcg_mfastv_" << v << "<0>(p, a, nullptr, s);\n    } else if (cls == 2) {\n"
+       << "      kcg_i128 c[" << std::max(F, 1) << "];\n      st = kcg_wide_" << v << "(q, c);\n"
+       << "      if (st == KCG_PT_OK) {\n        double t = 0.0;\n";
+    for (int j = 0; j < F; ++j) os << "        t = kcg_accum(t, a.al[" << off[v] + j << "], c[" << j << "], 0);\n";
+    os << "        s = t;\n      }\n    } else if (cls == 0) {\n      st = KCG_PT_ASSUMPTION_VIOLATED;\n"
+          "    } else {\n      st = KCG_PT_OVERFLOW;\n";
+    if (L.admit && L.admit->b128 >= 0) {
+      // beyond the count bound: admissibility still decides first (props.cpp:263-266)
+      os << "      if (";
+      for (int j = 0; j < L.n_params; ++j) os << (j ? " && " : "") << "q[" << j << "] <= " << L.admit->b128 << "ll";
+      if (L.n_params == 0) os << "true";
+      os << ") {\n        kcg_i128 none[1];\n        const int a0 = kcg_admit_" << v
+         << "(q, none);\n        if (a0 != KCG_PT_OK) st = a0;\n      }\n";
+    }
+    os << "    }\n    a.pred[(kcg_i64)" << v << " * a.ldp + i] = (st == KCG_PT_OK) ? s : kcg_nan();\n"
+       << "    if (a.status) a.status[(kcg_i64)" << v << " * a.lds + i] = (unsigned char)st;\n  }\n";
+  }
+  os << "}\n";
+  // one size from registers: shared products, then every variant -- one
+  // basic block (no per-variant branches), so the V independent
+  // accumulation chains interleave
+  os << "template <int ST>\n__device__ __forceinline__ void kcg_msize(const kcg_i64* p, const KcgMArgs& a, kcg_i64 i) {\n"
+        "  if (!kcg_mfast(p)) { kcg_mslow(a, i); return; }\n";
+  for (size_t m = 0; m < P.monos.size(); ++m) {
+    os << "  const double dm" << m << " = __ull2double_rn(";
+    bool first = true;
+    for (int j = 0; j < n_cols; ++j)
+      for (int e = 0; e < P.monos[m][j]; ++e) {
+        os << (first ? "" : " * ") << "(kcg_u64)p[" << j << "]";
+        first = false;
+      }
+    if (first) os << "1ull";
+    os << ");\n";
+  }
+  os << "  double sh[" << NW << "];\n";
+  for (size_t t = 0; t < P.wprods.size(); ++t)
+    os << "  sh[" << t << "] = __dmul_rn(a.shw[" << t << "], dm" << std::get<2>(P.wprods[t]) << ");\n";
+  for (int v = 0; v < V; ++v) os << "  double s" << v << ";\n  const int st" << v << " = kcg_mfastv_" << v << "<1>(p, a, sh, s" << v << ");\n";
+  for (int v = 0; v < V; ++v) os << "  __stcs(a.pred + (kcg_i64)" << v << " * a.ldp + i, s" << v << ");\n";
+  os << "  if (ST) {\n";
+  for (int v = 0; v < V; ++v) os << "    a.status[(kcg_i64)" << v << " * a.lds + i] = (unsigned char)st" << v << ";\n";
+  os << "  }\n}\n";
+  for (int stv = 0; stv < 2; ++stv) {
+    const std::string sfx = stv ? "_st" : "";
+    // plain grid-stride kernel (unaligned columns, small n)
+    os << "extern \"C\" __global__ void __launch_bounds__(256) " << name << sfx << "(const __grid_constant__ KcgMArgs a) {\n"
+          "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (kcg_i64)gridDim.x * blockDim.x) {\n"
+          "    kcg_i64 p[" << NP << "];\n";
+    for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = __ldcs(a.p[" << j << "] + i);\n";
+    os << "    kcg_msize<" << stv << ">(p, a, i);\n  }\n}\n";
+    // TMA ring kernel (persistent): one elected thread streams TP-point
+    // tiles of every column into the ring; each warp releases a stage when
+    // done and the last one refills it (as kcg_eval_<k>_tma)
+    const int S = multi_stages(n_cols);
+    os << "extern \"C\" __global__ void __launch_bounds__(256, " << multi_ctas() << ") " << name << "_tma" << sfx
+       << "(const __grid_constant__ KcgMArgs a) {\n"
+          "  constexpr int TP = " << multi_tile() << ", S = " << S << ", NP = " << NP << ";\n"
+          "  extern __shared__ __align__(128) unsigned char kcg_smem[];\n"
+          "  kcg_i64* buf = reinterpret_cast<kcg_i64*>(kcg_smem);\n"
+          "  __shared__ __align__(8) unsigned long long full[S];\n"
+          "  __shared__ unsigned reads[S];\n"
+          "  if (threadIdx.x < S) reads[threadIdx.x] = 0;\n"
+          "  const kcg_i64 ntiles = a.n / TP;\n"
+          "  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);\n"
+          "  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);\n"
+          "  if (threadIdx.x == 0) {\n"
+          "    for (int s = 0; s < S; ++s)\n"
+          "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(fb + 8 * s));\n"
+          "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+          "  }\n"
+          "  __syncthreads();\n"
+          "  auto issue = [&](int s, kcg_i64 tile) {\n"
+          "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+          "    asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(fb + 8 * s), \"r\"(NP * TP * 8) : \"memory\");\n"
+          "    for (int j = 0; j < NP; ++j)\n"
+          "      asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\"\n"
+          "                   :: \"r\"(bb + (unsigned)((s * NP + j) * TP * 8)), \"l\"(a.p[j] + tile * TP), \"r\"(TP * 8), \"r\"(fb + 8 * s) : \"memory\");\n"
+          "  };\n"
+          "  if (threadIdx.x == 0)\n"
+          "    for (int s = 0; s < S; ++s) {\n"
+          "      const kcg_i64 t = blockIdx.x + (kcg_i64)s * gridDim.x;\n"
+          "      if (t < ntiles) issue(s, t);\n"
+          "    }\n"
+          "  for (kcg_i64 k = 0;; ++k) {\n"
+          "    const kcg_i64 tile = blockIdx.x + k * gridDim.x;\n"
+          "    if (tile >= ntiles) break;\n"
+          "    const int s = (int)(k % S);\n"
+          "    const unsigned parity = (unsigned)((k / S) & 1);\n"
+          "    {\n"
+          "      unsigned done = 0;\n"
+          "      while (!done)\n"
+          "        asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\"\n"
+          "                     : \"=r\"(done) : \"r\"(fb + 8 * s), \"r\"(parity) : \"memory\");\n"
+          "    }\n"
+          "    const kcg_i64 rb = tile * TP;\n";
+    // the warp is done with stage s: the last warp to arrive refills it
+    const char* release =
+        "    __syncwarp();\n"
+        "    if ((threadIdx.x & 31) == 0) {\n"
+        "      __threadfence_block();\n"
+        "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
+        "        reads[s] = 0;\n"
+        "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+        "        if (nt < ntiles) issue(s, nt);\n"
+        "      }\n"
+        "    }\n";
+    if (multi_prefetch()) {
+      // the thread's share of the stage (TP / 256 points) is loaded up
+      // front and the stage released before any evaluation: the refill
+      // overlaps this stage's work, and the shared-memory latency is paid
+      // once (ncu: the first use of the LDS result was the top stall of
+      // the one-point-at-a-time loop)
+      os << "    kcg_i64 q[TP / 256][NP];\n"
+            "    #pragma unroll\n"
+            "    for (int u = 0; u < TP / 256; ++u)\n"
+            "      #pragma unroll\n"
+            "      for (int j = 0; j < NP; ++j) q[u][j] = buf[(s * NP + j) * TP + u * 256 + threadIdx.x];\n"
+         << release
+         << "    #pragma unroll\n"
+            "    for (int u = 0; u < TP / 256; ++u) kcg_msize<" << stv << ">(q[u], a, rb + u * 256 + threadIdx.x);\n"
+            "  }\n";
+    } else {
+      os << "    #pragma unroll 1\n"
+            "    for (int u = 0; u < TP / 256; ++u) {\n"
+            "      const int o = u * 256 + threadIdx.x;\n"
+            "      kcg_i64 q[NP];\n"
+            "      #pragma unroll\n"
+            "      for (int j = 0; j < NP; ++j) q[j] = buf[(s * NP + j) * TP + o];\n"
+            "      kcg_msize<" << stv << ">(q, a, rb + o);\n"
+            "    }\n"
+         << release << "  }\n";
+    }
+    os <<           "  for (kcg_i64 i = ntiles * TP + (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;\n"
+          "       i += (kcg_i64)gridDim.x * blockDim.x) {\n"
+          "    kcg_i64 p[NP];\n";
+    for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = a.p[" << j << "][i];\n";
+    os << "    kcg_msize<" << stv << ">(p, a, i);\n  }\n}\n";
+  }
+}
+
 std::string codegen(const std::vector<const Lowered*>& progs,
                     const std::vector<std::vector<int>>& pmaps, int n_cols, JitKind kind,
                     const std::string& name) {
@@ -935,13 +1246,16 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   for (size_t v = 0; v < progs.size(); ++v) {
     emit_fast(os, *progs[v], static_cast<int>(v), false);
     emit_fast(os, *progs[v], static_cast<int>(v), true);
-    if (kind == JitKind::eval || kind == JitKind::argmin || kind == JitKind::host_eval)
+    if (kind == JitKind::eval || kind == JitKind::argmin || kind == JitKind::host_eval || kind == JitKind::multi)
       emit_fast(os, *progs[v], static_cast<int>(v), true, nullptr, true);
     emit_body(os, *progs[v], static_cast<int>(v), false);
     emit_classify(os, *progs[v], static_cast<int>(v), pmaps[v]);
   }
   if ((kind == JitKind::eval || kind == JitKind::host_eval) && progs[0]->admit)
     emit_body(os, *progs[0]->admit, 0, false, "kcg_admit_");
+  if (kind == JitKind::multi)
+    for (size_t v = 0; v < progs.size(); ++v)
+      if (progs[v]->admit) emit_body(os, *progs[v]->admit, static_cast<int>(v), false, "kcg_admit_");
   const int NP = n_cols > 0 ? n_cols : 1;
 
   if (kind == JitKind::host_eval) {
@@ -981,6 +1295,11 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     emit_tma_kernel(os, n_cols, name + "_tma");
     emit_grid_kernel(os, n_cols, name + "_grid", 0);
     emit_grid_kernel(os, n_cols, name + "_grid_gen", 1);
+    return os.str();
+  }
+
+  if (kind == JitKind::multi) {
+    emit_multi(os, progs, pmaps, n_cols, name);
     return os.str();
   }
 

@@ -2,13 +2,14 @@
 #pragma once
 
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "kcg_host.hpp"
 
 namespace kcg {
 
-enum class JitKind { eval, argmin, gram, residual, host_eval };
+enum class JitKind { eval, argmin, gram, residual, host_eval, multi };
 
 /// CUDA source for one specialised kernel named `name`. pmaps[v][j] is the
 /// column (in the launch's parameter-column order) holding parameter j of
@@ -48,6 +49,25 @@ std::string gram_group_source(int F, const std::string& name);
 size_t gram_wide_smem(int F);
 int gram_wide_warps(int F);
 int gram_wide_ctas(int F);
+
+/// One-pass evaluate + predict of several programs over one binding stream
+/// (JitKind::multi): the products it shares across programs (see
+/// multi_plan in codegen.cpp) -- the host fills shk[t] = alpha[kprods[t]
+/// schema] * double(coef) and shw[t] = alpha[schema] * double(coef).
+struct MultiPlan {
+  int64_t bmin = 0;      // fast path: every parameter in [0, bmin]
+  bool all_small = true;
+  std::vector<std::pair<int, __int128>> kprods;           // (schema, constant count)
+  std::vector<std::tuple<int, __int128, int>> wprods;     // (schema, 2^k, monomial id)
+  std::vector<std::vector<int>> monos;                    // launch-column exponents
+  std::vector<std::vector<std::pair<int, int>>> use;      // [v][key]: (form, table index)
+};
+MultiPlan multi_plan(const std::vector<const Lowered*>& progs, const std::vector<std::vector<int>>& pmaps,
+                     int n_cols);
+/// its TMA ring, CTAs per SM and points per stage.
+size_t multi_smem_bytes(int n_cols);
+int multi_ctas_per_sm();
+int multi_tile();
 
 /// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.
 size_t tma_smem_bytes(int n_cols);

@@ -219,6 +219,13 @@ struct LCons {
 
 struct LKey {
   int32_t schema, expr;
+  // the key's ORIGINAL polynomial (before congruence substitution), when it
+  // is one term: form 1 = the constant `coef`; form 2 = coef * prod_j
+  // param_j^pexp[j] with coef a positive power of two (the multi-program
+  // kernel shares such products across programs); 0 = anything else
+  int form = 0;
+  i128 coef = 0;
+  std::vector<int> pexp;
 };
 
 struct Lowered {

@@ -77,5 +77,6 @@ int num_sms();
 // lane operations per second of one pipe (peaks.cu: 0 IMAD, 1 LOP3, 2 DFMA,
 // 3 IMAD+LOP3 issue mix); synchronous on the current device
 double measure_pipe_peak(int kind, unsigned long long iters);
+double measure_stream(int R, int W, unsigned long long n);
 
 }  // namespace kcg

@@ -68,6 +68,29 @@ __global__ void __launch_bounds__(256) kcg_peak_probe(unsigned long long iters, 
   }
 }
 
+// HBM stream with a given read/write mix: R int64 columns in, W fp64
+// columns out (16-byte vector accesses, streaming cache hints) -- the
+// "same-mix" bandwidth a kernel that reads R and writes W columns of n
+// points can at best reach (e.g. R = 3, W = 6 for the one-pass six-variant
+// evaluate + predict: one third reads)
+template <int R, int W>
+__global__ void __launch_bounds__(256) kcg_stream_probe(const long long* __restrict__ in, double* __restrict__ out,
+                                                        long long n) {
+  const long long nv = n >> 1;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nv; v += (long long)gridDim.x * blockDim.x) {
+    long long a = 0, b = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      const longlong2 x = __ldcs(reinterpret_cast<const longlong2*>(in + j * n) + v);
+      a += x.x;
+      b += x.y;
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+      __stcs(reinterpret_cast<double2*>(out + j * n) + v, make_double2((double)(a + j), (double)(b + j)));
+  }
+}
+
 void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -109,6 +132,46 @@ double measure_pipe_peak(int kind, unsigned long long iters) {
   std::sort(ms.begin(), ms.end());
   const double ops = static_cast<double>(grid) * 256.0 * static_cast<double>(iters) * kUnroll * kChains;
   return ops / (ms[1] / 1e3);
+}
+
+double measure_stream(int R, int W, unsigned long long n) {
+  n &= ~1ull;
+  long long* in = nullptr;
+  double* out = nullptr;
+  check(cudaMalloc(&in, n * 8 * R), "cudaMalloc");
+  check(cudaMalloc(&out, n * 8 * W), "cudaMalloc");
+  check(cudaMemset(in, 1, n * 8 * R), "cudaMemset");
+  const unsigned grid = static_cast<unsigned>(num_sms()) * 8;
+  auto launch = [&] {
+    const long long nn = static_cast<long long>(n);
+    if (R == 3 && W == 6) kcg_stream_probe<3, 6><<<grid, 256>>>(in, out, nn);
+    else if (R == 3 && W == 1) kcg_stream_probe<3, 1><<<grid, 256>>>(in, out, nn);
+    else if (R == 1 && W == 6) kcg_stream_probe<1, 6><<<grid, 256>>>(in, out, nn);
+    else if (R == 1 && W == 1) kcg_stream_probe<1, 1><<<grid, 256>>>(in, out, nn);
+    else if (R == 4 && W == 0) kcg_stream_probe<4, 0><<<grid, 256>>>(in, out, nn);
+    else throw std::runtime_error("unsupported stream mix");
+    check(cudaGetLastError(), "kcg_stream_probe launch");
+  };
+  cudaEvent_t e0, e1;
+  check(cudaEventCreate(&e0), "cudaEventCreate");
+  check(cudaEventCreate(&e1), "cudaEventCreate");
+  launch();
+  std::vector<float> ms;
+  for (int r = 0; r < 5; ++r) {
+    check(cudaEventRecord(e0), "cudaEventRecord");
+    launch();
+    check(cudaEventRecord(e1), "cudaEventRecord");
+    check(cudaEventSynchronize(e1), "cudaEventSynchronize");
+    float t = 0;
+    check(cudaEventElapsedTime(&t, e0, e1), "cudaEventElapsedTime");
+    ms.push_back(t);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(in);
+  cudaFree(out);
+  std::sort(ms.begin(), ms.end());
+  return static_cast<double>(n) * 8.0 * (R + W) / (ms[0] / 1e3);
 }
 
 }  // namespace kcg

@@ -69,6 +69,7 @@ def test_host_eval_bitwise_equals_device_path(monkeypatch, pinned, chunk):
     pred, st = kc.predict_host(progs, w, host, status=True, out=out)
     path = _capi.lib().kcg_host_last_path()
     assert bool(path & _capi.HOST_PINNED) == pinned
+    assert path & _capi.HOST_PATH_ONEPASS  # several programs: one launch per chunk
     if pinned:
         assert st.is_pinned() and path & _capi.HOST_PATH_2D
     dev = {k: v.cuda() for k, v in host.items()}
@@ -141,3 +142,22 @@ def test_host_eval_pitch_fallback_and_growing_streams(monkeypatch):
         pred = kc.predict_host(progs, w, b, pinned=False)
         for i in range(len(progs)):
             assert torch.equal(pred[i].view(torch.int64), want[i].view(torch.int64)), streams
+
+
+@pytest.mark.gpu
+def test_host_eval_onepass_equals_per_program_launches(monkeypatch):
+    """The one-pass multi-program chunk kernel and one launch per program
+    (KCG_HOST_ONEPASS=0) give the same bits, with status bytes."""
+    monkeypatch.setenv("KCG_HOST_CHUNK", "32768")
+    n = 4 * 32768 + 5
+    progs = [kc.load_program(v) for v in VARIANTS]
+    w = _weights()
+    b = _bindings(n, 21)
+    p1, s1 = kc.predict_host(progs, w, b, status=True)
+    assert _capi.lib().kcg_host_last_path() & _capi.HOST_PATH_ONEPASS
+    monkeypatch.setenv("KCG_HOST_ONEPASS", "0")
+    p0, s0 = kc.predict_host(progs, w, b, status=True)
+    assert not _capi.lib().kcg_host_last_path() & _capi.HOST_PATH_ONEPASS
+    import torch
+    assert torch.equal(p1.view(torch.int64), p0.view(torch.int64))
+    assert torch.equal(s1, s0)
