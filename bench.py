@@ -734,8 +734,9 @@ def _configs(kc, torch, dev, args, cols, progs, w):
         "points_per_s": total * len(progs) / sec, "sizes_per_s": total / sec,
         "bytes_per_size": 36, "hbm_frac": 36 * total / sec / 1e9 / hbm,
         "best_variant_histogram": torch.bincount(best.to(torch.int64) + 1, minlength=len(progs) + 1).tolist(),
-        "instruction_roofline": _instr_roofline(_ncu_lane_instr("r01_argmin_ncu.txt"), total * len(progs) / sec,
-                                                _pipe_peaks(kc), "profiles/r01_argmin_ncu.txt (ncu, same kernel)"),
+        "instruction_roofline": _instr_roofline(_ncu_lane_instr("r02_argmin_ncu.txt"), total * len(progs) / sec,
+                                                _pipe_peaks(kc), "profiles/r02_argmin_ncu.txt (ncu, kcg_multiam_v6_tma, 1-CTA build)"),
+        "kernel": "kcg_multiam_v6_tma (one-pass kernel, argmin epilogue)",
         "note": "one fused launch per step; 24 B bindings in, int32 + fp64 out per size"}
     # the same launch also writing every variant's prediction (variant-major):
     # all 1e9 predictions with the bindings read once (24 + 48 B per size

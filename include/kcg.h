@@ -191,11 +191,12 @@ int kcg_eval_predict_multi(const kcg_program* const* progs, int n_progs,
                            const double* alpha, double* pred_out, size_t ld_pred,
                            uint8_t* status_out, size_t ld_status, void* stream);
 
-/* The generated CUDA source of kcg_eval_predict_multi's kernels for these
- * programs (kernels kcg_multi_v<n_progs> and kcg_multi_v<n_progs>_tma;
- * diagnostics / compile checks). Owned by the library, valid until the
+/* The generated CUDA source of the one-pass kernels for these programs
+ * (diagnostics / compile checks): argmin = 0 kcg_eval_predict_multi's
+ * (kcg_multi_v<n>[_tma][_st]), argmin = 1 kcg_argmin's
+ * (kcg_multiam_v<n>[_tma][_p]). Owned by the library, valid until the
  * next call on this thread; NULL on error (see kcg_last_error).          */
-const char* kcg_multi_jit_source(const kcg_program* const* progs, int n_progs);
+const char* kcg_multi_jit_source(const kcg_program* const* progs, int n_progs, int argmin);
 
 /* ---- host buffers: the reference's own calling convention ---------------
  * Replaces the reference's per-point host loop `evaluate_properties` +

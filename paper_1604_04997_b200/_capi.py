@@ -105,7 +105,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_launch_count": (ctypes.c_uint64, []),
         "kcg_eval_predict_host": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_size_t, P, P, P, ctypes.c_uint]),
         "kcg_host_last_path": (ctypes.c_uint, []),
-        "kcg_multi_jit_source": (ctypes.c_char_p, [P, ctypes.c_int]),
+        "kcg_multi_jit_source": (ctypes.c_char_p, [P, ctypes.c_int, ctypes.c_int]),
         "kcg_eval_predict_multi": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_size_t, P, P, ctypes.c_size_t, P,
                                                   ctypes.c_size_t, P]),
         "kcg_measure_stream": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_double)]),

@@ -329,11 +329,12 @@ def predict_multi(progs: Sequence[Program], w: ModelWeights, bindings, status: b
     return (pred, st) if status else pred
 
 
-def multi_jit_source(progs: Sequence[Program]) -> str:
-    """Generated CUDA of the one-pass multi-program kernels (diagnostics)."""
+def multi_jit_source(progs: Sequence[Program], argmin: bool = False) -> str:
+    """Generated CUDA of the one-pass multi-program kernels (diagnostics):
+    predict_multi's, or (argmin=True) argmin's."""
     progs = list(progs)
     handles = (ctypes.c_void_p * len(progs))(*[p.handle.value for p in progs])
-    src = lib().kcg_multi_jit_source(handles, len(progs))
+    src = lib().kcg_multi_jit_source(handles, len(progs), int(argmin))
     if src is None:
         raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, lib().kcg_last_error().decode())
     return src.decode()

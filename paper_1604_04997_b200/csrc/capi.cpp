@@ -13,6 +13,7 @@
 #include <functional>
 #include <limits>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -45,6 +46,11 @@ struct kcg_program {
   void* jit_eval_grid_gen = nullptr;
   void* jit_gram = nullptr;
   void* jit_resid = nullptr;
+  uint64_t uid = next_uid();  // identity for caches keyed by program sets
+  static uint64_t next_uid() {
+    static std::atomic<uint64_t> c{1};
+    return c++;
+  }
 };
 
 namespace {
@@ -494,20 +500,134 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
   });
 }
 
-const char* kcg_multi_jit_source(const kcg_program* const* progs, int V) {
+const char* kcg_multi_jit_source(const kcg_program* const* progs, int V, int argmin) {
   static thread_local std::string src;
   if (!progs || V < 1) return nullptr;
   try {
     std::vector<const kcg::Lowered*> lows;
     std::vector<std::vector<int>> pmaps;
     variant_maps(progs, V, lows, pmaps);
-    src = kcg::codegen(lows, pmaps, progs[0]->low.n_params, kcg::JitKind::multi, "kcg_multi_v" + std::to_string(V));
+    src = kcg::codegen(lows, pmaps, progs[0]->low.n_params, argmin ? kcg::JitKind::multi_argmin : kcg::JitKind::multi,
+                       (argmin ? "kcg_multiam_v" : "kcg_multi_v") + std::to_string(V));
   } catch (const KcgError& e) {
     fail(e.code, e.what());
     return nullptr;
   }
   return src.c_str();
 }
+
+}  // extern "C"
+
+namespace {
+
+// One-pass multi-program launch (kcg_eval_predict_multi / kcg_argmin).
+// Returns false when the one-pass kernel does not apply (non-finite weights
+// or shared products, an interpreter-engine program): the caller falls back.
+// The generated source and kernel handles are cached per program set.
+struct MultiKey {
+  std::vector<uint64_t> uids;
+  bool argmin;
+  bool operator<(const MultiKey& o) const { return std::tie(uids, argmin) < std::tie(o.uids, o.argmin); }
+};
+struct MultiEntry {
+  std::string src, name;
+  kcg::MultiPlan plan;
+  std::map<std::string, void*> kernels;  // per kernel name (and device: handles are context-independent)
+};
+
+bool launch_multi(const kcg_program* const* progs, int V, const int64_t* const* param_cols, size_t n,
+                  const double* alpha, double* pred, size_t ldp, uint8_t* status, size_t lds, int32_t* best,
+                  double* best_t, void* stream, bool argmin) {
+  std::vector<const kcg::Lowered*> lows;
+  std::vector<std::vector<int>> pmaps;
+  variant_maps(progs, V, lows, pmaps);
+  const int np = progs[0]->low.n_params;
+  bool ok = !std::getenv("KCG_NO_MULTI");
+  std::vector<std::vector<double>> als(V), alfs(V);
+  for (int v = 0; v < V && ok; ++v) {
+    als[v].assign(std::max<size_t>(1, progs[v]->low.keys.size()), 0.0);
+    compact_alpha(progs[v], alpha, als[v].data());
+    bool fin = true;
+    alfs[v] = folded_alpha(progs[v], als[v], &fin);
+    ok = ok && fin && progs[v]->engine == KCG_ENGINE_JIT;
+  }
+  if (!ok) return false;
+  static std::mutex mu;
+  static std::map<MultiKey, std::shared_ptr<MultiEntry>> cache;
+  MultiKey key{{}, argmin};
+  for (int v = 0; v < V; ++v) key.uids.push_back(progs[v]->uid);
+  std::shared_ptr<MultiEntry> e;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) e = it->second;
+  }
+  if (!e) {
+    e = std::make_shared<MultiEntry>();
+    e->name = (argmin ? "kcg_multiam_v" : "kcg_multi_v") + std::to_string(V);
+    e->src = kcg::codegen(lows, pmaps, np, argmin ? kcg::JitKind::multi_argmin : kcg::JitKind::multi, e->name);
+    e->plan = kcg::multi_plan(lows, pmaps, np);
+    std::lock_guard<std::mutex> lock(mu);
+    if (cache.size() >= 256) cache.clear();  // bounded (program sets of one process)
+    cache[key] = e;
+  }
+  // shared products (multi_plan): alpha (x) constant count; alpha * 2^k
+  std::vector<double> shk, shw;
+  for (const auto& [schema, c] : e->plan.kprods) shk.push_back(alpha[schema] * static_cast<double>(static_cast<int64_t>(c)));
+  for (const auto& [schema, c, m] : e->plan.wprods) {
+    shw.push_back(alpha[schema] * static_cast<double>(c));
+    if (!std::isfinite(shw.back())) return false;
+  }
+  bool vec = true;
+  for (int j = 0; j < np; ++j) vec = vec && reinterpret_cast<uintptr_t>(param_cols[j]) % 16 == 0;
+  static const bool no_tma = std::getenv("KCG_NO_TMA") != nullptr;
+  const size_t tiles = n / static_cast<size_t>(kcg::multi_tile());
+  const bool tma = vec && !no_tma && np > 0 && tiles >= static_cast<size_t>(kcg::num_sms());
+  const bool extra = argmin ? pred != nullptr : status != nullptr;  // _p / _st kernels
+  const std::string kname = e->name + (tma ? "_tma" : "") + (extra ? (argmin ? "_p" : "_st") : "");
+  void* k = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = e->kernels.find(kname);
+    if (it != e->kernels.end()) k = it->second;
+  }
+  if (!k) {
+    k = kcg::jit_kernel(e->src, kname);
+    std::lock_guard<std::mutex> lock(mu);
+    e->kernels[kname] = k;
+  }
+  ArgBuf ab;
+  for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
+  ab.push<void*>(pred);
+  ab.push<void*>(status);
+  ab.push<void*>(best);
+  ab.push<void*>(best_t);
+  ab.push<int64_t>(static_cast<int64_t>(n));
+  ab.push<int64_t>(static_cast<int64_t>(ldp));
+  ab.push<int64_t>(static_cast<int64_t>(lds));
+  for (int v = 0; v < V; ++v)
+    for (double x : als[v]) ab.push<double>(x);
+  for (int v = 0; v < V; ++v)
+    for (double x : alfs[v]) ab.push<double>(x);
+  for (double x : shk) ab.push<double>(x);
+  if (shk.empty()) ab.push<double>(0.0);
+  for (double x : shw) ab.push<double>(x);
+  if (shw.empty()) ab.push<double>(0.0);
+  ab.finish();
+  if (tma) {
+    const unsigned grid = static_cast<unsigned>(
+        std::min<size_t>(tiles, static_cast<size_t>(kcg::num_sms()) * kcg::multi_ctas_per_sm(argmin)));
+    kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid, 256, stream, kcg::multi_smem_bytes(np, argmin));
+  } else {
+    kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid_for(n), 256, stream);
+  }
+  ++g_launches;
+  return true;
+}
+
+}  // namespace
+
+extern "C" {
 
 int kcg_eval_predict_multi(const kcg_program* const* progs, int V, const int64_t* const* param_cols, size_t n,
                            const double* alpha, double* pred_out, size_t ld_pred, uint8_t* status_out,
@@ -524,68 +644,18 @@ int kcg_eval_predict_multi(const kcg_program* const* progs, int V, const int64_t
     const int np = progs[0]->low.n_params;
     if (np > 0 && !param_cols) throw KcgError(KCG_E_INVALID_ARGUMENT, "null param_cols");
     if (n == 0) return KCG_OK;
-    // non-finite weights (skip rules matter) or the interpreter engine: one
-    // kcg_eval_predict per program (same results, V binding reads)
-    bool finite = true, jit = true;
-    std::vector<std::vector<double>> als(V), alfs(V);
-    for (int v = 0; v < V; ++v) {
-      als[v].assign(std::max<size_t>(1, progs[v]->low.keys.size()), 0.0);
-      compact_alpha(progs[v], alpha, als[v].data());
-      bool fin = true;
-      alfs[v] = folded_alpha(progs[v], als[v], &fin);
-      finite = finite && fin;
-      jit = jit && progs[v]->engine == KCG_ENGINE_JIT;
-    }
-    // shared products (multi_plan): alpha (x) constant count; alpha * 2^k
-    const kcg::MultiPlan plan = kcg::multi_plan(lows, pmaps, np);
-    std::vector<double> shk, shw;
-    for (const auto& [schema, c] : plan.kprods) shk.push_back(alpha[schema] * static_cast<double>(static_cast<int64_t>(c)));
-    for (const auto& [schema, c, m] : plan.wprods) {
-      shw.push_back(alpha[schema] * static_cast<double>(c));
-      finite = finite && std::isfinite(shw.back());
-    }
-    if (!finite || !jit || !pred_out || std::getenv("KCG_NO_MULTI")) {
-      for (int v = 0; v < V; ++v) {
-        std::vector<const int64_t*> cols(std::max(np, 1), nullptr);
-        for (int j = 0; j < progs[v]->low.n_params; ++j) cols[j] = param_cols[pmaps[v][j]];
-        const int rc = kcg_eval_predict(progs[v], cols.data(), n, alpha, pred_out ? pred_out + v * ld_pred : nullptr,
-                                        status_out ? status_out + v * ld_status : nullptr, nullptr, nullptr, 0, stream);
-        if (rc != KCG_OK) throw KcgError(rc, g_last_error);
-      }
+    if (pred_out && launch_multi(progs, V, param_cols, n, alpha, pred_out, ld_pred, status_out, ld_status, nullptr,
+                                 nullptr, stream, false))
       return KCG_OK;
+    // non-finite weights (skip rules matter), the interpreter engine or
+    // status-only calls: one kcg_eval_predict per program (same results)
+    for (int v = 0; v < V; ++v) {
+      std::vector<const int64_t*> cols(std::max(np, 1), nullptr);
+      for (int j = 0; j < progs[v]->low.n_params; ++j) cols[j] = param_cols[pmaps[v][j]];
+      const int rc = kcg_eval_predict(progs[v], cols.data(), n, alpha, pred_out ? pred_out + v * ld_pred : nullptr,
+                                      status_out ? status_out + v * ld_status : nullptr, nullptr, nullptr, 0, stream);
+      if (rc != KCG_OK) throw KcgError(rc, g_last_error);
     }
-    const std::string name = "kcg_multi_v" + std::to_string(V);
-    const std::string src = kcg::codegen(lows, pmaps, np, kcg::JitKind::multi, name);
-    bool vec = true;
-    for (int j = 0; j < np; ++j) vec = vec && reinterpret_cast<uintptr_t>(param_cols[j]) % 16 == 0;
-    static const bool no_tma = std::getenv("KCG_NO_TMA") != nullptr;
-    const size_t tiles = n / static_cast<size_t>(kcg::multi_tile());
-    const bool tma = vec && !no_tma && np > 0 && tiles >= static_cast<size_t>(kcg::num_sms());
-    void* k = kcg::jit_kernel(src, name + (tma ? "_tma" : "") + (status_out ? "_st" : ""));
-    ArgBuf ab;
-    for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
-    ab.push<void*>(pred_out);
-    ab.push<void*>(status_out);
-    ab.push<int64_t>(static_cast<int64_t>(n));
-    ab.push<int64_t>(static_cast<int64_t>(ld_pred));
-    ab.push<int64_t>(static_cast<int64_t>(ld_status));
-    for (int v = 0; v < V; ++v)
-      for (double x : als[v]) ab.push<double>(x);
-    for (int v = 0; v < V; ++v)
-      for (double x : alfs[v]) ab.push<double>(x);
-    for (double x : shk) ab.push<double>(x);
-    if (shk.empty()) ab.push<double>(0.0);
-    for (double x : shw) ab.push<double>(x);
-    if (shw.empty()) ab.push<double>(0.0);
-    ab.finish();
-    if (tma) {
-      const unsigned grid = static_cast<unsigned>(
-          std::min<size_t>(tiles, static_cast<size_t>(kcg::num_sms()) * kcg::multi_ctas_per_sm()));
-      kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid, 256, stream, kcg::multi_smem_bytes(np));
-    } else {
-      kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid_for(n), 256, stream);
-    }
-    ++g_launches;
     return KCG_OK;
   });
 }
@@ -598,6 +668,14 @@ int kcg_argmin(const kcg_program* const* progs, int V, const int64_t* const* par
   return guarded([&] {
     require_device();
     if (n == 0) return KCG_OK;
+    if (progs[0] && progs[0]->low.n_params > 0 && !param_cols)
+      throw KcgError(KCG_E_INVALID_ARGUMENT, "null param_cols");
+    // the one-pass kernel with the argmin epilogue (KCG_ARGMIN_LEGACY=1: the
+    // round-1 grid-stride argmin kernel below)
+    static const bool legacy = std::getenv("KCG_ARGMIN_LEGACY") != nullptr;
+    if (!legacy && launch_multi(progs, V, param_cols, n, alpha, preds_out, n, nullptr, 0, best_idx, best_t, stream,
+                                true))
+      return KCG_OK;
     const kcg_program* p0 = progs[0];
     const int np = p0->low.n_params;
     std::vector<const kcg::Lowered*> lows;

@@ -936,19 +936,26 @@ size_t tma_smem_bytes(int n_cols) {
 // per SM with a 72 KB ring (3 stages) 2.40-2.50 ms; 2 CTAs x 96 KB 2.74,
 // 3 CTAs x 64 KB 2.57-2.83, 1 CTA x 192 KB 2.89; loading the thread's
 // whole share of a stage up front (KCG_MULTI_PREFETCH=1) 2.60
-int multi_ctas() { return env_int("KCG_MULTI_CTAS", 1, 1, 4); }
-int multi_ring_kb() { return env_int("KCG_MULTI_RING_KB", 72, 16, 200); }
+// The argmin epilogue writes 12 B per size instead of 48: there the kernel
+// is latency-bound and more CTAs pay (1 CTA x 72 KB 2.25 ms, 2 CTAs 1.90,
+// 3 CTAs x 64 KB 1.65; KCG_MULTIAM_CTAS / KCG_MULTIAM_RING_KB)
+int multi_ctas(bool argmin = false) {
+  return argmin ? env_int("KCG_MULTIAM_CTAS", 3, 1, 4) : env_int("KCG_MULTI_CTAS", 1, 1, 4);
+}
+int multi_ring_kb(bool argmin = false) {
+  return argmin ? env_int("KCG_MULTIAM_RING_KB", 64, 16, 200) : env_int("KCG_MULTI_RING_KB", 72, 16, 200);
+}
 int multi_tile() { return 256 * env_int("KCG_MULTI_TILE_Q", 4, 1, 8); }
-int multi_ctas_per_sm() { return multi_ctas(); }
+int multi_ctas_per_sm(bool argmin) { return multi_ctas(argmin); }
 bool multi_share() { return env_int("KCG_MULTI_SHARE", 1, 0, 1) == 1; }
 bool multi_prefetch() { return env_int("KCG_MULTI_PREFETCH", 0, 0, 1) == 1; }
-int multi_stages(int n_cols) {
+int multi_stages(int n_cols, bool argmin) {
   const int per = (n_cols > 0 ? n_cols : 1) * multi_tile() * 8;
-  const int s = (multi_ring_kb() * 1024) / per;
+  const int s = (multi_ring_kb(argmin) * 1024) / per;
   return s < 2 ? 2 : (s > 8 ? 8 : s);
 }
-size_t multi_smem_bytes(int n_cols) {
-  return static_cast<size_t>(multi_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * multi_tile() * 8;
+size_t multi_smem_bytes(int n_cols, bool argmin) {
+  return static_cast<size_t>(multi_stages(n_cols, argmin)) * (n_cols > 0 ? n_cols : 1) * multi_tile() * 8;
 }
 
 // Which products the one-pass kernel forms once per point and shares:
@@ -1021,8 +1028,12 @@ MultiPlan multi_plan(const std::vector<const Lowered*>& progs, const std::vector
   return P;
 }
 
+// argmin = true: the config-4 autotuning epilogue instead of the prediction
+// stores -- per size the lowest-index variant with status OK and the
+// smallest prediction (best = -1, best_t = +inf if none), optionally all
+// predictions too (kernels <name>[_tma] and <name>[_tma]_p)
 void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs,
-                const std::vector<std::vector<int>>& pmaps, int n_cols, const std::string& name) {
+                const std::vector<std::vector<int>>& pmaps, int n_cols, const std::string& name, bool argmin) {
   const int V = static_cast<int>(progs.size());
   const int NP = n_cols > 0 ? n_cols : 1;
   const MultiPlan P = multi_plan(progs, pmaps, n_cols);
@@ -1034,9 +1045,9 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
   }
   const int NK = std::max<int>(1, static_cast<int>(P.kprods.size()));
   const int NW = std::max<int>(1, static_cast<int>(P.wprods.size()));
-  os << "struct KcgMArgs { const kcg_i64* p[" << NP << "]; double* pred; unsigned char* status; kcg_i64 n; "
-        "kcg_i64 ldp; kcg_i64 lds; double al[" << tot << "]; double alf[" << tot << "]; double shk[" << NK
-     << "]; double shw[" << NW << "]; };\n";
+  os << "struct KcgMArgs { const kcg_i64* p[" << NP << "]; double* pred; unsigned char* status; int* best; "
+        "double* best_t; kcg_i64 n; kcg_i64 ldp; kcg_i64 lds; double al[" << tot << "]; double alf[" << tot
+     << "]; double shk[" << NK << "]; double shw[" << NW << "]; };\n";
   // combined fast-path range: every parameter in [0, min_v b64_v]
   os << "__device__ __forceinline__ bool kcg_mfast(const kcg_i64* p) {\n";
   if (P.bmin < 0 || n_cols == 0) {
@@ -1078,7 +1089,8 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
           "      : \"=d\"(out) : \"r\"(st), \"d\"(s));\n  return st;\n}\n";
   }
   // out-of-line: every variant of size i, any parameter range
-  os << "__device__ __noinline__ void kcg_mslow(const KcgMArgs& a, kcg_i64 i) {\n  kcg_i64 p[" << NP << "];\n";
+  os << "__device__ __noinline__ void kcg_mslow(const KcgMArgs& a, kcg_i64 i) {\n  kcg_i64 p[" << NP << "];\n"
+        "  int bi = -1;\n  double bt = __longlong_as_double(0x7ff0000000000000ll);\n";
   for (int j = 0; j < n_cols; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
   for (int v = 0; v < V; ++v) {
     const Lowered& L = *progs[v];
@@ -1099,10 +1111,12 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
       os << ") {\n        kcg_i128 none[1];\n        const int a0 = kcg_admit_" << v
          << "(q, none);\n        if (a0 != KCG_PT_OK) st = a0;\n      }\n";
     }
-    os << "    }\n    a.pred[(kcg_i64)" << v << " * a.ldp + i] = (st == KCG_PT_OK) ? s : kcg_nan();\n"
-       << "    if (a.status) a.status[(kcg_i64)" << v << " * a.lds + i] = (unsigned char)st;\n  }\n";
+    os << "    }\n    if (st != KCG_PT_OK) s = kcg_nan();\n"
+       << "    if (a.pred) a.pred[(kcg_i64)" << v << " * a.ldp + i] = s;\n"
+       << "    if (a.status) a.status[(kcg_i64)" << v << " * a.lds + i] = (unsigned char)st;\n"
+       << "    if (st == KCG_PT_OK && s < bt) { bt = s; bi = " << v << "; }\n  }\n";
   }
-  os << "}\n";
+  os << "  if (a.best) { a.best[i] = bi; a.best_t[i] = bt; }\n}\n";
   // one size from registers: shared products, then every variant -- one
   // basic block (no per-variant branches), so the V independent
   // accumulation chains interleave
@@ -1123,12 +1137,24 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
   for (size_t t = 0; t < P.wprods.size(); ++t)
     os << "  sh[" << t << "] = __dmul_rn(a.shw[" << t << "], dm" << std::get<2>(P.wprods[t]) << ");\n";
   for (int v = 0; v < V; ++v) os << "  double s" << v << ";\n  const int st" << v << " = kcg_mfastv_" << v << "<1>(p, a, sh, s" << v << ");\n";
-  for (int v = 0; v < V; ++v) os << "  __stcs(a.pred + (kcg_i64)" << v << " * a.ldp + i, s" << v << ");\n";
-  os << "  if (ST) {\n";
-  for (int v = 0; v < V; ++v) os << "    a.status[(kcg_i64)" << v << " * a.lds + i] = (unsigned char)st" << v << ";\n";
-  os << "  }\n}\n";
+  // ST: pred mode -- status bytes too; argmin mode -- all predictions too
+  if (!argmin) {
+    for (int v = 0; v < V; ++v) os << "  __stcs(a.pred + (kcg_i64)" << v << " * a.ldp + i, s" << v << ");\n";
+    os << "  if (ST) {\n";
+    for (int v = 0; v < V; ++v) os << "    a.status[(kcg_i64)" << v << " * a.lds + i] = (unsigned char)st" << v << ";\n";
+    os << "  }\n}\n";
+  } else {
+    // lowest index wins ties (strict <); a non-OK variant holds NaN, which
+    // never compares below
+    os << "  int bi = -1;\n  double bt = __longlong_as_double(0x7ff0000000000000ll);\n";
+    for (int v = 0; v < V; ++v)
+      os << "  if (st" << v << " == KCG_PT_OK && s" << v << " < bt) { bt = s" << v << "; bi = " << v << "; }\n";
+    os << "  __stcs(a.best + i, bi);\n  __stcs(a.best_t + i, bt);\n  if (ST) {\n";
+    for (int v = 0; v < V; ++v) os << "    __stcs(a.pred + (kcg_i64)" << v << " * a.ldp + i, s" << v << ");\n";
+    os << "  }\n}\n";
+  }
   for (int stv = 0; stv < 2; ++stv) {
-    const std::string sfx = stv ? "_st" : "";
+    const std::string sfx = stv ? (argmin ? "_p" : "_st") : "";
     // plain grid-stride kernel (unaligned columns, small n)
     os << "extern \"C\" __global__ void __launch_bounds__(256) " << name << sfx << "(const __grid_constant__ KcgMArgs a) {\n"
           "  for (kcg_i64 i = (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n; i += (kcg_i64)gridDim.x * blockDim.x) {\n"
@@ -1138,8 +1164,8 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
     // TMA ring kernel (persistent): one elected thread streams TP-point
     // tiles of every column into the ring; each warp releases a stage when
     // done and the last one refills it (as kcg_eval_<k>_tma)
-    const int S = multi_stages(n_cols);
-    os << "extern \"C\" __global__ void __launch_bounds__(256, " << multi_ctas() << ") " << name << "_tma" << sfx
+    const int S = multi_stages(n_cols, argmin);
+    os << "extern \"C\" __global__ void __launch_bounds__(256, " << multi_ctas(argmin) << ") " << name << "_tma" << sfx
        << "(const __grid_constant__ KcgMArgs a) {\n"
           "  constexpr int TP = " << multi_tile() << ", S = " << S << ", NP = " << NP << ";\n"
           "  extern __shared__ __align__(128) unsigned char kcg_smem[];\n"
@@ -1246,14 +1272,15 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   for (size_t v = 0; v < progs.size(); ++v) {
     emit_fast(os, *progs[v], static_cast<int>(v), false);
     emit_fast(os, *progs[v], static_cast<int>(v), true);
-    if (kind == JitKind::eval || kind == JitKind::argmin || kind == JitKind::host_eval || kind == JitKind::multi)
+    if (kind == JitKind::eval || kind == JitKind::argmin || kind == JitKind::host_eval || kind == JitKind::multi ||
+        kind == JitKind::multi_argmin)
       emit_fast(os, *progs[v], static_cast<int>(v), true, nullptr, true);
     emit_body(os, *progs[v], static_cast<int>(v), false);
     emit_classify(os, *progs[v], static_cast<int>(v), pmaps[v]);
   }
   if ((kind == JitKind::eval || kind == JitKind::host_eval) && progs[0]->admit)
     emit_body(os, *progs[0]->admit, 0, false, "kcg_admit_");
-  if (kind == JitKind::multi)
+  if (kind == JitKind::multi || kind == JitKind::multi_argmin)
     for (size_t v = 0; v < progs.size(); ++v)
       if (progs[v]->admit) emit_body(os, *progs[v]->admit, static_cast<int>(v), false, "kcg_admit_");
   const int NP = n_cols > 0 ? n_cols : 1;
@@ -1298,8 +1325,8 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     return os.str();
   }
 
-  if (kind == JitKind::multi) {
-    emit_multi(os, progs, pmaps, n_cols, name);
+  if (kind == JitKind::multi || kind == JitKind::multi_argmin) {
+    emit_multi(os, progs, pmaps, n_cols, name, kind == JitKind::multi_argmin);
     return os.str();
   }
 

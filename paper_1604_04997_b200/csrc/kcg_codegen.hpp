@@ -9,7 +9,7 @@
 
 namespace kcg {
 
-enum class JitKind { eval, argmin, gram, residual, host_eval, multi };
+enum class JitKind { eval, argmin, gram, residual, host_eval, multi, multi_argmin };
 
 /// CUDA source for one specialised kernel named `name`. pmaps[v][j] is the
 /// column (in the launch's parameter-column order) holding parameter j of
@@ -65,8 +65,8 @@ struct MultiPlan {
 MultiPlan multi_plan(const std::vector<const Lowered*>& progs, const std::vector<std::vector<int>>& pmaps,
                      int n_cols);
 /// its TMA ring, CTAs per SM and points per stage.
-size_t multi_smem_bytes(int n_cols);
-int multi_ctas_per_sm();
+size_t multi_smem_bytes(int n_cols, bool argmin);
+int multi_ctas_per_sm(bool argmin);
 int multi_tile();
 
 /// Shared-memory ring of the TMA-staged eval kernel for n_cols columns.

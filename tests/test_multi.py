@@ -29,10 +29,11 @@ def test_multi_source_compiles_for_sm100a():
     for 3-parameter variants and for programs declaring parameters in
     another order."""
     progs = [kc.load_program(v) for v in MATMUL]
-    src = kc.multi_jit_source(progs)
-    for name in ("kcg_multi_v6", "kcg_multi_v6_tma"):
-        assert name in src
-        assert _capi.lib().kcg_jit_compile_check(src.encode(), name.encode()) == 0, _capi.lib().kcg_last_error()
+    for argmin, names in ((False, ("kcg_multi_v6", "kcg_multi_v6_tma_st")), (True, ("kcg_multiam_v6_tma", "kcg_multiam_v6_p"))):
+        src = kc.multi_jit_source(progs, argmin=argmin)
+        for name in names:
+            assert name in src
+            assert _capi.lib().kcg_jit_compile_check(src.encode(), name.encode()) == 0, _capi.lib().kcg_last_error()
 
 
 def test_multi_argument_errors():
@@ -147,3 +148,54 @@ def test_multi_nonfinite_weights_take_per_program_path():
     for i, p in enumerate(progs):
         want = kc.predict(w, p, dev)
         assert torch.equal(pred[i].view(torch.int64), want.view(torch.int64))
+
+
+def _argmin_ref(torch, preds, st):
+    """lowest index among status-OK variants with the smallest prediction"""
+    V, n = preds.shape
+    big = torch.where(st == 0, preds, torch.full_like(preds, float("inf")))
+    bt, _ = big.min(dim=0)
+    first = torch.full((n,), -1, dtype=torch.int64, device=preds.device)
+    for v in range(V - 1, -1, -1):
+        hit = (st[v] == 0) & (preds[v] == bt)
+        first = torch.where(hit, torch.full_like(first, v), first)
+    return first, bt
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [777, 148 * 1024 * 3 + 4321])
+def test_argmin_one_pass_equals_per_program_argmin(n):
+    """kcg_argmin through the one-pass kernel (argmin epilogue): best variant,
+    best time and every prediction equal the per-program predictions'
+    lowest-index argmin, on the TMA path and the grid-stride path, with
+    slow-path points (int128 counts, overflow, inadmissible, negative)."""
+    import torch
+    progs = [kc.load_program(v) for v in MATMUL]
+    w = _weights()
+    dev = {k: torch.from_numpy(v).cuda() for k, v in _bindings(n, n + 1).items()}
+    best, bt, preds = kc.argmin(progs, w, dev, return_preds=True)
+    best2, bt2 = kc.argmin(progs, w, dev)
+    ref = [kc.predict(w, p, dev, with_status=True) for p in progs]
+    P = torch.stack([r[0] for r in ref])
+    S = torch.stack([r[1] for r in ref])
+    assert torch.equal(preds.view(torch.int64), P.view(torch.int64))
+    rb, rt = _argmin_ref(torch, P, S)
+    assert torch.equal(best.to(torch.int64), rb) and torch.equal(best2.to(torch.int64), rb)
+    assert torch.equal(bt.view(torch.int64), rt.view(torch.int64)) and torch.equal(bt2.view(torch.int64), rt.view(torch.int64))
+    assert int((rb == -1).sum()) > 0 and int((rb >= 0).sum()) > 0
+
+
+@pytest.mark.gpu
+def test_argmin_ties_go_to_the_lowest_index():
+    import torch
+    p = kc.load_program("matmul_tiled_g16x16")
+    q = kc.load_program("matmul_naive_g16x16")
+    w = _weights()
+    n = 148 * 1024 * 2
+    dev = {k: torch.from_numpy(v).cuda() for k, v in _bindings(n, 2, scale=16).items()}
+    best, bt = kc.argmin([q, p, p, q], w, dev)
+    want = kc.predict(w, p, dev)
+    wq = kc.predict(w, q, dev)
+    ok = ~torch.isnan(want)
+    exp = torch.where(wq <= want, torch.zeros_like(best), torch.ones_like(best))
+    assert torch.equal(best[ok & (wq == wq)], exp[ok & (wq == wq)].to(best.dtype))
