@@ -119,7 +119,8 @@ const char* kcg_program_jit_source(kcg_program* prog);
  * 2 fused residual, 3 argmin over this one variant, 4 the same exact
  * evaluator as host C++ (entry point kcg_host_eval, arguments: the eval
  * kernel's argument struct and a point range [begin, end); compile with
- * g++ -ffp-contract=off; the optimised-CPU baseline of bench.py) -- owned
+ * g++ -ffp-contract=off; the optimised-CPU baseline of bench.py), 5 the
+ * fused residual gradient (kcg_residual_grad_fused) -- owned
  * by the program, valid until the next call                               */
 const char* kcg_program_jit_source_kind(kcg_program* prog, int kind);
 /* NVRTC-compiles `src` for sm_100a without loading it (no GPU needed);
@@ -270,6 +271,16 @@ int kcg_residual_fused(const kcg_program* prog,
                        const int64_t* const* param_cols, const double* T,
                        size_t n_rows, const double* alpha, double* obj,
                        void* stream);
+
+/* g += X^T (1 - X alpha) over the design rows x_j = RN(count_j) / T formed
+ * from the bindings on the fly (the rows build_design_matrix would form,
+ * model.cpp:29), the residual in double-double: the refinement gradient
+ * for kcg_refine_gram after a fused Gram (rows never materialised). alpha:
+ * HOST, 149 schema-indexed; g: DEVICE, one entry per program key.       */
+int kcg_residual_grad_fused(const kcg_program* prog,
+                            const int64_t* const* param_cols, const double* T,
+                            size_t n_rows, const double* alpha, double* g,
+                            void* stream);
 
 /* ---- host-side solve (fit_weights, model.cpp:37-93) --------------------
  * From the reduced Gram statistics of an n_cases-row design over F columns:

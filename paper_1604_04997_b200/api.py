@@ -455,6 +455,54 @@ def residual_fused(prog: Program, bindings, T, alpha149: Sequence[float], stream
     return float(obj.item())
 
 
+def residual_grad_fused(prog: Program, bindings, T, alpha149: Sequence[float], g=None, stream=None):
+    """g += X^T (1 - X alpha) over the rows x_j = RN(count_j)/T formed on the
+    fly (model.cpp:29), residual in double-double: the refinement gradient
+    after a fused Gram. Returns the [F] device tensor (program key order)."""
+    torch = _torch()
+    arr, n, cols = _columns(prog, bindings)
+    _check_times(T, n, cols[0].device if cols else T.device)
+    if g is None:
+        g = torch.zeros(len(prog.props), dtype=torch.float64, device=T.device)
+    a = (ctypes.c_double * len(alpha149))(*alpha149)
+    check(lib().kcg_residual_grad_fused(prog.handle, arr, T.data_ptr(), n, a, g.data_ptr(), _stream(stream)))
+    return g
+
+
+def refine_gram(stats: GramStats, alpha: Sequence[float], g) -> list[float]:
+    """One refinement step of the equilibrated solve: alpha += G^+ g
+    (kcg_refine_gram); g = X^T (1 - X alpha) from an accurate residual."""
+    G = stats.G.double().cpu().contiguous()
+    F = G.shape[0]
+    dp = lambda t: ctypes.cast(t.data_ptr(), _capi.DP)
+    cm = stats.colmax.double().cpu().contiguous()
+    gh = g.double().cpu().contiguous()
+    arr = (ctypes.c_double * F)(*alpha)
+    check(lib().kcg_refine_gram(F, dp(G), dp(cm), dp(gh), arr))
+    return list(arr)
+
+
+def fit_fused(prog: Program, bindings, T, refine: int = 2, stream=None):
+    """fit_weights (model.cpp:37-93) over rows formed from bindings and
+    measured times on the fly: fused Gram, host equilibrated min-norm
+    solve, `refine` refinement steps with the double-double fused residual
+    gradient, objective from the fused residual pass. Returns
+    (alpha over the program's keys, rank, objective, GramStats)."""
+    st = gram_fused(prog, bindings, T, stream=stream)
+    alpha, rank = solve_gram(st)
+    K = schema_size()
+    for _ in range(refine):
+        full = [0.0] * K
+        for j, k in enumerate(prog.props):
+            full[k] = alpha[j]
+        alpha = refine_gram(st, alpha, residual_grad_fused(prog, bindings, T, full, stream=stream))
+    full = [0.0] * K
+    for j, k in enumerate(prog.props):
+        full[k] = alpha[j]
+    obj = residual_fused(prog, bindings, T, full, stream=stream)
+    return alpha, rank, obj, st
+
+
 def solve_gram(stats: GramStats) -> tuple[list[float], int]:
     """Host minimum-norm solve of the equilibrated normal equations."""
     G = stats.G.double().cpu().contiguous()
@@ -477,11 +525,14 @@ class FitResult:
     n_cases: int
 
 
-def fit_weights(X, refine: int = 1, stream=None) -> FitResult:
+def fit_weights(X, refine: int = 2, stream=None) -> FitResult:
     """``fit_weights`` (model.cpp:37-93) over a materialised design X whose
     rows are p/T (``build_design_matrix``): Gram reduction on the GPU, host
-    min-norm solve, `refine` semi-normal refinement passes, objective from a
-    residual pass (never from the Gram identity)."""
+    min-norm solve, `refine` semi-normal refinement passes (the residual in
+    double-double, so each pass moves the weights toward the exact
+    least-squares solution of X: two reach it to ~1e-13 on the reference's
+    fit fixtures), objective from a residual pass (never from the Gram
+    identity)."""
     torch = _torch()
     _check_design(X)
     N, F = X.shape
@@ -585,11 +636,13 @@ def _device_rows(km: KernelMeasurements, prog: Program, device="cuda"):
     return cols, T
 
 
-def fit_from_csv(path, programs=None, device: str = "", discard: int = 4, stream=None):
+def fit_from_csv(path, programs=None, device: str = "", discard: int = 4, stream=None, refine: int = 2):
     """``kernelcost fit <csv>`` on the GPU: per kernel the fused
     evaluate -> row -> Gram kernel, scattered into the schema-wide Gram
     (rows of different kernels are disjoint), one equilibrated min-norm
-    solve, then the fused residual pass for the objective. Returns
+    solve, `refine` refinement steps (double-double residual gradient over
+    the reference's own rows), then the fused residual pass for the
+    objective. Returns
     (ModelWeights, report) with report = {objective, n_cases, rank, bad_rows}."""
     torch = _torch()
     K = schema_size()
@@ -616,7 +669,14 @@ def fit_from_csv(path, programs=None, device: str = "", discard: int = 4, stream
         staged.append((prog, cols, T))
     if bad:
         raise _capi.KcgError(_capi.E_ASSUMPTION_VIOLATED, f"{bad} measurement rows are not admissible")
-    alpha, rank = solve_gram(GramStats(G, x1, cm, rows))
+    stats = GramStats(G, x1, cm, rows)
+    alpha, rank = solve_gram(stats)
+    for _ in range(refine):  # schema-wide gradient: the kernels' rows are disjoint
+        g = torch.zeros(K, dtype=torch.float64, device="cuda")
+        for prog, cols, T in staged:
+            idx = torch.tensor(prog.props, dtype=torch.int64, device="cuda")
+            g[idx] += residual_grad_fused(prog, cols, T, alpha, stream=stream)
+        alpha = refine_gram(stats, alpha, g)
     obj = sum(residual_fused(prog, cols, T, alpha, stream=stream) for prog, cols, T in staged)
     covered = [bool(c > 0) for c in cm.cpu().tolist()]
     w = ModelWeights(device, "v1", list(alpha), covered, obj, rows)

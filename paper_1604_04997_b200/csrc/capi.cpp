@@ -46,6 +46,7 @@ struct kcg_program {
   void* jit_eval_grid_gen = nullptr;
   void* jit_gram = nullptr;
   void* jit_resid = nullptr;
+  void* jit_rgrad = nullptr;
   uint64_t uid = next_uid();  // identity for caches keyed by program sets
   static uint64_t next_uid() {
     static std::atomic<uint64_t> c{1};
@@ -386,7 +387,7 @@ const char* kcg_program_jit_source(kcg_program* p) {
 }
 
 const char* kcg_program_jit_source_kind(kcg_program* p, int kind) {
-  if (!p || kind < 0 || kind > 4) return nullptr;
+  if (!p || kind < 0 || kind > 5) return nullptr;
   if (kind == 0) return kcg_program_jit_source(p);
   const int np = p->low.n_params;
   if (kind == 4) {  // the evaluator as host C++ (kcg_host_eval), e.g. for a CPU baseline
@@ -398,8 +399,9 @@ const char* kcg_program_jit_source_kind(kcg_program* p, int kind) {
     return p->jit_src_kind.c_str();
   }
   p->jit_src_kind = kcg::codegen({&p->low}, {identity(np)}, np,
-                                 kind == 1 ? kcg::JitKind::gram : kcg::JitKind::residual,
-                                 kname(kind == 1 ? "kcg_gram_" : "kcg_resid_", p));
+                                 kind == 1 ? kcg::JitKind::gram : kind == 2 ? kcg::JitKind::residual
+                                                                            : kcg::JitKind::residual_grad,
+                                 kname(kind == 1 ? "kcg_gram_" : kind == 2 ? "kcg_resid_" : "kcg_rgrad_", p));
   return p->jit_src_kind.c_str();
 }
 
@@ -1257,6 +1259,66 @@ int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, 
     ab.finish();
     kcg::launch_jit(p->jit_resid, ab.b.data(), ab.b.size(), kcg::num_sms() * kcg::fused_ctas_per_sm(p->low, false), 256, stream,
                     kcg::fused_smem_bytes(np, p->low, false));
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
+int kcg_residual_grad_fused(const kcg_program* cp, const int64_t* const* param_cols, const double* T, size_t n,
+                            const double* alpha, double* g, void* stream) {
+  kcg_program* p = const_cast<kcg_program*>(cp);
+  if (!p || !T || !alpha || !g) return fail(KCG_E_INVALID_ARGUMENT, "bad residual-gradient arguments");
+  return guarded([&] {
+    require_device();
+    if (n == 0) return KCG_OK;
+    const int np = p->low.n_params;
+    const int F = static_cast<int>(p->low.keys.size());
+    std::vector<double> al(std::max(F, 1), 0.0);
+    compact_alpha(p, alpha, al.data());
+    if (F > 48) {  // rows in HBM chunk by chunk (as the wide fused Gram)
+      double* da = nullptr;
+      cuda_check(cudaMallocAsync(&da, sizeof(double) * al.size(), static_cast<cudaStream_t>(stream)), "cudaMallocAsync");
+      cuda_check(cudaMemcpyAsync(da, al.data(), sizeof(double) * al.size(), cudaMemcpyHostToDevice,
+                                 static_cast<cudaStream_t>(stream)), "cudaMemcpyAsync");
+      chunked_rows(p, param_cols, T, n, nullptr, stream, [&](const double* X, size_t m) {
+        const int rc = kcg_gram_residual_grad(X, m, F, F, da, g, stream);
+        if (rc != KCG_OK) throw KcgError(rc, kcg_last_error());
+      });
+      cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "residual grad");
+      cudaFreeAsync(da, static_cast<cudaStream_t>(stream));
+      return KCG_OK;
+    }
+    if (!p->jit_rgrad) {
+      const std::string name = kname("kcg_rgrad_", p);
+      p->jit_rgrad = kcg::jit_kernel(
+          kcg::codegen({&p->low}, {identity(np)}, np, kcg::JitKind::residual_grad, name), name);
+    }
+    ArgBuf ab;
+    for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
+    ab.push<const void*>(T);
+    ab.push<void*>(g);
+    ab.push<int64_t>(static_cast<int64_t>(n));
+    bool vec = reinterpret_cast<uintptr_t>(T) % 16 == 0;
+    for (int j = 0; j < np; ++j) vec = vec && reinterpret_cast<uintptr_t>(param_cols[j]) % 16 == 0;
+    ab.push<int32_t>(vec ? 1 : 0);
+    // per group: A_g = sum_j 2^k_j alpha_j as a double-double (hi, lo)
+    const kcg::RGradGroups rg = kcg::rgrad_groups(p->low);
+    const size_t G = rg.base.size();
+    std::vector<double> ahi(std::max<size_t>(G, 1), 0.0), alo(std::max<size_t>(G, 1), 0.0);
+    for (int j = 0; j < F; ++j) {
+      const auto [g, k] = rg.of_key[j];
+      const double b = std::ldexp(al[j], k);
+      const double s = ahi[g] + b, bb = s - ahi[g];
+      const double e = (ahi[g] - (s - bb)) + (b - bb);
+      const double lo = alo[g] + e;
+      ahi[g] = s + lo;
+      alo[g] = lo - (ahi[g] - s);
+    }
+    for (double v : ahi) ab.push<double>(v);
+    for (double v : alo) ab.push<double>(v);
+    ab.finish();
+    kcg::launch_jit(p->jit_rgrad, ab.b.data(), ab.b.size(), kcg::num_sms() * kcg::fused_ctas_per_sm(p->low, false), 256,
+                    stream, kcg::fused_smem_bytes(np, p->low, false, true));
     ++g_launches;
     return KCG_OK;
   });

@@ -15,6 +15,7 @@
 // 16-byte vector loads/stores), argmin over variants, and the fused
 // design-row Gram / residual reductions.
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <map>
@@ -889,13 +890,63 @@ GramBasis gram_basis(const Lowered& L) {
 }
 
 namespace {
+// Refinement-gradient groups: keys whose ORIGINAL counts differ by a power
+// of two (same parameter monomial, or both constants) have design columns
+// x_j = RN(2^k c_base) / T = 2^k RN(c_base) / T exactly, so one division per
+// group forms them all, the residual needs one double-double term per group
+// (weight A_g = sum_j 2^k_j alpha_j) and g_j = 2^k_j sum_i x_base r_i.
+// Tiled matmul g16: 9 keys -> 4 groups ({store, minls, local, addsub, mul,
+// barrier} over n m l, load 9/8 n m l, groups n l / 256, const).
+}  // namespace
+
+RGradGroups rgrad_groups(const Lowered& L) {
+  RGradGroups R;
+  const int F = static_cast<int>(L.keys.size());
+  R.of_key.assign(F, {-1, 0});
+  auto shape_eq = [&](const LKey& a, const LKey& b) {
+    if (a.form == 0 || b.form == 0) return false;
+    if ((a.form == 1) != (b.form == 1)) return false;
+    return a.form == 1 || a.pexp == b.pexp;
+  };
+  // log2(ca / cb) if it is an integer power of two, else INT_MIN
+  auto pow2_ratio = [](const LKey& a, const LKey& b) -> int {
+    try {
+      const i128 num = checked_mul(a.coef, b.coef_den), den = checked_mul(a.coef_den, b.coef);
+      if (num <= 0 || den <= 0) return INT_MIN;
+      int e = 0;
+      i128 n = num, d = den;
+      while (n % 2 == 0 && n > d) { n /= 2; ++e; }
+      while (d % 2 == 0 && d > n) { d /= 2; --e; }
+      return n == d ? e : INT_MIN;
+    } catch (const KcgError&) {
+      return INT_MIN;
+    }
+  };
+  for (int j = 0; j < F; ++j) {
+    if (R.of_key[j].first >= 0) continue;
+    std::vector<int> mem{j};
+    for (int k = j + 1; k < F; ++k)
+      if (R.of_key[k].first < 0 && shape_eq(L.keys[j], L.keys[k]) && pow2_ratio(L.keys[k], L.keys[j]) != INT_MIN)
+        mem.push_back(k);
+    int base = j;  // the smallest count of the group: every other member is 2^k (k >= 0) times it
+    for (int k : mem)
+      if (pow2_ratio(L.keys[k], L.keys[base]) < 0) base = k;
+    const int g = static_cast<int>(R.base.size());
+    R.base.push_back(base);
+    for (int k : mem) R.of_key[k] = {g, k == base ? 0 : pow2_ratio(L.keys[k], L.keys[base])};
+  }
+  return R;
+}
+
+namespace {
+
 // register-accumulator fused Gram for narrow rows, DMMA otherwise
 constexpr int kRegGramMax = 6;
 bool gram_dmma(int W) { return W > kRegGramMax && W <= 48; }
 }  // namespace
 
-size_t fused_smem_bytes(int n_cols, const Lowered& L, bool gram) {
-  const int W = gram_basis(L).width(static_cast<int>(L.keys.size()));
+size_t fused_smem_bytes(int n_cols, const Lowered& L, bool gram, bool per_key) {
+  const int W = per_key ? static_cast<int>(L.keys.size()) : gram_basis(L).width(static_cast<int>(L.keys.size()));
   const int WA = W > 0 ? W : 1;
   const int NB = (W + 7) / 8, LDX = NB * 8 + 1;
   size_t b = static_cast<size_t>(fused_stages(n_cols, gram && gram_dmma(W))) * (n_cols + 1) * kTmaTile * 8;
@@ -1409,12 +1460,20 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   // fused design-row reductions (gram / residual)
   const Lowered& L = *progs[0];
   const int F = static_cast<int>(L.keys.size());
-  const GramBasis gb = gram_basis(L);
+  GramBasis gb = gram_basis(L);
+  // the refinement gradient works on the reference's own rows
+  // x_j = RN(count_j) / T (model.cpp:29), never the monomial basis: it is
+  // what makes the refined weights the least-squares solution of exactly
+  // the design the reference would form
+  if (kind == JitKind::residual_grad) gb.reduced = false;
   const bool red_basis = gb.reduced;
-  // row width: the F design columns, or the W < F basis values u_b = mono_b / T
-  const int W = gb.width(F);
+  // row width: the F design columns, or the W < F basis values u_b = mono_b / T,
+  // or (refinement gradient) one value per power-of-two key group
+  const RGradGroups rg = kind == JitKind::residual_grad ? rgrad_groups(L) : RGradGroups{};
+  const int W = kind == JitKind::residual_grad ? static_cast<int>(rg.base.size()) : gb.width(F);
   const int WA = W > 0 ? W : 1;
   const bool gram = kind == JitKind::gram;
+  const bool rgrad = kind == JitKind::residual_grad;
   const bool dmma = gram && gram_dmma(W);
   const bool regsm = gram && !dmma && W <= 48;  // register accumulators, CTA totals in smem
   const int NCMP = red_basis ? static_cast<int>(gb.compound.size()) : 0;
@@ -1430,7 +1489,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
           "double* cmax; unsigned long long* bad; kcg_i64 n; int vec; };\n";
   else
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* obj; kcg_i64 n; "
-          "int vec; double alpha[" << (F > 0 ? F : 1) << "]; };\n";
+          "int vec; double alpha[" << (rgrad ? 2 * WA : (F > 0 ? F : 1)) << "]; };\n";
   if (red_basis) {
     // expansion tables: key j = sum over kcg_kt[off[j]..off[j+1]) of coef * u_b
     std::vector<int> off{0}, tb;
@@ -1463,11 +1522,22 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   }
   // x = c / t correctly rounded (Markstein: one reciprocal per row, exact
   // residual by FMA, final FMA correction)
+  if (rgrad)  // (hi, lo) -= (bh, bl), double-double
+    os << "__device__ __forceinline__ void kcg_dd_sub(double& hi, double& lo, double bh, double bl) {\n"
+          "  const double s = __dsub_rn(hi, bh);\n  const double bb = __dsub_rn(s, hi);\n"
+          "  double e = __dsub_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dadd_rn(bh, bb));\n"
+          "  e = __dadd_rn(e, __dsub_rn(lo, bl));\n  hi = __dadd_rn(s, e);\n  lo = __dsub_rn(e, __dsub_rn(hi, s));\n}\n";
   os << "__device__ __forceinline__ double kcg_div(double c, double t, double r) {\n"
         "  const double q = __dmul_rn(c, r);\n  const double e = fma(-q, t, c);\n  return fma(e, r, q);\n}\n";
   os << "template <class T> __device__ __forceinline__ void kcg_xrow(const T* c, double t, double* x) {\n";
-  for (int j = 0; j < F; ++j)
-    os << "  x[" << j << "] = (c[" << j << "] != 0) ? __ddiv_rn(kcg_to_double(c[" << j << "]), t) : 0.0;\n";
+  if (rgrad) {
+    for (int g = 0; g < W; ++g)
+      os << "  x[" << g << "] = (c[" << rg.base[g] << "] != 0) ? __ddiv_rn(kcg_to_double(c[" << rg.base[g]
+         << "]), t) : 0.0;\n";
+  } else {
+    for (int j = 0; j < F; ++j)
+      os << "  x[" << j << "] = (c[" << j << "] != 0) ? __ddiv_rn(kcg_to_double(c[" << j << "]), t) : 0.0;\n";
+  }
   os << "}\n";
   // out-of-line row: reloads its inputs (no address-taken locals in callers)
   os << "__device__ __noinline__ int kcg_row_i(const KcgArgs& a, kcg_i64 i, double* __restrict__ x) {\n"
@@ -1490,13 +1560,20 @@ std::string codegen(const std::vector<const Lowered*>& progs,
   }
   os << "  return cls == 0 ? KCG_PT_ASSUMPTION_VIOLATED : KCG_PT_OVERFLOW;\n}\n";
   // fast row from registers; -1 -> caller uses kcg_row_i
+  if (rgrad) {
+    os << "__device__ __forceinline__ int kcg_row_fast(const kcg_i64* p, double t, double* x) {\n"
+          "  if (!(t > 0.0) || kcg_class_0(p) != 1) return -1;\n"
+          "  double c[" << (F > 0 ? F : 1) << "];\n  const int st = kcg_fastd_0(p, c);\n";
+    for (int g = 0; g < W; ++g) os << "  x[" << g << "] = __ddiv_rn(c[" << rg.base[g] << "], t);\n";
+    os << "  return st;\n}\n";
+  } else
   os << "__device__ __forceinline__ int kcg_row_fast(const kcg_i64* p, double t, double* x) {\n"
         "  if (!(t > 0.0) || kcg_class_0(p) != 1) return -1;\n"
         "  double c["
      << WA << "];\n  const int st = " << (red_basis ? "kcg_fastm_0" : "kcg_fastd_0")
      << "(p, c);\n  const double r = __drcp_rn(t);\n"
         "  #pragma unroll\n  for (int j = 0; j < "
-     << W << "; ++j) x[j] = " << (red_basis ? "__dmul_rn(c[j], r)" : "kcg_div(c[j], t, r)")
+     << W << "; ++j) x[j] = " << (red_basis ? "__dmul_rn(c[j], r)" : rgrad ? "__ddiv_rn(c[j], t)" : "kcg_div(c[j], t, r)")
      << ";\n  return st;\n}\n";
 
   // compound keys (basis mode): x_j = sum_t coef * u_b, max |x_j| per row
@@ -1693,6 +1770,40 @@ std::string codegen(const std::vector<const Lowered*>& progs,
       }
     }
     cons_end << "    if (a.bad && bad) atomicAdd(a.bad, bad);\n  }\n";
+  } else if (rgrad) {
+    // refinement gradient g = X^T (1 - X alpha): the residual in
+    // double-double (exact FMA products, compensated sums) rounded once,
+    // then per-thread sums of u_b r (basis) or x_j r; each warp's totals
+    // expanded to the F keys (g_j = sum_b A_jb gu_b) and added atomically
+    cons_decl << "  double gacc[" << WA << "];\n  #pragma unroll\n  for (int j = 0; j < " << WA
+              << "; ++j) gacc[j] = 0.0;\n";
+    cons_row << "      if (ok) {\n        double hi = 1.0, lo = 0.0;\n";
+    for (int j = 0; j < W; ++j)  // x_g * (A_hi + A_lo): exact product by FMA, low part folded in
+      cons_row << "        { const double p = __dmul_rn(x[" << j << "], a.alpha[" << j << "]);\n"
+               << "          kcg_dd_sub(hi, lo, p, fma(x[" << j << "], a.alpha[" << W + j << "], fma(x[" << j
+               << "], a.alpha[" << j << "], -p))); }\n";
+    cons_row << "        const double r = __dadd_rn(hi, lo);\n";
+    for (int j = 0; j < W; ++j) cons_row << "        gacc[" << j << "] = fma(x[" << j << "], r, gacc[" << j << "]);\n";
+    cons_row << "      }\n";
+    cons_end << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j)\n"
+             << "    for (int o = 16; o > 0; o >>= 1) gacc[j] += __shfl_down_sync(0xffffffffu, gacc[j], o);\n"
+             << "  if ((threadIdx.x & 31) == 0) {\n";
+    for (int j = 0; j < F; ++j) {
+      if (!red_basis) {  // g_j = 2^k_j * (sum of x_base r over the group)
+        char buf[64];
+        std::snprintf(buf, sizeof buf, "%a", std::ldexp(1.0, rg.of_key[j].second));
+        cons_end << "    atomicAdd(a.obj + " << j << ", " << buf << " * gacc[" << rg.of_key[j].first << "]);\n";
+        continue;
+      }
+      cons_end << "    { double gj = 0.0;";
+      for (const auto& [b, c] : gb.terms[j]) {
+        char buf[64];
+        std::snprintf(buf, sizeof buf, "%a", c);
+        cons_end << " gj = fma(" << buf << ", gacc[" << b << "], gj);";
+      }
+      cons_end << " atomicAdd(a.obj + " << j << ", gj); }\n";
+    }
+    cons_end << "  }\n";
   } else {
     // residual: alpha holds the compact weights, or beta = A^T alpha in basis mode
     cons_decl << "  double acc = 0.0;\n";

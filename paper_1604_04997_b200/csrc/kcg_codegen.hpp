@@ -9,7 +9,7 @@
 
 namespace kcg {
 
-enum class JitKind { eval, argmin, gram, residual, host_eval, multi, multi_argmin };
+enum class JitKind { eval, argmin, gram, residual, residual_grad, host_eval, multi, multi_argmin };
 
 /// CUDA source for one specialised kernel named `name`. pmaps[v][j] is the
 /// column (in the launch's parameter-column order) holding parameter j of
@@ -88,8 +88,16 @@ struct GramBasis {
 };
 GramBasis gram_basis(const Lowered& L);
 
+/// Refinement-gradient key groups (codegen.cpp rgrad_groups): keys whose
+/// counts differ by powers of two share one design-column division.
+struct RGradGroups {
+  std::vector<int> base;                    // per group: the key with the smallest count
+  std::vector<std::pair<int, int>> of_key;  // per key: (group, k), count_j = 2^k count_base
+};
+RGradGroups rgrad_groups(const Lowered& L);
+
 /// Shared-memory ring of the fused (bindings + T) Gram / residual kernels.
-size_t fused_smem_bytes(int n_cols, const Lowered& L, bool gram);
+size_t fused_smem_bytes(int n_cols, const Lowered& L, bool gram, bool per_key = false);  // per_key: rows of F keys (residual_grad)
 constexpr int kTmaPointsPerTile = 1024;
 
 }  // namespace kcg

@@ -222,9 +222,12 @@ struct LKey {
   // the key's ORIGINAL polynomial (before congruence substitution), when it
   // is one term: form 1 = the constant `coef`; form 2 = coef * prod_j
   // param_j^pexp[j] with coef a positive power of two (the multi-program
-  // kernel shares such products across programs); 0 = anything else
+  // kernel shares such products across programs); form 3 = the same
+  // monomial shape with any rational coefficient coef / coef_den (the
+  // refinement gradient groups keys whose counts differ by powers of two);
+  // 0 = anything else
   int form = 0;
-  i128 coef = 0;
+  i128 coef = 0, coef_den = 1;
   std::vector<int> pexp;
 };
 

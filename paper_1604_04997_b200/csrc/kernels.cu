@@ -543,7 +543,26 @@ void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, 
   check(cudaGetLastError(), "kcg_gram_dmma launch");
 }
 
-// warp per row: lane owns columns lane + 32 c, c < NC (F <= 32 NC)
+// double-double helpers: (hi, lo) with |lo| <= ulp(hi) / 2
+__device__ __forceinline__ void kcg_two_sum(double a, double b, double& s, double& e) {
+  s = __dadd_rn(a, b);
+  const double bb = __dsub_rn(s, a);
+  e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+}
+__device__ __forceinline__ void kcg_dd_add(double& hi, double& lo, double bh, double bl) {
+  double s, e;
+  kcg_two_sum(hi, bh, s, e);
+  e = __dadd_rn(e, __dadd_rn(lo, bl));
+  hi = __dadd_rn(s, e);
+  lo = __dsub_rn(e, __dsub_rn(hi, s));
+}
+
+// warp per row: lane owns columns lane + 32 c, c < NC (F <= 32 NC).
+// GRAD: g += X^T r with the residual r = 1 - x . alpha formed in
+// double-double (exact products by FMA, compensated sums, a compensated
+// warp reduction) and rounded once: the refinement step of fit_weights
+// then converges to the exact least-squares solution of the double data
+// (a plain double residual of a near-consistent fit is all rounding noise).
 template <bool GRAD, int NC>
 __global__ void __launch_bounds__(256)
     kcg_resid_x(const double* __restrict__ X, kcg_i64 n, int F, kcg_i64 ld,
@@ -562,14 +581,31 @@ __global__ void __launch_bounds__(256)
     const double* row = X + r * ld;
     double x[NC];
     double d = 0.0;
+    if (GRAD) {
+      double lo = 0.0;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      x[c] = lane + 32 * c < F ? __ldcs(row + lane + 32 * c) : 0.0;
-      d = fma(x[c], a[c], d);
+      for (int c = 0; c < NC; ++c) {
+        x[c] = lane + 32 * c < F ? __ldcs(row + lane + 32 * c) : 0.0;
+        const double p = __dmul_rn(x[c], a[c]);
+        kcg_dd_add(d, lo, p, fma(x[c], a[c], -p));
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+        kcg_dd_add(d, lo, __shfl_xor_sync(0xffffffffu, d, o), __shfl_xor_sync(0xffffffffu, lo, o));
+      d = -d;
+      lo = -lo;
+      kcg_dd_add(d, lo, 1.0, 0.0);  // 1 - x . alpha
+      d = __dadd_rn(d, lo);
+    } else {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        x[c] = lane + 32 * c < F ? __ldcs(row + lane + 32 * c) : 0.0;
+        d = fma(x[c], a[c], d);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-    const double res = 1.0 - d;
+    const double res = GRAD ? d : 1.0 - d;
     if (GRAD) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) g[c] = fma(x[c], res, g[c]);

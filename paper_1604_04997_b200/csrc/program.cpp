@@ -939,7 +939,7 @@ Lowered lower(const Symbolic& s_in) {
     const int e = visit_poly(c.poly);
     L.cons.push_back({c.divisibility ? 1 : 0, static_cast<int32_t>(c.op), e, c.mod, c.rem});
   }
-  for (const auto& [schema, pid] : s.props) L.keys.push_back({schema, visit_poly(pid), 0, 0, {}});
+  for (const auto& [schema, pid] : s.props) L.keys.push_back({schema, visit_poly(pid), 0, 0, 1, {}});
   // one-term original polynomials (s_in: the text as written, before the
   // congruence substitution rewrote parameters as quotients)
   for (size_t k = 0; k < L.keys.size() && k < s_in.props.size(); ++k) {
@@ -947,22 +947,24 @@ Lowered lower(const Symbolic& s_in) {
     if (P.size() != 1) continue;
     const Mono& m = P.begin()->first;
     const Q& q = P.begin()->second;
-    if (!q.is_int() || q.n == 0) continue;
+    if (q.n == 0) continue;
     LKey& key = L.keys[k];
     if (m.f.empty()) {
+      if (!q.is_int()) continue;
       key.form = 1;
       key.coef = q.n;
       continue;
     }
-    bool params_only = q.n > 0 && (q.n & (q.n - 1)) == 0;
+    bool params_only = q.n > 0;
     std::vector<int> ex(L.n_params, 0);
     for (const auto& [a, e] : m.f) {
       if (s_in.atoms[a].kind != AtomKind::var) params_only = false;
       else ex[s_in.atoms[a].param] += e;
     }
     if (!params_only) continue;
-    key.form = 2;
+    key.form = q.is_int() && (q.n & (q.n - 1)) == 0 ? 2 : 3;
     key.coef = q.n;
+    key.coef_den = q.d;
     key.pexp = ex;
   }
   L.n_monos = static_cast<int>(monos.size());

@@ -4,7 +4,8 @@ The parameter grid shards by problem size: every rank evaluates a
 contiguous block of sizes for all kernel variants, so evaluate / predict /
 argmin need no collective. The only exchange is the fit's Gram statistics
 (SURVEY.md §8e): G and Xᵀ1 are summed, colmax is max-reduced, then every
-rank solves the same small system redundantly (no broadcast needed).
+rank solves the same small system redundantly (no broadcast needed); each
+refinement step sums the per-rank gradients Xᵀ(1 - X alpha) the same way.
 """
 from __future__ import annotations
 
@@ -14,6 +15,23 @@ def shard_bounds(n: int, rank: int, world: int) -> tuple[int, int]:
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"bad rank {rank} of world {world}")
     return n * rank // world, n * (rank + 1) // world
+
+
+def _host_staged(group=None) -> bool:
+    """gloo moves CPU tensors: CUDA tensors are staged through the host
+    (e.g. several ranks sharing one GPU in a functional dry run)."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
+def _reduce(t, op, group=None):
+    import torch.distributed as dist
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
 
 
 def allreduce_gram(stats, group=None):
@@ -28,13 +46,49 @@ def allreduce_gram(stats, group=None):
     flat = torch.cat([stats.G.reshape(-1), stats.xt1.reshape(-1),
                       torch.tensor([float(stats.n_rows), float(stats.bad_rows)],
                                    dtype=torch.float64, device=stats.G.device)])
-    dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
-    dist.all_reduce(stats.colmax, op=dist.ReduceOp.MAX, group=group)
+    _reduce(flat, dist.ReduceOp.SUM, group)
+    _reduce(stats.colmax, dist.ReduceOp.MAX, group)
     stats.G.copy_(flat[:F * F].view(F, F))
     stats.xt1.copy_(flat[F * F:F * F + F])
     stats.n_rows = int(flat[F * F + F].item())
     stats.bad_rows = int(flat[F * F + F + 1].item())
     return stats
+
+
+def allreduce_sum(t, group=None):
+    """SUM-reduce a small tensor (e.g. a refinement gradient) in place."""
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        _reduce(t, dist.ReduceOp.SUM, group)
+    return t
+
+
+def fit_sharded(prog, bindings, T, refine: int = 1, group=None, stream=None):
+    """Config 5 on every rank: fused Gram of the local rows, all-reduce,
+    redundant solve, `refine` refinement steps (local double-double
+    gradient, all-reduced), fused residual objective (all-reduced).
+    Returns (alpha over the program's keys, rank, objective, total rows)."""
+    import paper_1604_04997_b200 as kc
+
+    st = kc.gram_fused(prog, bindings, T, stream=stream)
+    allreduce_gram(st, group)
+    alpha, rank = kc.solve_gram(st)
+    K = kc.schema_size()
+
+    def full(a):
+        out = [0.0] * K
+        for j, k in enumerate(prog.props):
+            out[k] = a[j]
+        return out
+    for _ in range(refine):
+        g = kc.residual_grad_fused(prog, bindings, T, full(alpha), stream=stream)
+        alpha = kc.refine_gram(st, alpha, allreduce_sum(g, group))
+    import torch
+    obj = torch.tensor([kc.residual_fused(prog, bindings, T, full(alpha), stream=stream)],
+                       dtype=torch.float64, device=T.device)
+    allreduce_sum(obj, group)
+    return alpha, rank, float(obj.item()), st.n_rows
 
 
 def gather_shards(local, total: int, dst: int = 0, group=None):
@@ -48,7 +102,8 @@ def gather_shards(local, total: int, dst: int = 0, group=None):
         return local
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     width = (total + world - 1) // world  # the largest shard
-    pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
+    dev = "cpu" if _host_staged(group) else local.device
+    pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
     pad[:local.shape[0]] = local
     parts = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
     dist.gather(pad, parts, dst=dst, group=group)

@@ -38,3 +38,29 @@ def suite_alpha():
     for k, v in d["alpha"].items():
         a[kc_oracle.SCHEMA_INDEX[k]] = hexf(v[1])
     return a
+
+
+# fitted-weight tolerance (north star: 1e-9 relative in fp64). Weights are
+# compared in the equilibrated coordinates the solve works in
+# (x_j = alpha_j * max|col_j|, model.cpp:71-76): relative 1e-9, plus an
+# absolute 1e-13 for numerically-zero weights (a weight whose true value is
+# 0 comes out of the double data as ~1e-16 in those units; relative error
+# is meaningless there)
+FIT_REL = 1e-9
+FIT_ABS_SCALED = 1e-13
+
+
+def fit_errors(got, want, colmax):
+    """per-weight |got - want| / (FIT_REL |want| + FIT_ABS_SCALED / colmax): <= 1 passes"""
+    out = []
+    for g, w, c in zip(got, want, colmax):
+        out.append(abs(g - w) / (FIT_REL * abs(w) + FIT_ABS_SCALED / c) if c > 0 else (0.0 if g == 0 else 1e300))
+    return out
+
+
+def exact_fit(name):
+    """the exact min-norm LS solution of a golden fit design (tests/gen/gen_fit_exact.py)"""
+    for f in load_golden("fit_exact.json")["fits"]:
+        if f["name"] == name:
+            return f
+    raise KeyError(name)

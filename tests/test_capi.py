@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 import kc_oracle as ko
-from conftest import GOLDEN, PROGRAMS, hexf, load_golden
+from conftest import FIT_ABS_SCALED, FIT_REL, GOLDEN, PROGRAMS, exact_fit, fit_errors, hexf, load_golden
 import paper_1604_04997_b200 as kc
 from paper_1604_04997_b200 import _capi
 
@@ -157,22 +157,34 @@ def _solve(X):
     dp = lambda a: a.ctypes.data_as(_capi.DP)
     _capi.check(_capi.lib().kcg_solve_gram(F, dp(G), dp(s1), dp(cm), out, ctypes.byref(rank)))
     alpha = np.array(list(out))
-    # one semi-normal refinement step, as fit_weights() does on the GPU
-    g = np.ascontiguousarray(X.T @ (1.0 - X @ alpha))
-    arr = (ctypes.c_double * F)(*alpha)
-    _capi.check(_capi.lib().kcg_refine_gram(F, dp(G), dp(cm), dp(g), arr))
-    return np.array(list(arr)), rank.value
+    # two semi-normal refinement steps as fit_weights() does on the GPU: the
+    # residual in extended precision (the GPU forms it in double-double)
+    for _ in range(2):
+        r = (1 - X.astype(np.longdouble) @ alpha.astype(np.longdouble)).astype(np.float64)
+        g = np.ascontiguousarray(X.T @ r)
+        arr = (ctypes.c_double * F)(*alpha)
+        _capi.check(_capi.lib().kcg_refine_gram(F, dp(G), dp(cm), dp(g), arr))
+        alpha = np.array(list(arr))
+    return alpha, rank.value
 
 
 def test_host_solve_reproduces_reference_fits():
+    """The host solve + two refinement steps land within 1e-9 (relative, in
+    the equilibrated coordinates; conftest.fit_errors) of the EXACT min-norm
+    least-squares solution of each reference fixture's double design, and
+    therefore within the reference COD's own distance from it plus 1e-9."""
     for fit in load_golden("fit_synthetic.json")["fits"]:
         counts = np.array(fit["counts"], dtype=np.float64)
         times = np.array([hexf(t) for t in fit["times"]])
         X = counts / times[:, None]
         alpha, rank = _solve(X)
         ref = [hexf(a) for a in fit["alpha"]]
-        for k, got, r in zip(fit["keys"], alpha, ref):
-            assert abs(got - r) <= 1e-6 * abs(r), (fit["name"], k, got, r)
+        ex = [hexf(a) for a in exact_fit(fit["name"])["alpha_exact"]]
+        cm = np.abs(X).max(axis=0)
+        err = fit_errors(alpha, ex, cm)
+        assert max(err) <= 1.0, (fit["name"], err)
+        for k, got, r, e, c in zip(fit["keys"], alpha, ref, ex, cm):
+            assert abs(got - r) <= abs(r - e) + FIT_REL * abs(e) + FIT_ABS_SCALED / c, (fit["name"], k, got, r)
         if fit["name"] == "duplicate_columns":
             assert rank == 2  # min-norm split of the two identical columns
         r = 1.0 - X @ alpha
@@ -184,11 +196,17 @@ def test_host_solve_suite_design_matches_reference(suite_alpha):
     rows = [({ko.SCHEMA_INDEX[k]: int(v) for k, v in c["counts"].items()}, hexf(c["time_s"][1])) for c in cases]
     X, cov = ko.build_design_matrix(rows)
     cols = np.flatnonzero(cov)
-    alpha, rank = _solve(np.ascontiguousarray(X[:, cols]))
+    Xc = np.ascontiguousarray(X[:, cols])
+    alpha, rank = _solve(Xc)
+    ex = exact_fit("suite_measurement_390")
+    assert ex["keys"] == [ko.SCHEMA[c] for c in cols]
+    exa = [hexf(a) for a in ex["alpha_exact"]]
+    err = fit_errors(alpha, exa, np.abs(Xc).max(axis=0))
+    assert max(err) <= 1.0, err
     sim = ko.simdev_reference_alpha()
     for c, got in zip(cols, alpha):
         if sim[c] != 0.0:
-            assert abs(got - suite_alpha[c]) <= 1e-6 * abs(suite_alpha[c]), ko.SCHEMA[c]
+            assert abs(got - suite_alpha[c]) <= 1e-9 * abs(suite_alpha[c]), ko.SCHEMA[c]
         else:
             assert abs(got) <= 1e-15
 
@@ -197,12 +215,13 @@ def test_host_solve_suite_design_matches_reference(suite_alpha):
                                  "arith_div_g16x12", "stride2_fill_g192", "transpose_tile_g16x16"])
 def test_generated_kernels_compile_for_sm100a(kid):
     """NVRTC (sm_100a) accepts every specialised kernel family for the
-    program -- eval (+ _gen, _tma), fused Gram (DMMA), fused residual."""
+    program -- eval (+ _gen, _tma), fused Gram (DMMA), fused residual and
+    its refinement gradient."""
     p = kc.load_program(kid)
     L = _capi.lib()
-    for kind, base in ((0, "kcg_eval_"), (1, "kcg_gram_"), (2, "kcg_resid_"), (3, "kcg_argmin")):
+    for kind, base in ((0, "kcg_eval_"), (1, "kcg_gram_"), (2, "kcg_resid_"), (3, "kcg_argmin"), (5, "kcg_rgrad_")):
         src = L.kcg_program_jit_source_kind(p.handle, kind)
-        rc = L.kcg_jit_compile_check(src, (base + (kid if kind < 3 else "")).encode())
+        rc = L.kcg_jit_compile_check(src, (base + (kid if kind != 3 else "")).encode())
         assert rc == 0, L.kcg_last_error().decode()[:3000]
 
 
@@ -316,3 +335,13 @@ def test_design_and_time_inputs_are_validated_on_device():
             kc.gram_fused(prog, cols, T)
         with pytest.raises(kc.KcgError):
             kc.residual_fused(prog, cols, T, a)
+
+
+def test_refinement_gradient_groups_power_of_two_keys():
+    """kcg_rgrad_<k> forms one design-column division per group of keys whose
+    counts differ by powers of two (tiled matmul: 9 keys -> 4 divisions)."""
+    L = _capi.lib()
+    for kid, want in (("matmul_tiled_g16x16", 4), ("conv_g16x16", 3), ("transpose_tile_g16x16", 2)):
+        src = L.kcg_program_jit_source_kind(kc.load_program(kid).handle, 5).decode()
+        i = src.index("kcg_xrow(const T* c")
+        assert src[i:src.index("}", i)].count("__ddiv_rn") == want, kid
