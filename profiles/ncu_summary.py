@@ -17,7 +17,11 @@ WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
         "sm__cycles_elapsed.avg.per_second", "lts__t_bytes.sum",
-        "launch__occupancy_limit_registers"]
+        "launch__occupancy_limit_registers",
+        # tensor pipes (the DMMA Gram): matched by suffix, ncu prefixes them with a section name
+        "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+        "smsp__pipe_tensor_subpipe_dmma_cycles_active.avg",
+        "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"]
 
 
 def run(rep, points=None):
@@ -28,8 +32,9 @@ def run(rep, points=None):
         name = r[rows[0].index("Kernel Name")]
         out.append(f"kernel: {name}")
         for w in WANT:
-            if w in rows[0]:
-                i = rows[0].index(w)
+            hits = [i for i, h in enumerate(rows[0]) if h == w or h.endswith("." + w)]
+            if hits:
+                i = hits[0]
                 out.append(f"  {w} = {r[i]} {rows[1][i]}")
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                          capture_output=True, text=True).stdout
