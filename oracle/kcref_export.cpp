@@ -25,6 +25,7 @@
 #include <tuple>
 
 #include "json.hpp"
+#include "kcref_extract.hpp"
 #include "kcref_program.hpp"
 #include "kernelcost/campaign.hpp"
 #include "kernelcost/csvio.hpp"
@@ -556,77 +557,50 @@ int main(int argc, char** argv) {
   // ---- fd_stencil / nbody made grid-evaluable ---------
   // Symbolic extraction throws E_NEEDS_BINDING for these two kernels only
   // because array_stat() computes a footprint before classifying
-  // (props.cpp:211-212): fd_stencil's accesses all have lane stride 0 or 1,
-  // where classify_ratio ignores cells/fill (classify.cpp:15-17), and nbody's
-  // stride-3 `pos` footprint is the union of contained boxes, class 3/3 at
-  // every n. Every count is therefore a polynomial in n on the admissible
-  // lattice. We take the reference's own bound-mode counts at the first
-  // lattice points, interpolate each key exactly (rational Lagrange, degree
-  // <= 4), and keep the program only if it reproduces bound-mode extraction
-  // at every further lattice point the 2e7 enumeration cap allows.
+  // (props.cpp:211-212). The front-end extension kcref_extract.hpp
+  // (extract_properties_grid) classifies stride-0/1 accesses without the
+  // footprint (classify.cpp:15-17, 31-32) and takes the contained-box union
+  // for nbody's pos; it equals extract_properties on the 59 kernels the
+  // reference extracts (kcref_grid). Its symbolic PV is kept only if it
+  // reproduces the reference's bound-mode extraction at every lattice point
+  // the 2e7 enumeration cap allows.
   {
     json derived = json::array();
     for (const auto& [id, unit, qmax] :
-         std::vector<std::tuple<std::string, long, long>>{{"fd_stencil_g16x16", 16, 60},
-                                                         {"nbody_g256", 256, 9}}) {
+         std::vector<std::tuple<std::string, long, long>>{{"fd_stencil_g16x16", 16, 160},
+                                                         {"nbody_g256", 256, 16}}) {
       const kc::KernelIR& k = irs.at(id);
-      std::vector<kc::Int> ns;
-      std::vector<kc::PropertyVector> pvs;
-      for (long q = 1; q <= qmax; ++q) {
-        const kc::Binding b{{"n", kc::Int(unit * q)}};
-        try {
-          pvs.push_back(kc::extract_properties(k, b, kCap));
-          ns.push_back(kc::Int(unit * q));
-        } catch (const kc::Error&) {
-          break;
-        }
-      }
-      const int npts = 5;  // degree <= 4
-      json entry{{"id", id}, {"lattice_points", ns.size()}};
-      if (static_cast<int>(ns.size()) < npts + 3) {
-        entry["error"] = "not enough enumerable lattice points";
-        derived.push_back(entry);
-        continue;
-      }
-      kc::PropertyVector sym;
-      const kc::CountExpr n = kc::CountExpr::var("n");
-      for (size_t key = 0; key < kc::schema_size(); ++key) {
-        kc::CountExpr poly;
-        for (int i = 0; i < npts; ++i) {
-          const kc::Rat yi = pvs[i].entries[key].evaluate_rat({});
-          if (yi == 0) continue;
-          kc::CountExpr basis = kc::CountExpr::from_int(1);
-          kc::Rat den(1);
-          for (int j = 0; j < npts; ++j) {
-            if (j == i) continue;
-            basis = basis * (n - kc::CountExpr::from_int(ns[j]));
-            den *= kc::Rat(ns[i] - ns[j]);
-          }
-          poly = poly + basis.scaled(yi / den);
-        }
-        sym.entries[key] = poly;
-      }
+      const kc::PropertyVector sym = kcref::extract_properties_grid(k);
+      long checked = 0;
+      kc::Int last(0);
       bool ok = true;
-      for (size_t i = 0; i < ns.size() && ok; ++i) {
-        const kc::Binding b{{"n", ns[i]}};
-        const kc::PropertyVector ev = kc::evaluate_properties(k, sym, b);
-        ok = ev.integers() == pvs[i].integers();
+      for (long q = 1; q <= qmax && ok; ++q) {
+        const kc::Binding b{{"n", kc::Int(unit * q)}};
+        kc::PropertyVector ref;
+        try {
+          ref = kc::extract_properties(k, b, kCap);
+        } catch (const kc::Error&) {
+          break;  // past the enumeration cap
+        }
+        ok = kc::evaluate_properties(k, sym, b).integers() == ref.integers();
+        ++checked;
+        last = kc::Int(unit * q);
       }
-      entry["verified_points"] = ok ? ns.size() : 0;
-      entry["max_verified_n"] = ns.back().str();
-      if (ok) {
+      json entry{{"id", id}, {"method", "symbolic: oracle/kcref_extract.hpp extract_properties_grid"},
+                 {"verified_points", ok ? checked : 0}, {"max_verified_n", last.str()}};
+      if (ok && checked > 0) {
         std::string text = kcref::program_text(k, sym);
         text.insert(text.find('\n') + 1,
-                    "# derived: exact interpolation of bound-mode extraction, verified on " +
-                        std::to_string(ns.size()) + " lattice points up to n=" + ns.back().str() + "\n");
+                    "# symbolic: front-end extension oracle/kcref_extract.hpp (stride-first classification, "
+                    "contained-box footprint); equal to bound-mode extraction on " +
+                        std::to_string(checked) + " lattice points up to n=" + last.str() + "\n");
         std::ofstream(pdir + "/" + id + ".kcp") << text;
         entry["file"] = id + ".kcp";
       } else {
-        entry["error"] = "interpolation does not reproduce bound-mode counts";
+        entry["error"] = "extension does not reproduce bound-mode counts";
       }
       derived.push_back(entry);
-      std::cerr << "derived " << id << ": " << (ok ? "ok" : "FAILED") << " over " << ns.size()
-                << " points\n";
+      std::cerr << "extended " << id << ": " << (ok ? "ok" : "FAILED") << " over " << checked << " points\n";
     }
     write(pdir + "/derived.json", json{{"derived", derived}});
   }

@@ -618,6 +618,96 @@ def read_measurements(path, discard: int = 4) -> list[KernelMeasurements]:
         L.kcg_measurements_destroy(h)
 
 
+@dataclass
+class CampaignRecord:
+    """One simulated observation (MeasurementRecord / RawRun, csvio.hpp)."""
+    kernel: str
+    binding: dict
+    group_config: str
+    run_index: int
+    time_s: float
+
+
+def binding_str(b: Mapping) -> str:
+    """csvio.cpp:77-84: "k=v;..." in key order (std::map)."""
+    return ";".join(f"{k}={int(b[k])}" for k in sorted(b))
+
+
+def run_campaign(cases, alpha149: Sequence[float], sigma: float = 0.0, seed: int = 0, runs: int = 1,
+                 programs=None, stream=None):
+    """``kernelcost simulate`` on the GPU: run_campaign (campaign.cpp:11-45)
+    with simulate_time / simulate_runs (simdevice.cpp:96-128) for every case
+    (kernel, binding, group_config), all cases of one kernel in one batched
+    launch per run. Returns (records in case order, runs innermost, and
+    the diagnostics of failed cases "<kernel> [<binding>]: <error>", as the
+    reference reports instead of aborting)."""
+    torch = _torch()
+    if runs <= 0:
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "run count must be positive")
+    cases = [(k, {p: int(v) for p, v in b.items()}, g) for k, b, g in cases]
+    by_kernel = {}
+    for i, (k, _, _) in enumerate(cases):
+        by_kernel.setdefault(k, []).append(i)
+    times = [[0.0] * runs for _ in cases]
+    fails = {}
+    for k, idx in by_kernel.items():
+        prog = _program_for(k, programs)
+        cols = {}
+        for p in prog.params:
+            if any(p not in cases[i][1] for i in idx):
+                for i in idx:
+                    if p not in cases[i][1]:
+                        fails[i] = f"E_INVALID_ARGUMENT: binding missing parameter '{p}'"
+            cols[p] = torch.tensor([cases[i][1].get(p, 0) for i in idx], dtype=torch.int64, device="cuda")
+        for r in range(runs):
+            t, st = simulate_time(alpha149, prog, cols, sigma=sigma, seed=seed, run=r, with_status=True,
+                                  stream=stream)
+            t, st = t.cpu().tolist(), st.cpu().tolist()
+            for j, i in enumerate(idx):
+                if st[j] != _capi.PT_OK and i not in fails:
+                    fails[i] = ("E_ASSUMPTION_VIOLATED: binding violates the kernel's assumptions"
+                                if st[j] == _capi.PT_ASSUMPTION_VIOLATED
+                                else lib().kcg_point_status_str(st[j]).decode())
+                times[i][r] = t[j]
+    records, diags = [], []
+    for i, (k, b, g) in enumerate(cases):
+        if i in fails:
+            diags.append(f"{k} [{binding_str(b)}]: {fails[i]}")
+            continue
+        records.extend(CampaignRecord(k, b, g, r, times[i][r]) for r in range(runs))
+    return records, diags
+
+
+def write_measurements_csv(path, records) -> None:
+    """csvio.cpp:104-114 (kernel,binding,group_config,time_s; %.17g),
+    byte-identical to the reference's file for the same records."""
+    lines = ["kernel,binding,group_config,time_s"]
+    lines += [f"{r.kernel},{binding_str(r.binding)},{r.group_config},{r.time_s:.17g}" for r in records]
+    Path(path).write_text("\n".join(lines) + "\n")
+
+
+def write_raw_runs_csv(path, records) -> None:
+    """csvio.cpp:144-155 (... ,run_index,time_s)."""
+    lines = ["kernel,binding,group_config,run_index,time_s"]
+    lines += [f"{r.kernel},{binding_str(r.binding)},{r.group_config},{r.run_index},{r.time_s:.17g}" for r in records]
+    Path(path).write_text("\n".join(lines) + "\n")
+
+
+def write_campaign_columns(path, records) -> None:
+    """The same records as a kcg-columns v1 file (bulk campaigns): one int64
+    column per parameter, run_index and time_s (records of one kernel)."""
+    import numpy as np
+    if not records:
+        raise _capi.KcgError(_capi.E_EMPTY, "no records")
+    params = sorted(records[0].binding)
+    if any(r.kernel != records[0].kernel or sorted(r.binding) != params for r in records):
+        raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "a columns campaign file holds one kernel")
+    cols = {p: np.array([r.binding[p] for r in records], dtype=np.int64) for p in params}
+    cols["run_index"] = np.array([r.run_index for r in records], dtype=np.int64)
+    cols["time_s"] = np.array([r.time_s for r in records], dtype=np.float64)
+    write_columns(path, cols)
+
+
 def _program_for(kernel: str, programs) -> Program:
     if programs is None:
         return load_program(kernel)

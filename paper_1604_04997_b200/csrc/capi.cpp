@@ -2,6 +2,7 @@
 // host-side solve and weights I/O. No exception crosses this file's
 // functions; failures become KCG_E_* codes plus kcg_last_error().
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <atomic>
@@ -70,6 +71,15 @@ int fail(int code, const std::string& msg) {
 extern "C" void kcg_set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
 
 namespace {
+
+// NVTX range per C-ABI phase (visible in Nsight Systems / ncu
+// --nvtx); a no-op unless a tool is attached (nvtx3 is header-only)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 template <class F>
 int guarded(F&& f) {
@@ -421,6 +431,7 @@ int kcg_eval_predict(const kcg_program* cp, const int64_t* const* param_cols, si
   if (pred_out && !alpha) return fail(KCG_E_INVALID_ARGUMENT, "alpha required for predictions");
   if (p->low.n_params > 0 && !param_cols) return fail(KCG_E_INVALID_ARGUMENT, "null param_cols");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_eval_predict");
     require_device();
     if (n == 0) return KCG_OK;
     const int np = p->low.n_params;
@@ -639,6 +650,7 @@ int kcg_eval_predict_multi(const kcg_program* const* progs, int V, const int64_t
   if ((pred_out && ld_pred < n) || (status_out && ld_status < n))
     return fail(KCG_E_INVALID_ARGUMENT, "output leading dimension below n_points");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_eval_predict_multi");
     require_device();
     std::vector<const kcg::Lowered*> lows;
     std::vector<std::vector<int>> pmaps;
@@ -668,6 +680,7 @@ int kcg_argmin(const kcg_program* const* progs, int V, const int64_t* const* par
   if (!progs || V < 1 || !alpha || !best_idx || !best_t)
     return fail(KCG_E_INVALID_ARGUMENT, "bad argmin arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_argmin");
     require_device();
     if (n == 0) return KCG_OK;
     if (progs[0] && progs[0]->low.n_params > 0 && !param_cols)
@@ -923,6 +936,7 @@ int kcg_eval_predict_host(const kcg_program* const* progs, int V, const int64_t*
   if (!progs || V < 1 || !alpha || (!pred_out && !status_out))
     return fail(KCG_E_INVALID_ARGUMENT, "bad host eval arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_eval_predict_host");
     require_device();
     const kcg_program* p0 = progs[0];
     const int np = p0->low.n_params;
@@ -1048,6 +1062,7 @@ int kcg_gram_accumulate(const double* X, size_t n, int F, size_t ld, double* G, 
   if (!X || !G || !xt1 || !colmax || ld < static_cast<size_t>(F))
     return fail(KCG_E_INVALID_ARGUMENT, "bad gram arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_gram_accumulate");
     require_device();
     static const bool no_wide = std::getenv("KCG_NO_WIDE_DMMA") != nullptr;  // A/B knob
     // F <= KCG_DMMA_MAXF (default 72): the row-split DMMA kernel (one CTA per
@@ -1147,6 +1162,7 @@ int kcg_gram_fused(const kcg_program* cp, const int64_t* const* param_cols, cons
   kcg_program* p = const_cast<kcg_program*>(cp);
   if (!p || !T || !G || !xt1 || !colmax) return fail(KCG_E_INVALID_ARGUMENT, "bad gram arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_gram_fused");
     require_device();
     if (n == 0) return KCG_OK;
     const int np = p->low.n_params;
@@ -1188,6 +1204,7 @@ int kcg_residual_accumulate(const double* X, size_t n, int F, size_t ld, const d
   if (!X || !alpha || !obj || ld < static_cast<size_t>(F))
     return fail(KCG_E_INVALID_ARGUMENT, "bad residual arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_residual_accumulate");
     require_device();
     kcg::launch_residual(X, n, F, ld, alpha, obj, stream);
     ++g_launches;
@@ -1200,6 +1217,7 @@ int kcg_gram_residual_grad(const double* X, size_t n, int F, size_t ld, const do
   if (!X || !alpha || !g || ld < static_cast<size_t>(F))
     return fail(KCG_E_INVALID_ARGUMENT, "bad residual arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_gram_residual_grad");
     require_device();
     kcg::launch_residual_grad(X, n, F, ld, alpha, g, stream);
     ++g_launches;
@@ -1212,6 +1230,7 @@ int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, 
   kcg_program* p = const_cast<kcg_program*>(cp);
   if (!p || !T || !alpha || !obj) return fail(KCG_E_INVALID_ARGUMENT, "bad residual arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_residual_fused");
     require_device();
     if (n == 0) return KCG_OK;
     const int np = p->low.n_params;
@@ -1269,6 +1288,7 @@ int kcg_residual_grad_fused(const kcg_program* cp, const int64_t* const* param_c
   kcg_program* p = const_cast<kcg_program*>(cp);
   if (!p || !T || !alpha || !g) return fail(KCG_E_INVALID_ARGUMENT, "bad residual-gradient arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_residual_grad_fused");
     require_device();
     if (n == 0) return KCG_OK;
     const int np = p->low.n_params;
@@ -1333,6 +1353,7 @@ int kcg_simulate_time(const kcg_program* cp, const int64_t* const* param_cols, s
                                   /*simulate=*/1, stream);
   if (rc != KCG_OK || sigma == 0.0 || n == 0) return rc;  // simdevice.cpp:99
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_simulate_time");
     kcg::NoiseArgs a{};
     const int np = p->low.n_params;
     std::vector<int> order(np);
@@ -1369,6 +1390,7 @@ int kcg_geomean_accumulate(const double* pred, const double* actual, size_t n, d
   if (!pred || !actual || !log_sum || !count || !bad)
     return fail(KCG_E_INVALID_ARGUMENT, "bad geomean arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_geomean_accumulate");
     require_device();
     kcg::launch_geomean(pred, actual, n, log_sum, count, bad, stream);
     ++g_launches;
@@ -1381,6 +1403,7 @@ int kcg_solve_gram(int F, const double* G, const double* xt1, const double* colm
   if (F < 1 || !G || !xt1 || !colmax || !alpha_out)
     return fail(KCG_E_INVALID_ARGUMENT, "bad solve arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_solve_gram");
     std::vector<double> x;
     const int r = solve_equilibrated(F, G, colmax, xt1, x);
     std::copy(x.begin(), x.end(), alpha_out);
@@ -1394,6 +1417,7 @@ int kcg_refine_gram(int F, const double* G, const double* colmax, const double* 
   if (F < 1 || !G || !colmax || !g || !alpha)
     return fail(KCG_E_INVALID_ARGUMENT, "bad refine arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_refine_gram");
     std::vector<double> dx;
     solve_equilibrated(F, G, colmax, g, dx);
     for (int j = 0; j < F; ++j)
@@ -1567,6 +1591,7 @@ int kcg_enumerate_points(const kcg_enum_program* p, const int64_t* binding, uint
   if (!p || (!binding && p->e.n_params > 0) || !lo || !hi)
     return fail(KCG_E_INVALID_ARGUMENT, "bad enumerate arguments");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_enumerate_points");
     require_device();
     std::vector<i128> c(kcg::schema_keys().size(), 0);
     const int launches = kcg::enumerate_points(p->e, binding, cap, c.data(), points, stream);
@@ -1606,6 +1631,7 @@ extern "C" {
 
 int kcg_grid_bindings(const kcg_grid* g, uint64_t first, size_t n, int64_t* const* cols, void* stream) {
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_grid_bindings");
     check_grid(g, first, n);
     if (g->n_params > 0 && !cols) throw KcgError(KCG_E_INVALID_ARGUMENT, "null columns");
     require_device();
@@ -1623,6 +1649,7 @@ int kcg_eval_predict_grid(const kcg_program* cp, const kcg_grid* g, uint64_t fir
   if (!p) return fail(KCG_E_INVALID_ARGUMENT, "null program");
   if (pred_out && !alpha) return fail(KCG_E_INVALID_ARGUMENT, "alpha required for predictions");
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_eval_predict_grid");
     check_grid(g, first, n);
     const int np = p->low.n_params;
     if (g->n_params != np) throw KcgError(KCG_E_INVALID_ARGUMENT, "grid parameter count != program's");
@@ -1726,6 +1753,7 @@ const void* kcg_columns_data(const kcg_columns* c, int j) {
 
 int kcg_columns_load(kcg_columns* c, int j, uint64_t row0, size_t n, void* dev, void* stream) {
   return guarded([&] {
+    const NvtxRange nvtx_range("kcg_columns_load");
     require_device();
     kcg::columns_load(c, j, row0, n, dev, stream);
     return KCG_OK;

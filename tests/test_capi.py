@@ -342,6 +342,7 @@ def test_refinement_gradient_groups_power_of_two_keys():
     counts differ by powers of two (tiled matmul: 9 keys -> 4 divisions)."""
     L = _capi.lib()
     for kid, want in (("matmul_tiled_g16x16", 4), ("conv_g16x16", 3), ("transpose_tile_g16x16", 2)):
-        src = L.kcg_program_jit_source_kind(kc.load_program(kid).handle, 5).decode()
+        prog = kc.load_program(kid)  # the returned text is owned by the program: keep it alive
+        src = L.kcg_program_jit_source_kind(prog.handle, 5).decode()
         i = src.index("kcg_xrow(const T* c")
         assert src[i:src.index("}", i)].count("__ddiv_rn") == want, kid
