@@ -158,7 +158,7 @@ def run_reference_arm(args, rank, world):
         cpu_reference(threads, CPU_SAMPLE_SIZES // 10, offset=w * 7919)
     times, pts, last = [], 0, None
     for s in range(args.steps):
-        last = cpu_reference_line(threads, offset=(s * 1_000_003) % (SIDE ** 3 - CPU_SAMPLE_SIZES))
+        last = cpu_reference_line(threads)  # the in-line cpu_baseline's sample, every step
         times.append(last["seconds"])
         pts = last["points"]
     sec = sum(times) / len(times)
@@ -747,7 +747,7 @@ def _configs(kc, torch, dev, args, cols, progs, w):
         "bytes_per_size": 36, "hbm_frac": 36 * total / sec / 1e9 / hbm,
         "best_variant_histogram": torch.bincount(best.to(torch.int64) + 1, minlength=len(progs) + 1).tolist(),
         "instruction_roofline": _instr_roofline(_ncu_lane_instr("r02_argmin_ncu.txt"), total * len(progs) / sec,
-                                                _pipe_peaks(kc), "profiles/r02_argmin_ncu.txt (ncu, kcg_multiam_v6_tma, 1-CTA build)"),
+                                                _pipe_peaks(kc), "profiles/r02_argmin_ncu.txt (ncu, kcg_multiam_v6_tma, default 3-CTA build)"),
         "kernel": "kcg_multiam_v6_tma (one-pass kernel, argmin epilogue)",
         "note": "one fused launch per step; 24 B bindings in, int32 + fp64 out per size"}
     # the same launch also writing every variant's prediction (variant-major):
