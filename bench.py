@@ -326,9 +326,10 @@ def main():
                      "algorithmic_bytes_per_launch": bytes_per_launch, "avg_launch_ms": avg_launch * 1e3,
                      "same_mix_stream_gbs": mix, "frac_of_same_mix": achieved / mix,
                      "same_mix_note": "kcg_measure_stream(3, 6): a plain kernel reading 3 int64 and writing 6 "
-                                      "fp64 columns (this kernel's 1:2 read:write mix), measured live",
+                                      "fp64 columns (this kernel's 1:2 read:write mix), the best of 16-byte "
+                                      "streaming stores and smem-staged cp.async.bulk stores, measured live",
                      "traffic_source": "profiles/r02_traffic.json (ncu dram bytes of the same launch)",
-                     "kernel": "kcg_multi_v6_tma (NVRTC sm_100a)",
+                     "kernel": "kcg_multi_v6_tmab (NVRTC sm_100a: TMA-ring loads, per-warp cp.async.bulk stores)",
                      "per_point_8P_plus_8_GBps": 32.0 * n * V / avg_launch / 1e9,
                      "per_point_note": "SURVEY 8(d)'s per-point figure (8 P + 8 = 32 B per point, bindings "
                                        "counted once per variant) over the same launch time: what six "

@@ -405,8 +405,10 @@ int kcg_measure_pipe_peak(int kind, uint64_t iters, double* lane_ops_per_s);
 /* measured HBM bandwidth (bytes/s, best of 5) of a stream that reads
  * n_read int64 columns and writes n_write fp64 columns of n_points each:
  * the same-mix roofline of a kernel with that traffic (supported mixes:
- * 3/6, 3/1, 1/6, 1/1, 4/0). Allocates 8 (n_read + n_write) n_points bytes;
- * synchronous, default stream; not counted by kcg_launch_count.          */
+ * 3/6, 3/1, 1/6, 1/1). The best of 16-byte streaming stores and
+ * shared-memory-staged cp.async.bulk stores at 2 and 3 CTAs per SM.
+ * Allocates 8 (n_read + n_write) n_points bytes; synchronous, default
+ * stream; not counted by kcg_launch_count.                              */
 int kcg_measure_stream(int n_read, int n_write, uint64_t n_points, double* bytes_per_s);
 
 #ifdef __cplusplus

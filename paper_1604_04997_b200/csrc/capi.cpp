@@ -597,7 +597,11 @@ bool launch_multi(const kcg_program* const* progs, int V, const int64_t* const* 
   const size_t tiles = n / static_cast<size_t>(kcg::multi_tile());
   const bool tma = vec && !no_tma && np > 0 && tiles >= static_cast<size_t>(kcg::num_sms());
   const bool extra = argmin ? pred != nullptr : status != nullptr;  // _p / _st kernels
-  const std::string kname = e->name + (tma ? "_tma" : "") + (extra ? (argmin ? "_p" : "_st") : "");
+  // bulk-store variant: every program's output row 16-byte aligned
+  static const bool no_bulk = std::getenv("KCG_MULTI_BULK") && std::string(std::getenv("KCG_MULTI_BULK")) == "0";
+  const bool bulk = tma && !argmin && !no_bulk && V <= kcg::multi_bulk_vmax() &&
+                    reinterpret_cast<uintptr_t>(pred) % 16 == 0 && ldp % 2 == 0;
+  const std::string kname = e->name + (tma ? (bulk ? "_tmab" : "_tma") : "") + (extra ? (argmin ? "_p" : "_st") : "");
   void* k = nullptr;
   {
     std::lock_guard<std::mutex> lock(mu);
@@ -627,7 +631,11 @@ bool launch_multi(const kcg_program* const* progs, int V, const int64_t* const* 
   for (double x : shw) ab.push<double>(x);
   if (shw.empty()) ab.push<double>(0.0);
   ab.finish();
-  if (tma) {
+  if (bulk) {
+    const unsigned grid = static_cast<unsigned>(
+        std::min<size_t>(tiles, static_cast<size_t>(kcg::num_sms()) * kcg::multi_bulk_ctas()));
+    kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid, 256, stream, kcg::multi_bulk_smem_bytes(np, V));
+  } else if (tma) {
     const unsigned grid = static_cast<unsigned>(
         std::min<size_t>(tiles, static_cast<size_t>(kcg::num_sms()) * kcg::multi_ctas_per_sm(argmin)));
     kcg::launch_jit(k, ab.b.data(), ab.b.size(), grid, 256, stream, kcg::multi_smem_bytes(np, argmin));

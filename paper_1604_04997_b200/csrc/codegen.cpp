@@ -1000,6 +1000,19 @@ int multi_tile() { return 256 * env_int("KCG_MULTI_TILE_Q", 4, 1, 8); }
 int multi_ctas_per_sm(bool argmin) { return multi_ctas(argmin); }
 bool multi_share() { return env_int("KCG_MULTI_SHARE", 1, 0, 1) == 1; }
 bool multi_prefetch() { return env_int("KCG_MULTI_PREFETCH", 0, 0, 1) == 1; }
+// bulk-store variant (pred mode): predictions staged per warp in shared
+// memory and written by cp.async.bulk (profiles/stream_store_ab.cu: the
+// 3-read:6-write mix reaches 6.1-6.2 TB/s with bulk stores against
+// 5.2-5.8 with 16-byte streaming stores)
+// measured (profiles/gpu_r02_bulk*.sh, config-4 lattice): per-warp 1 KB bulk
+// stores with one staging buffer, 2 CTAs x 48 KB ring per SM: 2.055-2.08 ms
+// against 2.17 for the 16-byte-store kernel; double-buffered staging at one
+// CTA per SM 2.46, 3 CTAs with a 16 KB ring 2.38
+int multi_obuf() { return env_int("KCG_MULTI_OBUF", 1, 1, 2); }
+int multi_bulk_ctas() { return env_int("KCG_MULTI_BULK_CTAS", 2, 1, 3); }
+int multi_bulk_ring_kb() { return env_int("KCG_MULTI_BULK_RING_KB", 48, 16, 200); }
+bool multi_bulk_cta() { return env_int("KCG_MULTI_BULK_CTA", 0, 0, 1) == 1; }  // one 8 KB store per row per stage
+int multi_bulk_vmax() { return 10; }
 int multi_stages(int n_cols, bool argmin) {
   const int per = (n_cols > 0 ? n_cols : 1) * multi_tile() * 8;
   const int s = (multi_ring_kb(argmin) * 1024) / per;
@@ -1007,6 +1020,15 @@ int multi_stages(int n_cols, bool argmin) {
 }
 size_t multi_smem_bytes(int n_cols, bool argmin) {
   return static_cast<size_t>(multi_stages(n_cols, argmin)) * (n_cols > 0 ? n_cols : 1) * multi_tile() * 8;
+}
+int multi_bulk_stages(int n_cols) {
+  const int per = (n_cols > 0 ? n_cols : 1) * multi_tile() * 8;
+  const int s = (multi_bulk_ring_kb() * 1024) / per;
+  return s < 2 ? 2 : (s > 8 ? 8 : s);
+}
+size_t multi_bulk_smem_bytes(int n_cols, int V) {
+  return static_cast<size_t>(multi_bulk_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * multi_tile() * 8 +
+         static_cast<size_t>(8) * multi_obuf() * V * 128 * 8;
 }
 
 // Which products the one-pass kernel forms once per point and shares:
@@ -1140,7 +1162,9 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
           "      : \"=d\"(out) : \"r\"(st), \"d\"(s));\n  return st;\n}\n";
   }
   // out-of-line: every variant of size i, any parameter range
-  os << "__device__ __noinline__ void kcg_mslow(const KcgMArgs& a, kcg_i64 i) {\n  kcg_i64 p[" << NP << "];\n"
+  // ob != nullptr (bulk-store kernels): predictions go to the warp's
+  // shared-memory staging block ob[v * 128 + li] instead of global memory
+  os << "__device__ __noinline__ void kcg_mslow(const KcgMArgs& a, kcg_i64 i, double* ob, int li, int rs) {\n  kcg_i64 p[" << NP << "];\n"
         "  int bi = -1;\n  double bt = __longlong_as_double(0x7ff0000000000000ll);\n";
   for (int j = 0; j < n_cols; ++j) os << "  p[" << j << "] = a.p[" << j << "][i];\n";
   for (int v = 0; v < V; ++v) {
@@ -1163,7 +1187,7 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
          << "(q, none);\n        if (a0 != KCG_PT_OK) st = a0;\n      }\n";
     }
     os << "    }\n    if (st != KCG_PT_OK) s = kcg_nan();\n"
-       << "    if (a.pred) a.pred[(kcg_i64)" << v << " * a.ldp + i] = s;\n"
+       << "    if (ob) ob[" << v << " * rs + li] = s;\n    else if (a.pred) a.pred[(kcg_i64)" << v << " * a.ldp + i] = s;\n"
        << "    if (a.status) a.status[(kcg_i64)" << v << " * a.lds + i] = (unsigned char)st;\n"
        << "    if (st == KCG_PT_OK && s < bt) { bt = s; bi = " << v << "; }\n  }\n";
   }
@@ -1171,8 +1195,10 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
   // one size from registers: shared products, then every variant -- one
   // basic block (no per-variant branches), so the V independent
   // accumulation chains interleave
-  os << "template <int ST>\n__device__ __forceinline__ void kcg_msize(const kcg_i64* p, const KcgMArgs& a, kcg_i64 i) {\n"
-        "  if (!kcg_mfast(p)) { kcg_mslow(a, i); return; }\n";
+  // BULK > 0: predictions to the shared staging block ob[v * BULK + li]
+  os << "template <int ST, int BULK = 0>\n__device__ __forceinline__ void kcg_msize(const kcg_i64* p, const KcgMArgs& a, "
+        "kcg_i64 i, double* ob = nullptr, int li = 0) {\n"
+        "  if (!kcg_mfast(p)) { kcg_mslow(a, i, BULK ? ob : nullptr, li, BULK); return; }\n";
   for (size_t m = 0; m < P.monos.size(); ++m) {
     os << "  const double dm" << m << " = __ull2double_rn(";
     bool first = true;
@@ -1190,8 +1216,11 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
   for (int v = 0; v < V; ++v) os << "  double s" << v << ";\n  const int st" << v << " = kcg_mfastv_" << v << "<1>(p, a, sh, s" << v << ");\n";
   // ST: pred mode -- status bytes too; argmin mode -- all predictions too
   if (!argmin) {
-    for (int v = 0; v < V; ++v) os << "  __stcs(a.pred + (kcg_i64)" << v << " * a.ldp + i, s" << v << ");\n";
-    os << "  if (ST) {\n";
+    os << "  if (BULK) {\n";
+    for (int v = 0; v < V; ++v) os << "    ob[" << v << " * BULK + li] = s" << v << ";\n";
+    os << "  } else {\n";
+    for (int v = 0; v < V; ++v) os << "    __stcs(a.pred + (kcg_i64)" << v << " * a.ldp + i, s" << v << ");\n";
+    os << "  }\n  if (ST) {\n";
     for (int v = 0; v < V; ++v) os << "    a.status[(kcg_i64)" << v << " * a.lds + i] = (unsigned char)st" << v << ";\n";
     os << "  }\n}\n";
   } else {
@@ -1295,6 +1324,124 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
          << release << "  }\n";
     }
     os <<           "  for (kcg_i64 i = ntiles * TP + (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;\n"
+          "       i += (kcg_i64)gridDim.x * blockDim.x) {\n"
+          "    kcg_i64 p[NP];\n";
+    for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = a.p[" << j << "][i];\n";
+    os << "    kcg_msize<" << stv << ">(p, a, i);\n  }\n}\n";
+    if (argmin || V > multi_bulk_vmax() || n_cols == 0) continue;
+    // bulk-store TMA kernel (<name>_tmab[_st]): warp w owns points
+    // [128 w, 128 w + 128) of each stage; its lanes evaluate points
+    // 128 w + lane + 32 u into the warp's staging block [V][128] (double-
+    // buffered), then lane 0 writes the block's V rows to global memory
+    // with cp.async.bulk (1 KB each) -- no CTA barrier, warps drift freely
+    const int SB = multi_bulk_stages(n_cols), OB = multi_obuf();
+    os << "extern \"C\" __global__ void __launch_bounds__(256, " << multi_bulk_ctas() << ") " << name << "_tmab" << sfx
+       << "(const __grid_constant__ KcgMArgs a) {\n"
+          "  constexpr int TP = " << multi_tile() << ", S = " << SB << ", NP = " << NP << ", V = " << V
+       << ", OB = " << OB << ";\n"
+          "  static_assert(TP == 1024, \"bulk kernel: 8 warps x 128 points per stage\");\n"
+          "  extern __shared__ __align__(128) unsigned char kcg_smem[];\n"
+          "  kcg_i64* buf = reinterpret_cast<kcg_i64*>(kcg_smem);\n"
+          "  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;\n"
+          "  double* obase = reinterpret_cast<double*>(kcg_smem + (size_t)S * NP * TP * 8) + (size_t)w * OB * V * 128;\n"
+          "  __shared__ __align__(8) unsigned long long full[S];\n"
+          "  __shared__ unsigned reads[S];\n"
+          "  if (threadIdx.x < S) reads[threadIdx.x] = 0;\n"
+          "  const kcg_i64 ntiles = a.n / TP;\n"
+          "  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);\n"
+          "  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);\n"
+          "  if (threadIdx.x == 0) {\n"
+          "    for (int s = 0; s < S; ++s)\n"
+          "      asm volatile(\"mbarrier.init.shared::cta.b64 [%0], 1;\" :: \"r\"(fb + 8 * s));\n"
+          "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n"
+          "  }\n"
+          "  __syncthreads();\n"
+          "  auto issue = [&](int s, kcg_i64 tile) {\n"
+          "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+          "    asm volatile(\"mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\" :: \"r\"(fb + 8 * s), \"r\"(NP * TP * 8) : \"memory\");\n"
+          "    for (int j = 0; j < NP; ++j)\n"
+          "      asm volatile(\"cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\"\n"
+          "                   :: \"r\"(bb + (unsigned)((s * NP + j) * TP * 8)), \"l\"(a.p[j] + tile * TP), \"r\"(TP * 8), \"r\"(fb + 8 * s) : \"memory\");\n"
+          "  };\n"
+          "  if (threadIdx.x == 0)\n"
+          "    for (int s = 0; s < S; ++s) {\n"
+          "      const kcg_i64 t = blockIdx.x + (kcg_i64)s * gridDim.x;\n"
+          "      if (t < ntiles) issue(s, t);\n"
+          "    }\n"
+          "  for (kcg_i64 k = 0;; ++k) {\n"
+          "    const kcg_i64 tile = blockIdx.x + k * gridDim.x;\n"
+          "    if (tile >= ntiles) break;\n"
+          "    const int s = (int)(k % S);\n"
+          "    const unsigned parity = (unsigned)((k / S) & 1);\n"
+          "    {\n"
+          "      unsigned done = 0;\n"
+          "      while (!done)\n"
+          "        asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\"\n"
+          "                     : \"=r\"(done) : \"r\"(fb + 8 * s), \"r\"(parity) : \"memory\");\n"
+          "    }\n"
+"    " << "";
+    if (multi_bulk_cta())
+      os <<           "    // CTA-level staging: [V][TP] for the whole stage, one 8 KB bulk store per row\n"
+          "    double* ob = reinterpret_cast<double*>(kcg_smem + (size_t)S * NP * TP * 8);\n"
+          "    if (k > 0 && threadIdx.x == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
+          "    __syncthreads();\n"
+          "    const kcg_i64 rb = tile * TP;\n"
+          "    #pragma unroll 1\n"
+          "    for (int u = 0; u < 4; ++u) {\n"
+          "      const int li = u * 256 + threadIdx.x;\n"
+          "      kcg_i64 q[NP];\n"
+          "      #pragma unroll\n"
+          "      for (int j = 0; j < NP; ++j) q[j] = buf[(s * NP + j) * TP + li];\n"
+          "      kcg_msize<" << stv << ", TP>(q, a, rb + li, ob, li);\n"
+          "    }\n"
+          "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+          "    __syncthreads();\n"
+          "    if (threadIdx.x == 0) {\n"
+          "      const unsigned ob_s = (unsigned)__cvta_generic_to_shared(ob);\n"
+          "      #pragma unroll\n"
+          "      for (int v = 0; v < V; ++v)\n"
+          "        asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\"\n"
+          "                     :: \"l\"(a.pred + (kcg_i64)v * a.ldp + rb), \"r\"(ob_s + v * TP * 8), \"r\"(TP * 8) : \"memory\");\n"
+          "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
+          "      const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+          "      if (nt < ntiles) issue(s, nt);  // every thread is past its reads of stage s\n"
+          "    }\n"
+          "  }\n";
+    else
+      os <<           "    double* ob = obase + (int)(k % OB) * V * 128;\n"
+          "    if (k >= OB) {  // the block's previous bulk stores have finished reading it\n"
+          "      if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read %0;\" :: \"n\"(OB - 1) : \"memory\");\n"
+          "      __syncwarp();\n"
+          "    }\n"
+          "    const kcg_i64 rb = tile * TP + 128 * w;\n"
+          "    #pragma unroll 1\n"
+          "    for (int u = 0; u < 4; ++u) {\n"
+          "      const int li = lane + 32 * u;\n"
+          "      kcg_i64 q[NP];\n"
+          "      #pragma unroll\n"
+          "      for (int j = 0; j < NP; ++j) q[j] = buf[(s * NP + j) * TP + 128 * w + li];\n"
+          "      kcg_msize<" << stv << ", 128>(q, a, rb + li, ob, li);\n"
+          "    }\n"
+          "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+          "    __syncwarp();\n"
+          "    if (lane == 0) {\n"
+          "      __threadfence_block();\n"
+          "      const unsigned ob_s = (unsigned)__cvta_generic_to_shared(ob);\n"
+          "      #pragma unroll\n"
+          "      for (int v = 0; v < V; ++v)\n"
+          "        asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 1024;\"\n"
+          "                     :: \"l\"(a.pred + (kcg_i64)v * a.ldp + rb), \"r\"(ob_s + v * 1024) : \"memory\");\n"
+          "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
+          "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
+          "        reads[s] = 0;\n"
+          "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+          "        if (nt < ntiles) issue(s, nt);\n"
+          "      }\n"
+          "    }\n"
+          "  }\n"
+;
+    os <<           "  if (lane == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n"
+          "  for (kcg_i64 i = ntiles * TP + (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;\n"
           "       i += (kcg_i64)gridDim.x * blockDim.x) {\n"
           "    kcg_i64 p[NP];\n";
     for (int j = 0; j < n_cols; ++j) os << "    p[" << j << "] = a.p[" << j << "][i];\n";

@@ -66,6 +66,9 @@ MultiPlan multi_plan(const std::vector<const Lowered*>& progs, const std::vector
                      int n_cols);
 /// its TMA ring, CTAs per SM and points per stage.
 size_t multi_smem_bytes(int n_cols, bool argmin);
+size_t multi_bulk_smem_bytes(int n_cols, int n_progs);  // the bulk-store variant (<name>_tmab)
+int multi_bulk_ctas();
+int multi_bulk_vmax();
 int multi_ctas_per_sm(bool argmin);
 int multi_tile();
 

@@ -28,13 +28,13 @@ for i, d in k.items():
         continue
     us = d["gpu__time_duration.sum"] / 1e3 if d["gpu__time_duration.sum"] > 1e5 else d["gpu__time_duration.sum"]
     rd, wr = d["dram__bytes_read.sum"] / 1e9, d["dram__bytes_write.sum"] / 1e9
-    alg = (ALG["multi"] if name.startswith("kcg_multi") and name.endswith("_tma")
+    alg = (ALG["multi"] if name.startswith("kcg_multi") and name.endswith(("_tma", "_tmab"))
            else ALG["eval"] if name.startswith("kcg_eval") and name.endswith("_tma") else 0.0) / 1e9
     print(f"{i},{name},{us:.1f},{rd:.3f},{wr:.3f},{alg:.3f},{(rd + wr) / us * 1e6:.0f}")
-    if name.startswith("kcg_multi") and name.endswith("_tma"):
+    if name.startswith("kcg_multi") and name.endswith(("_tma", "_tmab")):
         tr.append((rd + wr) * 1e9)
 if len(sys.argv) > 3 and tr:
-    json.dump({"kernel": "kcg_multi_v6_tma", "traffic_bytes_per_launch": sum(tr) / len(tr),
+    json.dump({"kernel": "kcg_multi_v6_tmab", "traffic_bytes_per_launch": sum(tr) / len(tr),
                "sizes_per_launch": SIZES, "algorithmic_bytes_per_launch": ALG["multi"],
                "source": f"{sys.argv[2]} (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
                          f"mean over the {len(tr)} headline launches)"}, open(sys.argv[3], "w"), indent=1)

@@ -25,7 +25,8 @@ i = torch.arange(0, n, dtype=torch.int64, device="cuda")
 cols = {"n": ((i // (side * side) + 1) * 336).contiguous(), "m": (((i // side) % side + 1) * 336).contiguous(),
         "l": ((i % side + 1) * 336).contiguous()}
 del i
-out = torch.empty((6, n), dtype=torch.float64, device="cuda")
+# rows padded to a 16-byte multiple (as bench.py): every output row aligned
+out = torch.empty((6, (n + 1) // 2 * 2), dtype=torch.float64, device="cuda")
 
 
 def timed(fn, reps=5):
@@ -54,7 +55,7 @@ ref = out.clone()
 per_program()
 ref.copy_(out)
 t_multi = timed(lambda: kc.predict_multi(progs, w, cols, out=out))
-same = bool(torch.equal(out.view(torch.int64), ref.view(torch.int64)))
+same = bool(torch.equal(out[:, :n].view(torch.int64), ref[:, :n].view(torch.int64)))
 t_sep = timed(per_program) if "--sep" in sys.argv else None
 knobs = {k: v for k, v in os.environ.items() if k.startswith("KCG_")}
 uniq = n * (24 + 48)
@@ -63,4 +64,4 @@ print(json.dumps({"knobs": knobs, "ms_multi": t_multi, "points_per_s": 6 * n / t
                   "ms_per_program_x6": t_sep}))
 if "--stream" in sys.argv:
     print(json.dumps({"stream_GBps": {f"{r}r{w}w": kc.measure_stream(r, w, 1 << 27) / 1e9
-                                      for r, w in ((3, 6), (3, 1), (1, 6), (1, 1), (4, 0))}}))
+                                      for r, w in ((3, 6), (3, 1), (1, 6), (1, 1))}}))

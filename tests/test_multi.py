@@ -62,8 +62,10 @@ def _bindings(n, seed, scale=336):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("n", [1, 1000, 3 * 4096 + 17, 148 * 3 * 1024 * 2 + 333])
+@pytest.mark.parametrize("n", [1, 1000, 3 * 4096 + 17, 148 * 3 * 1024 * 2 + 333, 148 * 3 * 1024 * 2 + 334])
 def test_multi_bitwise_equals_per_program(n):
+    """odd n: the 16-byte-store TMA kernel; even n (rows 16-byte aligned):
+    the bulk-store kernel (kcg_multi_v6_tmab)"""
     import torch
     progs = [kc.load_program(v) for v in MATMUL]
     w = _weights()
