@@ -34,11 +34,26 @@ namespace {
 typedef long long i64;
 typedef unsigned long long u64;
 
-__device__ __forceinline__ i64 ke_raw(const KeRow& r, const i64* x, int nv) {
+__device__ __forceinline__ i64 ke_lin(const KeRow& r, const i64* x, int nv) {
   i64 v = r.c0;
 #pragma unroll
   for (int s = 0; s < KE_MAXV; ++s)
     if (s < nv) v += r.c[s] * x[s];
+  return v;
+}
+
+// floor(a / d), d > 0 (numeric.hpp:24-28)
+__device__ __forceinline__ i64 ke_floor_div(i64 a, i64 d) {
+  i64 q = a / d;
+  if (a % d != 0 && a < 0) q -= 1;
+  return q;
+}
+
+// the row's raw value, floor divisions over domain variables included
+__device__ __forceinline__ i64 ke_raw(const KeRow& r, const i64* x, int nv, const KeStmt& S) {
+  i64 v = ke_lin(r, x, nv);
+  for (int f = 0; f < S.nf; ++f)
+    if (r.cf[f] != 0) v += r.cf[f] * ke_floor_div(ke_lin(S.f[f].r, x, nv), S.f[f].div);
   return v;
 }
 
@@ -49,8 +64,8 @@ __device__ __forceinline__ i64 ke_ceil_div(i64 a, i64 d) {
   return q;
 }
 
-__device__ __forceinline__ bool ke_guard(const KeGuard& g, const i64* x, int nv) {
-  const i64 v = ke_raw(g.r, x, nv);
+__device__ __forceinline__ bool ke_guard(const KeGuard& g, const i64* x, int nv, const KeStmt& S) {
+  const i64 v = ke_raw(g.r, x, nv, S);
   if (g.divis) {
     i64 m = v % g.mod;
     if (m < 0) m += g.mod;
@@ -82,7 +97,7 @@ __device__ __forceinline__ void ke_mark(const KeStmt& S, const i64* x) {
     const KeMark& M = A.m;
     u64 lin = 0, lino = 0, fast = 0;
     for (int k = 0; k < M.nd; ++k) {
-      const u64 v = (u64)(ke_raw(A.idx[k], x, S.nv) - M.lo[k]);
+      const u64 v = (u64)(ke_raw(A.idx[k], x, S.nv, S) - M.lo[k]);
       lin = lin * (u64)M.ext[k] + v;
       if (k == M.fast)
         fast = v;
@@ -118,7 +133,7 @@ __global__ void __launch_bounds__(256) kcg_enum_walk(const KeStmt* __restrict__ 
     int dead = -1;
     for (int l = 0; l < nbe && dead < 0; ++l)
       for (int k = 0; k < S.ng; ++k)
-        if (S.g[k].depth == l && !ke_guard(S.g[k], x, nv)) {
+        if (S.g[k].depth == l && !ke_guard(S.g[k], x, nv, S)) {
           dead = l;
           break;
         }
@@ -136,8 +151,8 @@ __global__ void __launch_bounds__(256) kcg_enum_walk(const KeStmt* __restrict__ 
     // depth-first over the triangular levels nbox..nv-1
     i64 hi[KE_MAXV];
     int l = nbox;
-    x[l] = ke_ceil_div(ke_raw(S.lo[l], x, nv), S.lo[l].den);
-    hi[l] = ke_ceil_div(ke_raw(S.hi[l], x, nv), S.hi[l].den);
+    x[l] = ke_ceil_div(ke_raw(S.lo[l], x, nv, S), S.lo[l].den);
+    hi[l] = ke_ceil_div(ke_raw(S.hi[l], x, nv, S), S.hi[l].den);
     while (true) {
       if (x[l] >= hi[l]) {
         if (l == nbox) break;
@@ -148,7 +163,7 @@ __global__ void __launch_bounds__(256) kcg_enum_walk(const KeStmt* __restrict__ 
       }
       bool pass = true;
       for (int k = 0; k < S.ng; ++k)
-        if (S.g[k].depth == l && !ke_guard(S.g[k], x, nv)) {
+        if (S.g[k].depth == l && !ke_guard(S.g[k], x, nv, S)) {
           pass = false;
           break;
         }
@@ -165,8 +180,8 @@ __global__ void __launch_bounds__(256) kcg_enum_walk(const KeStmt* __restrict__ 
         continue;
       }
       ++l;
-      x[l] = ke_ceil_div(ke_raw(S.lo[l], x, nv), S.lo[l].den);
-      hi[l] = ke_ceil_div(ke_raw(S.hi[l], x, nv), S.hi[l].den);
+      x[l] = ke_ceil_div(ke_raw(S.lo[l], x, nv, S), S.lo[l].den);
+      hi[l] = ke_ceil_div(ke_raw(S.hi[l], x, nv, S), S.hi[l].den);
     }
   }
   for (int o = 16; o > 0; o >>= 1) {

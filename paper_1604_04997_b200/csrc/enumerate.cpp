@@ -97,9 +97,11 @@ bool fits64(i128 v) { return v >= -(static_cast<i128>(1) << 62) && v <= (static_
 // row c0 + sum c_s x_s (over den) of a linear poly: parameters and
 // parameter-only floordiv atoms fold into c0 (RowCompiler::compile)
 KeRow compile_row(const Evaluator& ev, int poly, const std::map<int, int>& slot, int n_params, int* depth,
-                  bool integral) {
+                  bool integral, std::vector<KeFd>* fds = nullptr) {
   Q c0(0);
   std::vector<std::pair<int, Q>> tm;
+  std::vector<std::pair<int, Q>> tf;  // (statement fd index, coefficient)
+  int fd_depth = -1;
   for (const auto& [m, c] : ev.s.polys[poly]) {
     if (m.f.empty()) {
       c0 = c0 + c;
@@ -117,12 +119,38 @@ KeRow compile_row(const Evaluator& ev, int poly, const std::map<int, int>& slot,
     }
     std::vector<int> vs;
     ev.atom_vars(atom, vs);
-    for (int v : vs)
-      if (v >= n_params) throw KcgError(KCG_E_UNSUPPORTED, "floordiv over a domain variable");
-    c0 = c0 + c * ev.atom(atom);
+    bool domain = false;
+    for (int v : vs) domain = domain || v >= n_params;
+    if (!domain) {
+      c0 = c0 + c * ev.atom(atom);
+      continue;
+    }
+    // floor division over domain variables (the reference's Walker case,
+    // enumerate.cpp:31-90): one statement-level term floor(row / div)
+    if (a.kind != AtomKind::floordiv || !fds)
+      throw KcgError(KCG_E_UNSUPPORTED, "min/max or nested floordiv over a domain variable");
+    int din = -1;
+    KeFd fd;
+    std::memset(&fd, 0, sizeof fd);
+    fd.r = compile_row(ev, a.num, slot, n_params, &din, false, nullptr);
+    const i128 div = checked_mul(fd.r.den, a.den);
+    if (!fits64(div)) throw KcgError(KCG_E_UNSUPPORTED, "floordiv divisor exceeds 64 bits");
+    fd.div = static_cast<int64_t>(div);
+    int f = -1;
+    for (size_t i = 0; i < fds->size(); ++i)
+      if (std::memcmp(&(*fds)[i], &fd, sizeof fd) == 0) f = static_cast<int>(i);
+    if (f < 0) {
+      if (static_cast<int>(fds->size()) >= KE_MAXF)
+        throw KcgError(KCG_E_UNSUPPORTED, "more than 4 floor divisions over domain variables in a statement");
+      f = static_cast<int>(fds->size());
+      fds->push_back(fd);
+    }
+    tf.emplace_back(f, c);
+    fd_depth = std::max(fd_depth, din);
   }
   i128 L = c0.d;
   for (const auto& [s, c] : tm) L = lcm128(L, c.d);
+  for (const auto& [f, c] : tf) L = lcm128(L, c.d);
   if (integral && L != 1) throw KcgError(KCG_E_UNSUPPORTED, "array index / divisibility operand is not integral");
   KeRow r;
   std::memset(&r, 0, sizeof r);
@@ -137,6 +165,12 @@ KeRow compile_row(const Evaluator& ev, int poly, const std::map<int, int>& slot,
     r.c[s] = static_cast<int64_t>(v);
     if (r.c[s] != 0) d = std::max(d, s);
   }
+  for (const auto& [f, c] : tf) {
+    const i128 v = checked_add(static_cast<i128>(r.cf[f]), checked_mul(c.n, L / c.d));
+    if (!fits64(v)) throw KcgError(KCG_E_UNSUPPORTED, "domain row exceeds 64 bits");
+    r.cf[f] = static_cast<int64_t>(v);
+    if (r.cf[f] != 0) d = std::max(d, fd_depth);
+  }
   if (depth) *depth = d;
   return r;
 }
@@ -145,12 +179,29 @@ struct Interval {
   i128 lo, hi;  // inclusive; lo > hi = empty
 };
 
-// range of a row's raw value over variable intervals
-Interval row_range(const KeRow& r, const std::vector<Interval>& iv, int nv) {
+i128 floor_div128(i128 a, i128 d) {  // d > 0
+  i128 q = a / d;
+  if (a % d != 0 && a < 0) q -= 1;
+  return q;
+}
+
+// range of a row's raw value over variable intervals (floor-division terms
+// over the range of their own rows)
+Interval row_range(const KeRow& r, const std::vector<Interval>& iv, int nv, const std::vector<KeFd>* fds = nullptr) {
   i128 lo = r.c0, hi = r.c0;
   for (int s = 0; s < nv; ++s) {
     if (r.c[s] == 0) continue;
     const i128 a = checked_mul(r.c[s], iv[s].lo), b = checked_mul(r.c[s], iv[s].hi);
+    lo = checked_add(lo, std::min(a, b));
+    hi = checked_add(hi, std::max(a, b));
+  }
+  for (int f = 0; f < KE_MAXF; ++f) {
+    if (r.cf[f] == 0) continue;
+    if (!fds || f >= static_cast<int>(fds->size())) throw KcgError(KCG_E_INTERNAL, "floordiv term without definition");
+    const KeFd& fd = (*fds)[f];
+    const Interval in = row_range(fd.r, iv, nv);
+    const i128 flo = floor_div128(in.lo, fd.div), fhi = floor_div128(in.hi, fd.div);
+    const i128 a = checked_mul(r.cf[f], flo), b = checked_mul(r.cf[f], fhi);
     lo = checked_add(lo, std::min(a, b));
     hi = checked_add(hi, std::max(a, b));
   }
@@ -234,6 +285,7 @@ int enumerate_points(const EnumSymbolic& E, const int64_t* binding, uint64_t cap
     const int nv = static_cast<int>(st.vars.size());
     if (nv > KE_MAXV) throw KcgError(KCG_E_UNSUPPORTED, "statement domain deeper than 12 variables");
     std::map<int, int> slot;
+    std::vector<KeFd> fds;  // floor divisions over this statement's domain variables
     k.nv = nv;
     std::vector<Interval> iv(nv);
     bool box = true;
@@ -241,10 +293,10 @@ int enumerate_points(const EnumSymbolic& E, const int64_t* binding, uint64_t cap
     for (int l = 0; l < nv; ++l) {
       const int vid = static_cast<int>(std::find(s.params.begin(), s.params.end(), st.vars[l].name) - s.params.begin());
       int dl, dh;
-      k.lo[l] = compile_row(ev, st.vars[l].lo, slot, P, &dl, false);
-      k.hi[l] = compile_row(ev, st.vars[l].hi, slot, P, &dh, false);
+      k.lo[l] = compile_row(ev, st.vars[l].lo, slot, P, &dl, false, &fds);
+      k.hi[l] = compile_row(ev, st.vars[l].hi, slot, P, &dh, false, &fds);
       slot[vid] = l;
-      const Interval rl = row_range(k.lo[l], iv, nv), rh = row_range(k.hi[l], iv, nv);
+      const Interval rl = row_range(k.lo[l], iv, nv, &fds), rh = row_range(k.hi[l], iv, nv, &fds);
       const i128 lmin = ceil_div128(rl.lo, k.lo[l].den), hmax = ceil_div128(rh.hi, k.hi[l].den);
       iv[l] = {lmin, hmax - 1};
       if (box && dl < 0 && dh < 0) {
@@ -263,7 +315,7 @@ int enumerate_points(const EnumSymbolic& E, const int64_t* binding, uint64_t cap
       KeGuard g;
       std::memset(&g, 0, sizeof g);
       int depth;
-      g.r = compile_row(ev, c.poly, slot, P, &depth, c.divisibility);
+      g.r = compile_row(ev, c.poly, slot, P, &depth, c.divisibility, &fds);
       g.depth = depth;
       g.divis = c.divisibility ? 1 : 0;
       g.op = static_cast<int>(c.op);
@@ -285,12 +337,12 @@ int enumerate_points(const EnumSymbolic& E, const int64_t* binding, uint64_t cap
       }
       if (k.ng >= KE_MAXG) throw KcgError(KCG_E_UNSUPPORTED, "more than 8 guards in a statement");
       // magnitude: |raw| over the domain box must stay within 64 bits
-      const Interval gr = row_range(g.r, iv, nv);
+      const Interval gr = row_range(g.r, iv, nv, &fds);
       if (!fits64(gr.lo) || !fits64(gr.hi)) throw KcgError(KCG_E_UNSUPPORTED, "guard value exceeds 64 bits");
       k.g[k.ng++] = g;
     }
     for (int l = 0; l < nv; ++l) {
-      const Interval a = row_range(k.lo[l], iv, nv), b = row_range(k.hi[l], iv, nv);
+      const Interval a = row_range(k.lo[l], iv, nv, &fds), b = row_range(k.hi[l], iv, nv, &fds);
       if (!fits64(a.lo) || !fits64(a.hi) || !fits64(b.lo) || !fits64(b.hi))
         throw KcgError(KCG_E_UNSUPPORTED, "domain bound exceeds 64 bits");
     }
@@ -320,8 +372,8 @@ int enumerate_points(const EnumSymbolic& E, const int64_t* binding, uint64_t cap
       if (static_cast<int>(a.idx.size()) > KE_MAXD) throw KcgError(KCG_E_UNSUPPORTED, "array rank above 4");
       std::vector<Interval> r;
       for (size_t d = 0; d < a.idx.size(); ++d) {
-        A.idx[d] = compile_row(ev, a.idx[d], slot, P, nullptr, true);
-        const Interval x = row_range(A.idx[d], iv, nv);
+        A.idx[d] = compile_row(ev, a.idx[d], slot, P, nullptr, true, &fds);
+        const Interval x = row_range(A.idx[d], iv, nv, &fds);
         if (!fits64(x.lo) || !fits64(x.hi)) throw KcgError(KCG_E_UNSUPPORTED, "array index exceeds 64 bits");
         r.push_back(x);
       }
@@ -340,6 +392,8 @@ int enumerate_points(const EnumSymbolic& E, const int64_t* binding, uint64_t cap
       }
       acc_iv[si].emplace_back(a.array, r);
     }
+    k.nf = static_cast<int32_t>(fds.size());
+    for (size_t f = 0; f < fds.size(); ++f) k.f[f] = fds[f];
   }
 
   // 2b. bitmaps per touched global array

@@ -183,3 +183,88 @@ def test_enumerate_equals_symbolic_on_every_suite_kernel_scaled():
     for kid, b in cases:
         counts, points = kc.load_enum_program(kid).enumerate_points(b)
         assert counts == _symbolic_counts(kid, b), (kid, b)
+
+
+def _fd_kernels():
+    return [k for k in load_golden("enum_fd.json")["kernels"] if "cases" in k]
+
+
+def test_floordiv_domain_kernels_parse():
+    ks = _fd_kernels()
+    assert len(ks) == 60
+    for k in ks:
+        kc.EnumProgram(k["enum_text"])
+
+
+@pytest.mark.gpu
+def test_enumerate_floordiv_over_domain_variables_matches_reference():
+    """60 random kernels whose loop bounds divide domain variables
+    (tests/gen/gen_enum_fd_kernels.py: `j = i // 3 .. (i + 1) // 2 + 1`,
+    `(i + n) // 3 + 1`, ...), which the reference walks with its generic
+    Walker (enumerate.cpp:31-90): counts, visited points and errors equal
+    its enumerate_points (tests/golden/enum_fd.json), and the domain walk
+    runs on the GPU (floor-division terms KeFd of the rows)."""
+    n_ok = 0
+    for k in _fd_kernels():
+        p = kc.EnumProgram(k["enum_text"])
+        for c in k["cases"]:
+            b = {q: int(v) for q, v in c["binding"].items()}
+            if c["status"] != "ok":
+                with pytest.raises(kc.KcgError) as e:
+                    p.enumerate_points(b)
+                assert e.value.name == c["status"], (k["id"], b)
+                continue
+            counts, points = p.enumerate_points(b)
+            want = {key: int(v) for key, v in c["counts"].items()}
+            assert counts == want, (k["id"], b, counts, want)
+            assert points == int(c["points"]), (k["id"], b, points, c["points"])
+            n_ok += 1
+    assert n_ok > 900
+
+
+GUARDED_FD = """kernelcost-enum v1
+kernel x_fdg
+param n
+assume n >= 1
+array a global 32 2 1
+array o global 32 2 1
+group (n)//2
+stmt assign
+var g0 0 | (n)//2
+var l0 0 | 4
+var i 0 | n
+var j 0 | (i)//2 + 1
+var k (j)//3 | (j + 1)//2 + 1
+guard i + l0 < n
+access o store 0 | j + 2*k | 3*j + 1
+access a load 0 | 3*k + 1 | g0 + 2*j
+op flop.f32.addsub 1
+op flop.f32.mul 2
+endstmt
+end
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2, 5, 8, 13])
+def test_enumerate_floordiv_with_guards_brute_force(n):
+    """A guarded statement with floordiv-over-domain loop bounds, the case
+    the reference's enumerate_points gets wrong (its FastDomain constructor
+    returns from the guard loop after a bound failed to compile with ok
+    still true and incomplete rows: 0 points, enumerate.cpp:204-214; see
+    DESIGN.md 4b) -- against a direct walk of the same domain with the
+    reference Walker's rules (a failing guard is one visited dead end)."""
+    leaves = visited = 0
+    for g0 in range(n // 2):
+        for l0 in range(4):
+            for i in range(n):
+                if not i + l0 < n:
+                    visited += 1
+                    continue
+                for j in range(0, i // 2 + 1):
+                    for k in range(j // 3, (j + 1) // 2 + 1):
+                        leaves += 1
+                        visited += 1
+    counts, points = kc.EnumProgram(GUARDED_FD).enumerate_points({"n": n})
+    assert points == visited
+    assert counts.get("flop.f32.addsub", 0) == leaves and counts.get("flop.f32.mul", 0) == 2 * leaves
