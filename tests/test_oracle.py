@@ -215,3 +215,28 @@ def test_keyed_gaussian_and_simulate_match_reference_bitwise():
             assert t0 * math.exp(d["sigma"] * ko.keyed_gaussian(d["seed"], c["key"], run)) == hexf(r)
     for gm in d["geomean"]:
         assert ko.geometric_mean_error(gm["pairs"]) == hexf(gm["geomean"])
+
+
+def test_markstein_division_is_correctly_rounded():
+    """The GPU's row formation kcg_div (q = RN(c r), e = RN(c - q t) exact by
+    FMA, RN(q + e r), r = RN(1/t)) equals IEEE division on random and
+    all-ones-mantissa operands (exact rational FMA emulation here; the full
+    300,000-case run is tests/gen/check_markstein_division.py)."""
+    import random
+    import struct
+    from fractions import Fraction as Fr
+
+    def fma(x, y, z):
+        return float(Fr(x) * Fr(y) + Fr(z))
+
+    def div_m(a, b):
+        r = float(Fr(1) / Fr(b))
+        q = a * r
+        return fma(fma(-q, b, a), r, q)
+
+    rng = random.Random(7)
+    for i in range(20000):
+        a = struct.unpack("<d", struct.pack("<Q", ((1023 + rng.randint(-60, 60)) << 52) | rng.getrandbits(52)))[0]
+        m = ((1 << 52) - 1 - rng.randint(0, 3)) if i % 3 == 0 else rng.getrandbits(52)
+        b = struct.unpack("<d", struct.pack("<Q", ((1023 + rng.randint(-60, 60)) << 52) | m))[0]
+        assert div_m(a, b) == a / b, (a, b)
