@@ -1028,7 +1028,7 @@ int multi_bulk_stages(int n_cols) {
 }
 size_t multi_bulk_smem_bytes(int n_cols, int V) {
   return static_cast<size_t>(multi_bulk_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * multi_tile() * 8 +
-         static_cast<size_t>(8) * multi_obuf() * V * 128 * 8;
+         static_cast<size_t>(multi_obuf()) * V * multi_tile() * 8;  // 8 warps x OB x [V][TP / 8]
 }
 
 // Which products the one-pass kernel forms once per point and shares:
@@ -1330,20 +1330,22 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
     os << "    kcg_msize<" << stv << ">(p, a, i);\n  }\n}\n";
     if (argmin || V > multi_bulk_vmax() || n_cols == 0) continue;
     // bulk-store TMA kernel (<name>_tmab[_st]): warp w owns points
-    // [128 w, 128 w + 128) of each stage; its lanes evaluate points
-    // 128 w + lane + 32 u into the warp's staging block [V][128] (double-
-    // buffered), then lane 0 writes the block's V rows to global memory
-    // with cp.async.bulk (1 KB each) -- no CTA barrier, warps drift freely
-    const int SB = multi_bulk_stages(n_cols), OB = multi_obuf();
+    // [PW w, PW w + PW) of each TP-point stage (PW = TP / 8); its lanes
+    // evaluate points PW w + lane + 32 u into the warp's staging block
+    // [V][PW] in shared memory, then lane 0 writes the block's V rows to
+    // global memory with cp.async.bulk (PW * 8 bytes each), after the
+    // block's previous stores have read it -- no CTA barrier, warps drift
+    // freely. KCG_MULTI_BULK_CTA=1: one CTA-wide [V][TP] block, one TP * 8
+    // byte store per row per stage, two barriers per stage.
+    const int SB = multi_bulk_stages(n_cols), OB = multi_obuf(), TPB = multi_tile(), PW = TPB / 8;
     os << "extern \"C\" __global__ void __launch_bounds__(256, " << multi_bulk_ctas() << ") " << name << "_tmab" << sfx
        << "(const __grid_constant__ KcgMArgs a) {\n"
-          "  constexpr int TP = " << multi_tile() << ", S = " << SB << ", NP = " << NP << ", V = " << V
-       << ", OB = " << OB << ";\n"
-          "  static_assert(TP == 1024, \"bulk kernel: 8 warps x 128 points per stage\");\n"
+          "  constexpr int TP = " << TPB << ", S = " << SB << ", NP = " << NP << ", V = " << V << ", OB = " << OB
+       << ", PW = " << PW << ";\n"
           "  extern __shared__ __align__(128) unsigned char kcg_smem[];\n"
           "  kcg_i64* buf = reinterpret_cast<kcg_i64*>(kcg_smem);\n"
           "  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;\n"
-          "  double* obase = reinterpret_cast<double*>(kcg_smem + (size_t)S * NP * TP * 8) + (size_t)w * OB * V * 128;\n"
+          "  double* obase = reinterpret_cast<double*>(kcg_smem + (size_t)S * NP * TP * 8) + (size_t)w * OB * V * PW;\n"
           "  __shared__ __align__(8) unsigned long long full[S];\n"
           "  __shared__ unsigned reads[S];\n"
           "  if (threadIdx.x < S) reads[threadIdx.x] = 0;\n"
@@ -1378,69 +1380,66 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
           "      while (!done)\n"
           "        asm volatile(\"{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }\"\n"
           "                     : \"=r\"(done) : \"r\"(fb + 8 * s), \"r\"(parity) : \"memory\");\n"
-          "    }\n"
-"    " << "";
+          "    }\n";
     if (multi_bulk_cta())
-      os <<           "    // CTA-level staging: [V][TP] for the whole stage, one 8 KB bulk store per row\n"
-          "    double* ob = reinterpret_cast<double*>(kcg_smem + (size_t)S * NP * TP * 8);\n"
-          "    if (k > 0 && threadIdx.x == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
-          "    __syncthreads();\n"
-          "    const kcg_i64 rb = tile * TP;\n"
-          "    #pragma unroll 1\n"
-          "    for (int u = 0; u < 4; ++u) {\n"
-          "      const int li = u * 256 + threadIdx.x;\n"
-          "      kcg_i64 q[NP];\n"
-          "      #pragma unroll\n"
-          "      for (int j = 0; j < NP; ++j) q[j] = buf[(s * NP + j) * TP + li];\n"
-          "      kcg_msize<" << stv << ", TP>(q, a, rb + li, ob, li);\n"
-          "    }\n"
-          "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
-          "    __syncthreads();\n"
-          "    if (threadIdx.x == 0) {\n"
-          "      const unsigned ob_s = (unsigned)__cvta_generic_to_shared(ob);\n"
-          "      #pragma unroll\n"
-          "      for (int v = 0; v < V; ++v)\n"
-          "        asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\"\n"
-          "                     :: \"l\"(a.pred + (kcg_i64)v * a.ldp + rb), \"r\"(ob_s + v * TP * 8), \"r\"(TP * 8) : \"memory\");\n"
-          "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
-          "      const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
-          "      if (nt < ntiles) issue(s, nt);  // every thread is past its reads of stage s\n"
-          "    }\n"
-          "  }\n";
+      os << "    double* ob = reinterpret_cast<double*>(kcg_smem + (size_t)S * NP * TP * 8);\n"
+            "    if (k > 0 && threadIdx.x == 0) asm volatile(\"cp.async.bulk.wait_group.read 0;\" ::: \"memory\");\n"
+            "    __syncthreads();\n"
+            "    const kcg_i64 rb = tile * TP;\n"
+            "    #pragma unroll 1\n"
+            "    for (int u = 0; u < TP / 256; ++u) {\n"
+            "      const int li = u * 256 + threadIdx.x;\n"
+            "      kcg_i64 q[NP];\n"
+            "      #pragma unroll\n"
+            "      for (int j = 0; j < NP; ++j) q[j] = buf[(s * NP + j) * TP + li];\n"
+            "      kcg_msize<" << stv << ", TP>(q, a, rb + li, ob, li);\n"
+            "    }\n"
+            "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+            "    __syncthreads();\n"
+            "    if (threadIdx.x == 0) {\n"
+            "      const unsigned ob_s = (unsigned)__cvta_generic_to_shared(ob);\n"
+            "      #pragma unroll\n"
+            "      for (int v = 0; v < V; ++v)\n"
+            "        asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\"\n"
+            "                     :: \"l\"(a.pred + (kcg_i64)v * a.ldp + rb), \"r\"(ob_s + v * TP * 8), \"r\"(TP * 8) : \"memory\");\n"
+            "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
+            "      const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+            "      if (nt < ntiles) issue(s, nt);  // every thread is past its reads of stage s\n"
+            "    }\n"
+            "  }\n";
     else
-      os <<           "    double* ob = obase + (int)(k % OB) * V * 128;\n"
-          "    if (k >= OB) {  // the block's previous bulk stores have finished reading it\n"
-          "      if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read %0;\" :: \"n\"(OB - 1) : \"memory\");\n"
-          "      __syncwarp();\n"
-          "    }\n"
-          "    const kcg_i64 rb = tile * TP + 128 * w;\n"
-          "    #pragma unroll 1\n"
-          "    for (int u = 0; u < 4; ++u) {\n"
-          "      const int li = lane + 32 * u;\n"
-          "      kcg_i64 q[NP];\n"
-          "      #pragma unroll\n"
-          "      for (int j = 0; j < NP; ++j) q[j] = buf[(s * NP + j) * TP + 128 * w + li];\n"
-          "      kcg_msize<" << stv << ", 128>(q, a, rb + li, ob, li);\n"
-          "    }\n"
-          "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
-          "    __syncwarp();\n"
-          "    if (lane == 0) {\n"
-          "      __threadfence_block();\n"
-          "      const unsigned ob_s = (unsigned)__cvta_generic_to_shared(ob);\n"
-          "      #pragma unroll\n"
-          "      for (int v = 0; v < V; ++v)\n"
-          "        asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 1024;\"\n"
-          "                     :: \"l\"(a.pred + (kcg_i64)v * a.ldp + rb), \"r\"(ob_s + v * 1024) : \"memory\");\n"
-          "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
-          "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
-          "        reads[s] = 0;\n"
-          "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
-          "        if (nt < ntiles) issue(s, nt);\n"
-          "      }\n"
-          "    }\n"
-          "  }\n"
-;
-    os <<           "  if (lane == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n"
+      os << "    double* ob = obase + (int)(k % OB) * V * PW;\n"
+            "    if (k >= OB) {  // the block's previous bulk stores have finished reading it\n"
+            "      if (lane == 0) asm volatile(\"cp.async.bulk.wait_group.read %0;\" :: \"n\"(OB - 1) : \"memory\");\n"
+            "      __syncwarp();\n"
+            "    }\n"
+            "    const kcg_i64 rb = tile * TP + PW * w;\n"
+            "    #pragma unroll 1\n"
+            "    for (int u = 0; u < PW / 32; ++u) {\n"
+            "      const int li = lane + 32 * u;\n"
+            "      kcg_i64 q[NP];\n"
+            "      #pragma unroll\n"
+            "      for (int j = 0; j < NP; ++j) q[j] = buf[(s * NP + j) * TP + PW * w + li];\n"
+            "      kcg_msize<" << stv << ", PW>(q, a, rb + li, ob, li);\n"
+            "    }\n"
+            "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+            "    __syncwarp();\n"
+            "    if (lane == 0) {\n"
+            "      __threadfence_block();\n"
+            "      const unsigned ob_s = (unsigned)__cvta_generic_to_shared(ob);\n"
+            "      #pragma unroll\n"
+            "      for (int v = 0; v < V; ++v)\n"
+            "        asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\"\n"
+            "                     :: \"l\"(a.pred + (kcg_i64)v * a.ldp + rb), \"r\"(ob_s + v * PW * 8), \"r\"(PW * 8) : \"memory\");\n"
+            "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
+            "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
+            "        reads[s] = 0;\n"
+            "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
+            "        if (nt < ntiles) issue(s, nt);\n"
+            "      }\n"
+            "    }\n"
+            "  }\n";
+    os << "  if (lane == 0) asm volatile(\"cp.async.bulk.wait_group 0;\" ::: \"memory\");\n"
           "  for (kcg_i64 i = ntiles * TP + (kcg_i64)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;\n"
           "       i += (kcg_i64)gridDim.x * blockDim.x) {\n"
           "    kcg_i64 p[NP];\n";
