@@ -1142,7 +1142,9 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
   for (int v = 0; v < V; ++v) {
     const Lowered& L = *progs[v];
     const int F = static_cast<int>(L.keys.size());
-    os << "template <int SH>\n__device__ __forceinline__ int kcg_mfastv_" << v
+    // NS = 0 (argmin without predictions): the raw sum, no NaN select --
+    // the epilogue tests the status itself
+    os << "template <int SH, int NS = 1>\n__device__ __forceinline__ int kcg_mfastv_" << v
        << "(const kcg_i64* p, const KcgMArgs& a, const double* sh, double& out) {\n";
     emit_gather(os, "q", "p", L, pmaps[v], "  ");
     os << "  double c[" << std::max(F, 1) << "];\n  const int st = kcg_fastp_" << v << "(q, c);\n  double s = 0.0;\n";
@@ -1158,8 +1160,8 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
     }
     // one opaque select (a plain ?: is pushed into every admissibility
     // check as a pair of FSELs on the result: 18 per variant)
-    os << "  asm(\"{ .reg .pred p; setp.eq.s32 p, %1, 0; selp.f64 %0, %2, 0d7FF8000000000000, p; }\"\n"
-          "      : \"=d\"(out) : \"r\"(st), \"d\"(s));\n  return st;\n}\n";
+    os << "  if (NS)\n    asm(\"{ .reg .pred p; setp.eq.s32 p, %1, 0; selp.f64 %0, %2, 0d7FF8000000000000, p; }\"\n"
+          "        : \"=d\"(out) : \"r\"(st), \"d\"(s));\n  else\n    out = s;\n  return st;\n}\n";
   }
   // out-of-line: every variant of size i, any parameter range
   // ob != nullptr (bulk-store kernels): predictions go to the warp's
@@ -1213,7 +1215,9 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
   os << "  double sh[" << NW << "];\n";
   for (size_t t = 0; t < P.wprods.size(); ++t)
     os << "  sh[" << t << "] = __dmul_rn(a.shw[" << t << "], dm" << std::get<2>(P.wprods[t]) << ");\n";
-  for (int v = 0; v < V; ++v) os << "  double s" << v << ";\n  const int st" << v << " = kcg_mfastv_" << v << "<1>(p, a, sh, s" << v << ");\n";
+  for (int v = 0; v < V; ++v)
+    os << "  double s" << v << ";\n  const int st" << v << " = kcg_mfastv_" << v << "<1, " << (argmin ? "ST" : "1")
+       << ">(p, a, sh, s" << v << ");\n";
   // ST: pred mode -- status bytes too; argmin mode -- all predictions too
   if (!argmin) {
     os << "  if (BULK) {\n";
