@@ -189,7 +189,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fit", action="store_true", help="skip the sharded fit (config 5)")
     ap.add_argument("--fit-rows", type=int, default=10**9, help="fit rows per rank")
-    ap.add_argument("--extras", action="store_true", help="also time config 1, config 5 on one GPU, the grid "
+    ap.add_argument("--extras", action="store_true", help="also time config 5 on one GPU, the grid "
                     "descriptor path and the enumeration oracle")
     ap.add_argument("--no-configs", action="store_true", help="skip argmin / config 2 / config 3 in the line")
     args = ap.parse_args()
@@ -689,11 +689,52 @@ def _fp64_peak(torch, dev):
 
 def _configs(kc, torch, dev, args, cols, progs, w):
     """Configs the default line carries beside the headline:
-    the fused config-4 argmin over the same lattice, config 2 (1e6 points of
-    the four test kernels) and the config-3 Gram (1e8 x 40 fp64 rows)."""
+    config 1 (the reference's campaign CSV -> fit -> test predictions, with
+    the reference CLI path timed beside it), the fused config-4 argmin over
+    the same lattice, config 2 (1e6 points of the four test kernels) and the
+    config-3 Gram (1e8 x 40 fp64 rows)."""
     out = {}
     hbm, _ = peaks()
     stream = torch.cuda.current_stream(dev).cuda_stream
+    sim_alpha = w.alpha
+
+    # ---- config 1: the reference's own campaign CSV (390 measurement cases,
+    # simdev-v1, sigma 0) -> fit -> predict the 16 test cases (suite.cpp
+    # test sizes, incl. fd_stencil n=512 and nbody n=2048) on the GPU; the
+    # reference CLI path (campaign + bound extraction + fit + eval) beside it
+    golden = ROOT / "tests" / "golden"
+    tests = json.loads((golden / "fit_suite.json").read_text())["test_predictions"]
+    tprogs = {t["kernel"]: kc.load_program(t["kernel"]) for t in tests}
+
+    def c1():
+        wf, rep = kc.fit_from_csv(golden / "meas_sigma0.csv", device="simdev-v1")
+        outp = []
+        for t in tests:
+            p = tprogs[t["kernel"]]
+            outp.append(kc.predict(wf, p, {q: torch.tensor([int(t["binding"][q])], dtype=torch.int64, device=dev)
+                                           for q in p.params}))
+        torch.cuda.synchronize()
+        return wf, rep, outp
+    c1()
+    t0 = time.perf_counter()
+    wf, rep, outp = c1()
+    sec1 = time.perf_counter() - t0
+    rel = max(abs(float(o.item()) - float.fromhex(t["predicted_s"][1])) / abs(float.fromhex(t["predicted_s"][1]))
+              for o, t in zip(outp, tests))
+    ref1 = None
+    exe = ROOT / "oracle" / "_ref" / "kcref_bench"
+    if exe.exists():
+        try:
+            ref1 = json.loads(subprocess.run([str(exe), "config1"], capture_output=True, text=True,
+                                             timeout=300).stdout)
+        except Exception as e:  # noqa: BLE001
+            ref1 = {"error": str(e)[:200]}
+    out["config1_suite_fit_eval"] = {
+        "cases": rep["n_cases"], "test_cases": len(tests), "gpu_ms": sec1 * 1e3,
+        "max_rel_diff_test_predictions_vs_reference": rel, "cpu_reference": ref1,
+        "note": "GPU: kcg_measurements_read_csv + per-kernel fused Gram + solve + 2 refinement steps + residual + 16 predictions "
+                "(wall clock, ~70 launches); CPU: the reference's run_campaign + extract_properties (bound, "
+                "cap 2e7) + fit_weights + predict, 1 thread"}
 
     # ---- config 2: 1e6 points over the 4 test kernels (250k each) ----------
     U = 250_000
@@ -797,52 +838,14 @@ def _configs(kc, torch, dev, args, cols, progs, w):
 
 
 def _extras(kc, torch, dev, args):
-    """Config 1, config 5 on one GPU, the grid-descriptor path and the GPU
-    enumeration oracle (--extras)."""
+    """Config 5 on one GPU, the grid-descriptor path and the GPU enumeration
+    oracle (--extras)."""
     import ctypes
     out = {}
     hbm, _ = peaks()
     sim_alpha = _simdev_alpha(kc)
     w = kc.ModelWeights(device="simdev-v1", alpha=sim_alpha, covered=[a != 0 for a in sim_alpha])
     stream = torch.cuda.current_stream(dev).cuda_stream
-
-    # ---- config 1: the reference's own campaign CSV (390 measurement cases,
-    # simdev-v1, sigma 0) -> fit -> predict the 16 test cases (suite.cpp
-    # test sizes, incl. fd_stencil n=512 and nbody n=2048) on the GPU; the
-    # reference CLI path (campaign + bound extraction + fit + eval) beside it
-    golden = ROOT / "tests" / "golden"
-    tests = json.loads((golden / "fit_suite.json").read_text())["test_predictions"]
-    tprogs = {t["kernel"]: kc.load_program(t["kernel"]) for t in tests}
-
-    def c1():
-        wf, rep = kc.fit_from_csv(golden / "meas_sigma0.csv", device="simdev-v1")
-        outp = []
-        for t in tests:
-            p = tprogs[t["kernel"]]
-            outp.append(kc.predict(wf, p, {q: torch.tensor([int(t["binding"][q])], dtype=torch.int64, device=dev)
-                                           for q in p.params}))
-        torch.cuda.synchronize()
-        return wf, rep, outp
-    c1()
-    t0 = time.perf_counter()
-    wf, rep, outp = c1()
-    sec1 = time.perf_counter() - t0
-    rel = max(abs(float(o.item()) - float.fromhex(t["predicted_s"][1])) / abs(float.fromhex(t["predicted_s"][1]))
-              for o, t in zip(outp, tests))
-    ref1 = None
-    exe = ROOT / "oracle" / "_ref" / "kcref_bench"
-    if exe.exists():
-        try:
-            ref1 = json.loads(subprocess.run([str(exe), "config1"], capture_output=True, text=True,
-                                             timeout=300).stdout)
-        except Exception as e:  # noqa: BLE001
-            ref1 = {"error": str(e)[:200]}
-    out["config1_suite_fit_eval"] = {
-        "cases": rep["n_cases"], "test_cases": len(tests), "gpu_ms": sec1 * 1e3,
-        "max_rel_diff_test_predictions_vs_reference": rel, "cpu_reference": ref1,
-        "note": "GPU: kcg_measurements_read_csv + per-kernel fused Gram + solve + residual + 16 predictions "
-                "(wall clock, ~70 launches); CPU: the reference's run_campaign + extract_properties (bound, "
-                "cap 2e7) + fit_weights + predict, 1 thread"}
 
     side = args.side
     total = side ** 3
