@@ -12,7 +12,9 @@ import re
 from pathlib import Path
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_lib" / "libkcg.so"
+# KCG_LIB: another build of the same library (e.g. the ASan/UBSan build of
+# `make -C paper_1604_04997_b200/csrc asan`, run under LD_PRELOAD=libasan)
+LIB_PATH = Path(os.environ["KCG_LIB"]) if os.environ.get("KCG_LIB") else _PKG / "_lib" / "libkcg.so"
 HEADER_PATH = _PKG.parent / "include" / "kcg.h"
 
 _lib = None
