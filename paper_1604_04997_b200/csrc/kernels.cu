@@ -543,6 +543,292 @@ void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, 
   check(cudaGetLastError(), "kcg_gram_dmma launch");
 }
 
+// ---------------------------------------------------------------------------
+// Hybrid DMMA + DFMA Gram for NB = 4, 5 (even F in (8 (NB - 1), 8 NB])
+//
+// On B200 the FP64 tensor instruction (DMMA m8n8k4) and DFMA share one FP64
+// datapath at the same flop rate: a warp mix of both runs in the sum of their
+// separate times (profiles/dmma_dfma_probe.cu, r02_dmma_dfma.json: 37.1 and
+// 37.0 TFLOP/s alone, mixed / sum = 1.05). So the block-diagonal 8 x 8 tiles,
+// where a DMMA spends 64 products on 36 distinct entries, are cheaper as
+// DFMAs of their upper triangles: at F = 40 a row costs 10 x 64 + 5 x 36 =
+// 820 FP64 multiply-adds instead of 15 x 64 = 960.
+//
+// Every warp issues both kinds, in the proportion of the work: a first
+// version with DFMA-only warps (one per SM sub-partition) ran at 8.1 ms
+// instead of 6.2 -- the scheduler hands the shared pipe out per instruction,
+// so the DFMA warp got one 2-cycle DFMA per 16-cycle DMMA and starved
+// (ncu: DMMA active 42%, the DMMA warps spinning on the stage barrier).
+// Measured at 1e8 x 40: 6.15 ms against 6.27 for kcg_gram_dmma (three
+// interleaved runs) -- the 15% fewer FP64 operations are mostly given back
+// because 36 DFMA accumulators hold a warp at 229 registers, so only two
+// warps share a sub-partition and tile-boundary latency (barrier wait,
+// shared loads, the stage release) is exposed; it is the default at F = 40
+// only (at F = 32 it is slower: 5.11 vs 4.52 ms).
+//
+// 256 threads, one CTA per SM (up to 255 registers: 20 DMMA accumulators,
+// 36 DFMA accumulators), two groups of 4 warps taking alternate R-row tiles.
+// Each warp owns RW = R / 4 rows of its group's tile: the DMMA k-steps of the
+// NB (NB - 1) / 2 off-diagonal tiles plus X^T 1 and the column maxima over
+// those rows (kcg_gram_dmma's k-step without the diagonal tiles), and the
+// diagonal blocks of the same rows on DFMA: lane l < NB J (J = 32 / NB) owns
+// block l % NB for rows j + J u (j = l / NB), loads the block's 8 values of a
+// row as four 16-byte shared loads and accumulates its 36 products. The
+// 16-byte loads are staggered per lane pair (pair s of the block is loaded
+// at step (s - c) mod 4, c = (l / 2) % 4) so the 8 lanes of a quarter-warp
+// hit 8 distinct bank groups at F = 40.
+template <int NB, int R, bool FULL>
+__global__ void __launch_bounds__(256, 1)
+    kcg_gram_hybrid(const double* __restrict__ X, kcg_i64 n, int F_, int stages,
+                    double* __restrict__ G, double* __restrict__ xt1, double* __restrict__ cmax) {
+  constexpr int NW = 8;
+  // FULL: F == 8 NB, a compile-time row pitch and no column predicates
+  const int F = FULL ? NB * 8 : F_;
+  constexpr int J = 32 / NB;
+  constexpr int NOFF = NB * (NB - 1) / 2;
+  constexpr int FP = NB * 8;
+  constexpr int RW = R / 4;  // rows per warp per tile (a tile belongs to one group of 4 warps)
+  constexpr int TD = RW / J;  // rows per DFMA lane per tile
+  static_assert(RW % 4 == 0 && RW % J == 0, "tile shape");
+  extern __shared__ __align__(128) unsigned char kcg_smem[];
+  double* buf = reinterpret_cast<double*>(kcg_smem);
+  const int stage_d = R * F;
+  double* red = buf + stages * stage_d;  // [FP][FP] + s1[FP] + mx[FP]
+  double* red_s1 = red + FP * FP;
+  double* red_mx = red_s1 + FP;
+  __shared__ __align__(8) unsigned long long full[16];
+  __shared__ unsigned reads[16];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int gid = lane >> 2, tig = lane & 3;
+  for (int k = tid; k < FP * FP + 2 * FP; k += blockDim.x) red[k] = 0.0;
+  if (tid < 16) reads[tid] = 0;
+  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);
+  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fb + 8 * s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const kcg_i64 ntiles = n / R;
+  const unsigned bytes = (unsigned)(stage_d * 8);
+  auto issue = [&](int s, kcg_i64 tile) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb + 8 * s), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     bb + (unsigned)(s * stage_d * 8)),
+                 "l"(X + tile * stage_d), "r"(bytes), "r"(fb + 8 * s)
+                 : "memory");
+  };
+  if (tid == 0)
+    for (int s = 0; s < stages; ++s) {
+      const kcg_i64 t = blockIdx.x + (kcg_i64)s * gridDim.x;
+      if (t < ntiles) issue(s, t);
+    }
+
+  // DMMA part: off-diagonal tiles, X^T 1, column maxima
+  double acc[NOFF][2];
+#pragma unroll
+  for (int t = 0; t < NOFF; ++t) acc[t][0] = acc[t][1] = 0.0;
+  double s1[NB];
+  unsigned long long mx[NB];
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    s1[b] = 0.0;
+    mx[b] = 0ull;
+  }
+  auto kstep = [&](const double* v) {
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      s1[b] += v[b];
+      const unsigned long long bits = abs_bits(v[b]);
+      mx[b] = bits > mx[b] ? bits : mx[b];
+    }
+    int t = 0;
+#pragma unroll
+    for (int I = 0; I < NB; ++I)
+#pragma unroll
+      for (int Jb = I + 1; Jb < NB; ++Jb, ++t) dmma_8x8x4(acc[t][0], acc[t][1], v[I], v[Jb]);
+  };
+  // DFMA part: one diagonal block per lane, 36 accumulators
+  const bool act = lane < NB * J;
+  const int db = lane % NB, dj = act ? lane / NB : 0;  // idle lanes re-read row 0: no predicate
+  const int dc = (lane >> 1) & 3;
+  int off[4];
+  bool ok[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    off[s] = 8 * db + 2 * ((s + dc) & 3);
+    ok[s] = FULL || off[s] < F;
+  }
+  double a[36];
+#pragma unroll
+  for (int k = 0; k < 36; ++k) a[k] = 0.0;
+  auto diag = [&](const double* row) {
+    double w[8];
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      // lanes >= NB J read real rows too; their accumulators are never
+      // written out
+      const double2 x = ok[s] ? *reinterpret_cast<const double2*>(row + off[s]) : make_double2(0.0, 0.0);
+      w[2 * s] = x.x;
+      w[2 * s + 1] = x.y;
+    }
+    int k = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q = p; q < 8; ++q, ++k) a[k] = fma(w[p], w[q], a[k]);
+  };
+
+  // warp group g = warp / 4 (one warp per SM sub-partition) takes the tiles
+  // k = g (mod 2): the two warps sharing a sub-partition work on different
+  // tiles, so one's barrier wait / load / release phase overlaps the
+  // other's FP64 work. `stages` is even, so stage s = k mod stages always
+  // belongs to the same group; s and the parity advance incrementally.
+  const int grp = warp >> 2, wg = warp & 3;
+  int s = grp;
+  unsigned parity = 0;
+  for (kcg_i64 k = grp;; k += 2) {
+    const kcg_i64 tile = blockIdx.x + k * gridDim.x;
+    if (tile >= ntiles) break;
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(fb + 8 * s), "r"(parity)
+                   : "memory");
+    const double* st = buf + s * stage_d + wg * RW * F;
+#pragma unroll
+    for (int u = 0; u < TD; ++u) diag(st + (dj + J * u) * F);
+#pragma unroll
+    for (int ks = 0; ks < RW / 4; ++ks) {
+      double v[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int col = 8 * b + gid;
+        v[b] = (FULL || col < F) ? st[(4 * ks + tig) * F + col] : 0.0;
+      }
+      kstep(v);
+    }
+    // the last of the group's 4 warps to finish reading stage s refills it
+    // with tile k + stages (same group)
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      if (atomicAdd(&reads[s], 1u) == 3) {
+        reads[s] = 0;
+        const kcg_i64 nt = blockIdx.x + (k + stages) * gridDim.x;
+        if (nt < ntiles) issue(s, nt);
+      }
+    }
+    s += 2;
+    if (s >= stages) {
+      s -= stages;
+      parity ^= 1u;
+    }
+  }
+  // tail rows straight from global (block 0 only)
+  if (blockIdx.x == 0) {
+    for (kcg_i64 r0 = ntiles * R + warp * 4; r0 < n; r0 += 4 * NW) {
+      const kcg_i64 r = r0 + tig;
+      double v[NB];
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        const int col = 8 * b + gid;
+        v[b] = (r < n && col < F) ? X[r * F + col] : 0.0;
+      }
+      kstep(v);
+    }
+    for (kcg_i64 r = ntiles * R + warp * J + dj; r < n; r += NW * J) diag(X + r * F);
+  }
+  // reduce through shared memory, then one atomic per entry
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    double x = s1[b];
+    unsigned long long m = mx[b];
+    x += __shfl_xor_sync(0xffffffffu, x, 1);
+    x += __shfl_xor_sync(0xffffffffu, x, 2);
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+      const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+      m = y > m ? y : m;
+    }
+    if (tig == 0) {
+      atomicAdd(red_s1 + 8 * b + gid, x);
+      atomicMax(reinterpret_cast<unsigned long long*>(red_mx + 8 * b + gid), m);
+    }
+  }
+  {
+    int t = 0;
+#pragma unroll
+    for (int I = 0; I < NB; ++I)
+#pragma unroll
+      for (int Jb = I + 1; Jb < NB; ++Jb, ++t) {
+        atomicAdd(red + (8 * I + gid) * FP + 8 * Jb + 2 * tig, acc[t][0]);
+        atomicAdd(red + (8 * I + gid) * FP + 8 * Jb + 2 * tig + 1, acc[t][1]);
+      }
+  }
+  if (act) {
+    int k = 0;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+#pragma unroll
+      for (int q = p; q < 8; ++q, ++k) {
+        const int fp = 2 * (((p >> 1) + dc) & 3) + (p & 1), fq = 2 * (((q >> 1) + dc) & 3) + (q & 1);
+        const int lo = fp < fq ? fp : fq, hi = fp < fq ? fq : fp;
+        atomicAdd(red + (8 * db + lo) * FP + 8 * db + hi, a[k]);
+      }
+  }
+  __syncthreads();
+  for (int e = tid; e < FP * FP; e += blockDim.x) {
+    const int r = e / FP, c = e % FP;
+    if (r >= F || c >= F || (c / 8) < (r / 8) || ((c / 8) == (r / 8) && c < r)) continue;
+    const double v = red[e];
+    atomicAdd(G + r * F + c, v);
+    if (c != r) atomicAdd(G + c * F + r, v);
+  }
+  for (int c = tid; c < F; c += blockDim.x) {
+    atomicAdd(xt1 + c, red_s1[c]);
+    atomicMax(reinterpret_cast<unsigned long long*>(cmax + c), (unsigned long long)__double_as_longlong(red_mx[c]));
+  }
+}
+
+template <int NB, int R = (NB == 5 ? 48 : 64)>
+void launch_gram_hybrid(const double* X, size_t n, int F, double* G, double* xt1, double* colmax,
+                        cudaStream_t stream) {
+  const size_t red_b = (size_t)(NB * 8 * NB * 8 + 2 * NB * 8) * sizeof(double);
+  static const int ring_kb = std::getenv("KCG_GRAM_HYBRID_RING_KB") ? std::atoi(std::getenv("KCG_GRAM_HYBRID_RING_KB")) : 200;
+  int stages = (int)(((size_t)ring_kb * 1024 - red_b) / ((size_t)R * F * 8));
+  stages = stages < 2 ? 2 : (stages > 16 ? 16 : stages);
+  stages &= ~1;  // even: a stage always holds the tiles of one warp group
+  const size_t smem = (size_t)stages * R * F * sizeof(double) + red_b;
+  static std::mutex mu;
+  static size_t attr_smem[64] = {};
+  int dev = 0;
+  check(cudaGetDevice(&dev), "cudaGetDevice");
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = attr_smem[dev & 63];
+    if (smem + 4096 > cur) {
+      check(cudaFuncSetAttribute(kcg_gram_hybrid<NB, R, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem + 4096),
+            "cudaFuncSetAttribute");
+      check(cudaFuncSetAttribute(kcg_gram_hybrid<NB, R, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem + 4096),
+            "cudaFuncSetAttribute");
+      cur = smem + 4096;
+    }
+  }
+  const kcg_i64 tiles = (kcg_i64)n / R;
+  kcg_i64 grid = (kcg_i64)num_sms();
+  if (grid > tiles) grid = tiles > 0 ? tiles : 1;
+  if (F == NB * 8)
+    kcg_gram_hybrid<NB, R, true><<<(unsigned)grid, 256, smem, stream>>>(X, (kcg_i64)n, F, stages, G, xt1, colmax);
+  else
+    kcg_gram_hybrid<NB, R, false><<<(unsigned)grid, 256, smem, stream>>>(X, (kcg_i64)n, F, stages, G, xt1, colmax);
+  check(cudaGetLastError(), "kcg_gram_hybrid launch");
+}
+
 // double-double helpers: (hi, lo) with |lo| <= ulp(hi) / 2
 __device__ __forceinline__ void kcg_two_sum(double a, double b, double& s, double& e) {
   s = __dadd_rn(a, b);
@@ -752,6 +1038,15 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
     static const bool tall = !(std::getenv("KCG_DMMA_TALL") && std::atoi(std::getenv("KCG_DMMA_TALL")) == 0);
     // 256-row tiles for NB = 3 too (F = 24: 2.81 -> 2.74 ms, 7.0 TB/s); KCG_DMMA_TALL3=0 restores 128
     static const bool tall3 = !(std::getenv("KCG_DMMA_TALL3") && std::atoi(std::getenv("KCG_DMMA_TALL3")) == 0);
+    // DMMA off-diagonal + DFMA diagonal blocks (kcg_gram_hybrid): the
+    // default at F = 40 (1e8 rows: 6.15 vs 6.27 ms, three interleaved runs,
+    // profiles/ab_gram_hybrid.sh); KCG_GRAM_HYBRID=1 takes it for every even
+    // F in 26..40 (F = 32: 5.11 vs 4.52 ms, slower), =0 never
+    static const int hybrid_mode = std::getenv("KCG_GRAM_HYBRID") ? std::atoi(std::getenv("KCG_GRAM_HYBRID")) : -1;
+    const bool hybrid = hybrid_mode == 1 || (hybrid_mode == -1 && F == 40);
+    if (hybrid && F % 2 == 0 && (nb == 4 || nb == 5))
+      return nb == 4 ? launch_gram_hybrid<4>(X, n, F, G, xt1, colmax, st)
+                     : launch_gram_hybrid<5>(X, n, F, G, xt1, colmax, st);
     switch (nb) {
       case 1:
         // very narrow rows: taller tiles keep every bulk copy >= 16 KB

@@ -580,13 +580,13 @@ def test_predict_detail_matches_reference_predictions():
 
 def test_gram_accumulate_random_shapes():
     """Every Gram path (DMMA row-split for F <= 72 -- two CTAs per SM up to
-    F = 40, one beyond --, per-width DMMA for 73..160, CUDA-core for strided
-    / unaligned X) against torch fp64 on random widths, row counts (tails
-    included) and layouts."""
+    F = 40, one beyond --, the DMMA + DFMA hybrid at F = 40,
+    per-width DMMA for 73..160, CUDA-core for strided / unaligned X) against
+    torch fp64 on random widths, row counts (tails included) and layouts."""
     rng = np.random.default_rng(123)
-    widths = [1, 2, 5, 8, 13, 31, 41, 48, 49, 57, 64, 65, 72, 73, 80, 81, 111, 131, 149, 160]
+    widths = [1, 2, 5, 8, 13, 26, 31, 32, 34, 40, 41, 48, 49, 57, 64, 65, 72, 73, 80, 81, 111, 131, 149, 160]
     for F in widths:
-        N = int(rng.integers(1, 5000)) + (70_000 if F in (2, 41, 57, 72, 131) else 0)
+        N = int(rng.integers(1, 5000)) + (70_000 if F in (2, 32, 40, 41, 57, 72, 131) else 0)
         ld = F + (3 if F % 3 == 0 else 0)  # some strided layouts
         base = torch.tensor(rng.uniform(0.5, 2.0, size=(N, ld)) * 10.0 ** rng.integers(-2, 3, size=ld),
                             device="cuda")
@@ -670,3 +670,33 @@ def test_fit_fused_reaches_the_exact_min_norm_solution():
         alpha, rk, obj, st = kc.fit_fused(prog, dev, Td)
         err = fit_errors(alpha, [float(a) for a in exa], np.abs(X[:, cols]).max(axis=0))
         assert max(err) <= 1.0, (kid, rank, err)
+
+
+_HYBRID_CHECK = r"""
+import numpy as np, torch
+import paper_1604_04997_b200 as kc
+rng = np.random.default_rng(7)
+for F, N in ((26, 4813), (32, 100_003), (34, 50_017), (40, 200_041), (40, 47)):
+    X = torch.tensor(rng.uniform(0.5, 2.0, size=(N, F)) * 10.0 ** rng.integers(-2, 3, size=F), device="cuda")
+    st = kc.gram_accumulate(X)
+    torch.testing.assert_close(st.G, X.T @ X, rtol=1e-12, atol=0, msg=f"F={F} N={N}")
+    torch.testing.assert_close(st.xt1, X.sum(0), rtol=1e-12, atol=0)
+    assert torch.equal(st.colmax, X.abs().max(0).values), F
+print("ok")
+"""
+
+
+def test_gram_hybrid_opt_in_matches_torch():
+    """The opt-in DMMA + DFMA Gram (KCG_GRAM_HYBRID=1: off-diagonal 8 x 8
+    blocks on DMMA, diagonal blocks' upper triangles on DFMA, even F in
+    26..40) against torch fp64, tails included. In a subprocess: the switch
+    is read once per process."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    env = {**os.environ, "KCG_GRAM_HYBRID": "1"}
+    r = subprocess.run([sys.executable, "-c", _HYBRID_CHECK], env=env, capture_output=True, text=True, timeout=900,
+                       cwd=str(Path(__file__).resolve().parent.parent))
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
