@@ -831,7 +831,7 @@ def _configs(kc, torch, dev, args, cols, progs, w):
         "hbm_achieved_GBps": 8 * F * N / sec / 1e9, "hbm_frac": 8 * F * N / sec / 1e9 / hbm,
         "fp64_tflops": flops / sec / 1e12, "fp64_peak_tflops_measured_dgemm": fp64,
         "fp64_frac": flops / sec / 1e12 / fp64, "slice_rel_err_vs_torch": rel,
-        "kernel": "kcg_gram_hybrid<5,48,true> (AOT: off-diagonal 8x8 blocks on DMMA m8n8k4 f64, diagonal blocks' upper triangles on DFMA, TMA-staged rows)"}
+        "kernel": "kcg_gram_hybrid<5,96,true> (AOT: off-diagonal 8x8 blocks on DMMA m8n8k4 f64, diagonal blocks' upper triangles on DFMA, TMA-staged rows)"}
     del X, Xs, st, st2, ref
 
     return out

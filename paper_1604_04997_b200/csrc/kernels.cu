@@ -559,12 +559,13 @@ void launch_gram_dmma(const double* X, size_t n, int F, double* G, double* xt1, 
 // instead of 6.2 -- the scheduler hands the shared pipe out per instruction,
 // so the DFMA warp got one 2-cycle DFMA per 16-cycle DMMA and starved
 // (ncu: DMMA active 42%, the DMMA warps spinning on the stage barrier).
-// Measured at 1e8 x 40: 6.15 ms against 6.27 for kcg_gram_dmma (three
-// interleaved runs) -- the 15% fewer FP64 operations are mostly given back
-// because 36 DFMA accumulators hold a warp at 229 registers, so only two
-// warps share a sub-partition and tile-boundary latency (barrier wait,
-// shared loads, the stage release) is exposed; it is the default at F = 40
-// only (at F = 32 it is slower: 5.11 vs 4.52 ms).
+// Measured at 1e8 x 40: 5.95 ms against 6.19 for kcg_gram_dmma
+// (interleaved runs) with 96-row warp-group tiles (48 rows: 6.15 ms) --
+// most of the 15% fewer FP64 operations are given back because 36 DFMA
+// accumulators hold a warp at 250 registers, so only two warps share a
+// sub-partition and tile-boundary latency (barrier wait, shared loads, the
+// stage release) is exposed. Default for NB = 5 (at F = 32 it is slower:
+// 4.72 vs 4.53 ms).
 //
 // 256 threads, one CTA per SM (up to 255 registers: 20 DMMA accumulators,
 // 36 DFMA accumulators), two groups of 4 warps taking alternate R-row tiles.
@@ -793,7 +794,7 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-template <int NB, int R = (NB == 5 ? 48 : 64)>
+template <int NB, int R>
 void launch_gram_hybrid(const double* X, size_t n, int F, double* G, double* xt1, double* colmax,
                         cudaStream_t stream) {
   const size_t red_b = (size_t)(NB * 8 * NB * 8 + 2 * NB * 8) * sizeof(double);
@@ -1039,14 +1040,24 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
     // 256-row tiles for NB = 3 too (F = 24: 2.81 -> 2.74 ms, 7.0 TB/s); KCG_DMMA_TALL3=0 restores 128
     static const bool tall3 = !(std::getenv("KCG_DMMA_TALL3") && std::atoi(std::getenv("KCG_DMMA_TALL3")) == 0);
     // DMMA off-diagonal + DFMA diagonal blocks (kcg_gram_hybrid): the
-    // default at F = 40 (1e8 rows: 6.15 vs 6.27 ms, three interleaved runs,
-    // profiles/ab_gram_hybrid.sh); KCG_GRAM_HYBRID=1 takes it for every even
-    // F in 26..40 (F = 32: 5.11 vs 4.52 ms, slower), =0 never
+    // default for even F in 34..40 (1e8 rows, interleaved runs,
+    // profiles/ab_gram_hybrid_r.sh: F = 40 5.95 vs 6.19 ms, F = 36 6.18 vs
+    // 6.23); KCG_GRAM_HYBRID=1 takes it for even F in 26..32 too (F = 32:
+    // 4.72 vs 4.53 ms, slower), =0 never
     static const int hybrid_mode = std::getenv("KCG_GRAM_HYBRID") ? std::atoi(std::getenv("KCG_GRAM_HYBRID")) : -1;
-    const bool hybrid = hybrid_mode == 1 || (hybrid_mode == -1 && F == 40);
+    const bool hybrid = hybrid_mode == 1 || (hybrid_mode == -1 && nb == 5);
     if (hybrid && F % 2 == 0 && (nb == 4 || nb == 5))
-      return nb == 4 ? launch_gram_hybrid<4>(X, n, F, G, xt1, colmax, st)
-                     : launch_gram_hybrid<5>(X, n, F, G, xt1, colmax, st);
+    {
+      static const int hr = std::getenv("KCG_GRAM_HYBRID_R") ? std::atoi(std::getenv("KCG_GRAM_HYBRID_R")) : 96;
+      // rows per warp-group tile: 96 at NB = 5 (48: 6.15 ms, 144: 6.10 ms at
+      // F = 40), 128 at NB = 4 (64: 5.12 ms at F = 32)
+      static const int hr4 = std::getenv("KCG_GRAM_HYBRID_R4") ? std::atoi(std::getenv("KCG_GRAM_HYBRID_R4")) : 128;
+      if (nb == 4) return hr4 == 128 ? launch_gram_hybrid<4, 128>(X, n, F, G, xt1, colmax, st)
+                                     : launch_gram_hybrid<4, 64>(X, n, F, G, xt1, colmax, st);
+      if (hr == 48) return launch_gram_hybrid<5, 48>(X, n, F, G, xt1, colmax, st);
+      if (hr == 144) return launch_gram_hybrid<5, 144>(X, n, F, G, xt1, colmax, st);
+      return launch_gram_hybrid<5, 96>(X, n, F, G, xt1, colmax, st);
+    }
     switch (nb) {
       case 1:
         // very narrow rows: taller tiles keep every bulk copy >= 16 KB

@@ -580,7 +580,7 @@ def test_predict_detail_matches_reference_predictions():
 
 def test_gram_accumulate_random_shapes():
     """Every Gram path (DMMA row-split for F <= 72 -- two CTAs per SM up to
-    F = 40, one beyond --, the DMMA + DFMA hybrid at F = 40,
+    F = 40, one beyond --, the DMMA + DFMA hybrid for even F in 34..40,
     per-width DMMA for 73..160, CUDA-core for strided / unaligned X) against
     torch fp64 on random widths, row counts (tails included) and layouts."""
     rng = np.random.default_rng(123)
