@@ -723,9 +723,7 @@ void emit_tma_kernel(std::ostringstream& os, int n_cols, const std::string& name
                       "    }\n"
                       "    __syncwarp();\n"
                       "    if ((threadIdx.x & 31) == 0) {\n"
-                      "      __threadfence_block();\n"
-                      "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
-                      "        reads[s] = 0;\n"
+                      "      if (kcg_ring_release(&reads[s], blockDim.x / 32)) {\n"
                       "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
                       "        if (nt < ntiles) issue(s, nt);\n"
                       "      }\n"
@@ -1294,9 +1292,7 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
     const char* release =
         "    __syncwarp();\n"
         "    if ((threadIdx.x & 31) == 0) {\n"
-        "      __threadfence_block();\n"
-        "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
-        "        reads[s] = 0;\n"
+        "      if (kcg_ring_release(&reads[s], blockDim.x / 32)) {\n"
         "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
         "        if (nt < ntiles) issue(s, nt);\n"
         "      }\n"
@@ -1429,15 +1425,13 @@ void emit_multi(std::ostringstream& os, const std::vector<const Lowered*>& progs
             "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
             "    __syncwarp();\n"
             "    if (lane == 0) {\n"
-            "      __threadfence_block();\n"
             "      const unsigned ob_s = (unsigned)__cvta_generic_to_shared(ob);\n"
             "      #pragma unroll\n"
             "      for (int v = 0; v < V; ++v)\n"
             "        asm volatile(\"cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\"\n"
             "                     :: \"l\"(a.pred + (kcg_i64)v * a.ldp + rb), \"r\"(ob_s + v * PW * 8), \"r\"(PW * 8) : \"memory\");\n"
             "      asm volatile(\"cp.async.bulk.commit_group;\" ::: \"memory\");\n"
-            "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
-            "        reads[s] = 0;\n"
+            "      if (kcg_ring_release(&reads[s], blockDim.x / 32)) {\n"
             "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
             "        if (nt < ntiles) issue(s, nt);\n"
             "      }\n"
@@ -2043,9 +2037,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
       "    // warps drift apart freely between tiles)\n"
       "    __syncwarp();\n"
       "    if ((threadIdx.x & 31) == 0) {\n"
-      "      __threadfence_block();\n"
-      "      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {\n"
-      "        reads[s] = 0;\n"
+      "      if (kcg_ring_release(&reads[s], blockDim.x / 32)) {\n"
       "        const kcg_i64 nt = blockIdx.x + (k + S) * gridDim.x;\n"
       "        if (nt < ntiles) issue(s, nt);\n"
       "      }\n"

@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include "kcg_device.cuh"
 #include "kcg_kernels.hpp"
@@ -324,6 +325,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// stage hand-back: kcg_ring_release (kcg_device.cuh)
 // R: rows per tile (64 * m): narrow designs take taller tiles so every
 // stage is still a multi-KB bulk copy
 template <int NB, int R, int CT>
@@ -446,13 +448,9 @@ __global__ void __launch_bounds__(256, CT)
       v[b] = col < F ? st[(warp * RW + RW - 4 + tig) * F + col] : 0.0;
     }
     __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      if (atomicAdd(&reads[s], 1u) == blockDim.x / 32 - 1) {
-        reads[s] = 0;
-        const kcg_i64 nt = blockIdx.x + (k + stages) * gridDim.x;
-        if (nt < ntiles) issue(s, nt);
-      }
+    if (lane == 0 && kcg_ring_release(&reads[s], blockDim.x / 32)) {
+      const kcg_i64 nt = blockIdx.x + (k + stages) * gridDim.x;
+      if (nt < ntiles) issue(s, nt);
     }
     kstep_regs(v);
   }
@@ -714,13 +712,9 @@ __global__ void __launch_bounds__(256, 1)
     // the last of the group's 4 warps to finish reading stage s refills it
     // with tile k + stages (same group)
     __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      if (atomicAdd(&reads[s], 1u) == 3) {
-        reads[s] = 0;
-        const kcg_i64 nt = blockIdx.x + (k + stages) * gridDim.x;
-        if (nt < ntiles) issue(s, nt);
-      }
+    if (lane == 0 && kcg_ring_release(&reads[s], 4)) {
+      const kcg_i64 nt = blockIdx.x + (k + stages) * gridDim.x;
+      if (nt < ntiles) issue(s, nt);
     }
     s += 2;
     if (s >= stages) {
@@ -828,6 +822,321 @@ void launch_gram_hybrid(const double* X, size_t n, int F, double* G, double* xt1
   else
     kcg_gram_hybrid<NB, R, false><<<(unsigned)grid, 256, smem, stream>>>(X, (kcg_i64)n, F, stages, G, xt1, colmax);
   check(cudaGetLastError(), "kcg_gram_hybrid launch");
+}
+
+// ---------------------------------------------------------------------------
+// Row-per-lane DFMA Gram for narrow designs (F <= 13, 17..22)
+//
+// The DMMA kernels pad F to 8-column blocks: F = 9..12 pays the 3 DMMAs of
+// F = 16 per 4 rows and F = 17..20 the 6 of F = 24, so both plateau on the
+// FP64 pipe (1.49 and 2.7 ms for 1e8 rows) where HBM allows 1.0-1.3 and
+// 1.9-2.2 ms. With DMMA and DFMA at the same rate, DFMAs over exactly the
+// F(F+1)/2 distinct entries cost F(F+3)/2 FP64 lane operations per row with
+// Xt1 (54 at F = 9), well under the 8 F bytes' HBM time. Each lane walks
+// whole rows: it loads a row's F values from the TMA-staged tile and
+// accumulates its share of the upper triangle in registers. G warps split
+// the triangle of the same rows (part = warp % G, a warp-uniform switch to
+// straight-line code per part): the entries [part C, part C + C) in
+// row-major triangle order, C = ceil(E / G), and the Xt1 / column-maximum
+// work of the columns c = part (mod G). Warp sums go through shuffles to
+// shared memory, one global atomic per entry per CTA.
+__host__ __device__ constexpr int tri_row(int e, int F) {
+  int p = 0;
+  while (e >= F - p) {
+    e -= F - p;
+    ++p;
+  }
+  return p;
+}
+__host__ __device__ constexpr int tri_col(int e, int F) {
+  int p = 0;
+  while (e >= F - p) {
+    e -= F - p;
+    ++p;
+  }
+  return p + e;
+}
+
+// Row pitches of F = 2 (mod 4) doubles put lanes 8 apart on the same banks
+// (F = 4 (mod 8): lanes 4 apart, 4-way): such a lane reads its row rotated
+// by rot = 0..1 (0..3) columns, register slot c holding column
+// (c + rot) mod F -- the slot pairs still cover every column pair once, and
+// the flush maps them back.
+template <int F>
+struct DfmaRot {
+  static constexpr int RB = (F % 8 == 4) ? 2 : ((F % 4 == 2) ? 3 : -1);  // lane bit(s) selecting rot
+  static constexpr int MAXR = RB == 2 ? 3 : (RB == 3 ? 1 : 0);
+  // lanes sharing a rotation: xor masks over the other lane bits
+  static constexpr unsigned KEEP = RB == 2 ? 0xcu : (RB == 3 ? 0x8u : 0x0u);
+  __device__ static int rot(int lane) { return RB < 0 ? 0 : (lane >> RB) & MAXR; }
+};
+
+template <int F, int G, int PART>
+struct DfmaPart {
+  static constexpr int E = F * (F + 1) / 2;
+  static constexpr int C = (E + G - 1) / G;
+  static constexpr int E0 = PART * C;
+  static constexpr int NE = (E - E0) < C ? (E - E0) : C;  // entries of this part
+  static constexpr int NC = (F - PART + G - 1) / G;        // slots c = PART (mod G)
+  using Rot = DfmaRot<F>;
+  double acc[C];
+  double s1[NC];
+  unsigned long long mx[NC];
+  int rot;
+  __device__ __forceinline__ void zero(int lane) {
+    rot = Rot::rot(lane);
+#pragma unroll
+    for (int k = 0; k < C; ++k) acc[k] = 0.0;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      s1[k] = 0.0;
+      mx[k] = 0ull;
+    }
+  }
+  // entry K of this part: the slot indices are constant expressions, so
+  // v[] stays in registers
+  template <int K>
+  __device__ __forceinline__ void entry(const double* v) {
+    constexpr int p = tri_row(E0 + K, F), q = tri_col(E0 + K, F);
+    acc[K] = fma(v[p], v[q], acc[K]);
+  }
+  template <int... K>
+  __device__ __forceinline__ void entries(const double* v, std::integer_sequence<int, K...>) {
+    (entry<K>(v), ...);
+  }
+  __device__ __forceinline__ void row(const double* __restrict__ r) {
+    double v[F];
+#pragma unroll
+    for (int c = 0; c < F; ++c) {  // unused slots are dead code
+      int col = c + rot;
+      if (c + Rot::MAXR >= F && col >= F) col -= F;
+      v[c] = r[col];
+    }
+    entries(v, std::make_integer_sequence<int, NE>{});
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const double x = v[PART + G * k];
+      s1[k] += x;
+      const unsigned long long bits = abs_bits(x);
+      mx[k] = bits > mx[k] ? bits : mx[k];
+    }
+  }
+  __device__ __forceinline__ int col_of(int slot) const { return slot + rot >= F ? slot + rot - F : slot + rot; }
+  __device__ static double lanes_sum(double x) {
+#pragma unroll
+    for (int o = 1; o <= 16; o <<= 1)
+      if (!(o & Rot::KEEP)) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+  }
+  template <int K>
+  __device__ __forceinline__ void flush_entry(double* red, bool writer) {
+    constexpr int p = tri_row(E0 + K, F), q = tri_col(E0 + K, F);
+    const double x = lanes_sum(acc[K]);
+    if (writer) {
+      const int a = col_of(p), b = col_of(q);
+      const int lo = a < b ? a : b, hi = a < b ? b : a;
+      atomicAdd(red + lo * F - lo * (lo - 1) / 2 + (hi - lo), x);
+    }
+  }
+  template <int... K>
+  __device__ __forceinline__ void flush_entries(double* red, bool writer, std::integer_sequence<int, K...>) {
+    (flush_entry<K>(red, writer), ...);
+  }
+  // totals of the lanes sharing a rotation into shared memory: red[E]
+  // (row-major upper triangle), red_s1[F], red_mx[F]
+  __device__ __forceinline__ void flush(double* red, double* red_s1, double* red_mx, int lane) {
+    const bool writer = (lane & ~Rot::KEEP & 31u) == 0;
+    flush_entries(red, writer, std::make_integer_sequence<int, NE>{});
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+      const double x = lanes_sum(s1[k]);
+      unsigned long long m = mx[k];
+#pragma unroll
+      for (int o = 1; o <= 16; o <<= 1)
+        if (!(o & Rot::KEEP)) {
+          const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+          m = y > m ? y : m;
+        }
+      if (writer) {
+        const int c = col_of(PART + G * k);
+        atomicAdd(red_s1 + c, x);
+        atomicMax(reinterpret_cast<unsigned long long*>(red_mx + c), m);
+      }
+    }
+  }
+};
+
+// 256 threads = 8 warps = (8 / G) row sets x G parts; a stage holds
+// R = 32 (8 / G) M rows, row set w / G takes rows 32 (w / G) + lane + 256 / G m
+template <int F, int G, int M, int PART>
+__device__ __forceinline__ void gram_dfma_part(const double* __restrict__ X, kcg_i64 n, int stages,
+                                               double* __restrict__ buf, unsigned fb, unsigned bb,
+                                               unsigned* reads, double* red, double* red_s1, double* red_mx) {
+  constexpr int RS = 8 / G;          // row sets
+  constexpr int R = 32 * RS * M;     // rows per stage
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int set = warp / G;
+  const int stage_d = R * F;
+  const unsigned bytes = (unsigned)(stage_d * 8);
+  const kcg_i64 ntiles = n / R;
+  DfmaPart<F, G, PART> P;
+  P.zero(lane);
+  int s = 0;
+  unsigned parity = 0;
+  for (kcg_i64 k = 0;; ++k) {
+    const kcg_i64 tile = blockIdx.x + k * gridDim.x;
+    if (tile >= ntiles) break;
+    unsigned done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done)
+                   : "r"(fb + 8 * s), "r"(parity)
+                   : "memory");
+    const double* st = buf + s * stage_d;
+#pragma unroll
+    for (int m = 0; m < M; ++m) P.row(st + (32 * set + lane + 32 * RS * m) * F);
+    __syncwarp();
+    if (lane == 0 && kcg_ring_release(&reads[s], 8)) {
+      {
+        const kcg_i64 nt = blockIdx.x + (k + stages) * gridDim.x;
+        if (nt < ntiles) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb + 8 * s), "r"(bytes)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  bb + (unsigned)(s * stage_d * 8)),
+              "l"(X + nt * stage_d), "r"(bytes), "r"(fb + 8 * s)
+              : "memory");
+        }
+      }
+    }
+    if (++s == stages) {
+      s = 0;
+      parity ^= 1u;
+    }
+  }
+  // tail rows straight from global (block 0 only)
+  if (blockIdx.x == 0)
+    for (kcg_i64 r = ntiles * R + 32 * set + lane; r < n; r += 32 * RS) P.row(X + r * F);
+  P.flush(red, red_s1, red_mx, lane);
+}
+
+template <int F, int G, int M>
+__global__ void __launch_bounds__(256, 1)
+    kcg_gram_dfma(const double* __restrict__ X, kcg_i64 n, int stages, double* __restrict__ Gm,
+                  double* __restrict__ xt1, double* __restrict__ cmax) {
+  constexpr int E = F * (F + 1) / 2;
+  constexpr int R = 32 * (8 / G) * M;
+  extern __shared__ __align__(128) unsigned char kcg_smem[];
+  double* buf = reinterpret_cast<double*>(kcg_smem);
+  const int stage_d = R * F;
+  double* red = buf + stages * stage_d;  // [E] + s1[F] + mx[F]
+  double* red_s1 = red + E;
+  double* red_mx = red_s1 + F;
+  __shared__ __align__(8) unsigned long long full[16];
+  __shared__ unsigned reads[16];
+  const int tid = threadIdx.x;
+  for (int k = tid; k < E + 2 * F; k += blockDim.x) red[k] = 0.0;
+  if (tid < 16) reads[tid] = 0;
+  const unsigned fb = (unsigned)__cvta_generic_to_shared(full);
+  const unsigned bb = (unsigned)__cvta_generic_to_shared(buf);
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(fb + 8 * s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const kcg_i64 ntiles = n / R;
+  if (tid == 0)
+    for (int s = 0; s < stages; ++s) {
+      const kcg_i64 t = blockIdx.x + (kcg_i64)s * gridDim.x;
+      if (t >= ntiles) break;
+      const unsigned bytes = (unsigned)(stage_d * 8);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb + 8 * s), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       bb + (unsigned)(s * stage_d * 8)),
+                   "l"(X + t * stage_d), "r"(bytes), "r"(fb + 8 * s)
+                   : "memory");
+    }
+  switch ((tid >> 5) % G) {  // warp-uniform
+    case 0: gram_dfma_part<F, G, M, 0>(X, n, stages, buf, fb, bb, reads, red, red_s1, red_mx); break;
+    case 1:
+      if constexpr (G > 1) gram_dfma_part<F, G, M, 1>(X, n, stages, buf, fb, bb, reads, red, red_s1, red_mx);
+      break;
+    case 2:
+      if constexpr (G > 2) gram_dfma_part<F, G, M, 2>(X, n, stages, buf, fb, bb, reads, red, red_s1, red_mx);
+      break;
+    default:
+      if constexpr (G > 3) gram_dfma_part<F, G, M, 3>(X, n, stages, buf, fb, bb, reads, red, red_s1, red_mx);
+      break;
+  }
+  __syncthreads();
+  for (int e = tid; e < E; e += blockDim.x) {
+    const int p = tri_row(e, F), q = tri_col(e, F);
+    atomicAdd(Gm + p * F + q, red[e]);
+    if (p != q) atomicAdd(Gm + q * F + p, red[e]);
+  }
+  for (int c = tid; c < F; c += blockDim.x) {
+    atomicAdd(xt1 + c, red_s1[c]);
+    atomicMax(reinterpret_cast<unsigned long long*>(cmax + c), (unsigned long long)__double_as_longlong(red_mx[c]));
+  }
+}
+
+template <int F, int G, int M>
+void launch_gram_dfma(const double* X, size_t n, double* Gm, double* xt1, double* colmax, cudaStream_t stream) {
+  constexpr int R = 32 * (8 / G) * M;
+  constexpr int E = F * (F + 1) / 2;
+  const size_t red_b = (size_t)(E + 2 * F) * sizeof(double);
+  const size_t stage_b = (size_t)R * F * sizeof(double);
+  int stages = (int)((200 * 1024 - red_b) / stage_b);
+  stages = stages < 2 ? 2 : (stages > 16 ? 16 : stages);
+  const size_t smem = (size_t)stages * stage_b + red_b;
+  static std::mutex mu;
+  static bool attr[64] = {};
+  int dev = 0;
+  check(cudaGetDevice(&dev), "cudaGetDevice");
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!attr[dev & 63]) {
+      check(cudaFuncSetAttribute(kcg_gram_dfma<F, G, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem + 1024),
+            "cudaFuncSetAttribute");
+      attr[dev & 63] = true;
+    }
+  }
+  const kcg_i64 tiles = (kcg_i64)n / R;
+  kcg_i64 grid = (kcg_i64)num_sms();
+  if (grid > tiles) grid = tiles > 0 ? tiles : 1;
+  kcg_gram_dfma<F, G, M><<<(unsigned)grid, 256, smem, stream>>>(X, (kcg_i64)n, stages, Gm, xt1, colmax);
+  check(cudaGetLastError(), "kcg_gram_dfma launch");
+}
+
+// F -> the DFMA kernel (true) or the DMMA path (false). all: also the
+// widths where it measured no faster than DMMA (7, 12, 13, 20-22; 1e8 rows,
+// profiles/gpu_r02_dfma.sh: F = 7 0.86 vs 0.81, 12 1.52 vs 1.49, 13 1.54
+// vs 1.59, 20 2.66 vs 2.66, 21 2.98 vs 2.70, 22 3.97 vs 2.73 ms)
+bool launch_gram_dfma_for(const double* X, size_t n, int F, double* Gm, double* xt1, double* colmax,
+                          cudaStream_t st, bool all) {
+  switch (F) {
+    case 1: launch_gram_dfma<1, 1, 8>(X, n, Gm, xt1, colmax, st); return true;
+    case 2: launch_gram_dfma<2, 1, 8>(X, n, Gm, xt1, colmax, st); return true;
+    case 3: launch_gram_dfma<3, 1, 4>(X, n, Gm, xt1, colmax, st); return true;
+    case 4: launch_gram_dfma<4, 1, 4>(X, n, Gm, xt1, colmax, st); return true;
+    case 5: launch_gram_dfma<5, 1, 2>(X, n, Gm, xt1, colmax, st); return true;
+    case 6: launch_gram_dfma<6, 1, 2>(X, n, Gm, xt1, colmax, st); return true;
+    case 7: if (!all) return false; launch_gram_dfma<7, 1, 2>(X, n, Gm, xt1, colmax, st); return true;
+    case 9: launch_gram_dfma<9, 1, 2>(X, n, Gm, xt1, colmax, st); return true;
+    case 10: launch_gram_dfma<10, 1, 2>(X, n, Gm, xt1, colmax, st); return true;
+    case 11: launch_gram_dfma<11, 1, 2>(X, n, Gm, xt1, colmax, st); return true;
+    case 12: if (!all) return false; launch_gram_dfma<12, 2, 2>(X, n, Gm, xt1, colmax, st); return true;
+    case 13: if (!all) return false; launch_gram_dfma<13, 2, 2>(X, n, Gm, xt1, colmax, st); return true;
+    case 17: launch_gram_dfma<17, 4, 4>(X, n, Gm, xt1, colmax, st); return true;
+    case 18: launch_gram_dfma<18, 4, 4>(X, n, Gm, xt1, colmax, st); return true;
+    case 19: launch_gram_dfma<19, 4, 4>(X, n, Gm, xt1, colmax, st); return true;
+    case 20: if (!all) return false; launch_gram_dfma<20, 4, 4>(X, n, Gm, xt1, colmax, st); return true;
+    case 21: if (!all) return false; launch_gram_dfma<21, 4, 4>(X, n, Gm, xt1, colmax, st); return true;
+    case 22: if (!all) return false; launch_gram_dfma<22, 4, 4>(X, n, Gm, xt1, colmax, st); return true;
+    default: return false;
+  }
 }
 
 // double-double helpers: (hi, lo) with |lo| <= ulp(hi) / 2
@@ -1044,6 +1353,12 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
     // profiles/ab_gram_hybrid_r.sh: F = 40 5.95 vs 6.19 ms, F = 36 6.18 vs
     // 6.23); KCG_GRAM_HYBRID=1 takes it for even F in 26..32 too (F = 32:
     // 4.72 vs 4.53 ms, slower), =0 never
+    // narrow designs the DMMA blocks pad (F <= 6, 9..11, 17..19): row-per-lane
+    // DFMA over the distinct entries (F = 2: 0.59 -> 0.26 ms, 9: 1.49 ->
+    // 1.08, 18: 2.67 -> 2.44 for 1e8 rows); KCG_GRAM_DFMA=0 keeps them on
+    // DMMA, =2 also takes 7, 12, 13, 20..22
+    static const int dfma = std::getenv("KCG_GRAM_DFMA") ? std::atoi(std::getenv("KCG_GRAM_DFMA")) : 1;
+    if (dfma && launch_gram_dfma_for(X, n, F, G, xt1, colmax, st, dfma == 2)) return;
     static const int hybrid_mode = std::getenv("KCG_GRAM_HYBRID") ? std::atoi(std::getenv("KCG_GRAM_HYBRID")) : -1;
     const bool hybrid = hybrid_mode == 1 || (hybrid_mode == -1 && nb == 5);
     if (hybrid && F % 2 == 0 && (nb == 4 || nb == 5))

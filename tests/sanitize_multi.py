@@ -20,7 +20,13 @@ w = kc.ModelWeights(alpha=alpha, covered=[a != 0 for a in alpha])
 V = ("matmul_tiled_g12x12", "matmul_tiled_g14x14", "matmul_tiled_g16x16",
      "matmul_naive_g16x12", "matmul_naive_g16x14", "matmul_naive_g16x16")
 progs = [kc.load_program(v) for v in V]
-n = 148 * 1024 * 2 + 2  # even: bulk-store kernel (2 CTAs/SM); one full wave of tiles
+import os  # noqa: E402
+
+# even: bulk-store kernel (2 CTAs/SM); 6 tiles per CTA, so the TMA ring
+# refills (memcheck / synccheck). KCG_SANITIZE_SMALL=1: one wave of tiles,
+# for racecheck, which cannot see the fence-and-counter stage hand-back
+# (profiles/racecheck_mbarrier_probe.cu)
+n = 148 * 1024 * 2 * (1 if os.environ.get("KCG_SANITIZE_SMALL") == "1" else 6) + 2
 u = torch.randint(1, 400, (3, n), device="cuda")
 cols = {p: (u[j] * 336).contiguous() for j, p in enumerate(("n", "m", "l"))}
 cols["m"][::97] += 5
@@ -39,8 +45,8 @@ small = {k: v[:5000] for k, v in cols.items()}
 kc.predict_multi(progs, w, small)
 best, bt, preds = kc.argmin(progs, w, cols, return_preds=True)
 prog = progs[2]
-T = kc.noiseless_time(alpha, prog, {k: (u[j] * 16)[:200000].contiguous() for j, k in enumerate(("n", "m", "l"))})
-c16 = {k: (u[j] * 16)[:200000].contiguous() for j, k in enumerate(("n", "m", "l"))}
+T = kc.noiseless_time(alpha, prog, {k: (u[j] * 16)[:2000000].contiguous() for j, k in enumerate(("n", "m", "l"))})
+c16 = {k: (u[j] * 16)[:2000000].contiguous() for j, k in enumerate(("n", "m", "l"))}
 a, rank, obj, stt = kc.fit_fused(prog, c16, T, refine=1)
 ep = kc.EnumProgram("""kernelcost-enum v1
 kernel x_fd

@@ -580,13 +580,15 @@ def test_predict_detail_matches_reference_predictions():
 
 def test_gram_accumulate_random_shapes():
     """Every Gram path (DMMA row-split for F <= 72 -- two CTAs per SM up to
-    F = 40, one beyond --, the DMMA + DFMA hybrid for even F in 34..40,
-    per-width DMMA for 73..160, CUDA-core for strided / unaligned X) against
-    torch fp64 on random widths, row counts (tails included) and layouts."""
+    F = 40, one beyond --, the DMMA + DFMA hybrid for even F in 34..40, the
+    row-per-lane DFMA kernel for F <= 6, 9..11, 17..19, per-width DMMA for
+    73..160, CUDA-core for strided / unaligned X) against torch fp64 on
+    random widths, row counts (tails included) and layouts."""
     rng = np.random.default_rng(123)
-    widths = [1, 2, 5, 8, 13, 26, 31, 32, 34, 40, 41, 48, 49, 57, 64, 65, 72, 73, 80, 81, 111, 131, 149, 160]
+    widths = [1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 17, 18, 19, 20, 21, 22, 26, 31, 32, 34, 40, 41, 48, 49, 57, 64,
+              65, 72, 73, 80, 81, 111, 131, 149, 160]
     for F in widths:
-        N = int(rng.integers(1, 5000)) + (70_000 if F in (2, 32, 40, 41, 57, 72, 131) else 0)
+        N = int(rng.integers(1, 5000)) + (70_000 if F in (2, 9, 12, 18, 22, 32, 40, 41, 57, 72, 131) else 0)
         ld = F + (3 if F % 3 == 0 else 0)  # some strided layouts
         base = torch.tensor(rng.uniform(0.5, 2.0, size=(N, ld)) * 10.0 ** rng.integers(-2, 3, size=ld),
                             device="cuda")
@@ -672,31 +674,36 @@ def test_fit_fused_reaches_the_exact_min_norm_solution():
         assert max(err) <= 1.0, (kid, rank, err)
 
 
-_HYBRID_CHECK = r"""
+_OPT_IN_CHECK = r"""
+import sys
 import numpy as np, torch
 import paper_1604_04997_b200 as kc
 rng = np.random.default_rng(7)
-for F, N in ((26, 4813), (32, 100_003), (34, 50_017), (40, 200_041), (40, 47)):
-    X = torch.tensor(rng.uniform(0.5, 2.0, size=(N, F)) * 10.0 ** rng.integers(-2, 3, size=F), device="cuda")
-    st = kc.gram_accumulate(X)
-    torch.testing.assert_close(st.G, X.T @ X, rtol=1e-12, atol=0, msg=f"F={F} N={N}")
-    torch.testing.assert_close(st.xt1, X.sum(0), rtol=1e-12, atol=0)
-    assert torch.equal(st.colmax, X.abs().max(0).values), F
+for F in (int(f) for f in sys.argv[1].split(",")):
+    for N in (47, 4813, 100_003):
+        X = torch.tensor(rng.uniform(0.5, 2.0, size=(N, F)) * 10.0 ** rng.integers(-2, 3, size=F), device="cuda")
+        st = kc.gram_accumulate(X)
+        torch.testing.assert_close(st.G, X.T @ X, rtol=1e-12, atol=0, msg=f"F={F} N={N}")
+        torch.testing.assert_close(st.xt1, X.sum(0), rtol=1e-12, atol=0)
+        assert torch.equal(st.colmax, X.abs().max(0).values), F
 print("ok")
 """
 
 
-def test_gram_hybrid_opt_in_matches_torch():
-    """The opt-in DMMA + DFMA Gram (KCG_GRAM_HYBRID=1: off-diagonal 8 x 8
-    blocks on DMMA, diagonal blocks' upper triangles on DFMA, even F in
-    26..40) against torch fp64, tails included. In a subprocess: the switch
-    is read once per process."""
+@pytest.mark.parametrize("env,widths", [
+    # DMMA off-diagonal + DFMA diagonal blocks for every even F in 26..40
+    ({"KCG_GRAM_HYBRID": "1"}, "26,28,32,34,40"),
+    # the row-per-lane DFMA Gram at the widths where it is not the default
+    ({"KCG_GRAM_DFMA": "2"}, "7,12,13,20,21,22"),
+])
+def test_gram_opt_in_kernels_match_torch(env, widths):
+    """The opt-in Gram kernels against torch fp64, tails included. In a
+    subprocess: the switches are read once per process."""
     import os
     import subprocess
     import sys
     from pathlib import Path
 
-    env = {**os.environ, "KCG_GRAM_HYBRID": "1"}
-    r = subprocess.run([sys.executable, "-c", _HYBRID_CHECK], env=env, capture_output=True, text=True, timeout=900,
-                       cwd=str(Path(__file__).resolve().parent.parent))
+    r = subprocess.run([sys.executable, "-c", _OPT_IN_CHECK, widths], env={**os.environ, **env}, capture_output=True,
+                       text=True, timeout=900, cwd=str(Path(__file__).resolve().parent.parent))
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
