@@ -36,7 +36,6 @@ __device__ __forceinline__ kcg_i128 kcg_const<kcg_i128>(kcg_i64 lo, kcg_i64 hi) 
   return (kcg_i128)(((kcg_u128)(kcg_u64)hi << 64) | (kcg_u128)(kcg_u64)lo);
 }
 
-// floor(a / b) for b > 0
 // Stage hand-back of the TMA rings: each consumer warp's lane 0 (after
 // __syncwarp, its shared-memory reads of the stage done) publishes them with
 // a release fence and a counter increment; the last to arrive acquires
@@ -47,6 +46,7 @@ __device__ __forceinline__ kcg_i128 kcg_const<kcg_i128>(kcg_i64 lo, kcg_i64 hi) 
 // neither (profiles/racecheck_mbarrier_probe.cu: an mbarrier-ordered store is
 // reported like an unsynchronised one), so racecheck runs at sizes where the
 // rings do not refill.
+#ifdef __CUDACC__  // not in the host build of the evaluator (source kind 4)
 __device__ __forceinline__ bool kcg_ring_release(unsigned* count, unsigned consumers) {
   __threadfence_block();
   if (atomicAdd(count, 1u) != consumers - 1) return false;
@@ -54,6 +54,9 @@ __device__ __forceinline__ bool kcg_ring_release(unsigned* count, unsigned consu
   *count = 0;
   return true;
 }
+#endif
+
+// floor(a / b) for b > 0
 
 template <class T>
 __device__ __forceinline__ T kcg_floordiv(T a, T b) {
