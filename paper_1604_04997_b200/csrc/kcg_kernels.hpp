@@ -31,6 +31,11 @@ void launch_interp_eval(const KcgDevProg* dprog, const KcgDevProg* dadmit,
 void launch_gram(const double* X, size_t n, int F, size_t ld, double* G,
                  double* xt1, double* colmax, void* stream);
 
+/// Integer-sliced Gram on the int8 tensor cores (gram_sliced.cu); false
+/// when F is outside its range (17..40).
+bool launch_gram_sliced(const double* X, size_t n, int F, double* G, double* xt1,
+                        double* colmax, cudaStream_t stream);
+
 /// obj += sum (1 - X alpha)^2
 void launch_residual(const double* X, size_t n, int F, size_t ld,
                      const double* alpha, double* obj, void* stream);

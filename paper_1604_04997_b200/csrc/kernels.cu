@@ -1357,6 +1357,9 @@ void launch_gram(const double* X, size_t n, int F, size_t ld, double* G, double*
     // DFMA over the distinct entries (F = 2: 0.59 -> 0.26 ms, 9: 1.49 ->
     // 1.08, 18: 2.67 -> 2.44 for 1e8 rows); KCG_GRAM_DFMA=0 keeps them on
     // DMMA, =2 also takes 7, 12, 13, 20..22
+    // integer-sliced Gram on the int8 tensor pipe (gram_sliced.cu), F in 17..40
+    static const int sliced = std::getenv("KCG_GRAM_SLICED") ? std::atoi(std::getenv("KCG_GRAM_SLICED")) : 0;
+    if (sliced && launch_gram_sliced(X, n, F, G, xt1, colmax, st)) return;
     static const int dfma = std::getenv("KCG_GRAM_DFMA") ? std::atoi(std::getenv("KCG_GRAM_DFMA")) : 1;
     if (dfma && launch_gram_dfma_for(X, n, F, G, xt1, colmax, st, dfma == 2)) return;
     static const int hybrid_mode = std::getenv("KCG_GRAM_HYBRID") ? std::atoi(std::getenv("KCG_GRAM_HYBRID")) : -1;
