@@ -59,6 +59,8 @@
 #include <stdexcept>
 #include <string>
 
+#include <cstdio>
+
 #include <cuda_runtime.h>
 
 #include "kcg_device.cuh"
@@ -108,13 +110,25 @@ __device__ __forceinline__ void sl_mma(unsigned d, uint64_t a, uint64_t b, uint3
       "l"(a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+// mbarrier phase wait; a wait that outlives ~4 s of clocks is a protocol bug:
+// report the barrier and trap instead of hanging the device
 __device__ __forceinline__ void sl_wait(unsigned mbar, unsigned parity) {
   unsigned done = 0;
-  while (!done)
+  long long t0 = 0;
+  while (!done) {
     asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                  : "=r"(done)
                  : "r"(mbar), "r"(parity)
                  : "memory");
+    if (!done) {
+      const long long now = clock64();
+      if (t0 == 0) t0 = now;
+      else if (now - t0 > 8000000000ll) {
+        printf("kcg_gram_sliced: mbarrier %#x parity %u stuck (block %d thread %d)\n", mbar, parity, blockIdx.x, threadIdx.x);
+        __trap();
+      }
+    }
+  }
 }
 __device__ __forceinline__ void sl_bar() { asm volatile("bar.sync 1, %0;" ::"n"(SL_THREADS) : "memory"); }
 __device__ __forceinline__ bool sl_bar_or(bool v) {
