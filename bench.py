@@ -832,7 +832,22 @@ def _configs(kc, torch, dev, args, cols, progs, w):
         "fp64_tflops": flops / sec / 1e12, "fp64_peak_tflops_measured_dgemm": fp64,
         "fp64_frac": flops / sec / 1e12 / fp64, "slice_rel_err_vs_torch": rel,
         "kernel": "kcg_gram_hybrid<5,96,true> (AOT: off-diagonal 8x8 blocks on DMMA m8n8k4 f64, diagonal blocks' upper triangles on DFMA, TMA-staged rows)"}
-    del X, Xs, st, st2, ref
+
+    # the same Gram on the int8 tensor cores (tcgen05.mma kind::i8, TMEM accumulators):
+    # the alternative back end kcg_gram_accumulate_sliced, not the default
+    def c3s():
+        st.G.zero_(); st.xt1.zero_(); st.colmax.zero_()
+        kc.api.check(kc.api.lib().kcg_gram_accumulate_sliced(X.data_ptr(), N, F, F, st.G.data_ptr(),
+                                                              st.xt1.data_ptr(), st.colmax.data_ptr(), stream))
+    sec_s = _timed(torch, c3s, reps=3)
+    st3 = kc.gram_accumulate(Xs, sliced=True)
+    A = Xs.abs()
+    out["config3_gram_1e8x40"]["int8_tensor_core_alternative"] = {
+        "ms": sec_s * 1e3, "hbm_frac": 8 * F * N / sec_s / 1e9 / hbm,
+        "slice_err_rel_to_abs_scale": float(((st3.G - ref).abs() / (A.T @ A)).max().item()),
+        "kernel": "kcg_gram_sliced<40,true> (7 signed 8-bit digits per value, tcgen05.mma kind::i8 M=128 N=144/144/80 "
+                  "per 32-row K step, int32 TMEM accumulators drained per segment; DESIGN.md section 4)"}
+    del X, Xs, st, st2, st3, ref, A
 
     return out
 

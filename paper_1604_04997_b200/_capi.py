@@ -63,6 +63,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_eval_predict": (ctypes.c_int, [P, P, ctypes.c_size_t, DP, P, P, P, P, ctypes.c_int, P]),
         "kcg_argmin": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_size_t, DP, P, P, P, P]),
         "kcg_gram_accumulate": (ctypes.c_int, [P, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t, P, P, P, P]),
+        "kcg_gram_accumulate_sliced": (ctypes.c_int, [P, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t, P, P, P, P]),
         "kcg_gram_fused": (ctypes.c_int, [P, P, P, ctypes.c_size_t, P, P, P, P, P]),
         "kcg_residual_accumulate": (ctypes.c_int, [P, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t, P, P, P]),
         "kcg_residual_fused": (ctypes.c_int, [P, P, P, ctypes.c_size_t, DP, P, P]),

@@ -416,13 +416,16 @@ def _check_times(T, n: int, device) -> None:
                              f"T must be {n} contiguous CUDA float64 times on {device}")
 
 
-def gram_accumulate(X, stats: GramStats | None = None, stream=None) -> GramStats:
-    """G += XᵀX, Xᵀ1, colmax over a materialised design X [N, F] fp64."""
+def gram_accumulate(X, stats: GramStats | None = None, stream=None, sliced: bool = False) -> GramStats:
+    """G += XᵀX, Xᵀ1, colmax over a materialised design X [N, F] fp64.
+    sliced=True takes the int8 tensor-core back end (kcg_gram_accumulate_sliced,
+    17 <= F <= 40, contiguous X)."""
     _check_design(X)
     N, F = X.shape
     stats = stats or GramStats.zeros(F, X.device)
-    check(lib().kcg_gram_accumulate(X.data_ptr(), N, F, X.stride(0), stats.G.data_ptr(),
-                                    stats.xt1.data_ptr(), stats.colmax.data_ptr(), _stream(stream)))
+    fn = lib().kcg_gram_accumulate_sliced if sliced else lib().kcg_gram_accumulate
+    check(fn(X.data_ptr(), N, F, X.stride(0), stats.G.data_ptr(),
+             stats.xt1.data_ptr(), stats.colmax.data_ptr(), _stream(stream)))
     stats.n_rows += N
     return stats
 

@@ -1118,6 +1118,21 @@ int kcg_gram_accumulate(const double* X, size_t n, int F, size_t ld, double* G, 
   });
 }
 
+int kcg_gram_accumulate_sliced(const double* X, size_t n, int F, size_t ld, double* G, double* xt1,
+                               double* colmax, void* stream) {
+  if (!X || !G || !xt1 || !colmax || F < 17 || F > 40 || ld != static_cast<size_t>(F) ||
+      reinterpret_cast<uintptr_t>(X) % 16 != 0)
+    return fail(KCG_E_INVALID_ARGUMENT, "sliced gram: needs 17 <= n_cols <= 40, ld == n_cols, 16-byte aligned X");
+  return guarded([&] {
+    const NvtxRange nvtx_range("kcg_gram_accumulate_sliced");
+    require_device();
+    if (n == 0) return KCG_OK;
+    kcg::launch_gram_sliced(X, n, F, G, xt1, colmax, static_cast<cudaStream_t>(stream));
+    ++g_launches;
+    return KCG_OK;
+  });
+}
+
 namespace {
 
 // Fused Gram / residual for programs whose design rows stay wider than 48
