@@ -35,21 +35,24 @@
 // [2^-960, 2^960) or be 0 (smaller magnitudes round to 0 at 2^-1013
 // absolute); a non-finite value makes the CTA's G and X^T 1 contribution NaN.
 //
-// Layout. Tiles of KT = 128 rows arrive by TMA (cp.async.bulk, one
-// contiguous 40 KB copy at F = 40) into a 3-stage fp64 ring. Twenty slicer
-// warps turn a tile into its digit matrix in a 2-stage operand ring:
+// Layout. A CTA per SM walks its tiles of KT = 128 rows (tile blockIdx.x +
+// t gridDim.x). Ten warps slice: thread (c, i) owns feature i of rows
+// 16c..16c+15, loads them straight from HBM one tile ahead (whole tiles
+// are bulk-prefetched into L2 six tiles ahead), and writes their seven
+// digits as seven 16-byte core-matrix rows of a 3-stage operand ring:
 // index (a, i) -> a FP + i (FP = F rounded up to 8), K = the tile's rows,
 // K-major, no swizzle (8-row x 16-byte core matrices, LBO = 128 B, SBO =
-// 1 KB). Thread pair (c, i) owns feature i of rows 16c..16c+15 (one
-// core-matrix row per digit), each thread 8 of the rows: 8 ds loads,
-// 8 DMUL + F2I, a 4x8 byte transpose (PRMT) per 4 rows, seven 8-byte
-// stores. One elected thread issues per 32-row K step
+// 1 KB). Per tile one CTA barrier (a bar.red that also ORs the segment
+// test) hands the previous tile to thread 0, which issues per 32-row K step
 //   MMA1  A = digits 0..2 (M = 128 lanes), B = rows [0, N1)    -> TMEM [0, N1)
 //   MMA2  A = digits 0..2,                 B = rows [N1, 2N1)  -> TMEM [N1, 2 N1)
 //   MMA3  A = digit 3.. (lanes < FP used), B = digits 3, 4     -> TMEM [2 N1, 2 N1 + N2)
 // with N1 = 144, N2 = 80 at F = 40 (368 of the 512 TMEM columns), and
-// commits to the stage's `empty` mbarrier. Slicer warps 0..3 (TMEM lane
-// quarters 0..3) drain the cells at the end of each segment.
+// commits to the stage's mbarrier. Warps 0..3 (TMEM lane quarters 0..3)
+// drain the cells at the end of each segment. Measured 7.6-7.8 ms at 1e8 x
+// 40 against 5.94 ms for the FP64 hybrid: DESIGN.md section 4 has the
+// version history and what bounds it (shared memory and load latency, not
+// the tensor pipe).
 //
 // (c) this repository; the algorithm follows the reference's normal
 // equations only through the Gram contract (model.cpp:37-60).
