@@ -1179,6 +1179,19 @@ void chunked_rows(const kcg_program* p, const int64_t* const* param_cols, const 
 
 }  // namespace
 
+namespace {
+// CTAs per SM a persistent fused kernel launches: its register-cap target,
+// but no more than shared memory lets reside at once (a grid beyond that
+// runs a second wave that starts only when the first has finished its whole
+// share of the tiles). The HBM-bound fused Gram and residual showed no
+// difference (profiles/ab_fused_grid.sh); the FP64-bound refinement
+// gradient uses it
+int resident_ctas(int want, size_t smem) {
+  const int fit = static_cast<int>((228u * 1024u) / (smem + 1024u));
+  return std::max(1, std::min(want, fit));
+}
+}  // namespace
+
 int kcg_gram_fused(const kcg_program* cp, const int64_t* const* param_cols, const double* T,
                    size_t n, double* G, double* xt1, double* colmax,
                    unsigned long long* bad_rows, void* stream) {
@@ -1360,8 +1373,14 @@ int kcg_residual_grad_fused(const kcg_program* cp, const int64_t* const* param_c
     for (double v : ahi) ab.push<double>(v);
     for (double v : alo) ab.push<double>(v);
     ab.finish();
-    kcg::launch_jit(p->jit_rgrad, ab.b.data(), ab.b.size(), kcg::num_sms() * kcg::fused_ctas_per_sm(p->low, false), 256,
-                    stream, kcg::fused_smem_bytes(np, p->low, false, true));
+    // grid: the CTAs that are resident at once (the persistent loop's stride);
+    // the register cap (__launch_bounds__) may ask for more than shared
+    // memory admits (a second wave of CTAs would start only after the first
+    // finished its whole share)
+    const size_t rg_smem = kcg::fused_smem_bytes(np, p->low, false, true);
+    static const int grid_ctas_env = static_cast<int>(env_ll("KCG_RGRAD_GRID", 0, 0, 8));
+    const int grid_ctas = grid_ctas_env ? grid_ctas_env : resident_ctas(kcg::rgrad_ctas_per_sm(), rg_smem);
+    kcg::launch_jit(p->jit_rgrad, ab.b.data(), ab.b.size(), kcg::num_sms() * grid_ctas, 256, stream, rg_smem);
     ++g_launches;
     return KCG_OK;
   });

@@ -618,6 +618,12 @@ int env_int(const char* name, int dflt, int lo, int hi);
 // 64 KB ring each (measured: Gram 5.35 -> 6.12 TB/s, residual 6.25 -> 7.0
 // TB/s); the DMMA Gram keeps 2 CTAs (its row buffers need the shared memory).
 int fused_ctas(bool dmma) { return env_int("KCG_FUSED_CTAS", dmma ? 2 : 3, 1, 4); }
+// the refinement gradient (FP64-bound, not HBM-bound) has its own defaults:
+// profiles/ab_rgrad_knobs.sh
+// (64-register cap and rows tid + 256 u: 7.71 -> 6.86 ms per 1e9 rows with
+// the grid at the resident CTA count)
+int rgrad_ctas() { return env_int("KCG_RGRAD_CTAS", 4, 1, 4); }
+bool rgrad_strided() { return env_int("KCG_RGRAD_STRIDED", 1, 0, 1) == 1; }
 bool fused_rowwise(bool dmma) { return env_int("KCG_FUSED_ROWWISE", dmma ? 0 : 1, 0, 1) == 1; }
 // row order and unroll of the row-wise consumer: the Gram is fastest with
 // rows tid + 256 u fully unrolled (6.17 -> 6.45 TB/s), the residual with
@@ -958,6 +964,8 @@ size_t fused_smem_bytes(int n_cols, const Lowered& L, bool gram, bool per_key) {
 int fused_ctas_per_sm(const Lowered& L, bool gram) {
   return fused_ctas(gram && gram_dmma(gram_basis(L).width(static_cast<int>(L.keys.size()))));
 }
+
+int rgrad_ctas_per_sm() { return rgrad_ctas(); }
 
 size_t tma_smem_bytes(int n_cols) {
   return static_cast<size_t>(tma_stages(n_cols)) * (n_cols > 0 ? n_cols : 1) * tma_tile() * 8;
@@ -1990,7 +1998,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     os << "        }\n      }\n";
   };
 
-  os << "extern \"C\" __global__ void __launch_bounds__(256, " << fused_ctas(dmma) << ") " << name
+  os << "extern \"C\" __global__ void __launch_bounds__(256, " << (rgrad ? rgrad_ctas() : fused_ctas(dmma)) << ") " << name
      << "(const __grid_constant__ KcgArgs a) {\n"
         "  constexpr int TP = "
      << kTmaTile << ", S = " << S << ", NC = " << NC
@@ -2050,7 +2058,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     // one row at a time straight from the stage (fewer live registers), the
     // stage released after the thread's 4 rows
     // rows tid + 256 u (conflict-free stage loads) or 4 tid + u
-    const bool strided = fused_strided(gram);
+    const bool strided = rgrad ? rgrad_strided() : fused_strided(gram);
     const std::string off = strided ? "u * 256 + threadIdx.x" : "4 * threadIdx.x + u";
     os << "    const kcg_i64 base = tile * TP;\n"
           "    #pragma unroll "

@@ -76,6 +76,7 @@ int multi_tile();
 size_t tma_smem_bytes(int n_cols);
 int tma_ctas_per_sm();
 int fused_ctas_per_sm(const Lowered& L, bool gram);  // fused Gram / residual kernels (KCG_FUSED_CTAS)
+int rgrad_ctas_per_sm();  // fused refinement gradient (KCG_RGRAD_CTAS)
 /// Monomial basis of a program's property columns for the fused design-row
 /// reductions. Every key is count_j = sum_t coef_t * mono_t / D_j, so a
 /// design row x_j = count_j / T is A_j . u with u_b = mono_b / T. When the
