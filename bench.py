@@ -589,7 +589,9 @@ def _sharded_fit(kc, torch, dev, world, rank, rows):
     its own block of sizes, T = noiseless_time on the GPU) and reduces them
     through the fused evaluate -> row -> Gram kernel; G / Xᵀ1 / colmax are
     all-reduced over NCCL, every rank solves the same small system, then
-    re-predicts its shard in the fused residual pass (objective all-reduced).
+    takes one refinement step whose pass also sums the squared residuals, so
+    the objective at the refined weights follows from the all-reduced sums
+    and the Gram (api.refined_objective) without a third pass.
     Timed on the device from the Gram launch to the reduced objective, max
     over ranks (host solve included)."""
     import torch.distributed as dist
@@ -622,18 +624,19 @@ def _sharded_fit(kc, torch, dev, world, rank, rows):
         import ctypes
         # one refinement step: the double-double gradient over the rows the
         # reference would form (fused, never materialised), all-reduced
+        # and the sum of squared residuals, which with the Gram gives the
+        # objective at the refined weights (api.refined_objective)
         g = torch.zeros(len(prog.props), dtype=torch.float64, device=dev)
+        r2 = torch.zeros(1, dtype=torch.float64, device=dev)
         fa = full(a)
-        kc.api.check(kc.api.lib().kcg_residual_grad_fused(prog.handle, arr, T.data_ptr(), rows,
-                                                          (ctypes.c_double * len(fa))(*fa), g.data_ptr(), stream))
-        a = kc.refine_gram(st, a, allreduce_sum(g))
-        fa = full(a)
-        obj = torch.zeros(1, dtype=torch.float64, device=dev)
-        kc.api.check(kc.api.lib().kcg_residual_fused(prog.handle, arr, T.data_ptr(), rows,
-                                                     (ctypes.c_double * len(fa))(*fa), obj.data_ptr(), stream))
-        if world > 1:
-            dist.all_reduce(obj)
-        return rank_, float(obj.item()), st.n_rows
+        kc.api.check(kc.api.lib().kcg_residual_grad_obj_fused(prog.handle, arr, T.data_ptr(), rows,
+                                                              (ctypes.c_double * len(fa))(*fa), g.data_ptr(),
+                                                              r2.data_ptr(), stream))
+        g = allreduce_sum(g)
+        r2 = allreduce_sum(r2)
+        a2 = kc.refine_gram(st, a, g)
+        obj = kc.refined_objective(st, a, a2, g, r2)
+        return rank_, obj, st.n_rows
 
     once()  # JIT + warm-up
     if world > 1:
@@ -654,12 +657,13 @@ def _sharded_fit(kc, torch, dev, world, rank, rows):
             "rank": rk, "objective": obj, "scaling": "weak",
             "workload": f"config5: {rows} rows/rank (matmul_tiled_g16x16, T = noiseless_time), fused "
                         "evaluate->row->Gram (monomial basis) + NCCL all-reduce + host min-norm solve + one "
-                        "refinement step (fused double-double residual gradient over the reference's rows, "
-                        "all-reduced) + fused residual",
-            # three streaming passes over the rows (Gram, refinement
-            # gradient, residual at the refined weights), 8*P + 8 = 32 B per row each
-            "bytes_per_row": 96,
-            "hbm_frac": 96.0 * rows / sec / 1e9 / peaks()[0],
+                        "refinement step (fused gradient over the reference's rows with the residual in twice "
+                        "the working precision, and its sum of squares, all-reduced); the objective at the "
+                        "refined weights from those sums and the Gram (no third pass)",
+            # two streaming passes over the rows (Gram, refinement gradient),
+            # 8*P + 8 = 32 B per row each
+            "bytes_per_row": 64,
+            "hbm_frac": 64.0 * rows / sec / 1e9 / peaks()[0],
             "peak_note": "the peak is MEASURED_PEAKS' copy rate (read + write); these passes only read, "
                          "and read streams run above it"}
 

@@ -291,6 +291,14 @@ int kcg_residual_grad_fused(const kcg_program* prog,
                             const int64_t* const* param_cols, const double* T,
                             size_t n_rows, const double* alpha, double* g,
                             void* stream);
+/* The same gradient, plus r2 (DEVICE fp64, nullable) += sum_r (1 - x_r.alpha)^2
+ * from the same (twice-working-precision) residuals. After the refinement
+ * step alpha' = alpha + delta, the objective follows without another pass
+ * over the rows: obj(alpha') = r2 - 2 delta.g + delta^T G delta, G the
+ * Gram of the same rows (api.refined_objective; model.cpp:81-92's sum). */
+int kcg_residual_grad_obj_fused(const kcg_program* prog, const int64_t* const* param_cols,
+                                const double* T, size_t n_rows, const double* alpha,
+                                double* g, double* r2, void* stream);
 
 /* ---- host-side solve (fit_weights, model.cpp:37-93) --------------------
  * From the reduced Gram statistics of an n_cases-row design over F columns:

@@ -68,6 +68,7 @@ def _declare(L: ctypes.CDLL) -> None:
         "kcg_residual_accumulate": (ctypes.c_int, [P, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t, P, P, P]),
         "kcg_residual_fused": (ctypes.c_int, [P, P, P, ctypes.c_size_t, DP, P, P]),
         "kcg_residual_grad_fused": (ctypes.c_int, [P, P, P, ctypes.c_size_t, DP, P, P]),
+        "kcg_residual_grad_obj_fused": (ctypes.c_int, [P, P, P, ctypes.c_size_t, DP, P, P, P]),
         "kcg_gram_residual_grad": (ctypes.c_int, [P, ctypes.c_size_t, ctypes.c_int, ctypes.c_size_t, P, P, P]),
         "kcg_simulate_time": (ctypes.c_int, [P, P, ctypes.c_size_t, DP, ctypes.c_double, ctypes.c_uint64,
                                              ctypes.c_uint64, P, P, P]),

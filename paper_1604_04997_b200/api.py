@@ -458,18 +458,39 @@ def residual_fused(prog: Program, bindings, T, alpha149: Sequence[float], stream
     return float(obj.item())
 
 
-def residual_grad_fused(prog: Program, bindings, T, alpha149: Sequence[float], g=None, stream=None):
+def residual_grad_fused(prog: Program, bindings, T, alpha149: Sequence[float], g=None, stream=None, r2=None):
     """g += X^T (1 - X alpha) over the rows x_j = RN(count_j)/T formed on the
-    fly (model.cpp:29), residual in double-double: the refinement gradient
-    after a fused Gram. Returns the [F] device tensor (program key order)."""
+    fly (model.cpp:29), residual in twice the working precision: the
+    refinement gradient after a fused Gram. Returns the [F] device tensor
+    (program key order). r2 (a [1] fp64 device tensor, optional) += the sum
+    of the squared residuals, for refined_objective."""
     torch = _torch()
     arr, n, cols = _columns(prog, bindings)
     _check_times(T, n, cols[0].device if cols else T.device)
     if g is None:
         g = torch.zeros(len(prog.props), dtype=torch.float64, device=T.device)
     a = (ctypes.c_double * len(alpha149))(*alpha149)
-    check(lib().kcg_residual_grad_fused(prog.handle, arr, T.data_ptr(), n, a, g.data_ptr(), _stream(stream)))
+    if r2 is None:
+        check(lib().kcg_residual_grad_fused(prog.handle, arr, T.data_ptr(), n, a, g.data_ptr(), _stream(stream)))
+    else:
+        if not (r2.is_cuda and r2.dtype == torch.float64 and r2.numel() >= 1):
+            raise _capi.KcgError(_capi.E_INVALID_ARGUMENT, "r2 must be a CUDA float64 tensor")
+        check(lib().kcg_residual_grad_obj_fused(prog.handle, arr, T.data_ptr(), n, a, g.data_ptr(), r2.data_ptr(),
+                                                _stream(stream)))
     return g
+
+
+def refined_objective(stats: GramStats, alpha_old: Sequence[float], alpha_new: Sequence[float], g, r2) -> float:
+    """sum (1 - x.alpha_new)^2 (model.cpp:81-92) from the refinement pass at
+    alpha_old -- r2 = sum r^2, g = X^T r with r = 1 - X alpha_old -- and the
+    Gram: |r - X d|^2 = r2 - 2 d.g + d^T G d, d = alpha_new - alpha_old.
+    The two correction terms are second order in a refinement step, so the
+    result carries r2's relative accuracy; no further pass over the rows."""
+    import numpy as np
+    G = stats.G.double().cpu().numpy()
+    gh = g.double().cpu().numpy()
+    d = np.asarray(alpha_new, dtype=np.float64) - np.asarray(alpha_old, dtype=np.float64)
+    return float(float(r2.double().sum().item()) - 2.0 * float(d @ gh) + float(d @ (G @ d)))
 
 
 def refine_gram(stats: GramStats, alpha: Sequence[float], g) -> list[float]:
@@ -488,21 +509,30 @@ def refine_gram(stats: GramStats, alpha: Sequence[float], g) -> list[float]:
 def fit_fused(prog: Program, bindings, T, refine: int = 2, stream=None):
     """fit_weights (model.cpp:37-93) over rows formed from bindings and
     measured times on the fly: fused Gram, host equilibrated min-norm
-    solve, `refine` refinement steps with the double-double fused residual
-    gradient, objective from the fused residual pass. Returns
+    solve, `refine` refinement steps with the fused residual gradient, the
+    objective at the refined weights from the last of them
+    (refined_objective; the fused residual pass when refine = 0). Returns
     (alpha over the program's keys, rank, objective, GramStats)."""
+    torch = _torch()
     st = gram_fused(prog, bindings, T, stream=stream)
     alpha, rank = solve_gram(st)
     K = schema_size()
-    for _ in range(refine):
-        full = [0.0] * K
+
+    def full(a):
+        out = [0.0] * K
         for j, k in enumerate(prog.props):
-            full[k] = alpha[j]
-        alpha = refine_gram(st, alpha, residual_grad_fused(prog, bindings, T, full, stream=stream))
-    full = [0.0] * K
-    for j, k in enumerate(prog.props):
-        full[k] = alpha[j]
-    obj = residual_fused(prog, bindings, T, full, stream=stream)
+            out[k] = a[j]
+        return out
+    if refine == 0:
+        return alpha, rank, residual_fused(prog, bindings, T, full(alpha), stream=stream), st
+    for step in range(refine):
+        last = step == refine - 1
+        r2 = torch.zeros(1, dtype=torch.float64, device=T.device) if last else None
+        g = residual_grad_fused(prog, bindings, T, full(alpha), stream=stream, r2=r2)
+        new = refine_gram(st, alpha, g)
+        if last:  # the objective at the refined weights from this pass (no residual pass)
+            obj = refined_objective(st, alpha, new, g, r2)
+        alpha = new
     return alpha, rank, obj, st
 
 

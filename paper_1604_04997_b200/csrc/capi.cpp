@@ -1321,6 +1321,11 @@ int kcg_residual_fused(const kcg_program* cp, const int64_t* const* param_cols, 
 
 int kcg_residual_grad_fused(const kcg_program* cp, const int64_t* const* param_cols, const double* T, size_t n,
                             const double* alpha, double* g, void* stream) {
+  return kcg_residual_grad_obj_fused(cp, param_cols, T, n, alpha, g, nullptr, stream);
+}
+
+int kcg_residual_grad_obj_fused(const kcg_program* cp, const int64_t* const* param_cols, const double* T, size_t n,
+                                const double* alpha, double* g, double* r2, void* stream) {
   kcg_program* p = const_cast<kcg_program*>(cp);
   if (!p || !T || !alpha || !g) return fail(KCG_E_INVALID_ARGUMENT, "bad residual-gradient arguments");
   return guarded([&] {
@@ -1337,7 +1342,8 @@ int kcg_residual_grad_fused(const kcg_program* cp, const int64_t* const* param_c
       cuda_check(cudaMemcpyAsync(da, al.data(), sizeof(double) * al.size(), cudaMemcpyHostToDevice,
                                  static_cast<cudaStream_t>(stream)), "cudaMemcpyAsync");
       chunked_rows(p, param_cols, T, n, nullptr, stream, [&](const double* X, size_t m) {
-        const int rc = kcg_gram_residual_grad(X, m, F, F, da, g, stream);
+        int rc = kcg_gram_residual_grad(X, m, F, F, da, g, stream);
+        if (rc == KCG_OK && r2) rc = kcg_residual_accumulate(X, m, F, F, da, r2, stream);
         if (rc != KCG_OK) throw KcgError(rc, kcg_last_error());
       });
       cuda_check(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)), "residual grad");
@@ -1353,6 +1359,7 @@ int kcg_residual_grad_fused(const kcg_program* cp, const int64_t* const* param_c
     for (int j = 0; j < std::max(np, 1); ++j) ab.push<const void*>(j < np ? param_cols[j] : nullptr);
     ab.push<const void*>(T);
     ab.push<void*>(g);
+    ab.push<void*>(r2);
     ab.push<int64_t>(static_cast<int64_t>(n));
     bool vec = reinterpret_cast<uintptr_t>(T) % 16 == 0;
     for (int j = 0; j < np; ++j) vec = vec && reinterpret_cast<uintptr_t>(param_cols[j]) % 16 == 0;

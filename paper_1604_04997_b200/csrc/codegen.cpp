@@ -1640,8 +1640,9 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* G; double* xt1; "
           "double* cmax; unsigned long long* bad; kcg_i64 n; int vec; };\n";
   else
-    os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* obj; kcg_i64 n; "
-          "int vec; double alpha[" << (rgrad ? 2 * WA : (F > 0 ? F : 1)) << "]; };\n";
+    os << "struct KcgArgs { const kcg_i64* p[" << NP << "]; const double* t; double* obj; "
+       << (rgrad ? "double* r2; " : "") << "kcg_i64 n; int vec; double alpha[" << (rgrad ? 2 * WA : (F > 0 ? F : 1))
+       << "]; };\n";
   if (red_basis) {
     // expansion tables: key j = sum over kcg_kt[off[j]..off[j+1]) of coef * u_b
     std::vector<int> off{0}, tb;
@@ -1928,7 +1929,7 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     // then per-thread sums of u_b r (basis) or x_j r; each warp's totals
     // expanded to the F keys (g_j = sum_b A_jb gu_b) and added atomically
     cons_decl << "  double gacc[" << WA << "];\n  #pragma unroll\n  for (int j = 0; j < " << WA
-              << "; ++j) gacc[j] = 0.0;\n";
+              << "; ++j) gacc[j] = 0.0;\n  double rr = 0.0;\n";
     // 1 - sum_g x_g (A_hi + A_lo) as a compensated dot product (Ogita, Rump
     // and Oishi's Dot2: TwoSum of the running sum with each rounded product,
     // the product errors (exact by FMA), the A_lo terms and the sum errors
@@ -1945,10 +1946,14 @@ std::string codegen(const std::vector<const Lowered*>& progs,
                << "          hi = s; lo = __dadd_rn(lo, __dsub_rn(e, pe)); }\n";
     cons_row << "        const double r = __dadd_rn(hi, lo);\n";
     for (int j = 0; j < W; ++j) cons_row << "        gacc[" << j << "] = fma(x[" << j << "], r, gacc[" << j << "]);\n";
+    // sum of r^2 at these weights (a.r2, nullable): with the gradient and the
+    // Gram it gives the objective after the refinement step (api.refined_objective)
+    cons_row << "        rr = fma(r, r, rr);\n";
     cons_row << "      }\n";
     cons_end << "  #pragma unroll\n  for (int j = 0; j < " << W << "; ++j)\n"
              << "    for (int o = 16; o > 0; o >>= 1) gacc[j] += __shfl_down_sync(0xffffffffu, gacc[j], o);\n"
-             << "  if ((threadIdx.x & 31) == 0) {\n";
+             << "  for (int o = 16; o > 0; o >>= 1) rr += __shfl_down_sync(0xffffffffu, rr, o);\n"
+             << "  if ((threadIdx.x & 31) == 0) {\n    if (a.r2) atomicAdd(a.r2, rr);\n";
     for (int j = 0; j < F; ++j) {
       if (!red_basis) {  // g_j = 2^k_j * (sum of x_base r over the group)
         char buf[64];

@@ -66,8 +66,10 @@ def allreduce_sum(t, group=None):
 
 def fit_sharded(prog, bindings, T, refine: int = 1, group=None, stream=None):
     """Config 5 on every rank: fused Gram of the local rows, all-reduce,
-    redundant solve, `refine` refinement steps (local double-double
-    gradient, all-reduced), fused residual objective (all-reduced).
+    redundant solve, `refine` refinement steps (local gradient in twice the
+    working precision, all-reduced); the objective at the refined weights
+    from the last step's all-reduced sums (api.refined_objective), or the
+    fused residual pass when refine = 0.
     Returns (alpha over the program's keys, rank, objective, total rows)."""
     import paper_1604_04997_b200 as kc
 
@@ -81,14 +83,21 @@ def fit_sharded(prog, bindings, T, refine: int = 1, group=None, stream=None):
         for j, k in enumerate(prog.props):
             out[k] = a[j]
         return out
-    for _ in range(refine):
-        g = kc.residual_grad_fused(prog, bindings, T, full(alpha), stream=stream)
-        alpha = kc.refine_gram(st, alpha, allreduce_sum(g, group))
     import torch
-    obj = torch.tensor([kc.residual_fused(prog, bindings, T, full(alpha), stream=stream)],
-                       dtype=torch.float64, device=T.device)
-    allreduce_sum(obj, group)
-    return alpha, rank, float(obj.item()), st.n_rows
+    if refine == 0:
+        obj = torch.tensor([kc.residual_fused(prog, bindings, T, full(alpha), stream=stream)],
+                           dtype=torch.float64, device=T.device)
+        allreduce_sum(obj, group)
+        return alpha, rank, float(obj.item()), st.n_rows
+    for step in range(refine):
+        last = step == refine - 1
+        r2 = torch.zeros(1, dtype=torch.float64, device=T.device) if last else None
+        g = allreduce_sum(kc.residual_grad_fused(prog, bindings, T, full(alpha), stream=stream, r2=r2), group)
+        new = kc.refine_gram(st, alpha, g)
+        if last:  # objective at the refined weights from this pass's all-reduced sums (no residual pass)
+            obj = kc.refined_objective(st, alpha, new, g, allreduce_sum(r2, group))
+        alpha = new
+    return alpha, rank, obj, st.n_rows
 
 
 def gather_shards(local, total: int, dst: int = 0, group=None):
