@@ -736,7 +736,7 @@ def _configs(kc, torch, dev, args, cols, progs, w):
     out["config1_suite_fit_eval"] = {
         "cases": rep["n_cases"], "test_cases": len(tests), "gpu_ms": sec1 * 1e3,
         "max_rel_diff_test_predictions_vs_reference": rel, "cpu_reference": ref1,
-        "note": "GPU: kcg_measurements_read_csv + per-kernel fused Gram + solve + 2 refinement steps + residual + 16 predictions "
+        "note": "GPU: kcg_measurements_read_csv + per-kernel fused Gram + solve + 2 refinement steps (objective from the last) + 16 predictions "
                 "(wall clock, ~70 launches); CPU: the reference's run_campaign + extract_properties (bound, "
                 "cap 2e7) + fit_weights + predict, 1 thread"}
 

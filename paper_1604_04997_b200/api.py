@@ -763,9 +763,10 @@ def fit_from_csv(path, programs=None, device: str = "", discard: int = 4, stream
     """``kernelcost fit <csv>`` on the GPU: per kernel the fused
     evaluate -> row -> Gram kernel, scattered into the schema-wide Gram
     (rows of different kernels are disjoint), one equilibrated min-norm
-    solve, `refine` refinement steps (double-double residual gradient over
-    the reference's own rows), then the fused residual pass for the
-    objective. Returns
+    solve, `refine` refinement steps (residual gradient over the reference's
+    own rows in twice the working precision), the objective at the refined
+    weights from the last of them (refined_objective; the fused residual
+    pass when refine = 0). Returns
     (ModelWeights, report) with report = {objective, n_cases, rank, bad_rows}."""
     torch = _torch()
     K = schema_size()
@@ -794,13 +795,19 @@ def fit_from_csv(path, programs=None, device: str = "", discard: int = 4, stream
         raise _capi.KcgError(_capi.E_ASSUMPTION_VIOLATED, f"{bad} measurement rows are not admissible")
     stats = GramStats(G, x1, cm, rows)
     alpha, rank = solve_gram(stats)
-    for _ in range(refine):  # schema-wide gradient: the kernels' rows are disjoint
+    if refine == 0:
+        obj = sum(residual_fused(prog, cols, T, alpha, stream=stream) for prog, cols, T in staged)
+    for step in range(refine):  # schema-wide gradient: the kernels' rows are disjoint
+        last = step == refine - 1
         g = torch.zeros(K, dtype=torch.float64, device="cuda")
+        r2 = torch.zeros(1, dtype=torch.float64, device="cuda") if last else None
         for prog, cols, T in staged:
             idx = torch.tensor(prog.props, dtype=torch.int64, device="cuda")
-            g[idx] += residual_grad_fused(prog, cols, T, alpha, stream=stream)
-        alpha = refine_gram(stats, alpha, g)
-    obj = sum(residual_fused(prog, cols, T, alpha, stream=stream) for prog, cols, T in staged)
+            g[idx] += residual_grad_fused(prog, cols, T, alpha, stream=stream, r2=r2)
+        new = refine_gram(stats, alpha, g)
+        if last:  # objective at the refined weights from this pass (no residual pass per kernel)
+            obj = refined_objective(stats, alpha, new, g, r2)
+        alpha = new
     covered = [bool(c > 0) for c in cm.cpu().tolist()]
     w = ModelWeights(device, "v1", list(alpha), covered, obj, rows)
     return w, {"objective": obj, "n_cases": rows, "rank": rank, "bad_rows": bad}
