@@ -84,17 +84,25 @@ constexpr int SL_PF = 6;                   // tiles prefetched into L2 ahead of 
 constexpr int SL_S2 = 3;                   // operand ring stages
 constexpr int SL_THREADS = 320;            // 10 slicer warps (one thread per feature and 16-row chunk)
 constexpr int SL_SEG_CAP = 256;            // tiles per segment (int32 headroom: 2^14 * 2^15 < 2^31)
-constexpr long long SL_OFF = 0x0080808080808080ll;
 
-template <int FP>
+// S = 7 digits (56-bit fixed point, the default) or 6 (48-bit: one N = 6 FP
+// MMA for digits 0..2 and digit 3 x 3 only -- 27% fewer operand bytes per
+// tile, KCG_SLICED_DIGITS=6 for the A/B)
+template <int FP, int S>
 struct SlGeom {
-  static constexpr int N1 = ((7 * FP + 1) / 2 + 15) / 16 * 16;
-  static constexpr int N2 = (2 * FP + 15) / 16 * 16;
+  static constexpr int NB1 = S == 7 ? 2 : 1;  // MMAs over digits 0..2 x all digits
+  static constexpr int N1 = S == 7 ? ((7 * FP + 1) / 2 + 15) / 16 * 16 : (6 * FP + 15) / 16 * 16;
+  static constexpr int B2 = S == 7 ? 2 : 1;   // digit 3 against digits 3 .. 3 + B2 - 1
+  static constexpr int N2 = (B2 * FP + 15) / 16 * 16;
+  static constexpr int G2 = NB1 * N1;         // TMEM column of the digit-3 block
   static constexpr int ROWS_A = 3 * FP + 128;
-  static constexpr int NROWS = (2 * N1 > ROWS_A ? 2 * N1 : ROWS_A);
+  static constexpr int NROWS = (NB1 * N1 > ROWS_A ? NB1 * N1 : ROWS_A);
   static constexpr int OPB = NROWS * SL_KT;  // operand stage bytes
+  static constexpr int SCALE = 8 * S - 3;    // v = rn(x 2^(SCALE - e)), |v| < 2^(8 S - 2)
+  static constexpr long long OFF = S == 7 ? 0x0080808080808080ll : 0x0000808080808080ll;
+  static_assert(S == 6 || S == 7, "digits");
   static_assert(3 * FP <= 128, "three digit planes per M = 128 MMA");
-  static_assert(2 * N1 + N2 <= 512, "TMEM columns");
+  static_assert(G2 + N2 <= 512, "TMEM columns");
   static_assert(N1 <= 256 && N2 <= 256, "MMA N");
 };
 
@@ -155,9 +163,9 @@ __device__ __forceinline__ unsigned sl_prmt(unsigned a, unsigned b, unsigned s) 
 // the end: G = P + P^T). Called by the 4 warps of TMEM lane quarters 0..3.
 // pj[b][j] = 2^(e_j - 5 - 8 b), so D_ab[i][j] pj[a][i] pj[b][j] is the
 // digit pair's contribution to x_i x_j (a, b = 0 the top digit).
-template <int FP>
+template <int FP, int S>
 __device__ __forceinline__ void sl_drain(unsigned tmem, int F, const double* pj, double* P) {
-  using Gm = SlGeom<FP>;
+  using Gm = SlGeom<FP, S>;
   const int m = threadIdx.x;  // TMEM lane (warps 0..3)
   const unsigned lane_base = tmem + ((unsigned)(threadIdx.x & ~31) << 16);
   // digits 0..2 (lanes < 3 FP) against every digit b >= a
@@ -171,7 +179,7 @@ __device__ __forceinline__ void sl_drain(unsigned tmem, int F, const double* pj,
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.0;
 #pragma unroll
-      for (int b = 0; b < 7; ++b) {
+      for (int b = 0; b < S; ++b) {
         unsigned r[8];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
@@ -199,13 +207,13 @@ __device__ __forceinline__ void sl_drain(unsigned tmem, int F, const double* pj,
 #pragma unroll
       for (int q = 0; q < 8; ++q) acc[q] = 0.0;
 #pragma unroll
-      for (int b = 3; b < 5; ++b) {
+      for (int b = 3; b < 3 + Gm::B2; ++b) {
         unsigned r[8];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t"
             "tcgen05.wait::ld.sync.aligned;"
             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
-            : "r"(lane_base + (unsigned)(2 * Gm::N1 + (b - 3) * FP + j0))
+            : "r"(lane_base + (unsigned)(Gm::G2 + (b - 3) * FP + j0))
             : "memory");
         const double w = b == 3 ? 0.5 : 1.0;
 #pragma unroll
@@ -219,11 +227,11 @@ __device__ __forceinline__ void sl_drain(unsigned tmem, int F, const double* pj,
   }
 }
 
-template <int FP, bool FULL>
+template <int FP, bool FULL, int S>
 __global__ void __launch_bounds__(SL_THREADS, 1)
     kcg_gram_sliced(const double* __restrict__ X, kcg_i64 n, int F_, double* __restrict__ G,
                     double* __restrict__ xt1, double* __restrict__ cmax) {
-  using Gm = SlGeom<FP>;
+  using Gm = SlGeom<FP, S>;
   // FULL: F == FP, a compile-time row pitch
   const int F = FULL ? FP : F_;
   extern __shared__ __align__(1024) unsigned char sl_smem[];
@@ -285,8 +293,8 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
       const unsigned kb = base + ks * 256;
       const unsigned acc = (first && ks == 0) ? 0u : 1u;
       sl_mma(tmem, sl_sdesc(kb), sl_sdesc(kb), id1, acc);
-      sl_mma(tmem + Gm::N1, sl_sdesc(kb), sl_sdesc(kb + (Gm::N1 / 8) * SL_SB), id1, acc);
-      sl_mma(tmem + 2 * Gm::N1, sl_sdesc(kb + (3 * FP / 8) * SL_SB), sl_sdesc(kb + (3 * FP / 8) * SL_SB), id2, acc);
+      if (Gm::NB1 == 2) sl_mma(tmem + Gm::N1, sl_sdesc(kb), sl_sdesc(kb + (Gm::N1 / 8) * SL_SB), id1, acc);
+      sl_mma(tmem + Gm::G2, sl_sdesc(kb + (3 * FP / 8) * SL_SB), sl_sdesc(kb + (3 * FP / 8) * SL_SB), id2, acc);
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(oeb + 8 * s2)
                  : "memory");
@@ -300,7 +308,7 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
   constexpr bool ALL = FULL && 8 * FP == SL_THREADS;  // every thread owns a real column
   const bool real = ALL || (act && i < F);
   int e = -960;  // segment exponent of column i
-  double scale = sl_pow2(53 - e);
+  double scale = sl_pow2(Gm::SCALE - e);
   unsigned lim_hi = 0u;           // high word of 2^(e + 1): the first tile always opens a segment
   unsigned cm_hi = 0u;            // high word of cm
   unsigned long long cm = 0ull;   // running max |x| bits
@@ -354,7 +362,7 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
       if (t > 0) {
         mma_done(t - 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (warp < 4) sl_drain<FP>(tmem, F, pj, P);
+        if (warp < 4) sl_drain<FP, S>(tmem, F, pj, P);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       }
       sl_bar();
@@ -368,11 +376,11 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
         sE[i] = en;
         tcm[i] = 0u;
 #pragma unroll
-        for (int b = 0; b < 7; ++b) pj[b * FP + i] = real ? sl_pow2(en - 5 - 8 * b) : 0.0;
+        for (int b = 0; b < S; ++b) pj[b * FP + i] = real ? sl_pow2(en - 5 - 8 * b) : 0.0;
       }
       sl_bar();
       e = sE[i];
-      scale = sl_pow2(53 - e);
+      scale = sl_pow2(Gm::SCALE - e);
       lim_hi = e >= 1023 ? 0x7FF00000u : (unsigned)(e + 1 + 1023) << 20;
       seg_n = 0;
     }
@@ -389,7 +397,7 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
       for (int q = 0; q < 4; ++q) {
         xacc += x[4 * g + q];
         const long long v = __double2ll_rn(x[4 * g + q] * scale);
-        const long long w = v + SL_OFF;
+        const long long w = v + Gm::OFF;
         L[q] = (unsigned)w;
         H[q] = (unsigned)((unsigned long long)w >> 32);
       }
@@ -397,19 +405,19 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
       const unsigned b0 = sl_prmt(L[2], L[3], 0x5140), b1 = sl_prmt(L[2], L[3], 0x7362);
       const unsigned h0 = sl_prmt(H[0], H[1], 0x5140), h1 = sl_prmt(H[0], H[1], 0x7362);
       const unsigned k0 = sl_prmt(H[2], H[3], 0x5140), k1 = sl_prmt(H[2], H[3], 0x7362);
-      // digit a = byte (6 - a) of w, xor 0x80 per byte
-      wd[6][g] = sl_prmt(a0, b0, 0x5410) ^ 0x80808080u;
-      wd[5][g] = sl_prmt(a0, b0, 0x7632) ^ 0x80808080u;
-      wd[4][g] = sl_prmt(a1, b1, 0x5410) ^ 0x80808080u;
-      wd[3][g] = sl_prmt(a1, b1, 0x7632) ^ 0x80808080u;
-      wd[2][g] = sl_prmt(h0, k0, 0x5410) ^ 0x80808080u;
-      wd[1][g] = sl_prmt(h0, k0, 0x7632) ^ 0x80808080u;
-      wd[0][g] = sl_prmt(h1, k1, 0x5410) ^ 0x80808080u;
+      // digit a = byte (S - 1 - a) of w, xor 0x80 per byte
+      wd[S - 1][g] = sl_prmt(a0, b0, 0x5410) ^ 0x80808080u;
+      wd[S - 2][g] = sl_prmt(a0, b0, 0x7632) ^ 0x80808080u;
+      wd[S - 3][g] = sl_prmt(a1, b1, 0x5410) ^ 0x80808080u;
+      wd[S - 4][g] = sl_prmt(a1, b1, 0x7632) ^ 0x80808080u;
+      wd[S - 5][g] = sl_prmt(h0, k0, 0x5410) ^ 0x80808080u;
+      wd[S - 6][g] = sl_prmt(h0, k0, 0x7632) ^ 0x80808080u;
+      if (S == 7) wd[0][g] = sl_prmt(h1, k1, 0x5410) ^ 0x80808080u;
     }
     if (act) {
       unsigned char* dst = dst0 + (t % SL_S2) * Gm::OPB;
 #pragma unroll
-      for (int a = 0; a < 7; ++a)
+      for (int a = 0; a < S; ++a)
         *reinterpret_cast<uint4*>(dst + a * (FP / 8) * SL_SB) = make_uint4(wd[a][0], wd[a][1], wd[a][2], wd[a][3]);
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -420,7 +428,7 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
     if (tid == 0) issue_mma(ct - 1, prev_first);
     mma_done(ct - 1);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp < 4) sl_drain<FP>(tmem, F, pj, P);
+    if (warp < 4) sl_drain<FP, S>(tmem, F, pj, P);
   }
   if (real) {
     atomicAdd(sx1 + i, xacc);
@@ -470,9 +478,9 @@ __global__ void __launch_bounds__(SL_THREADS, 1)
   }
 }
 
-template <int FP, bool FULL>
+template <int FP, bool FULL, int S>
 void launch_sliced(const double* X, size_t n, int F, double* G, double* xt1, double* colmax, cudaStream_t st) {
-  using Gm = SlGeom<FP>;
+  using Gm = SlGeom<FP, S>;
   const size_t smem = (size_t)SL_S2 * Gm::OPB + (size_t)FP * FP * 8 +
                       7 * FP * 8 + FP * 8 + FP * 8 + FP * 4 + FP * 4;
   static std::mutex mu;
@@ -482,7 +490,7 @@ void launch_sliced(const double* X, size_t n, int F, double* G, double* xt1, dou
   {
     std::lock_guard<std::mutex> lk(mu);
     if (smem > attr[dev & 63]) {
-      check(cudaFuncSetAttribute(kcg_gram_sliced<FP, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
+      check(cudaFuncSetAttribute(kcg_gram_sliced<FP, FULL, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem),
             "cudaFuncSetAttribute");
       attr[dev & 63] = smem;
     }
@@ -490,7 +498,7 @@ void launch_sliced(const double* X, size_t n, int F, double* G, double* xt1, dou
   const kcg_i64 tiles = (kcg_i64)n / SL_KT;
   kcg_i64 grid = num_sms();
   if (grid > tiles) grid = tiles > 0 ? tiles : 1;
-  kcg_gram_sliced<FP, FULL><<<(unsigned)grid, SL_THREADS, smem, st>>>(X, (kcg_i64)n, F, G, xt1, colmax);
+  kcg_gram_sliced<FP, FULL, S><<<(unsigned)grid, SL_THREADS, smem, st>>>(X, (kcg_i64)n, F, G, xt1, colmax);
   check(cudaGetLastError(), "kcg_gram_sliced launch");
 }
 
@@ -500,12 +508,20 @@ void launch_sliced(const double* X, size_t n, int F, double* G, double* xt1, dou
 bool launch_gram_sliced(const double* X, size_t n, int F, double* G, double* xt1, double* colmax,
                         cudaStream_t st) {
   if (F < 17 || F > 40) return false;
-  if (F == 24) launch_sliced<24, true>(X, n, F, G, xt1, colmax, st);
-  else if (F == 32) launch_sliced<32, true>(X, n, F, G, xt1, colmax, st);
-  else if (F == 40) launch_sliced<40, true>(X, n, F, G, xt1, colmax, st);
-  else if (F < 24) launch_sliced<24, false>(X, n, F, G, xt1, colmax, st);
-  else if (F < 32) launch_sliced<32, false>(X, n, F, G, xt1, colmax, st);
-  else launch_sliced<40, false>(X, n, F, G, xt1, colmax, st);
+  static const int digits = std::getenv("KCG_SLICED_DIGITS") && std::atoi(std::getenv("KCG_SLICED_DIGITS")) == 6 ? 6 : 7;
+  if (digits == 6) {  // A/B only: 48-bit digits
+    if (F == 40) launch_sliced<40, true, 6>(X, n, F, G, xt1, colmax, st);
+    else if (F <= 24) launch_sliced<24, false, 6>(X, n, F, G, xt1, colmax, st);
+    else if (F <= 32) launch_sliced<32, false, 6>(X, n, F, G, xt1, colmax, st);
+    else launch_sliced<40, false, 6>(X, n, F, G, xt1, colmax, st);
+    return true;
+  }
+  if (F == 24) launch_sliced<24, true, 7>(X, n, F, G, xt1, colmax, st);
+  else if (F == 32) launch_sliced<32, true, 7>(X, n, F, G, xt1, colmax, st);
+  else if (F == 40) launch_sliced<40, true, 7>(X, n, F, G, xt1, colmax, st);
+  else if (F < 24) launch_sliced<24, false, 7>(X, n, F, G, xt1, colmax, st);
+  else if (F < 32) launch_sliced<32, false, 7>(X, n, F, G, xt1, colmax, st);
+  else launch_sliced<40, false, 7>(X, n, F, G, xt1, colmax, st);
   return true;
 }
 
