@@ -1931,19 +1931,54 @@ std::string codegen(const std::vector<const Lowered*>& progs,
     cons_decl << "  double gacc[" << WA << "];\n  #pragma unroll\n  for (int j = 0; j < " << WA
               << "; ++j) gacc[j] = 0.0;\n  double rr = 0.0;\n";
     // 1 - sum_g x_g (A_hi + A_lo) as a compensated dot product (Ogita, Rump
-    // and Oishi's Dot2: TwoSum of the running sum with each rounded product,
-    // the product errors (exact by FMA), the A_lo terms and the sum errors
-    // gathered in one double) -- as accurate as twice the working precision,
-    // 11 FP64 operations per group instead of 14 for the double-double
-    // subtraction used before
-    cons_row << "      if (ok) {\n        double hi = 1.0, lo = 0.0;\n";
-    for (int j = 0; j < W; ++j)
-      cons_row << "        { const double p = __dmul_rn(x[" << j << "], a.alpha[" << j << "]);\n"
-               << "          const double pe = fma(x[" << j << "], a.alpha[" << W + j << "], fma(x[" << j
-               << "], a.alpha[" << j << "], -p));\n"
-               << "          const double s = __dsub_rn(hi, p), bb = __dsub_rn(s, hi);\n"
-               << "          const double e = __dadd_rn(__dsub_rn(hi, __dsub_rn(s, bb)), __dsub_rn(-p, bb));\n"
-               << "          hi = s; lo = __dadd_rn(lo, __dsub_rn(e, pe)); }\n";
+    // and Oishi's Dot2 class: TwoSums of the rounded products, the product
+    // errors (exact by FMA), the A_lo terms and the sum errors gathered in
+    // one double) -- as accurate as twice the working precision, ~11 FP64
+    // operations per group instead of 14 for a double-double subtraction
+    // The W products are summed as a pairwise tree of TwoSums (log2 W levels
+    // of independent work instead of a W-long dependent chain), then
+    // TwoSum(1, -S); every TwoSum error and product error is gathered in one
+    // double: the same Dot2-class accuracy with shorter dependence chains.
+    cons_row << "      if (ok) {\n";
+    {
+      std::vector<std::string> errs;  // error terms, summed as a tree at the end
+      for (int j = 0; j < W; ++j) {
+        cons_row << "        const double p" << j << " = __dmul_rn(x[" << j << "], a.alpha[" << j << "]);\n"
+                 << "        const double q" << j << " = fma(x[" << j << "], a.alpha[" << W + j << "], fma(x[" << j
+                 << "], a.alpha[" << j << "], -p" << j << "));\n";
+        errs.push_back("q" + std::to_string(j));
+      }
+      std::vector<std::string> lv;
+      for (int j = 0; j < W; ++j) lv.push_back("p" + std::to_string(j));
+      int tmp = 0;
+      while (lv.size() > 1) {
+        std::vector<std::string> nx;
+        for (size_t k = 0; k + 1 < lv.size(); k += 2) {
+          const std::string t = std::to_string(tmp++);
+          cons_row << "        const double t" << t << " = __dadd_rn(" << lv[k] << ", " << lv[k + 1] << ");\n"
+                   << "        const double b" << t << " = __dsub_rn(t" << t << ", " << lv[k] << ");\n"
+                   << "        const double u" << t << " = __dadd_rn(__dsub_rn(" << lv[k] << ", __dsub_rn(t" << t << ", b"
+                   << t << ")), __dsub_rn(" << lv[k + 1] << ", b" << t << "));\n";
+          nx.push_back("t" + t);
+          errs.push_back("u" + t);
+        }
+        if (lv.size() % 2) nx.push_back(lv.back());
+        lv = nx;
+      }
+      while (errs.size() > 1) {
+        std::vector<std::string> nx;
+        for (size_t k = 0; k + 1 < errs.size(); k += 2) {
+          const std::string v = "v" + std::to_string(tmp++);
+          cons_row << "        const double " << v << " = __dadd_rn(" << errs[k] << ", " << errs[k + 1] << ");\n";
+          nx.push_back(v);
+        }
+        if (errs.size() % 2) nx.push_back(errs.back());
+        errs = nx;
+      }
+      cons_row << "        double hi, lo;\n        { const double s = __dsub_rn(1.0, " << lv[0] << "), bb = __dsub_rn(s, 1.0);\n"
+               << "          const double e = __dadd_rn(__dsub_rn(1.0, __dsub_rn(s, bb)), __dsub_rn(-" << lv[0]
+               << ", bb));\n          hi = s; lo = __dsub_rn(e, " << errs[0] << "); }\n";
+    }
     cons_row << "        const double r = __dadd_rn(hi, lo);\n";
     for (int j = 0; j < W; ++j) cons_row << "        gacc[" << j << "] = fma(x[" << j << "], r, gacc[" << j << "]);\n";
     // sum of r^2 at these weights (a.r2, nullable): with the gradient and the
