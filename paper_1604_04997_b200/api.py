@@ -776,33 +776,36 @@ def fit_from_csv(path, programs=None, device: str = "", discard: int = 4, stream
     meas = read_measurements(path, discard)
     if not meas:
         raise _capi.KcgError(_capi.E_EMPTY, "no fit cases")
-    rows, bad = 0, 0
+    rows = 0
     staged = []
+    bad_dev = torch.zeros(1, dtype=torch.int64, device="cuda")  # read once, after every kernel
     for km in meas:
         if (km.times <= 0).any():
             raise _capi.KcgError(_capi.E_NONPOSITIVE_TIME, f"observed time must be positive ({km.kernel})")
         prog = _program_for(km.kernel, programs)
         cols, T = _device_rows(km, prog)
-        st = gram_fused(prog, cols, T, stream=stream)
+        arr, n, _ = _columns(prog, cols)
+        st = GramStats.zeros(len(prog.props), "cuda")
+        check(lib().kcg_gram_fused(prog.handle, arr, T.data_ptr(), n, st.G.data_ptr(), st.xt1.data_ptr(),
+                                   st.colmax.data_ptr(), bad_dev.data_ptr(), _stream(stream)))
         idx = torch.tensor(prog.props, dtype=torch.int64, device="cuda")
         G[idx.unsqueeze(1), idx.unsqueeze(0)] += st.G
         x1[idx] += st.xt1
         cm[idx] = torch.maximum(cm[idx], st.colmax)
-        rows += st.n_rows
-        bad += st.bad_rows
-        staged.append((prog, cols, T))
+        rows += n
+        staged.append((prog, cols, T, idx))
+    bad = int(bad_dev.item())
     if bad:
         raise _capi.KcgError(_capi.E_ASSUMPTION_VIOLATED, f"{bad} measurement rows are not admissible")
     stats = GramStats(G, x1, cm, rows)
     alpha, rank = solve_gram(stats)
     if refine == 0:
-        obj = sum(residual_fused(prog, cols, T, alpha, stream=stream) for prog, cols, T in staged)
+        obj = sum(residual_fused(prog, cols, T, alpha, stream=stream) for prog, cols, T, _ in staged)
     for step in range(refine):  # schema-wide gradient: the kernels' rows are disjoint
         last = step == refine - 1
         g = torch.zeros(K, dtype=torch.float64, device="cuda")
         r2 = torch.zeros(1, dtype=torch.float64, device="cuda") if last else None
-        for prog, cols, T in staged:
-            idx = torch.tensor(prog.props, dtype=torch.int64, device="cuda")
+        for prog, cols, T, idx in staged:
             g[idx] += residual_grad_fused(prog, cols, T, alpha, stream=stream, r2=r2)
         new = refine_gram(stats, alpha, g)
         if last:  # objective at the refined weights from this pass (no residual pass per kernel)
