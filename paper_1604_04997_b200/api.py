@@ -741,9 +741,15 @@ def write_campaign_columns(path, records) -> None:
     write_columns(path, cols)
 
 
+_SUITE_PROGRAMS: dict = {}  # bundled programs used by the CSV fit / eval (parsed and lowered once)
+
+
 def _program_for(kernel: str, programs) -> Program:
     if programs is None:
-        return load_program(kernel)
+        prog = _SUITE_PROGRAMS.get(kernel)
+        if prog is None:
+            prog = _SUITE_PROGRAMS[kernel] = load_program(kernel)
+        return prog
     if isinstance(programs, Mapping):
         return programs[kernel]
     return Program.from_file(Path(programs) / f"{kernel}.kcp")
