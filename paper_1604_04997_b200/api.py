@@ -799,20 +799,28 @@ def fit_from_csv(path, programs=None, device: str = "", discard: int = 4, stream
         x1[idx] += st.xt1
         cm[idx] = torch.maximum(cm[idx], st.colmax)
         rows += n
-        staged.append((prog, cols, T, idx))
+        staged.append((prog, cols, T, idx, arr, n))
     bad = int(bad_dev.item())
     if bad:
         raise _capi.KcgError(_capi.E_ASSUMPTION_VIOLATED, f"{bad} measurement rows are not admissible")
     stats = GramStats(G, x1, cm, rows)
     alpha, rank = solve_gram(stats)
     if refine == 0:
-        obj = sum(residual_fused(prog, cols, T, alpha, stream=stream) for prog, cols, T, _ in staged)
+        obj = sum(residual_fused(prog, cols, T, alpha, stream=stream) for prog, cols, T, *_ in staged)
     for step in range(refine):  # schema-wide gradient: the kernels' rows are disjoint
         last = step == refine - 1
         g = torch.zeros(K, dtype=torch.float64, device="cuda")
         r2 = torch.zeros(1, dtype=torch.float64, device="cuda") if last else None
-        for prog, cols, T, idx in staged:
-            g[idx] += residual_grad_fused(prog, cols, T, alpha, stream=stream, r2=r2)
+        a = (ctypes.c_double * len(alpha))(*alpha)  # one host weight array for every kernel of the step
+        for prog, cols, T, idx, arr, n in staged:
+            gk = torch.zeros(len(prog.props), dtype=torch.float64, device="cuda")
+            if r2 is None:
+                check(lib().kcg_residual_grad_fused(prog.handle, arr, T.data_ptr(), n, a, gk.data_ptr(),
+                                                    _stream(stream)))
+            else:
+                check(lib().kcg_residual_grad_obj_fused(prog.handle, arr, T.data_ptr(), n, a, gk.data_ptr(),
+                                                        r2.data_ptr(), _stream(stream)))
+            g[idx] += gk
         new = refine_gram(stats, alpha, g)
         if last:  # objective at the refined weights from this pass (no residual pass per kernel)
             obj = refined_objective(stats, alpha, new, g, r2)
